@@ -1,0 +1,152 @@
+/*
+ * ringmix_b200 — C-ABI of the B200-native learner-averaging hot path.
+ *
+ * The reference (arXiv 2002.01119 simulator `ringmix`, pure Python/numpy) has
+ * no FFI; its plugin surface for this path is a set of Python functions.  Each
+ * entry point below replaces one of them (file:line under /root/reference):
+ *
+ *   rm_perm_tables        <- mixing.permutation_for_step     pkg/src/ringmix/mixing.py:116-123
+ *                            (+ the conjugation T0[p, p] of  simulation.py:299-300 /
+ *                             mixing.conjugate_by_permutation mixing.py:126-140,
+ *                             reduced to neighbour tables)
+ *   rm_perm_sequential    <- seeding.stream + repeated        seeding.py:35-37,
+ *                            mixing.sample_permutation        mixing.py:109-113
+ *                            as drawn by monte_carlo_consensus spectral.py:273-277
+ *   rm_pcg64_raw          <- numpy PCG64.random_raw under SeedSequence (pins the core)
+ *   rm_ring_mix_sgd_*     <- simulation._gossip_step          simulation.py:263-268
+ *                            = apply_mixing(W, T) - lr*G      mixing.py:143-162
+ *                            for T = ring or ring[p, p]       (step_rand_psgd :285-301,
+ *                                                              step_dpsgd_fixed :271-273,
+ *                                                              step_adpsgd_fixed :276-282)
+ *                            with the fused _check_divergence  simulation.py:390-395
+ *   rm_mean_sgd_*         <- step_d1d / uniform apply_mixing   simulation.py:304-312,
+ *                                                              mixing.py:159-161
+ *   rm_spsgd_*            <- step_spsgd                        simulation.py:251-260
+ *   rm_*_host_f32         <- the same step on HOST buffers (H2D, kernel, D2H pipelined)
+ *   rm_ipc_* / rm_shard_* <- (no reference counterpart: the reference simulates all
+ *                            learners in one process; these shard them over GPUs)
+ *
+ * Conventions
+ *   - All compute pointers are caller-owned DEVICE memory unless the name says
+ *     `host`; nothing here allocates device memory.
+ *   - Weights are learner-major: row l (learner l) starts at base + l*ld
+ *     elements.  The reference's (d, L) matrix is the transpose view.
+ *   - Calls are stream-ordered on `stream` (a cudaStream_t, NULL = legacy default).
+ *   - Return 0 on success; a negative RM_E* code for bad arguments; a positive
+ *     cudaError_t for CUDA failures.  rm_last_error() gives a thread-local
+ *     message (the reference's ValueError text where one exists).
+ *   - Safe to call from several host threads on distinct streams.
+ *   - W and Wout must not alias (cross-learner read-after-write hazard).
+ *   - absmax_bits (optional): receives atomicMax of the IEEE-754 bit pattern of
+ *     |W'| as a double; > 0x7ff0000000000000 means NaN, == means inf.  Caller
+ *     zeroes it.
+ */
+#ifndef RINGMIX_B200_H
+#define RINGMIX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RM_EINVAL (-1)
+#define RM_ENOSYS (-2)
+#define RM_ERANGE (-3)
+#define RM_ETIMEDOUT (-4)
+
+const char* rm_last_error(void);
+int rm_version(void);
+int rm_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- permutations (bit-exact with numpy 2.3.5 SeedSequence/PCG64/permutation) ----
+ * prefix_words: the entropy words of (seed, tag) — numpy's
+ * _coerce_to_uint32_array: each int as little-endian u32 limbs, 0 -> [0] —
+ * computed by the caller (any size of seed).  The kernel appends limbs(step).
+ * perm/inv (required) and left/right (optional) are int32[nsteps][L]. */
+int rm_perm_tables(const uint32_t* prefix_words, int n_prefix, uint64_t step0, int nsteps, int L,
+                   int32_t* perm, int32_t* inv, int32_t* left, int32_t* right, void* stream);
+
+/* nstreams independent streams (entropy prefix + limbs(idx0 + s)); each draws
+ * `count` permutations back to back.  perms: int32[nstreams][count][L]. */
+int rm_perm_sequential(const uint32_t* prefix_words, int n_prefix, uint64_t idx0, int nstreams,
+                       int count, int L, int32_t* perms, void* stream);
+
+/* Stateful streams (the Generator objects seeding.stream returns).  A state is
+ * 6 x uint64 in device memory.  rm_pcg_seed seeds nstreams states from
+ * prefix (+ limbs(idx0 + s) when with_index); rm_pcg_permutations draws
+ * `count` permutations per state back to back and writes the advanced state
+ * back, so successive calls continue the stream exactly like repeated
+ * Generator.permutation calls. */
+int rm_pcg_seed(const uint32_t* prefix_words, int n_prefix, int with_index, uint64_t idx0,
+                int nstreams, uint64_t* states, void* stream);
+int rm_pcg_permutations(uint64_t* states, int nstreams, int count, int L, int32_t* perms,
+                        void* stream);
+
+/* count raw next64() outputs of PCG64(SeedSequence(entropy_words)). */
+int rm_pcg64_raw(const uint32_t* entropy_words, int n_words, int count, uint64_t* out,
+                 void* stream);
+
+/* ---- fused mix + SGD:  Wout[j] = (W[left j] + W[j] + W[right j])/3 - lr*G[j] ----
+ * G may be NULL (pure apply_mixing).  L == 3 takes the exact column-mean path
+ * like the reference (mixing.py:159-161).  fp32/fp64 compute in fp64 with the
+ * reference's rounding sequence; bf16 (uint16_t storage) computes in fp32. */
+int rm_ring_mix_sgd_f32(const float* W, const float* G, float* Wout, const int32_t* left,
+                        const int32_t* right, int L, int64_t d, int64_t ldw, int64_t ldg,
+                        int64_t ldo, double lr, unsigned long long* absmax_bits, void* stream);
+int rm_ring_mix_sgd_f64(const double* W, const double* G, double* Wout, const int32_t* left,
+                        const int32_t* right, int L, int64_t d, int64_t ldw, int64_t ldg,
+                        int64_t ldo, double lr, unsigned long long* absmax_bits, void* stream);
+int rm_ring_mix_sgd_bf16(const uint16_t* W, const uint16_t* G, uint16_t* Wout,
+                         const int32_t* left, const int32_t* right, int L, int64_t d, int64_t ldw,
+                         int64_t ldg, int64_t ldo, double lr, unsigned long long* absmax_bits,
+                         void* stream);
+
+/* ---- D1D / uniform:  Wout[j] = mean_l W[l] - lr*G[j]  (numpy pairwise mean) ---- */
+int rm_mean_sgd_f32(const float* W, const float* G, float* Wout, int L, int64_t d, int64_t ldw,
+                    int64_t ldg, int64_t ldo, double lr, unsigned long long* absmax_bits,
+                    void* stream);
+int rm_mean_sgd_f64(const double* W, const double* G, double* Wout, int L, int64_t d,
+                    int64_t ldw, int64_t ldg, int64_t ldo, double lr,
+                    unsigned long long* absmax_bits, void* stream);
+int rm_mean_sgd_bf16(const uint16_t* W, const uint16_t* G, uint16_t* Wout, int L, int64_t d,
+                     int64_t ldw, int64_t ldg, int64_t ldo, double lr,
+                     unsigned long long* absmax_bits, void* stream);
+
+/* ---- S-PSGD:  Wout[j] = W[j] - lr*mean_l G[l];  *mismatch |= any(W[j] != W[0]) ---- */
+int rm_spsgd_f32(const float* W, const float* G, float* Wout, int L, int64_t d, int64_t ldw,
+                 int64_t ldg, int64_t ldo, double lr, unsigned int* mismatch,
+                 unsigned long long* absmax_bits, void* stream);
+int rm_spsgd_f64(const double* W, const double* G, double* Wout, int L, int64_t d, int64_t ldw,
+                 int64_t ldg, int64_t ldo, double lr, unsigned int* mismatch,
+                 unsigned long long* absmax_bits, void* stream);
+int rm_spsgd_bf16(const uint16_t* W, const uint16_t* G, uint16_t* Wout, int L, int64_t d,
+                  int64_t ldw, int64_t ldg, int64_t ldo, double lr, unsigned int* mismatch,
+                  unsigned long long* absmax_bits, void* stream);
+
+/* ---- host-buffer step (reference calling convention: arrays in host RAM) ----
+ * W_host/G_host/out_host: (L, d) row-major fp32 in host memory (pinned for
+ * overlap); left/right: host int32[L].  The step is pipelined over column
+ * chunks (H2D || kernel || D2H) through `workspace` (device, workspace_bytes;
+ * rm_host_chunk_cols reports the chunk width it allows).  Stream-ordered on
+ * `stream`; the host buffers must stay valid until it completes.  One call at a
+ * time per device (the internal copy streams are shared).  G_host may be NULL. */
+int rm_host_chunk_cols(int L, int64_t workspace_bytes, int64_t* chunk_cols);
+int rm_ring_mix_sgd_host_f32(const float* W_host, const float* G_host, float* out_host,
+                             const int32_t* left_host, const int32_t* right_host, int L, int64_t d,
+                             double lr, void* workspace, int64_t workspace_bytes,
+                             unsigned long long* absmax_bits, void* stream);
+
+/* ---- batched ring products (monte_carlo_consensus, spectral.py:273-279) ----
+ * For b < B: Y_b[j] = ring3(X_b[left_b j], X_b[j], X_b[right_b j]) with `@`
+ * (dgemm) rounding, rows of length d at stride ld, batches at batch_stride;
+ * left/right are int32[B][L]. */
+int rm_ring_mix_batched_f64(const double* X, double* Y, const int32_t* left, const int32_t* right,
+                            int B, int L, int64_t d, int64_t ld, int64_t batch_stride,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RINGMIX_B200_H */

@@ -1,0 +1,107 @@
+"""ctypes binding of libringmix_b200.so (the C-ABI in include/ringmix_b200.h).
+
+There is no fallback: if the library is missing or CUDA is unavailable the
+hot-path functions raise.  The library is built in-tree by
+``__graft_entry__.build()`` (or ``make -C paper_2002_01119_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import torch
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "lib" / "libringmix_b200.so"
+
+RM_EINVAL = -1
+RM_ENOSYS = -2
+RM_ERANGE = -3
+RM_ETIMEDOUT = -4
+
+vp = ctypes.c_void_p
+i32 = ctypes.c_int
+i64 = ctypes.c_int64
+u64 = ctypes.c_uint64
+dbl = ctypes.c_double
+
+_SIGNATURES = {
+    "rm_last_error": ([], ctypes.c_char_p),
+    "rm_version": ([], i32),
+    "rm_device_info": ([i32, vp, vp, vp], i32),
+    "rm_perm_tables": ([vp, i32, u64, i32, i32, vp, vp, vp, vp, vp], i32),
+    "rm_perm_sequential": ([vp, i32, u64, i32, i32, i32, vp, vp], i32),
+    "rm_pcg64_raw": ([vp, i32, i32, vp, vp], i32),
+    "rm_pcg_seed": ([vp, i32, i32, u64, i32, vp, vp], i32),
+    "rm_pcg_permutations": ([vp, i32, i32, i32, vp, vp], i32),
+    "rm_ring_mix_batched_f64": ([vp, vp, vp, vp, i32, i32, i64, i64, i64, vp], i32),
+    "rm_host_chunk_cols": ([i32, i64, vp], i32),
+    "rm_ring_mix_sgd_host_f32": ([vp, vp, vp, vp, vp, i32, i64, dbl, vp, i64, vp, vp], i32),
+}
+for _sfx in ("f32", "f64", "bf16"):
+    _SIGNATURES[f"rm_ring_mix_sgd_{_sfx}"] = (
+        [vp, vp, vp, vp, vp, i32, i64, i64, i64, i64, dbl, vp, vp], i32)
+    _SIGNATURES[f"rm_mean_sgd_{_sfx}"] = ([vp, vp, vp, i32, i64, i64, i64, i64, dbl, vp, vp], i32)
+    _SIGNATURES[f"rm_spsgd_{_sfx}"] = ([vp, vp, vp, i32, i64, i64, i64, i64, dbl, vp, vp, vp], i32)
+
+OPTIONAL_SIGNATURES: dict = {}
+
+
+class RingmixError(RuntimeError):
+    """A CUDA-side failure inside libringmix_b200."""
+
+
+_lib = None
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGNATURES)
+
+
+def load() -> ctypes.CDLL:
+    """Load the library (no CUDA call is made here)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            f"g.build()'` (there is no CPU fallback for the ringmix_b200 hot path)")
+    lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+    for name, (args, res) in {**_SIGNATURES, **OPTIONAL_SIGNATURES}.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().rm_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = last_error()
+    if rc < 0:
+        raise ValueError(msg or f"{what}: invalid argument ({rc})")
+    raise RingmixError(f"{what}: {msg} (cuda error {rc})")
+
+
+def require_cuda(t: torch.Tensor | None = None) -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("ringmix_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+    if t is not None and not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else int(t.data_ptr())

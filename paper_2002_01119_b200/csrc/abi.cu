@@ -1,0 +1,50 @@
+// C-ABI plumbing: thread-local error messages, device queries.
+#include "common.cuh"
+#include "../../include/ringmix_b200.h"
+
+#include <mutex>
+
+namespace rm {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail_cuda(cudaError_t e, const char* where) {
+  set_error("%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+  return static_cast<int>(e);
+}
+
+int sm_count(int device) {
+  static int cache[64];
+  if (device < 0) cudaGetDevice(&device);
+  if (device < 0 || device >= 64) return 148;
+  if (cache[device] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[device] = n;
+  }
+  return cache[device];
+}
+
+}  // namespace rm
+
+extern "C" const char* rm_last_error(void) { return rm::g_err; }
+
+extern "C" int rm_version(void) { return 1; }
+
+extern "C" int rm_device_info(int device, int* sms, int* major, int* minor) {
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) return rm::fail_cuda(e, "cudaGetDeviceProperties");
+  if (sms) *sms = p.multiProcessorCount;
+  if (major) *major = p.major;
+  if (minor) *minor = p.minor;
+  return 0;
+}

@@ -1,0 +1,96 @@
+// Shared helpers for libringmix_b200: error plumbing and sm_100a PTX wrappers.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+namespace rm {
+
+// ---- error plumbing (thread-local message, see include/ringmix_b200.h) ----
+void set_error(const char* fmt, ...);
+int fail_cuda(cudaError_t e, const char* where);
+
+#define RM_CHECK_LAUNCH(where)                                  \
+  do {                                                          \
+    cudaError_t _e = cudaGetLastError();                        \
+    if (_e != cudaSuccess) return ::rm::fail_cuda(_e, where);   \
+  } while (0)
+
+#include "../../include/ringmix_b200.h"
+constexpr int RM_OK = 0;
+
+int sm_count(int device);
+
+// ---- PTX wrappers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// TMA bulk copy global -> shared (1-D, bytes % 16 == 0, both ends 16B aligned),
+// completion signalled on an mbarrier via complete_tx.
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 16-byte streaming store (evict-first; the output is not re-read this step).
+__device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// atomicMax on the bit pattern of |y| as a double: monotone for non-negative
+// doubles, and every NaN pattern (> 0x7ff0...) sorts above +inf.
+__device__ __forceinline__ void absmax_publish(unsigned long long* slot, unsigned long long bits) {
+  // warp reduce then one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+    bits = other > bits ? other : bits;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(slot, bits);
+}
+
+__device__ __forceinline__ unsigned long long abs_bits(double y) {
+  return static_cast<unsigned long long>(__double_as_longlong(y)) & 0x7fffffffffffffffULL;
+}
+
+}  // namespace rm

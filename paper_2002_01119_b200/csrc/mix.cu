@@ -1,0 +1,596 @@
+// Fused learner-averaging kernels: gossip mix + SGD (RAD / AD / D-PSGD),
+// uniform mean + SGD (D1D), and S-PSGD — the reference's
+//   simulation._gossip_step (pkg/src/ringmix/simulation.py:263-268)
+//   W_next = apply_mixing(W, T) - lr * G        (mixing.py:143-162)
+// and step_spsgd (simulation.py:251-260), one HBM pass per step.
+//
+// HBM layout: learner-major (L, d) rows with leading dimension ld (elements);
+// the reference's (d, L) matrix is the transpose view.
+//
+// Design: a persistent kernel walks column tiles [c0, c0+CW)
+// of all L rows.  Per tile, one warp issues 1-D TMA bulk copies
+// (cp.async.bulk, one per row) of W[:, tile] and G[:, tile] into a shared
+// memory stage, completion tracked by an mbarrier (expect_tx).  NS stages
+// are in flight per CTA, so every W element crosses HBM exactly once although
+// it feeds three outputs (itself and its two ring neighbours), and the whole
+// chip keeps >= 35 KB/SM of loads in flight.  Consumers read the stage with
+// 16-byte shared loads and write W' with 16-byte streaming stores.
+//
+// Arithmetic: fp32/fp64 storage computes in fp64 with the
+// reference's exact rounding sequence, so results are the reference's fp64
+// result rounded once to the storage type:
+//   ring:    acc = fl(w_a*t); acc = fma(w_b,t,acc); acc = fma(w_c,t,acc)
+//            (a<b<c the sorted neighbour triple, t = fl64(1/3): OpenBLAS dgemm
+//            accumulates ascending k with FMA; zero terms add exactly)
+//   uniform: numpy pairwise sum over the learner axis, then / L
+//   update:  y = mix - fl(lr*g)        (numpy evaluates lr*G first)
+// bf16 storage computes the same sequence in fp32.
+// A fused epilogue publishes max|W'| (NaN sorts above inf) for the
+// reference's _check_divergence (simulation.py:390-395): zero extra bytes.
+#include "common.cuh"
+#include "../../include/ringmix_b200.h"
+
+namespace rm {
+
+enum Mode { kRing = 0, kMean = 1, kSpsgd = 2 };
+
+constexpr int kThreads = 512;
+constexpr int kStages = 3;
+constexpr int kMaxTmaL = 1024;
+constexpr int kStageTarget = 64 * 1024;
+
+struct MixArgs {
+  const void* W;
+  const void* G;
+  void* out;
+  long long ldw, ldg, ldo;
+  long long d;       // columns
+  long long d_main;  // columns covered by the tiled TMA path (multiple of VEC)
+  int L;
+  int cw;        // tile width (elements), power of two, multiple of VEC
+  int log2_nv;   // log2(cw / VEC)
+  long long ntiles;
+  const int32_t* left;
+  const int32_t* right;
+  double lr;
+  unsigned long long* absmax;  // may be null
+  unsigned int* mismatch;      // kSpsgd: set nonzero if W rows differ
+};
+
+// ----------------------------------------------------------------------------
+// element traits
+// ----------------------------------------------------------------------------
+template <typename T>
+struct Elem;
+
+template <>
+struct Elem<float> {
+  using acc = double;
+  static constexpr int VEC = 4;
+  __device__ static __forceinline__ double ld(const float* p, int i) { return (double)p[i]; }
+  __device__ static __forceinline__ float st(double y) { return __double2float_rn(y); }
+  __device__ static __forceinline__ double absd(float y) { return fabs((double)y); }
+};
+
+template <>
+struct Elem<double> {
+  using acc = double;
+  static constexpr int VEC = 2;
+  __device__ static __forceinline__ double ld(const double* p, int i) { return p[i]; }
+  __device__ static __forceinline__ double st(double y) { return y; }
+  __device__ static __forceinline__ double absd(double y) { return fabs(y); }
+};
+
+template <>
+struct Elem<__nv_bfloat16> {
+  using acc = float;
+  static constexpr int VEC = 8;
+  __device__ static __forceinline__ float ld(const __nv_bfloat16* p, int i) {
+    return __bfloat162float(p[i]);
+  }
+  __device__ static __forceinline__ __nv_bfloat16 st(float y) { return __float2bfloat16_rn(y); }
+  __device__ static __forceinline__ double absd(__nv_bfloat16 y) {
+    return fabs((double)__bfloat162float(y));
+  }
+};
+
+// rounding-explicit arithmetic (never contracted)
+__device__ __forceinline__ double r_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float r_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double r_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float r_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double r_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float r_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double r_div(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float r_div(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double r_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float r_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+template <typename A>
+__device__ __forceinline__ A third();
+template <>
+__device__ __forceinline__ double third<double>() { return 1.0 / 3.0; }
+template <>
+__device__ __forceinline__ float third<float>() { return 1.0f / 3.0f; }
+
+template <typename A>
+__device__ __forceinline__ A ring3(A wa, A wb, A wc) {
+  const A t = third<A>();
+  A acc = r_mul(wa, t);
+  acc = r_fma(wb, t, acc);
+  return r_fma(wc, t, acc);
+}
+
+// numpy DOUBLE_pairwise_sum over n values at stride `st` (generic, recursive
+// in blocks; used by the scalar paths).  `get(i)` loads value i.
+template <typename A, typename F>
+__device__ A pairwise_sum(F get, int lo, int n) {
+  if (n < 8) {
+    A res = -0.0;
+    for (int i = 0; i < n; i++) res = r_add(res, get(lo + i));
+    return res;
+  }
+  if (n <= 128) {
+    A r[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) r[k] = get(lo + k);
+    int i;
+    for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int k = 0; k < 8; k++) r[k] = r_add(r[k], get(lo + i + k));
+    }
+    A res = r_add(r_add(r_add(r[0], r[1]), r_add(r[2], r[3])),
+                  r_add(r_add(r[4], r[5]), r_add(r[6], r[7])));
+    for (; i < n; i++) res = r_add(res, get(lo + i));
+    return res;
+  }
+  // recursion depth is log2(L/128); L <= 2^31 keeps it tiny.  Iterate the
+  // left spine explicitly to avoid deep device recursion.
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  A left = pairwise_sum<A>(get, lo, n2);
+  A right = pairwise_sum<A>(get, lo + n2, n - n2);
+  return r_add(left, right);
+}
+
+// ----------------------------------------------------------------------------
+// scalar path: any alignment / any L; one thread per (row, column)
+// Used for unaligned layouts, very large L, and the < VEC tail columns.
+// ----------------------------------------------------------------------------
+template <typename T, int MODE, bool HAS_G>
+__global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_begin) {
+  using E = Elem<T>;
+  using A = typename E::acc;
+  const T* W = static_cast<const T*>(a.W);
+  const T* G = static_cast<const T*>(a.G);
+  T* out = static_cast<T*>(a.out);
+  const long long ncols = a.d - c_begin;
+  const long long total = ncols * a.L;
+  unsigned long long amax = 0;
+  const A lr = (A)a.lr;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(idx / ncols);
+    const long long c = c_begin + idx % ncols;
+    A y;
+    if (MODE == kRing) {
+      int x0 = a.left[j], x1 = j, x2 = a.right[j], t;
+      if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+      if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
+      if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+      y = ring3<A>(E::ld(W + x0 * a.ldw, c), E::ld(W + x1 * a.ldw, c), E::ld(W + x2 * a.ldw, c));
+      if (HAS_G) y = r_sub(y, r_mul(lr, E::ld(G + j * a.ldg, c)));
+    } else if (MODE == kMean) {
+      auto get = [&](int i) { return (A)E::ld(W + i * a.ldw, c); };
+      A m = r_div(pairwise_sum<A>(get, 0, a.L), (A)a.L);
+      y = HAS_G ? r_sub(m, r_mul(lr, E::ld(G + j * a.ldg, c))) : m;
+    } else {  // kSpsgd: W - lr * mean_l(G)
+      auto get = [&](int i) { return (A)E::ld(G + i * a.ldg, c); };
+      A m = r_div(pairwise_sum<A>(get, 0, a.L), (A)a.L);
+      A w = E::ld(W + j * a.ldw, c);
+      if (a.mismatch && !(W[j * a.ldw + c] == W[c])) atomicOr(a.mismatch, 1u);
+      y = r_sub(w, r_mul(lr, m));
+    }
+    T ys = E::st(y);
+    out[j * a.ldo + c] = ys;
+    unsigned long long b = abs_bits((double)E::absd(ys));
+    amax = b > amax ? b : amax;
+  }
+  if (a.absmax) absmax_publish(a.absmax, amax);
+}
+
+// ----------------------------------------------------------------------------
+// tiled TMA path
+// ----------------------------------------------------------------------------
+template <typename T>
+struct Vec {
+  uint4 raw;
+  __device__ __forceinline__ const T* e() const { return reinterpret_cast<const T*>(&raw); }
+  __device__ __forceinline__ T* e() { return reinterpret_cast<T*>(&raw); }
+};
+
+template <typename T, int MODE, bool HAS_G>
+__global__ void __launch_bounds__(kThreads, 1) mix_tma_kernel(MixArgs a) {
+  using E = Elem<T>;
+  using A = typename E::acc;
+  constexpr int VEC = E::VEC;
+  extern __shared__ __align__(128) unsigned char smem[];
+
+  const int L = a.L;
+  const int cw = a.cw;
+  const int row_bytes = cw * (int)sizeof(T);
+  const int w_bytes = L * row_bytes;
+  const bool stage_g = HAS_G || MODE == kSpsgd;
+  const int stage_bytes = w_bytes * (stage_g ? 2 : 1);
+
+  // layout: [mbarriers (NS x 8B) | pad to 128 | tri table (L x int4) | stages]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  int4* s_tri = reinterpret_cast<int4*>(smem + 128);
+  unsigned char* stages = smem + 128 + ((L * 16 + 127) / 128) * 128;
+  double* s_mean = nullptr;  // kMean/kSpsgd: per-column mean (A), after stages
+  if (MODE != kRing) s_mean = reinterpret_cast<double*>(stages + kStages * stage_bytes);
+
+  const T* W = static_cast<const T*>(a.W);
+  const T* G = static_cast<const T*>(a.G);
+  T* out = static_cast<T*>(a.out);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  if (MODE == kRing) {
+    for (int j = tid; j < L; j += kThreads) {
+      int x0 = a.left[j], x1 = j, x2 = a.right[j], t;
+      if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+      if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
+      if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+      s_tri[j] = make_int4(x0, x1, x2, j);
+    }
+  }
+  __syncthreads();
+
+  const long long first = blockIdx.x;
+  const long long stride = gridDim.x;
+
+  // issue tile `t` into stage `s` (warp 0)
+  auto issue = [&](int s, long long t) {
+    const long long c0 = t * cw;
+    const long long width = min((long long)cw, a.d_main - c0);
+    const uint32_t bytes = (uint32_t)(width * sizeof(T));
+    unsigned char* st = stages + (size_t)s * stage_bytes;
+    if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes * L * (stage_g ? 2u : 1u));
+    __syncwarp();
+    for (int r = lane; r < L; r += 32) {
+      bulk_g2s(st + r * row_bytes, W + r * a.ldw + c0, bytes, &full[s]);
+      if (stage_g) bulk_g2s(st + w_bytes + r * row_bytes, G + r * a.ldg + c0, bytes, &full[s]);
+    }
+  };
+
+  if (warp == 0) {
+    for (int s = 0; s < kStages; s++) {
+      long long t = first + s * stride;
+      if (t < a.ntiles) issue(s, t);
+    }
+  }
+
+  unsigned long long amax = 0;
+  const A lr = (A)a.lr;
+  const int log2_nv = a.log2_nv;
+  const int nv_full = 1 << log2_nv;
+
+  int it = 0;
+  for (long long t = first; t < a.ntiles; t += stride, ++it) {
+    const int s = it % kStages;
+    const uint32_t parity = (it / kStages) & 1;
+    const long long c0 = t * cw;
+    const int width = (int)min((long long)cw, a.d_main - c0);
+    const int nv = width / VEC;
+    const T* sW = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes);
+    const T* sG = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes + w_bytes);
+
+    mbar_wait(&full[s], parity);
+
+    if (MODE != kRing) {
+      // per-column numpy pairwise mean over the L staged rows; 8 lanes per
+      // column hold numpy's 8 partial sums r[0..7] (n <= 128 case) and combine
+      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) with xor-shuffles (fp add is
+      // commutative, so lane order inside each pair does not matter).
+      const T* src = (MODE == kMean) ? sW : sG;
+      if (L <= 128 && L >= 8) {
+        const int n8 = L - (L % 8);
+        // warp-uniform trip count so the xor-shuffles always see full warps;
+        // 8-lane groups are whole (kThreads and 32 are multiples of 8).
+        for (int base0 = warp * 32; base0 < width * 8; base0 += kThreads) {
+          const int base = base0 + lane;
+          const bool active = base < width * 8;
+          const int col = base >> 3, k = base & 7;
+          A r = 0;
+          if (active) {
+            r = (A)E::ld(src + k * cw, col);
+            for (int i = 8 + k; i < n8; i += 8) r = r_add(r, (A)E::ld(src + i * cw, col));
+          }
+          r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 1));
+          r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 2));
+          r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 4));
+          if (active && k == 0) {
+            for (int i = n8; i < L; i++) r = r_add(r, (A)E::ld(src + i * cw, col));
+            s_mean[col] = (double)r_div(r, (A)L);
+          }
+        }
+      } else {
+        for (int col = tid; col < width; col += kThreads) {
+          auto get = [&](int i) { return (A)E::ld(src + i * cw, col); };
+          s_mean[col] = (double)r_div(pairwise_sum<A>(get, 0, L), (A)L);
+        }
+      }
+      __syncthreads();
+    }
+
+    const int total = L << log2_nv;
+    for (int idx = tid; idx < total; idx += kThreads) {
+      const int j = idx >> log2_nv;
+      const int v = idx & (nv_full - 1);
+      if (v >= nv) continue;
+      Vec<T> y;
+      if (MODE == kRing) {
+        const int4 tri = s_tri[j];
+        Vec<T> va, vb, vc, vg;
+        va.raw = *reinterpret_cast<const uint4*>(sW + tri.x * cw + v * VEC);
+        vb.raw = *reinterpret_cast<const uint4*>(sW + tri.y * cw + v * VEC);
+        vc.raw = *reinterpret_cast<const uint4*>(sW + tri.z * cw + v * VEC);
+        if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + j * cw + v * VEC);
+#pragma unroll
+        for (int e = 0; e < VEC; e++) {
+          A m = ring3<A>((A)E::ld(va.e(), e), (A)E::ld(vb.e(), e), (A)E::ld(vc.e(), e));
+          if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
+          y.e()[e] = E::st(m);
+        }
+      } else if (MODE == kMean) {
+        Vec<T> vg;
+        if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + j * cw + v * VEC);
+#pragma unroll
+        for (int e = 0; e < VEC; e++) {
+          A m = (A)s_mean[v * VEC + e];
+          if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
+          y.e()[e] = E::st(m);
+        }
+      } else {  // kSpsgd
+        Vec<T> vw, w0;
+        vw.raw = *reinterpret_cast<const uint4*>(sW + j * cw + v * VEC);
+        w0.raw = *reinterpret_cast<const uint4*>(sW + v * VEC);
+        bool diff = false;
+#pragma unroll
+        for (int e = 0; e < VEC; e++) {
+          diff |= !(vw.e()[e] == w0.e()[e]);
+          A m = (A)s_mean[v * VEC + e];
+          y.e()[e] = E::st(r_sub((A)E::ld(vw.e(), e), r_mul(lr, m)));
+        }
+        if (diff && a.mismatch) atomicOr(a.mismatch, 1u);
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; e++) {
+        unsigned long long b = abs_bits(E::absd(y.e()[e]));
+        amax = b > amax ? b : amax;
+      }
+      st_cs_v4(out + j * a.ldo + c0 + v * VEC, y.raw);
+    }
+
+    __syncthreads();  // stage s fully consumed (and s_mean free)
+    if (warp == 0) {
+      long long tn = t + (long long)kStages * stride;
+      if (tn < a.ntiles) issue(s, tn);
+    }
+  }
+  if (a.absmax) absmax_publish(a.absmax, amax);
+}
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+template <typename T, int MODE, bool HAS_G>
+static int launch_scalar(const MixArgs& a, long long c_begin, cudaStream_t st) {
+  long long total = (a.d - c_begin) * a.L;
+  if (total <= 0) return RM_OK;
+  long long blocks = (total + 255) / 256;
+  int cap = sm_count(-1) * 8;
+  if (blocks > cap) blocks = cap;
+  mix_scalar_kernel<T, MODE, HAS_G><<<(int)blocks, 256, 0, st>>>(a, c_begin);
+  RM_CHECK_LAUNCH("mix_scalar_kernel");
+  return RM_OK;
+}
+
+static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode) {
+  size_t stage = (size_t)L * cw * elem * (stage_g ? 2 : 1);
+  size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kStages * stage;
+  if (mode != kRing) bytes += (size_t)cw * sizeof(double);
+  return bytes;
+}
+
+template <typename T, int MODE, bool HAS_G>
+static int launch_mix(MixArgs a, cudaStream_t st) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  const size_t esz = sizeof(T);
+  const bool stage_g = HAS_G || MODE == kSpsgd;
+  const uintptr_t align_bits =
+      reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.out) |
+      (stage_g ? reinterpret_cast<uintptr_t>(a.G) : 0) |
+      (uintptr_t)(a.ldw * esz) | (uintptr_t)(a.ldo * esz) | (stage_g ? (uintptr_t)(a.ldg * esz) : 0);
+  const bool aligned = (align_bits & 15) == 0;
+  static int max_optin = -1;
+  if (max_optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  long long d_main = (a.d / VEC) * VEC;
+  bool use_tma = aligned && a.L <= kMaxTmaL && d_main > 0;
+  int cw = 0;
+  if (use_tma) {
+    // tile width: power of two, stage ~kStageTarget, and enough tiles to
+    // spread over every SM several times.
+    size_t per_col = (size_t)a.L * esz * (stage_g ? 2 : 1);
+    cw = 1;
+    while ((size_t)(cw * 2) * per_col <= (size_t)kStageTarget && cw * 2 <= 4096) cw *= 2;
+    const long long want_tiles = 4LL * sm_count(-1);
+    while (cw > VEC && (d_main + cw - 1) / cw < want_tiles && cw * esz > 256) cw /= 2;
+    if (cw < VEC) cw = VEC;
+    if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE) > (size_t)max_optin) use_tma = false;
+  }
+  if (!use_tma) return launch_scalar<T, MODE, HAS_G>(a, 0, st);
+
+  a.cw = cw;
+  a.d_main = d_main;
+  int nv = cw / VEC, lg = 0;
+  while ((1 << lg) < nv) lg++;
+  a.log2_nv = lg;
+  a.ntiles = (d_main + cw - 1) / cw;
+  size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(mix_tma_kernel)");
+    attr_set = true;
+  }
+  long long grid = sm_count(-1);
+  if (grid > a.ntiles) grid = a.ntiles;
+  mix_tma_kernel<T, MODE, HAS_G><<<(int)grid, kThreads, smem, st>>>(a);
+  RM_CHECK_LAUNCH("mix_tma_kernel");
+  if (d_main < a.d) return launch_scalar<T, MODE, HAS_G>(a, d_main, st);
+  return RM_OK;
+}
+
+template <typename T, int MODE>
+static int dispatch(const void* W, const void* G, void* out, int L, long long d, long long ldw,
+                    long long ldg, long long ldo, const int32_t* left, const int32_t* right,
+                    double lr, unsigned long long* absmax, unsigned int* mismatch, void* stream) {
+  if (L < 1 || d < 0 || W == nullptr || out == nullptr) {
+    set_error("invalid arguments: L=%d d=%lld", L, d);
+    return RM_EINVAL;
+  }
+  if (ldw < d || ldo < d || (G != nullptr && ldg < d)) {
+    set_error("leading dimension smaller than d");
+    return RM_EINVAL;
+  }
+  if (MODE == kRing && L == 3) {
+    // mixing.py:159-161: every entry of the 3-ring equals 1/L, so the
+    // reference takes the exact column-mean path.
+    return dispatch<T, kMean>(W, G, out, L, d, ldw, ldg, ldo, nullptr, nullptr, lr, absmax,
+                              nullptr, stream);
+  }
+  if (MODE == kRing) {
+    if (L < 3) {
+      set_error("degenerate ring topology: need at least 3 learners, got %d", L);
+      return RM_EINVAL;
+    }
+    if (left == nullptr || right == nullptr) {
+      set_error("ring mix needs left/right neighbour tables");
+      return RM_EINVAL;
+    }
+  }
+  if (MODE == kSpsgd && G == nullptr) {
+    set_error("spsgd needs gradients");
+    return RM_EINVAL;
+  }
+  if (W == out) {
+    set_error("in-place mixing is a read-after-write hazard across learners; use distinct buffers");
+    return RM_EINVAL;
+  }
+  if (d == 0) return RM_OK;
+  MixArgs a{};
+  a.W = W;
+  a.G = G;
+  a.out = out;
+  a.ldw = ldw;
+  a.ldg = ldg;
+  a.ldo = ldo;
+  a.d = d;
+  a.L = L;
+  a.left = left;
+  a.right = right;
+  a.lr = lr;
+  a.absmax = absmax;
+  a.mismatch = mismatch;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (MODE == kSpsgd || G != nullptr) return launch_mix<T, MODE, true>(a, st);
+  return launch_mix<T, MODE, false>(a, st);
+}
+
+}  // namespace rm
+
+using namespace rm;
+
+#define RM_DEFINE_MIX(SUFFIX, CT, T)                                                              \
+  extern "C" int rm_ring_mix_sgd_##SUFFIX(const CT* W, const CT* G, CT* Wout,                   \
+                                          const int32_t* left, const int32_t* right, int L,      \
+                                          int64_t d, int64_t ldw, int64_t ldg, int64_t ldo,      \
+                                          double lr, unsigned long long* absmax_bits,            \
+                                          void* stream) {                                        \
+    return dispatch<T, kRing>(W, G, Wout, L, d, ldw, ldg, ldo, left, right, lr, absmax_bits,     \
+                              nullptr, stream);                                                  \
+  }                                                                                              \
+  extern "C" int rm_mean_sgd_##SUFFIX(const CT* W, const CT* G, CT* Wout, int L, int64_t d,     \
+                                      int64_t ldw, int64_t ldg, int64_t ldo, double lr,          \
+                                      unsigned long long* absmax_bits, void* stream) {           \
+    return dispatch<T, kMean>(W, G, Wout, L, d, ldw, ldg, ldo, nullptr, nullptr, lr,             \
+                              absmax_bits, nullptr, stream);                                     \
+  }                                                                                              \
+  extern "C" int rm_spsgd_##SUFFIX(const CT* W, const CT* G, CT* Wout, int L, int64_t d,        \
+                                   int64_t ldw, int64_t ldg, int64_t ldo, double lr,             \
+                                   unsigned int* mismatch, unsigned long long* absmax_bits,      \
+                                   void* stream) {                                               \
+    return dispatch<T, kSpsgd>(W, G, Wout, L, d, ldw, ldg, ldo, nullptr, nullptr, lr,            \
+                               absmax_bits, mismatch, stream);                                   \
+  }
+
+RM_DEFINE_MIX(f32, float, float)
+RM_DEFINE_MIX(f64, double, double)
+RM_DEFINE_MIX(bf16, uint16_t, __nv_bfloat16)
+
+// ----------------------------------------------------------------------------
+// Batched ring products for monte_carlo_consensus (spectral.py:273-279):
+// product @ T_k for B independent trials, each with its own neighbour tables.
+// Uses `@` semantics (dgemm FMA chain, no uniform shortcut even at L == 3).
+// ----------------------------------------------------------------------------
+namespace rm {
+__global__ void __launch_bounds__(256)
+    ring_batched_kernel(const double* __restrict__ X, double* __restrict__ Y,
+                        const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+                        int B, int L, long long d, long long ld, long long bstride) {
+  const long long total = (long long)B * L * d;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long c = idx % d;
+    const long long bj = idx / d;
+    const int j = (int)(bj % L);
+    const int b = (int)(bj / L);
+    int x0 = left[(long long)b * L + j], x1 = j, x2 = right[(long long)b * L + j], t;
+    if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+    if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
+    if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+    const double* xb = X + b * bstride;
+    Y[b * bstride + j * ld + c] = ring3<double>(xb[x0 * ld + c], xb[x1 * ld + c], xb[x2 * ld + c]);
+  }
+}
+}  // namespace rm
+
+extern "C" int rm_ring_mix_batched_f64(const double* X, double* Y, const int32_t* left,
+                                       const int32_t* right, int B, int L, int64_t d, int64_t ld,
+                                       int64_t batch_stride, void* stream) {
+  if (B < 0 || L < 3 || d < 0 || ld < d || X == nullptr || Y == nullptr || X == Y ||
+      left == nullptr || right == nullptr || batch_stride < (int64_t)L * ld) {
+    rm::set_error("invalid batched ring mix arguments (B=%d L=%d d=%lld)", B, L, (long long)d);
+    return RM_EINVAL;
+  }
+  long long total = (long long)B * L * d;
+  if (total == 0) return 0;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 8LL * rm::sm_count(-1)) blocks = 8LL * rm::sm_count(-1);
+  rm::ring_batched_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      X, Y, left, right, B, L, d, ld, batch_stride);
+  RM_CHECK_LAUNCH("ring_batched_kernel");
+  return 0;
+}
