@@ -302,12 +302,15 @@ def run_ours(args):
                   __import__("paper_2002_01119_b200.simulation", fromlist=["x"])
                   .fixed_ring_tables(L, dev))
     launches = {"perm": 0, "mix": 0}
+    tab0 = {"k": None}   # first step covered by the current table block
 
     def step(k, bufs, ev_pair=None):
         src, dst = bufs
-        if args.strategy == "rand_psgd" and k % block == 0:
+        if args.strategy == "rand_psgd" and (tab0["k"] is None or k >= tab0["k"] + block):
+            # one launch generates the tables of the next `block` steps
             _lib.check(lib.rm_perm_tables(words.ctypes.data, len(words), k, block, L,
                                           *(t.data_ptr() for t in tabs), sptr))
+            tab0["k"] = k
             launches["perm"] += 1
         if ev_pair is not None:
             ev_pair[0].record(stream)
@@ -316,7 +319,8 @@ def run_ours(args):
                          G.stride(0), dst.stride(0), LR, amax[k].data_ptr(), sptr)
         else:
             if args.strategy == "rand_psgd":
-                lp, rp = tabs[2][k % block].data_ptr(), tabs[3][k % block].data_ptr()
+                lp = tabs[2][k - tab0["k"]].data_ptr()
+                rp = tabs[3][k - tab0["k"]].data_ptr()
             else:
                 lp, rp = fl.data_ptr(), fr.data_ptr()
             rc = ring_fn(src.data_ptr(), G.data_ptr(), dst.data_ptr(), lp, rp, L, d,
@@ -345,6 +349,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches = {"perm": 0, "mix": 0}
+    tab0["k"] = None   # the timed region generates its own tables
     if clocks:
         clocks.mark(True)
     t_start.record(stream)

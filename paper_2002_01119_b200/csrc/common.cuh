@@ -55,8 +55,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Bounded wait: a correct pipeline never waits more than microseconds; if the
+// expected bytes never arrive (a bug), trap after ~4 s instead of hanging the
+// GPU until the job's wall-clock limit.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > 8000000000LL) __trap();
   }
 }
 

@@ -30,13 +30,17 @@
 #include "common.cuh"
 #include "../../include/ringmix_b200.h"
 
+#include <stdlib.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 namespace rm {
 
 enum Mode { kRing = 0, kMean = 1, kSpsgd = 2 };
 
 constexpr int kThreads = 512;
 constexpr int kStages = 3;
-constexpr int kMaxTmaL = 1024;
+constexpr int kMaxTmaL = 256;   // one TMA row box per tile
 constexpr int kStageTarget = 64 * 1024;
 
 struct MixArgs {
@@ -63,10 +67,20 @@ struct MixArgs {
 template <typename T>
 struct Elem;
 
+// max|y| is tracked on the bit pattern of |y| in the storage type (monotone for
+// non-negative IEEE values; NaN patterns sort above inf) and widened to the
+// double bit pattern once at the end.
 template <>
 struct Elem<float> {
   using acc = double;
+  using amax_t = uint32_t;
   static constexpr int VEC = 4;
+  __device__ static __forceinline__ uint32_t amax_acc(uint32_t m, float y) {
+    return max(m, __float_as_uint(y) & 0x7fffffffu);
+  }
+  __device__ static __forceinline__ unsigned long long amax_bits(uint32_t m) {
+    return abs_bits((double)__uint_as_float(m));
+  }
   __device__ static __forceinline__ double ld(const float* p, int i) { return (double)p[i]; }
   __device__ static __forceinline__ float st(double y) { return __double2float_rn(y); }
   __device__ static __forceinline__ double absd(float y) { return fabs((double)y); }
@@ -75,7 +89,15 @@ struct Elem<float> {
 template <>
 struct Elem<double> {
   using acc = double;
+  using amax_t = unsigned long long;
   static constexpr int VEC = 2;
+  __device__ static __forceinline__ unsigned long long amax_acc(unsigned long long m, double y) {
+    unsigned long long b = abs_bits(y);
+    return b > m ? b : m;
+  }
+  __device__ static __forceinline__ unsigned long long amax_bits(unsigned long long m) {
+    return m;
+  }
   __device__ static __forceinline__ double ld(const double* p, int i) { return p[i]; }
   __device__ static __forceinline__ double st(double y) { return y; }
   __device__ static __forceinline__ double absd(double y) { return fabs(y); }
@@ -84,7 +106,14 @@ struct Elem<double> {
 template <>
 struct Elem<__nv_bfloat16> {
   using acc = float;
+  using amax_t = uint32_t;
   static constexpr int VEC = 8;
+  __device__ static __forceinline__ uint32_t amax_acc(uint32_t m, __nv_bfloat16 y) {
+    return max(m, (uint32_t)(__bfloat16_as_ushort(y) & 0x7fffu));
+  }
+  __device__ static __forceinline__ unsigned long long amax_bits(uint32_t m) {
+    return abs_bits((double)__bfloat162float(__ushort_as_bfloat16((unsigned short)m)));
+  }
   __device__ static __forceinline__ float ld(const __nv_bfloat16* p, int i) {
     return __bfloat162float(p[i]);
   }
@@ -200,7 +229,15 @@ __global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_
 }
 
 // ----------------------------------------------------------------------------
-// tiled TMA path
+// tiled TMA path (2-D tensor maps)
+//
+// Each tile is [L rows x cw columns] of W (and of G).  One elected thread
+// loads it with cp.async.bulk.tensor.2d boxes of at most 256 x 256 elements —
+// one TMA instruction per tensor per tile for L <= 256 — into a shared-memory
+// stage laid out row-major [L][cw].  (A first version issued one 1-D bulk copy
+// per row; ncu showed the per-copy cost of 128 x 512 B copies per tile capped
+// DRAM at 35 %: profiles/r1_v1_bulk1d.md.)  Out-of-range columns of the last
+// tile are zero-filled by TMA and skipped by the consumers.
 // ----------------------------------------------------------------------------
 template <typename T>
 struct Vec {
@@ -209,8 +246,25 @@ struct Vec {
   __device__ __forceinline__ T* e() { return reinterpret_cast<T*>(&raw); }
 };
 
+__device__ __forceinline__ void tma_load_2d(void* sdst, const CUtensorMap* map, int c, int r,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(sdst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(r), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+constexpr int kBox = 256;  // TMA box dimension limit (elements)
+
 template <typename T, int MODE, bool HAS_G>
-__global__ void __launch_bounds__(kThreads, 1) mix_tma_kernel(MixArgs a) {
+__global__ void __launch_bounds__(kThreads, 1)
+    mix_tma_kernel(MixArgs a, const __grid_constant__ CUtensorMap tmW,
+                   const __grid_constant__ CUtensorMap tmG) {
   using E = Elem<T>;
   using A = typename E::acc;
   constexpr int VEC = E::VEC;
@@ -218,25 +272,23 @@ __global__ void __launch_bounds__(kThreads, 1) mix_tma_kernel(MixArgs a) {
 
   const int L = a.L;
   const int cw = a.cw;
-  const int row_bytes = cw * (int)sizeof(T);
-  const int w_bytes = L * row_bytes;
-  const bool stage_g = HAS_G || MODE == kSpsgd;
+  const int w_bytes = L * cw * (int)sizeof(T);
+  constexpr bool stage_g = HAS_G || MODE == kSpsgd;
   const int stage_bytes = w_bytes * (stage_g ? 2 : 1);
 
-  // layout: [mbarriers (NS x 8B) | pad to 128 | tri table (L x int4) | stages]
+  // layout: [mbarriers | tri table (L x int4) | stages | per-column mean]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   int4* s_tri = reinterpret_cast<int4*>(smem + 128);
   unsigned char* stages = smem + 128 + ((L * 16 + 127) / 128) * 128;
-  double* s_mean = nullptr;  // kMean/kSpsgd: per-column mean (A), after stages
+  double* s_mean = nullptr;
   if (MODE != kRing) s_mean = reinterpret_cast<double*>(stages + kStages * stage_bytes);
 
-  const T* W = static_cast<const T*>(a.W);
-  const T* G = static_cast<const T*>(a.G);
   T* out = static_cast<T*>(a.out);
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
 
   if (tid == 0) {
+    tma_prefetch_desc(&tmW);
+    if (stage_g) tma_prefetch_desc(&tmG);
     for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
@@ -253,94 +305,102 @@ __global__ void __launch_bounds__(kThreads, 1) mix_tma_kernel(MixArgs a) {
 
   const long long first = blockIdx.x;
   const long long stride = gridDim.x;
+  const int box_c = cw < kBox ? cw : kBox;
 
-  // issue tile `t` into stage `s` (warp 0)
+  // tile t -> stage s (one thread)
   auto issue = [&](int s, long long t) {
-    const long long c0 = t * cw;
-    const long long width = min((long long)cw, a.d_main - c0);
-    const uint32_t bytes = (uint32_t)(width * sizeof(T));
+    const int c0 = (int)(t * cw);
     unsigned char* st = stages + (size_t)s * stage_bytes;
-    if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes * L * (stage_g ? 2u : 1u));
-    __syncwarp();
-    for (int r = lane; r < L; r += 32) {
-      bulk_g2s(st + r * row_bytes, W + r * a.ldw + c0, bytes, &full[s]);
-      if (stage_g) bulk_g2s(st + w_bytes + r * row_bytes, G + r * a.ldg + c0, bytes, &full[s]);
+    mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+    // L <= 256: one row box; column boxes of box_c land one after another,
+    // each [L][box_c] (see sidx)
+    for (int cc = 0; cc < cw; cc += box_c) {
+      const int off = cc * L * (int)sizeof(T);
+      tma_load_2d(st + off, &tmW, c0 + cc, 0, &full[s]);
+      if (stage_g) tma_load_2d(st + w_bytes + off, &tmG, c0 + cc, 0, &full[s]);
     }
   };
+  // element (r, c) of a stage tile (box_c is a power of two)
+  const int lg_bc = __ffs(box_c) - 1;
+  const int box_stride = L << lg_bc;
+  auto sidx = [&](int r, int c) -> int {
+    return (c >> lg_bc) * box_stride + (r << lg_bc) + (c & (box_c - 1));
+  };
 
-  if (warp == 0) {
+  if (tid == 0) {
     for (int s = 0; s < kStages; s++) {
       long long t = first + s * stride;
       if (t < a.ntiles) issue(s, t);
     }
   }
 
-  unsigned long long amax = 0;
+  typename E::amax_t amax = 0;
   const A lr = (A)a.lr;
   const int log2_nv = a.log2_nv;
   const int nv_full = 1 << log2_nv;
+  const int warp = tid >> 5, lane = tid & 31;
 
   int it = 0;
   for (long long t = first; t < a.ntiles; t += stride, ++it) {
     const int s = it % kStages;
     const uint32_t parity = (it / kStages) & 1;
     const long long c0 = t * cw;
-    const int width = (int)min((long long)cw, a.d_main - c0);
-    const int nv = width / VEC;
+    const int width = (int)min((long long)cw, a.d - c0);
     const T* sW = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes);
     const T* sG = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes + w_bytes);
 
     mbar_wait(&full[s], parity);
 
     if (MODE != kRing) {
-      // per-column numpy pairwise mean over the L staged rows; 8 lanes per
-      // column hold numpy's 8 partial sums r[0..7] (n <= 128 case) and combine
+      // numpy pairwise mean per column over the L staged rows; 8 lanes per
+      // column hold numpy's partial sums r[0..7] (8 <= n <= 128) and combine
       // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) with xor-shuffles (fp add is
-      // commutative, so lane order inside each pair does not matter).
+      // commutative, so the order inside each pair does not matter).
       const T* src = (MODE == kMean) ? sW : sG;
       if (L <= 128 && L >= 8) {
         const int n8 = L - (L % 8);
-        // warp-uniform trip count so the xor-shuffles always see full warps;
-        // 8-lane groups are whole (kThreads and 32 are multiples of 8).
         for (int base0 = warp * 32; base0 < width * 8; base0 += kThreads) {
           const int base = base0 + lane;
           const bool active = base < width * 8;
           const int col = base >> 3, k = base & 7;
           A r = 0;
           if (active) {
-            r = (A)E::ld(src + k * cw, col);
-            for (int i = 8 + k; i < n8; i += 8) r = r_add(r, (A)E::ld(src + i * cw, col));
+            r = (A)E::ld(src, sidx(k, col));
+            for (int i = 8 + k; i < n8; i += 8) r = r_add(r, (A)E::ld(src, sidx(i, col)));
           }
           r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 1));
           r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 2));
           r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 4));
           if (active && k == 0) {
-            for (int i = n8; i < L; i++) r = r_add(r, (A)E::ld(src + i * cw, col));
+            for (int i = n8; i < L; i++) r = r_add(r, (A)E::ld(src, sidx(i, col)));
             s_mean[col] = (double)r_div(r, (A)L);
           }
         }
       } else {
         for (int col = tid; col < width; col += kThreads) {
-          auto get = [&](int i) { return (A)E::ld(src + i * cw, col); };
+          auto get = [&](int i) { return (A)E::ld(src, sidx(i, col)); };
           s_mean[col] = (double)r_div(pairwise_sum<A>(get, 0, L), (A)L);
         }
       }
       __syncthreads();
     }
 
+    const int nv = (width + VEC - 1) / VEC;
     const int total = L << log2_nv;
+#pragma unroll 2
     for (int idx = tid; idx < total; idx += kThreads) {
       const int j = idx >> log2_nv;
       const int v = idx & (nv_full - 1);
       if (v >= nv) continue;
+      const int c = v * VEC;
       Vec<T> y;
       if (MODE == kRing) {
         const int4 tri = s_tri[j];
         Vec<T> va, vb, vc, vg;
-        va.raw = *reinterpret_cast<const uint4*>(sW + tri.x * cw + v * VEC);
-        vb.raw = *reinterpret_cast<const uint4*>(sW + tri.y * cw + v * VEC);
-        vc.raw = *reinterpret_cast<const uint4*>(sW + tri.z * cw + v * VEC);
-        if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + j * cw + v * VEC);
+        va.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.x, c));
+        vb.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.y, c));
+        vc.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.z, c));
+        if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
           A m = ring3<A>((A)E::ld(va.e(), e), (A)E::ld(vb.e(), e), (A)E::ld(vc.e(), e));
@@ -349,41 +409,49 @@ __global__ void __launch_bounds__(kThreads, 1) mix_tma_kernel(MixArgs a) {
         }
       } else if (MODE == kMean) {
         Vec<T> vg;
-        if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + j * cw + v * VEC);
+        if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
-          A m = (A)s_mean[v * VEC + e];
+          A m = (A)s_mean[c + e];
           if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
           y.e()[e] = E::st(m);
         }
       } else {  // kSpsgd
         Vec<T> vw, w0;
-        vw.raw = *reinterpret_cast<const uint4*>(sW + j * cw + v * VEC);
-        w0.raw = *reinterpret_cast<const uint4*>(sW + v * VEC);
+        vw.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
+        w0.raw = *reinterpret_cast<const uint4*>(sW + sidx(0, c));
         bool diff = false;
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
-          diff |= !(vw.e()[e] == w0.e()[e]);
-          A m = (A)s_mean[v * VEC + e];
+          if (c + e < width) diff |= !(vw.e()[e] == w0.e()[e]);
+          A m = (A)s_mean[c + e];
           y.e()[e] = E::st(r_sub((A)E::ld(vw.e(), e), r_mul(lr, m)));
         }
         if (diff && a.mismatch) atomicOr(a.mismatch, 1u);
       }
+      T* dst = out + j * a.ldo + c0 + c;
+      if (c + VEC <= width) {
 #pragma unroll
-      for (int e = 0; e < VEC; e++) {
-        unsigned long long b = abs_bits(E::absd(y.e()[e]));
-        amax = b > amax ? b : amax;
+        for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
+        st_cs_v4(dst, y.raw);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; e++) {
+          if (c + e < width) {
+            amax = E::amax_acc(amax, y.e()[e]);
+            dst[e] = y.e()[e];
+          }
+        }
       }
-      st_cs_v4(out + j * a.ldo + c0 + v * VEC, y.raw);
     }
 
     __syncthreads();  // stage s fully consumed (and s_mean free)
-    if (warp == 0) {
+    if (tid == 0) {
       long long tn = t + (long long)kStages * stride;
       if (tn < a.ntiles) issue(s, tn);
     }
   }
-  if (a.absmax) absmax_publish(a.absmax, amax);
+  if (a.absmax) absmax_publish(a.absmax, E::amax_bits(amax));
 }
 
 // ----------------------------------------------------------------------------
@@ -408,6 +476,51 @@ static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode)
   return bytes;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <typename T>
+struct TmaType;
+template <>
+struct TmaType<float> {
+  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+};
+template <>
+struct TmaType<double> {
+  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+};
+template <>
+struct TmaType<__nv_bfloat16> {
+  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+};
+
+template <typename T>
+static bool make_map(CUtensorMap* m, const void* base, long long d, int L, long long ld, int box_c,
+                     int box_r) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)L};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * sizeof(T))};
+  cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, TmaType<T>::v, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <typename T, int MODE, bool HAS_G>
 static int launch_mix(MixArgs a, cudaStream_t st) {
   using E = Elem<T>;
@@ -416,8 +529,8 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   const bool stage_g = HAS_G || MODE == kSpsgd;
   const uintptr_t align_bits =
       reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.out) |
-      (stage_g ? reinterpret_cast<uintptr_t>(a.G) : 0) |
-      (uintptr_t)(a.ldw * esz) | (uintptr_t)(a.ldo * esz) | (stage_g ? (uintptr_t)(a.ldg * esz) : 0);
+      (stage_g ? reinterpret_cast<uintptr_t>(a.G) : 0) | (uintptr_t)(a.ldw * esz) |
+      (uintptr_t)(a.ldo * esz) | (stage_g ? (uintptr_t)(a.ldg * esz) : 0);
   const bool aligned = (align_bits & 15) == 0;
   static int max_optin = -1;
   if (max_optin < 0) {
@@ -425,28 +538,46 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
-  long long d_main = (a.d / VEC) * VEC;
-  bool use_tma = aligned && a.L <= kMaxTmaL && d_main > 0;
+  bool use_tma = aligned && a.L <= kMaxTmaL && a.d >= VEC && a.d < (1LL << 31) &&
+                 encode_fn() != nullptr;
   int cw = 0;
   if (use_tma) {
-    // tile width: power of two, stage ~kStageTarget, and enough tiles to
-    // spread over every SM several times.
+    // tile width: power of two, stage ~kStageTarget, enough tiles to spread
+    // over every SM several times
     size_t per_col = (size_t)a.L * esz * (stage_g ? 2 : 1);
-    cw = 1;
-    while ((size_t)(cw * 2) * per_col <= (size_t)kStageTarget && cw * 2 <= 4096) cw *= 2;
+    cw = VEC;
+    while ((size_t)(cw * 2) * per_col <= (size_t)kStageTarget && cw * 2 <= 2048) cw *= 2;
     const long long want_tiles = 4LL * sm_count(-1);
-    while (cw > VEC && (d_main + cw - 1) / cw < want_tiles && cw * esz > 256) cw /= 2;
-    if (cw < VEC) cw = VEC;
+    while (cw > VEC && (a.d + cw - 1) / cw < want_tiles && cw * esz > 256) cw /= 2;
+    if (const char* env = getenv("RINGMIX_TILE_COLS")) {  // tuning override
+      int v = atoi(env);
+      if (v >= VEC && (v & (v - 1)) == 0) cw = v;
+    }
     if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE) > (size_t)max_optin) use_tma = false;
   }
   if (!use_tma) return launch_scalar<T, MODE, HAS_G>(a, 0, st);
 
   a.cw = cw;
-  a.d_main = d_main;
+  a.d_main = a.d;
   int nv = cw / VEC, lg = 0;
   while ((1 << lg) < nv) lg++;
   a.log2_nv = lg;
-  a.ntiles = (d_main + cw - 1) / cw;
+  a.ntiles = (a.d + cw - 1) / cw;
+  const int box_c = cw < kBox ? cw : kBox;
+  const int box_r = a.L < kBox ? a.L : kBox;
+  CUtensorMap tmW, tmG;
+  if (!make_map<T>(&tmW, a.W, a.d, a.L, a.ldw, box_c, box_r)) {
+    set_error("cuTensorMapEncodeTiled failed for W");
+    return RM_EINVAL;
+  }
+  if (stage_g) {
+    if (!make_map<T>(&tmG, a.G, a.d, a.L, a.ldg, box_c, box_r)) {
+      set_error("cuTensorMapEncodeTiled failed for G");
+      return RM_EINVAL;
+    }
+  } else {
+    tmG = tmW;
+  }
   size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE);
   static bool attr_set = false;
   if (!attr_set) {
@@ -457,9 +588,8 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   }
   long long grid = sm_count(-1);
   if (grid > a.ntiles) grid = a.ntiles;
-  mix_tma_kernel<T, MODE, HAS_G><<<(int)grid, kThreads, smem, st>>>(a);
+  mix_tma_kernel<T, MODE, HAS_G><<<(int)grid, kThreads, smem, st>>>(a, tmW, tmG);
   RM_CHECK_LAUNCH("mix_tma_kernel");
-  if (d_main < a.d) return launch_scalar<T, MODE, HAS_G>(a, d_main, st);
   return RM_OK;
 }
 
