@@ -12,11 +12,13 @@ prints ONE JSON line on rank 0.
 * N = 1 workload: BASELINE.json configs[1] — RAD-PSGD, 64 learners x 25,557,032
   fp32 params (ResNet-50-sized flat vectors), synthetic N(0,1) weights and
   gradients, lr = 0.01.  3 x 6.54 GB buffers >> 126 MB L2, so no L2 flush.
-* N > 1 (torchrun, one process per GPU): coordinate-sharded layout — every
-  rank holds all 64 learners for its own 25,557,032-column stripe (rows of W
-  are independent) and derives the same permutation from the
-  shared seed, so there is no data-path collective: weak scaling.
-  (`--layout learner` runs the learner-sharded NVLink path instead.)
+* N > 1 (torchrun, one process per GPU), strong scaling of the same C2
+  problem: `--layout coord` (default) gives every rank a column stripe of all
+  64 learners (rows of W are independent) and every rank derives
+  the same permutation from the shared seed: no data-path
+  collective.  `--layout learner` (north-star (d)) gives every rank 64/N
+  learners; the fused kernel pulls remote neighbour rows over NVLink (CUDA IPC)
+  and a 4-byte NCCL all-reduce orders consecutive steps.
 * `value`: whole-job learner-params / s, device time (CUDA events), max over ranks.
 * `e2e`: the same step through the public host-buffer API
   (mixing.ring_mix_sgd_host -> rm_ring_mix_sgd_host_f32): W, G in pinned host
@@ -238,7 +240,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic N(0,1) weights and gradients",
         "config": config_dict(args, ws),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -255,7 +257,8 @@ def config_dict(args, ws):
             "learners": args.learners, "params_per_learner": args.dim,
             "strategy": args.strategy, "lr": LR, "perm_seed": SEED,
             "layout": args.layout if ws > 1 else "single-gpu",
-            "parallelism": f"{args.layout}-sharded x{ws}" if ws > 1 else "1 GPU",
+            "parallelism": (f"{args.layout}-sharded over {ws} GPUs (strong scaling: the whole "
+                            f"{args.learners} x {args.dim} problem)") if ws > 1 else "1 GPU",
             "l2": "inputs (3 x L x d x 4 B) far larger than the 126 MB L2; no flush needed"}
 
 
@@ -263,78 +266,138 @@ def config_dict(args, ws):
 # GPU arm
 # ----------------------------------------------------------------------------
 
+class Workload:
+    """One benchmark step for a layout: permutation tables (a block of 64 future
+    steps per launch) + the fused mix launch(es) for this rank's share."""
+
+    def __init__(self, args, torch, dev, ws, rank):
+        from paper_2002_01119_b200 import _lib, distributed as D, mixing, seeding, simulation
+
+        self.torch, self._lib, self.mixing = torch, _lib, mixing
+        self.args, self.dev, self.ws, self.rank = args, dev, ws, rank
+        dtype = {"float32": torch.float32, "bfloat16": torch.bfloat16,
+                 "float64": torch.float64}[args.dtype]
+        L, d = args.learners, args.dim
+        self.L, self.d = L, d
+        self.layout = "single" if ws == 1 else args.layout
+        self.uniform = args.strategy == "d1d"
+        gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+
+        def synth(rows, cols):
+            X = mixing.empty_learner_major(rows, cols, dtype, dev)
+            for r in range(rows):
+                X[r].copy_(torch.randn(cols, generator=gen, device=dev,
+                                       dtype=torch.float32).to(dtype))
+            return X
+
+        if self.layout in ("single", "coord"):
+            cols = D.CoordinateShards(d, ws, rank).width if self.layout == "coord" else d
+            self.rows, self.cols = L, cols
+            self.W = [synth(L, cols), mixing.empty_learner_major(L, cols, dtype, dev)]
+            self.G = synth(L, cols)
+        else:
+            if self.uniform:
+                lay = D.ShardLayout(L, ws)
+                b, e = lay.rows(rank)
+                self.rows, self.cols = e - b, d
+                self.W = [synth(e - b, d), mixing.empty_learner_major(e - b, d, dtype, dev)]
+                self.d1d = D.LearnerShardedD1D(L, d, e - b, dev)
+            else:
+                self.ring = D.LearnerShardedRing(L, d, dtype)
+                self.rows, self.cols = self.ring.Lg, d
+                for r in range(self.ring.Lg):
+                    self.ring.W[0][r].copy_(torch.randn(d, generator=gen, device=dev,
+                                                        dtype=torch.float32).to(dtype))
+            self.G = synth(self.rows, d)
+        self.local_params = self.rows * self.cols
+        self.amax = torch.zeros(args.warmup + args.steps + 1, dtype=torch.int64, device=dev)
+        self.lib = _lib.load()
+        sfx = mixing._suffix(self.G)
+        self.ring_fn = getattr(self.lib, f"rm_ring_mix_sgd_{sfx}")
+        self.mean_fn = getattr(self.lib, f"rm_mean_sgd_{sfx}")
+        self.words = seeding.entropy_words(SEED, 1)
+        self.block = 64
+        self.tabs = [torch.empty((self.block, L), dtype=torch.int32, device=dev)
+                     for _ in range(4)]
+        if args.strategy == "adpsgd_fixed":
+            self.fixed = tuple(t.contiguous() for t in simulation.fixed_ring_tables(L, dev))
+        self.tab0 = None
+        self.launches = {"perm": 0, "mix": 0, "barrier_allreduce": 0}
+        self.cur = 0
+
+    def reset_tables(self):
+        self.tab0 = None
+
+    def step(self, k, ev_pair=None):
+        torch, _lib = self.torch, self._lib
+        stream = torch.cuda.current_stream()
+        sptr = stream.cuda_stream
+        L = self.L
+        if self.args.strategy == "rand_psgd" and (self.tab0 is None or
+                                                  k >= self.tab0 + self.block):
+            _lib.check(self.lib.rm_perm_tables(self.words.ctypes.data, len(self.words), k,
+                                               self.block, L,
+                                               *(t.data_ptr() for t in self.tabs), sptr))
+            self.tab0 = k
+            self.launches["perm"] += 1
+        if self.args.strategy == "rand_psgd":
+            lt, rt = self.tabs[2][k - self.tab0], self.tabs[3][k - self.tab0]
+        elif self.args.strategy == "adpsgd_fixed":
+            lt, rt = self.fixed
+        if ev_pair is not None:
+            ev_pair[0].record(stream)
+        am = self.amax[k].data_ptr()
+        if self.layout == "learner":
+            if self.uniform:
+                src, dst = self.W[self.cur], self.W[1 - self.cur]
+                self.d1d.step(src, self.G, LR, dst, self.amax[k])
+                self.cur = 1 - self.cur
+            else:
+                self.ring.step(lt, rt, self.G, LR, self.amax[k], barrier=False)
+        else:
+            src, dst = self.W[self.cur], self.W[1 - self.cur]
+            if self.uniform:
+                rc = self.mean_fn(src.data_ptr(), self.G.data_ptr(), dst.data_ptr(), L,
+                                  self.cols, src.stride(0), self.G.stride(0), dst.stride(0), LR,
+                                  am, sptr)
+            else:
+                rc = self.ring_fn(src.data_ptr(), self.G.data_ptr(), dst.data_ptr(),
+                                  lt.data_ptr(), rt.data_ptr(), L, self.cols, src.stride(0),
+                                  self.G.stride(0), dst.stride(0), LR, am, sptr)
+            _lib.check(rc, "mix")
+            self.cur = 1 - self.cur
+        if ev_pair is not None:
+            ev_pair[1].record(stream)
+        self.launches["mix"] += (2 * len(self.d1d.chunks)
+                                 if self.layout == "learner" and self.uniform else 1)
+        if self.layout == "learner" and not self.uniform:
+            self.ring.barrier()              # next step reads this step's rows on peers
+            self.launches["barrier_allreduce"] += 1
+
+    def close(self):
+        if self.layout == "learner" and not self.uniform:
+            self.ring.close()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2002_01119_b200 import _lib, mixing
+    from paper_2002_01119_b200 import mixing
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
-    dtype = {"float32": torch.float32, "bfloat16": torch.bfloat16,
-             "float64": torch.float64}[args.dtype]
     L, d = args.learners, args.dim
     uniform = args.strategy == "d1d"
-
-    # synthetic inputs, resident in HBM before the timed region
-    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    Wa = mixing.empty_learner_major(L, d, dtype, dev)
-    Wb = mixing.empty_learner_major(L, d, dtype, dev)
-    G = mixing.empty_learner_major(L, d, dtype, dev)
-    for X in (Wa, G):
-        for r in range(L):
-            X[r].copy_(torch.randn(d, generator=gen, device=dev, dtype=torch.float32).to(dtype))
-    amax = torch.zeros(args.warmup + args.steps, dtype=torch.int64, device=dev)
+    wl = Workload(args, torch, dev, ws, rank)
     stream = torch.cuda.current_stream()
-    lib = _lib.load()
-    sfx = mixing._suffix(Wa)
-    ring_fn = getattr(lib, f"rm_ring_mix_sgd_{sfx}")
-    mean_fn = getattr(lib, f"rm_mean_sgd_{sfx}")
-    words = __import__("paper_2002_01119_b200.seeding", fromlist=["x"]).entropy_words(SEED, 1)
-    block = 64
-    tabs = [torch.empty((block, L), dtype=torch.int32, device=dev) for _ in range(4)]
-    sptr = stream.cuda_stream
-    if args.strategy == "adpsgd_fixed":
-        fl, fr = (t.contiguous() for t in
-                  __import__("paper_2002_01119_b200.simulation", fromlist=["x"])
-                  .fixed_ring_tables(L, dev))
-    launches = {"perm": 0, "mix": 0}
-    tab0 = {"k": None}   # first step covered by the current table block
 
-    def step(k, bufs, ev_pair=None):
-        src, dst = bufs
-        if args.strategy == "rand_psgd" and (tab0["k"] is None or k >= tab0["k"] + block):
-            # one launch generates the tables of the next `block` steps
-            _lib.check(lib.rm_perm_tables(words.ctypes.data, len(words), k, block, L,
-                                          *(t.data_ptr() for t in tabs), sptr))
-            tab0["k"] = k
-            launches["perm"] += 1
-        if ev_pair is not None:
-            ev_pair[0].record(stream)
-        if uniform:
-            rc = mean_fn(src.data_ptr(), G.data_ptr(), dst.data_ptr(), L, d, src.stride(0),
-                         G.stride(0), dst.stride(0), LR, amax[k].data_ptr(), sptr)
-        else:
-            if args.strategy == "rand_psgd":
-                lp = tabs[2][k - tab0["k"]].data_ptr()
-                rp = tabs[3][k - tab0["k"]].data_ptr()
-            else:
-                lp, rp = fl.data_ptr(), fr.data_ptr()
-            rc = ring_fn(src.data_ptr(), G.data_ptr(), dst.data_ptr(), lp, rp, L, d,
-                         src.stride(0), G.stride(0), dst.stride(0), LR, amax[k].data_ptr(), sptr)
-        if ev_pair is not None:
-            ev_pair[1].record(stream)
-        launches["mix"] += 1
-        _lib.check(rc, "mix")
-
-    bufs = [Wa, Wb]
     k = 0
     for _ in range(args.warmup):
-        step(k, (bufs[0], bufs[1]))
-        bufs.reverse()
+        wl.step(k)
         k += 1
     torch.cuda.synchronize()
 
@@ -348,25 +411,22 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches = {"perm": 0, "mix": 0}
-    tab0["k"] = None   # the timed region generates its own tables
+    wl.launches = {key: 0 for key in wl.launches}
+    wl.reset_tables()   # the timed region generates its own tables
     if clocks:
         clocks.mark(True)
     t_start.record(stream)
     for i in range(args.steps):
-        step(k, (bufs[0], bufs[1]), kev[i])
-        bufs.reverse()
+        wl.step(k, kev[i])
         k += 1
     t_stop.record(stream)
     torch.cuda.synchronize()
     if clocks:
         clocks.mark(False)
-    if ws > 1:
-        dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_stop)
     kern_ms = [a.elapsed_time(b) for a, b in kev]
-    # divergence flags of every step, checked after the timed region
-    bits = amax.cpu().numpy().view(np.float64)
+    launches = dict(wl.launches)
+    bits = wl.amax[:k].cpu().numpy().view(np.float64)
     if not np.all(np.isfinite(bits)):
         raise RuntimeError("non-finite weights in the benchmark run")
     if ws > 1:
@@ -375,48 +435,50 @@ def run_ours(args):
         elapsed_ms = float(t.item())
     clock_info = clocks.stop() if clocks else None
 
-    params_per_step = L * d * ws
+    params_per_step = L * d                       # strong scaling: the whole C2 problem
     value = params_per_step * args.steps / (elapsed_ms / 1e3)
     kern_avg_s = statistics.mean(kern_ms) / 1e3
     bpp = BYTES_PER_PARAM[args.dtype]
-    algo_bytes = bpp * L * d
+    algo_bytes = bpp * wl.local_params           # this rank's HBM bytes per launch
     peak, peak_src = measured_peaks()
     achieved = algo_bytes / kern_avg_s / 1e9
-    key = f"mix_{args.strategy}_{args.dtype}_L{L}_d{d}"
-    traffic = ncu_traffic(key)
+    key = f"mix_{args.strategy}_{args.dtype}_L{L}_d{d}" if ws == 1 else None
+    traffic = ncu_traffic(key) if key else None
 
-    # end-to-end through the public host-buffer API
     e2e = None
     if not args.no_e2e and rank == 0 and args.dtype == "float32" and not uniform:
         e2e = run_e2e(args, torch, mixing, dev)
+        if ws > 1:
+            e2e["note"] = "host-buffer API measured on rank 0 for the whole problem"
     if ws > 1:
         dist.barrier()
+    wl.close()
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        del Wa, Wb, G
+        del wl
         cpu = cpu_baseline(L, uniform, args.cpu_seconds)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": {"float32": "f32", "bfloat16": "bf16", "float64": "f64"}[args.dtype],
             "data": "synthetic: N(0,1) weights and gradients generated on device (torch "
                     "Generator), permutations from the device generator (seed 12345)",
             "config": config_dict(args, ws),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"mix_tma_kernel ({args.strategy}, {args.dtype})",
+                         "kernel": ("mix_shard_kernel" if ws > 1 and args.layout == "learner"
+                                    else "mix_tma_kernel") + f" ({args.strategy}, {args.dtype})",
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "avg_launch_ms": kern_avg_s * 1e3, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches["perm"] + launches["mix"],
-            "gpu_launches_detail": dict(launches),
+            "gpu_launches_detail": launches,
             "clocks": clock_info,
-            "hbm_gbs_step": algo_bytes / (elapsed_ms / args.steps / 1e3) / 1e9,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -137,6 +137,61 @@ int rm_ring_mix_sgd_host_f32(const float* W_host, const float* G_host, float* ou
                              double lr, void* workspace, int64_t workspace_bytes,
                              unsigned long long* absmax_bits, void* stream);
 
+/* ---- learner-sharded multi-GPU path (one process per GPU) ----
+ * CUDA IPC: export / map a peer process's device allocation (handles are
+ * rm_ipc_handle_size() bytes, exchanged by the caller, e.g. torch.distributed).
+ * offset_out = byte offset of dptr inside the exported allocation; the importer
+ * adds it to the base rm_ipc_open_handle returns. */
+int rm_ipc_handle_size(void);
+int rm_ipc_get_handle(const void* dptr, void* handle_out, uint64_t* offset_out);
+int rm_ipc_open_handle(const void* handle, void** dptr_out);
+int rm_ipc_close_handle(void* dptr);
+
+/* Per-step plan for the rank owning learners [row0, row0+Lg): distinct remote
+ * neighbour ids and each local learner's staged input indices in global-id
+ * order.  plan: device int32[rm_shard_plan_ints(Lg)]; left/right: device
+ * int32[L] (the step's global tables from rm_perm_tables). */
+int rm_shard_plan_ints(int Lg);
+int rm_shard_plan(const int32_t* left, const int32_t* right, int L, int row0, int Lg,
+                  int32_t* plan, void* stream);
+
+/* Fused step for the local learners: out[j] = ring3(...) - lr*G_local[j]; local
+ * rows by TMA, remote neighbour rows pulled from peer HBM over NVLink inside the
+ * kernel.  row_ptrs: device uint64[L], row l of the current W of every rank
+ * (local or IPC-mapped peer address).  Bit-identical to the single-GPU step.
+ * The caller orders steps across ranks (a barrier between steps). */
+int rm_ring_mix_sgd_sharded_f32(const uint64_t* row_ptrs, const float* W_local,
+                                const float* G_local, float* out, int L, int row0, int Lg,
+                                int64_t d, int64_t ldw, int64_t ldg, int64_t ldo,
+                                const int32_t* plan, double lr, unsigned long long* absmax_bits,
+                                void* stream);
+int rm_ring_mix_sgd_sharded_f64(const uint64_t* row_ptrs, const double* W_local,
+                                const double* G_local, double* out, int L, int row0, int Lg,
+                                int64_t d, int64_t ldw, int64_t ldg, int64_t ldo,
+                                const int32_t* plan, double lr, unsigned long long* absmax_bits,
+                                void* stream);
+int rm_ring_mix_sgd_sharded_bf16(const uint64_t* row_ptrs, const uint16_t* W_local,
+                                 const uint16_t* G_local, uint16_t* out, int L, int row0, int Lg,
+                                 int64_t d, int64_t ldw, int64_t ldg, int64_t ldo,
+                                 const int32_t* plan, double lr,
+                                 unsigned long long* absmax_bits, void* stream);
+
+/* D1D across ranks: S[c] = sum of the local rows (fp64), all-reduced by the
+ * caller (NCCL), then out[j] = S/L - lr*G[j]. */
+int rm_partial_sum_f32(const float* W, int Lg, int64_t d, int64_t ld, double* S, void* stream);
+int rm_partial_sum_f64(const double* W, int Lg, int64_t d, int64_t ld, double* S, void* stream);
+int rm_partial_sum_bf16(const uint16_t* W, int Lg, int64_t d, int64_t ld, double* S,
+                        void* stream);
+int rm_apply_mean_sgd_f32(const double* S, const float* G, float* out, int Lg, int L, int64_t d,
+                          int64_t ldg, int64_t ldo, double lr, unsigned long long* absmax_bits,
+                          void* stream);
+int rm_apply_mean_sgd_f64(const double* S, const double* G, double* out, int Lg, int L,
+                          int64_t d, int64_t ldg, int64_t ldo, double lr,
+                          unsigned long long* absmax_bits, void* stream);
+int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, int Lg, int L,
+                           int64_t d, int64_t ldg, int64_t ldo, double lr,
+                           unsigned long long* absmax_bits, void* stream);
+
 /* ---- batched ring products (monte_carlo_consensus, spectral.py:273-279) ----
  * For b < B: Y_b[j] = ring3(X_b[left_b j], X_b[j], X_b[right_b j]) with `@`
  * (dgemm) rounding, rows of length d at stride ld, batches at batch_stride;

@@ -39,8 +39,19 @@ _SIGNATURES = {
     "rm_ring_mix_batched_f64": ([vp, vp, vp, vp, i32, i32, i64, i64, i64, vp], i32),
     "rm_host_chunk_cols": ([i32, i64, vp], i32),
     "rm_ring_mix_sgd_host_f32": ([vp, vp, vp, vp, vp, i32, i64, dbl, vp, i64, vp, vp], i32),
+    "rm_ipc_handle_size": ([], i32),
+    "rm_ipc_get_handle": ([vp, vp, vp], i32),
+    "rm_ipc_open_handle": ([vp, vp], i32),
+    "rm_ipc_close_handle": ([vp], i32),
+    "rm_shard_plan_ints": ([i32], i32),
+    "rm_shard_plan": ([vp, vp, i32, i32, i32, vp, vp], i32),
 }
 for _sfx in ("f32", "f64", "bf16"):
+    _SIGNATURES[f"rm_ring_mix_sgd_sharded_{_sfx}"] = (
+        [vp, vp, vp, vp, i32, i32, i32, i64, i64, i64, i64, vp, dbl, vp, vp], i32)
+    _SIGNATURES[f"rm_partial_sum_{_sfx}"] = ([vp, i32, i64, i64, vp, vp], i32)
+    _SIGNATURES[f"rm_apply_mean_sgd_{_sfx}"] = ([vp, vp, vp, i32, i32, i64, i64, i64, dbl, vp, vp],
+                                                i32)
     _SIGNATURES[f"rm_ring_mix_sgd_{_sfx}"] = (
         [vp, vp, vp, vp, vp, i32, i64, i64, i64, i64, dbl, vp, vp], i32)
     _SIGNATURES[f"rm_mean_sgd_{_sfx}"] = ([vp, vp, vp, i32, i64, i64, i64, i64, dbl, vp, vp], i32)

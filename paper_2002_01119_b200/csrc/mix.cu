@@ -28,6 +28,7 @@
 // A fused epilogue publishes max|W'| (NaN sorts above inf) for the
 // reference's _check_divergence (simulation.py:390-395): zero extra bytes.
 #include "common.cuh"
+#include "arith.cuh"
 #include "../../include/ringmix_b200.h"
 
 #include <stdlib.h>
@@ -62,127 +63,6 @@ struct MixArgs {
 };
 
 // ----------------------------------------------------------------------------
-// element traits
-// ----------------------------------------------------------------------------
-template <typename T>
-struct Elem;
-
-// max|y| is tracked on the bit pattern of |y| in the storage type (monotone for
-// non-negative IEEE values; NaN patterns sort above inf) and widened to the
-// double bit pattern once at the end.
-template <>
-struct Elem<float> {
-  using acc = double;
-  using amax_t = uint32_t;
-  static constexpr int VEC = 4;
-  __device__ static __forceinline__ uint32_t amax_acc(uint32_t m, float y) {
-    return max(m, __float_as_uint(y) & 0x7fffffffu);
-  }
-  __device__ static __forceinline__ unsigned long long amax_bits(uint32_t m) {
-    return abs_bits((double)__uint_as_float(m));
-  }
-  __device__ static __forceinline__ double ld(const float* p, int i) { return (double)p[i]; }
-  __device__ static __forceinline__ float st(double y) { return __double2float_rn(y); }
-  __device__ static __forceinline__ double absd(float y) { return fabs((double)y); }
-};
-
-template <>
-struct Elem<double> {
-  using acc = double;
-  using amax_t = unsigned long long;
-  static constexpr int VEC = 2;
-  __device__ static __forceinline__ unsigned long long amax_acc(unsigned long long m, double y) {
-    unsigned long long b = abs_bits(y);
-    return b > m ? b : m;
-  }
-  __device__ static __forceinline__ unsigned long long amax_bits(unsigned long long m) {
-    return m;
-  }
-  __device__ static __forceinline__ double ld(const double* p, int i) { return p[i]; }
-  __device__ static __forceinline__ double st(double y) { return y; }
-  __device__ static __forceinline__ double absd(double y) { return fabs(y); }
-};
-
-template <>
-struct Elem<__nv_bfloat16> {
-  using acc = float;
-  using amax_t = uint32_t;
-  static constexpr int VEC = 8;
-  __device__ static __forceinline__ uint32_t amax_acc(uint32_t m, __nv_bfloat16 y) {
-    return max(m, (uint32_t)(__bfloat16_as_ushort(y) & 0x7fffu));
-  }
-  __device__ static __forceinline__ unsigned long long amax_bits(uint32_t m) {
-    return abs_bits((double)__bfloat162float(__ushort_as_bfloat16((unsigned short)m)));
-  }
-  __device__ static __forceinline__ float ld(const __nv_bfloat16* p, int i) {
-    return __bfloat162float(p[i]);
-  }
-  __device__ static __forceinline__ __nv_bfloat16 st(float y) { return __float2bfloat16_rn(y); }
-  __device__ static __forceinline__ double absd(__nv_bfloat16 y) {
-    return fabs((double)__bfloat162float(y));
-  }
-};
-
-// rounding-explicit arithmetic (never contracted)
-__device__ __forceinline__ double r_mul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ float r_mul(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ double r_sub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ float r_sub(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ double r_add(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ float r_add(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double r_div(double a, double b) { return __ddiv_rn(a, b); }
-__device__ __forceinline__ float r_div(float a, float b) { return __fdiv_rn(a, b); }
-__device__ __forceinline__ double r_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
-__device__ __forceinline__ float r_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-
-template <typename A>
-__device__ __forceinline__ A third();
-template <>
-__device__ __forceinline__ double third<double>() { return 1.0 / 3.0; }
-template <>
-__device__ __forceinline__ float third<float>() { return 1.0f / 3.0f; }
-
-template <typename A>
-__device__ __forceinline__ A ring3(A wa, A wb, A wc) {
-  const A t = third<A>();
-  A acc = r_mul(wa, t);
-  acc = r_fma(wb, t, acc);
-  return r_fma(wc, t, acc);
-}
-
-// numpy DOUBLE_pairwise_sum over n values at stride `st` (generic, recursive
-// in blocks; used by the scalar paths).  `get(i)` loads value i.
-template <typename A, typename F>
-__device__ A pairwise_sum(F get, int lo, int n) {
-  if (n < 8) {
-    A res = -0.0;
-    for (int i = 0; i < n; i++) res = r_add(res, get(lo + i));
-    return res;
-  }
-  if (n <= 128) {
-    A r[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) r[k] = get(lo + k);
-    int i;
-    for (i = 8; i < n - (n % 8); i += 8) {
-#pragma unroll
-      for (int k = 0; k < 8; k++) r[k] = r_add(r[k], get(lo + i + k));
-    }
-    A res = r_add(r_add(r_add(r[0], r[1]), r_add(r[2], r[3])),
-                  r_add(r_add(r[4], r[5]), r_add(r[6], r[7])));
-    for (; i < n; i++) res = r_add(res, get(lo + i));
-    return res;
-  }
-  // recursion depth is log2(L/128); L <= 2^31 keeps it tiny.  Iterate the
-  // left spine explicitly to avoid deep device recursion.
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  A left = pairwise_sum<A>(get, lo, n2);
-  A right = pairwise_sum<A>(get, lo + n2, n - n2);
-  return r_add(left, right);
-}
-
-// ----------------------------------------------------------------------------
 // scalar path: any alignment / any L; one thread per (row, column)
 // Used for unaligned layouts, very large L, and the < VEC tail columns.
 // ----------------------------------------------------------------------------
@@ -207,16 +87,17 @@ __global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_
       if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
       if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
       if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
-      y = ring3<A>(E::ld(W + x0 * a.ldw, c), E::ld(W + x1 * a.ldw, c), E::ld(W + x2 * a.ldw, c));
-      if (HAS_G) y = r_sub(y, r_mul(lr, E::ld(G + j * a.ldg, c)));
+      y = ring3<A>(E::ld(W + x0 * a.ldw + c, 0), E::ld(W + x1 * a.ldw + c, 0),
+                   E::ld(W + x2 * a.ldw + c, 0));
+      if (HAS_G) y = r_sub(y, r_mul(lr, E::ld(G + j * a.ldg + c, 0)));
     } else if (MODE == kMean) {
-      auto get = [&](int i) { return (A)E::ld(W + i * a.ldw, c); };
+      auto get = [&](int i) { return (A)E::ld(W + i * a.ldw + c, 0); };
       A m = r_div(pairwise_sum<A>(get, 0, a.L), (A)a.L);
       y = HAS_G ? r_sub(m, r_mul(lr, E::ld(G + j * a.ldg, c))) : m;
     } else {  // kSpsgd: W - lr * mean_l(G)
-      auto get = [&](int i) { return (A)E::ld(G + i * a.ldg, c); };
+      auto get = [&](int i) { return (A)E::ld(G + i * a.ldg + c, 0); };
       A m = r_div(pairwise_sum<A>(get, 0, a.L), (A)a.L);
-      A w = E::ld(W + j * a.ldw, c);
+      A w = E::ld(W + j * a.ldw + c, 0);
       if (a.mismatch && !(W[j * a.ldw + c] == W[c])) atomicOr(a.mismatch, 1u);
       y = r_sub(w, r_mul(lr, m));
     }
@@ -239,26 +120,6 @@ __global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_
 // DRAM at 35 %: profiles/r1_v1_bulk1d.md.)  Out-of-range columns of the last
 // tile are zero-filled by TMA and skipped by the consumers.
 // ----------------------------------------------------------------------------
-template <typename T>
-struct Vec {
-  uint4 raw;
-  __device__ __forceinline__ const T* e() const { return reinterpret_cast<const T*>(&raw); }
-  __device__ __forceinline__ T* e() { return reinterpret_cast<T*>(&raw); }
-};
-
-__device__ __forceinline__ void tma_load_2d(void* sdst, const CUtensorMap* map, int c, int r,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(sdst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(r), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-
 constexpr int kBox = 256;  // TMA box dimension limit (elements)
 
 template <typename T, int MODE, bool HAS_G>

@@ -1,0 +1,526 @@
+// Learner-sharded multi-GPU path (north-star (d)).
+//
+// Rank g owns learners [row0, row0 + Lg) of the global ring.  Per RAD step
+// every rank derives the same permutation from the shared seed (no
+// communication); the only cross-GPU traffic is the
+// neighbour rows its learners need from other ranks.
+//
+// mix_shard_kernel fuses that exchange into the mix itself: for every column
+// tile, one elected thread TMA-loads the local W and G rows from HBM while all
+// threads pull the remote neighbour rows straight out of the peers' HBM over
+// NVLink with cp.async (16 B, peer pointers from CUDA IPC); both land in the
+// same shared-memory stage and complete on one mbarrier (expect_tx for the TMA
+// bytes + one cp.async.mbarrier.arrive per thread).  So the NVLink transfer of
+// tile t+2 overlaps the HBM stream and the math of tile t, tile by tile.
+//
+// The arithmetic is the single-GPU kernel's (ascending *global* learner id FMA
+// chain), so a sharded step is bit-identical to the single-GPU step.
+//
+// D1D: rm_partial_sum (local column sums, fp64) -> NCCL all-reduce (host side,
+// chunk-pipelined on a side stream) -> rm_apply_mean_sgd.
+#include "common.cuh"
+#include "arith.cuh"
+#include "../../include/ringmix_b200.h"
+
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+#include <string.h>
+
+namespace rm {
+
+constexpr int kShThreads = 512;
+constexpr int kShStages = 3;
+constexpr int kShStageTarget = 64 * 1024;
+
+// plan layout (int32): [0] = R (distinct remote rows), [1 .. 1+2Lg) remote
+// global ids, [1+2Lg .. 1+2Lg+4Lg) per local learner: staged indices of its
+// three inputs ordered by global learner id, then j.
+__host__ __device__ inline int plan_ints(int Lg) { return 1 + 2 * Lg + 4 * Lg; }
+
+__global__ void shard_plan_kernel(const int32_t* __restrict__ left,
+                                  const int32_t* __restrict__ right, int L, int row0, int Lg,
+                                  int32_t* __restrict__ plan) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int32_t* rem = plan + 1;
+  int32_t* tri = plan + 1 + 2 * Lg;
+  int R = 0;
+  auto staged = [&](int x) -> int {
+    if (x >= row0 && x < row0 + Lg) return x - row0;
+    for (int i = 0; i < R; i++)
+      if (rem[i] == x) return Lg + i;
+    rem[R] = x;
+    return Lg + R++;
+  };
+  for (int j = 0; j < Lg; j++) {
+    const int g = row0 + j;
+    int x0 = left[g], x1 = g, x2 = right[g], t;
+    if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+    if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
+    if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+    tri[4 * j + 0] = staged(x0);
+    tri[4 * j + 1] = staged(x1);
+    tri[4 * j + 2] = staged(x2);
+    tri[4 * j + 3] = j;
+  }
+  plan[0] = R;
+  (void)L;
+}
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+struct ShardArgs {
+  const uint64_t* row_ptrs;  // L device pointers: row l of the current W (local or peer)
+  void* out;
+  long long ldo;
+  long long d;
+  int L, row0, Lg, Rmax;
+  int cw, log2_nv;
+  long long ntiles;
+  const int32_t* plan;
+  double lr;
+  unsigned long long* absmax;
+};
+
+template <typename T, bool HAS_G>
+__global__ void __launch_bounds__(kShThreads, 1)
+    mix_shard_kernel(ShardArgs a, const __grid_constant__ CUtensorMap tmW,
+                     const __grid_constant__ CUtensorMap tmG) {
+  using E = Elem<T>;
+  using A = typename E::acc;
+  constexpr int VEC = E::VEC;
+  extern __shared__ __align__(128) unsigned char smem[];
+
+  const int Lg = a.Lg;
+  const int cw = a.cw;
+  const int tid = threadIdx.x;
+  const int R = a.plan[0];
+  const int Srows = Lg + R;
+  const int w_bytes_max = (Lg + a.Rmax) * cw * (int)sizeof(T);
+  const int g_bytes = HAS_G ? Lg * cw * (int)sizeof(T) : 0;
+  const int stage_bytes = w_bytes_max + g_bytes;
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  int4* s_tri = reinterpret_cast<int4*>(smem + 128);
+  const T** s_rptr = reinterpret_cast<const T**>(smem + 128 + ((Lg * 16 + 127) / 128) * 128);
+  unsigned char* stages = reinterpret_cast<unsigned char*>(s_rptr) +
+                          (((a.Rmax > 0 ? a.Rmax : 1) * 8 + 127) / 128) * 128;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tmW);
+    if (HAS_G) tma_prefetch_desc(&tmG);
+    for (int s = 0; s < kShStages; s++) mbar_init(&full[s], 1 + kShThreads);
+    fence_mbar_init();
+  }
+  for (int j = tid; j < Lg; j += kShThreads) {
+    const int32_t* t = a.plan + 1 + 2 * Lg + 4 * j;
+    s_tri[j] = make_int4(t[0], t[1], t[2], t[3]);
+  }
+  for (int i = tid; i < R; i += kShThreads)
+    s_rptr[i] = reinterpret_cast<const T*>(a.row_ptrs[a.plan[1 + i]]);
+  __syncthreads();
+
+  const int box_c = cw < 256 ? cw : 256;
+  const int lg_bc = __ffs(box_c) - 1;
+  const int w_box_stride = Srows << lg_bc;
+  const int g_box_stride = Lg << lg_bc;
+  auto widx = [&](int r, int c) -> int {
+    return (c >> lg_bc) * w_box_stride + (r << lg_bc) + (c & (box_c - 1));
+  };
+  auto gidx = [&](int r, int c) -> int {
+    return (c >> lg_bc) * g_box_stride + (r << lg_bc) + (c & (box_c - 1));
+  };
+  const int nchunk = cw / VEC;  // 16-byte chunks per row per tile
+
+  // refill stage s with tile t: local rows by TMA (one thread), remote rows by
+  // cp.async over NVLink (all threads); every thread arrives once.
+  auto issue = [&](int s, long long t) {
+    const int c0 = (int)(t * cw);
+    unsigned char* st = stages + (size_t)s * stage_bytes;
+    T* sW = reinterpret_cast<T*>(st);
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&full[s], (uint32_t)((Lg * cw + (HAS_G ? Lg * cw : 0)) * sizeof(T)));
+      for (int cc = 0; cc < cw; cc += box_c) {
+        tma_load_2d(sW + widx(0, cc), &tmW, c0 + cc, 0, &full[s]);
+        if (HAS_G)
+          tma_load_2d(reinterpret_cast<T*>(st + w_bytes_max) + gidx(0, cc), &tmG, c0 + cc, 0,
+                      &full[s]);
+      }
+    }
+    const long long dvec = (a.d - c0 + VEC - 1) / VEC;  // chunks inside the row
+    for (int q = tid; q < R * nchunk; q += kShThreads) {
+      const int i = q / nchunk, ch = q - i * nchunk;
+      if (ch < dvec) cp_async16(sW + widx(Lg + i, ch * VEC), s_rptr[i] + c0 + ch * VEC);
+    }
+    cp_async_mbar_arrive_noinc(&full[s]);
+  };
+
+  const long long first = blockIdx.x, stride = gridDim.x;
+  for (int s = 0; s < kShStages; s++) {
+    long long t = first + s * stride;
+    if (t < a.ntiles) issue(s, t);
+  }
+
+  typename E::amax_t amax = 0;
+  const A lr = (A)a.lr;
+  const int log2_nv = a.log2_nv;
+  const int nv_full = 1 << log2_nv;
+  T* out = static_cast<T*>(a.out);
+
+  int it = 0;
+  for (long long t = first; t < a.ntiles; t += stride, ++it) {
+    const int s = it % kShStages;
+    const uint32_t parity = (it / kShStages) & 1;
+    const long long c0 = t * cw;
+    const int width = (int)min((long long)cw, a.d - c0);
+    const T* sW = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes);
+    const T* sG = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes + w_bytes_max);
+    mbar_wait(&full[s], parity);
+
+    const int nv = (width + VEC - 1) / VEC;
+    const int total = Lg << log2_nv;
+#pragma unroll 2
+    for (int idx = tid; idx < total; idx += kShThreads) {
+      const int j = idx >> log2_nv;
+      const int v = idx & (nv_full - 1);
+      if (v >= nv) continue;
+      const int c = v * VEC;
+      const int4 tri = s_tri[j];
+      Vec<T> va, vb, vc, vg, y;
+      va.raw = *reinterpret_cast<const uint4*>(sW + widx(tri.x, c));
+      vb.raw = *reinterpret_cast<const uint4*>(sW + widx(tri.y, c));
+      vc.raw = *reinterpret_cast<const uint4*>(sW + widx(tri.z, c));
+      if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + gidx(j, c));
+#pragma unroll
+      for (int e = 0; e < VEC; e++) {
+        A m = ring3<A>((A)E::ld(va.e(), e), (A)E::ld(vb.e(), e), (A)E::ld(vc.e(), e));
+        if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
+        y.e()[e] = E::st(m);
+      }
+      T* dst = out + j * a.ldo + c0 + c;
+      if (c + VEC <= width) {
+#pragma unroll
+        for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
+        st_cs_v4(dst, y.raw);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; e++)
+          if (c + e < width) {
+            amax = E::amax_acc(amax, y.e()[e]);
+            dst[e] = y.e()[e];
+          }
+      }
+    }
+    __syncthreads();
+    long long tn = t + (long long)kShStages * stride;
+    if (tn < a.ntiles) issue(s, tn);
+  }
+  if (a.absmax) absmax_publish(a.absmax, E::amax_bits(amax));
+}
+
+// ---- D1D pieces ----
+template <typename T>
+__global__ void __launch_bounds__(256)
+    partial_sum_kernel(const T* __restrict__ W, int Lg, long long d, long long ld,
+                       double* __restrict__ S) {
+  using E = Elem<T>;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
+       c += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < Lg; l++) s = __dadd_rn(s, (double)E::ld(W + l * ld + c, 0));
+    S[c] = s;
+  }
+}
+
+template <typename T, bool HAS_G>
+__global__ void __launch_bounds__(256)
+    apply_mean_kernel(const double* __restrict__ S, const T* __restrict__ G, T* __restrict__ out,
+                      int Lg, int L, long long d, long long ldg, long long ldo, double lr,
+                      unsigned long long* absmax) {
+  using E = Elem<T>;
+  using A = typename E::acc;
+  typename E::amax_t amax = 0;
+  const long long total = (long long)Lg * d;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / d);
+    const long long c = idx - (long long)j * d;
+    A m = (A)__ddiv_rn(S[c], (double)L);
+    if (HAS_G) m = r_sub(m, r_mul((A)lr, (A)E::ld(G + j * ldg + c, 0)));
+    T y = E::st(m);
+    out[j * ldo + c] = y;
+    amax = E::amax_acc(amax, y);
+  }
+  if (absmax) absmax_publish(absmax, E::amax_bits(amax));
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 sh_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <typename T>
+struct ShTmaType;
+template <>
+struct ShTmaType<float> {
+  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+};
+template <>
+struct ShTmaType<double> {
+  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+};
+template <>
+struct ShTmaType<__nv_bfloat16> {
+  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+};
+
+template <typename T, bool HAS_G>
+static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G_local,
+                        long long ldg, cudaStream_t st) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  const size_t esz = sizeof(T);
+  auto fn = sh_encode_fn();
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return RM_ENOSYS;
+  }
+  static int max_optin = -1;
+  if (max_optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  const int rows = a.Lg * 2 + a.Rmax;  // staged rows per column (W local+remote, G)
+  int cw = VEC;
+  while ((size_t)(cw * 2) * rows * esz <= (size_t)kShStageTarget && cw * 2 <= 2048) cw *= 2;
+  while (cw > VEC && (a.d + cw - 1) / cw < 4LL * sm_count(-1) && cw * esz > 256) cw /= 2;
+  if (const char* env = getenv("RINGMIX_TILE_COLS")) {
+    int v = atoi(env);
+    if (v >= VEC && (v & (v - 1)) == 0) cw = v;
+  }
+  const size_t stage = (size_t)rows * cw * esz;
+  const size_t smem = 128 + ((size_t)(a.Lg * 16 + 127) / 128) * 128 +
+                      ((size_t)((a.Rmax > 0 ? a.Rmax : 1) * 8 + 127) / 128) * 128 +
+                      kShStages * stage;
+  if (smem > (size_t)max_optin) {
+    set_error("sharded tile does not fit shared memory (Lg=%d)", a.Lg);
+    return RM_ERANGE;
+  }
+  a.cw = cw;
+  int nv = cw / VEC, lg = 0;
+  while ((1 << lg) < nv) lg++;
+  a.log2_nv = lg;
+  a.ntiles = (a.d + cw - 1) / cw;
+  const int box_c = cw < 256 ? cw : 256;
+  CUtensorMap tmW, tmG;
+  cuuint64_t dims[2] = {(cuuint64_t)a.d, (cuuint64_t)a.Lg};
+  cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)a.Lg};
+  cuuint32_t estr[2] = {1, 1};
+  cuuint64_t sw[1] = {(cuuint64_t)(ldw * esz)};
+  if (fn(&tmW, ShTmaType<T>::v, 2, const_cast<T*>(W_local), dims, sw, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed for local W");
+    return RM_EINVAL;
+  }
+  tmG = tmW;
+  if (HAS_G) {
+    cuuint64_t sg[1] = {(cuuint64_t)(ldg * esz)};
+    if (fn(&tmG, ShTmaType<T>::v, 2, const_cast<T*>(G_local), dims, sg, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed for local G");
+      return RM_EINVAL;
+    }
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(mix_shard_kernel<T, HAS_G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(mix_shard_kernel)");
+    attr = true;
+  }
+  long long grid = sm_count(-1);
+  if (grid > a.ntiles) grid = a.ntiles;
+  mix_shard_kernel<T, HAS_G><<<(int)grid, kShThreads, smem, st>>>(a, tmW, tmG);
+  RM_CHECK_LAUNCH("mix_shard_kernel");
+  return RM_OK;
+}
+
+template <typename T>
+static int shard_dispatch(const uint64_t* row_ptrs, const T* W_local, const T* G_local, T* out,
+                          int L, int row0, int Lg, long long d, long long ldw, long long ldg,
+                          long long ldo, const int32_t* plan, double lr,
+                          unsigned long long* absmax, void* stream) {
+  using E = Elem<T>;
+  const size_t esz = sizeof(T);
+  if (row_ptrs == nullptr || W_local == nullptr || out == nullptr || plan == nullptr || L < 4 ||
+      Lg < 1 || row0 < 0 || row0 + Lg > L || d < 1 || Lg > 256) {
+    set_error("invalid sharded mix arguments (L=%d row0=%d Lg=%d)", L, row0, Lg);
+    return RM_EINVAL;
+  }
+  const uintptr_t al = reinterpret_cast<uintptr_t>(W_local) | reinterpret_cast<uintptr_t>(out) |
+                       (G_local ? reinterpret_cast<uintptr_t>(G_local) : 0) |
+                       (uintptr_t)(ldw * esz) | (uintptr_t)(ldo * esz) |
+                       (G_local ? (uintptr_t)(ldg * esz) : 0);
+  if ((al & 15) != 0 || ldw < (d + E::VEC - 1) / E::VEC * E::VEC) {
+    set_error("sharded mix needs 16-byte aligned rows padded to a multiple of 16 bytes");
+    return RM_EINVAL;
+  }
+  ShardArgs a{};
+  a.row_ptrs = row_ptrs;
+  a.out = out;
+  a.ldo = ldo;
+  a.d = d;
+  a.L = L;
+  a.row0 = row0;
+  a.Lg = Lg;
+  a.Rmax = (2 * Lg < L - Lg) ? 2 * Lg : L - Lg;
+  a.plan = plan;
+  a.lr = lr;
+  a.absmax = absmax;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (G_local) return launch_shard<T, true>(a, W_local, ldw, G_local, ldg, st);
+  return launch_shard<T, false>(a, W_local, ldw, nullptr, ldw, st);
+}
+
+}  // namespace rm
+
+using namespace rm;
+
+extern "C" int rm_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+// The handle names the whole allocation that contains dptr (allocators such as
+// PyTorch's sub-allocate), so the byte offset of dptr inside it is returned too;
+// the importer adds it to the mapped base.
+extern "C" int rm_ipc_get_handle(const void* dptr, void* handle_out, uint64_t* offset_out) {
+  if (dptr == nullptr || handle_out == nullptr || offset_out == nullptr) {
+    set_error("null pointer");
+    return RM_EINVAL;
+  }
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dptr));
+  if (e != cudaSuccess) return fail_cuda(e, "cudaIpcGetMemHandle");
+  memcpy(handle_out, &h, sizeof(h));
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  if (range == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      set_error("cuMemGetAddressRange unavailable");
+      return RM_ENOSYS;
+    }
+    range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS) {
+    set_error("cuMemGetAddressRange failed");
+    return RM_EINVAL;
+  }
+  *offset_out = reinterpret_cast<uint64_t>(dptr) - (uint64_t)base;
+  return 0;
+}
+
+extern "C" int rm_ipc_open_handle(const void* handle, void** dptr_out) {
+  if (handle == nullptr || dptr_out == nullptr) {
+    set_error("null pointer");
+    return RM_EINVAL;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail_cuda(e, "cudaIpcOpenMemHandle");
+  return 0;
+}
+
+extern "C" int rm_ipc_close_handle(void* dptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dptr);
+  if (e != cudaSuccess) return fail_cuda(e, "cudaIpcCloseMemHandle");
+  return 0;
+}
+
+extern "C" int rm_shard_plan_ints(int Lg) { return plan_ints(Lg); }
+
+extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, int row0, int Lg,
+                             int32_t* plan, void* stream) {
+  if (left == nullptr || right == nullptr || plan == nullptr || L < 1 || Lg < 1 || row0 < 0 ||
+      row0 + Lg > L) {
+    set_error("invalid shard plan arguments (L=%d row0=%d Lg=%d)", L, row0, Lg);
+    return RM_EINVAL;
+  }
+  shard_plan_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(left, right, L, row0, Lg,
+                                                                     plan);
+  RM_CHECK_LAUNCH("shard_plan_kernel");
+  return 0;
+}
+
+#define RM_DEFINE_SHARD(SUFFIX, CT, T)                                                          \
+  extern "C" int rm_ring_mix_sgd_sharded_##SUFFIX(                                              \
+      const uint64_t* row_ptrs, const CT* W_local, const CT* G_local, CT* out, int L, int row0, \
+      int Lg, int64_t d, int64_t ldw, int64_t ldg, int64_t ldo, const int32_t* plan,           \
+      double lr, unsigned long long* absmax_bits, void* stream) {                               \
+    return shard_dispatch<T>(row_ptrs, reinterpret_cast<const T*>(W_local),                    \
+                             reinterpret_cast<const T*>(G_local), reinterpret_cast<T*>(out), L, \
+                             row0, Lg, d, ldw, ldg, ldo, plan, lr, absmax_bits, stream);        \
+  }                                                                                             \
+  extern "C" int rm_partial_sum_##SUFFIX(const CT* W, int Lg, int64_t d, int64_t ld, double* S, \
+                                         void* stream) {                                        \
+    if (W == nullptr || S == nullptr || Lg < 0 || d < 0 || ld < d) {                            \
+      set_error("invalid partial sum arguments");                                               \
+      return RM_EINVAL;                                                                         \
+    }                                                                                           \
+    if (d == 0) return 0;                                                                       \
+    long long blocks = (d + 255) / 256;                                                         \
+    if (blocks > 16LL * sm_count(-1)) blocks = 16LL * sm_count(-1);                             \
+    partial_sum_kernel<T><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(         \
+        reinterpret_cast<const T*>(W), Lg, d, ld, S);                                           \
+    RM_CHECK_LAUNCH("partial_sum_kernel");                                                      \
+    return 0;                                                                                   \
+  }                                                                                             \
+  extern "C" int rm_apply_mean_sgd_##SUFFIX(const double* S, const CT* G, CT* out, int Lg,      \
+                                            int L, int64_t d, int64_t ldg, int64_t ldo,         \
+                                            double lr, unsigned long long* absmax_bits,         \
+                                            void* stream) {                                     \
+    if (S == nullptr || out == nullptr || Lg < 0 || L < 1 || d < 0 || ldo < d) {                \
+      set_error("invalid apply-mean arguments");                                                \
+      return RM_EINVAL;                                                                         \
+    }                                                                                           \
+    long long total = (long long)Lg * d;                                                        \
+    if (total == 0) return 0;                                                                   \
+    long long blocks = (total + 255) / 256;                                                     \
+    if (blocks > 16LL * sm_count(-1)) blocks = 16LL * sm_count(-1);                             \
+    if (G)                                                                                      \
+      apply_mean_kernel<T, true><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(  \
+          S, reinterpret_cast<const T*>(G), reinterpret_cast<T*>(out), Lg, L, d, ldg, ldo, lr, \
+          absmax_bits);                                                                         \
+    else                                                                                        \
+      apply_mean_kernel<T, false><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>( \
+          S, nullptr, reinterpret_cast<T*>(out), Lg, L, d, ldg, ldo, lr, absmax_bits);         \
+    RM_CHECK_LAUNCH("apply_mean_kernel");                                                       \
+    return 0;                                                                                   \
+  }
+
+RM_DEFINE_SHARD(f32, float, float)
+RM_DEFINE_SHARD(f64, double, double)
+RM_DEFINE_SHARD(bf16, uint16_t, __nv_bfloat16)

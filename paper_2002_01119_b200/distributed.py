@@ -1,0 +1,287 @@
+"""Multi-GPU layouts of the learner-averaging step.
+
+One process per GPU; ``torch.distributed`` is plumbing only (handle exchange,
+a step barrier, and the D1D all-reduce).  Two layouts:
+
+* :class:`CoordinateShards` — rank g owns a column stripe of all L learners.
+  Rows of W are independent (``(W @ T)[r, :]`` only reads row r) and every
+  rank derives the same permutation from the shared seed, so
+  there is no data-path communication at all.
+* :class:`LearnerShardedRing` / :class:`LearnerShardedD1D` — rank g owns
+  learners [row0, row0 + Lg) (north-star (d)).  The ring step pulls the
+  neighbour rows it needs from the peers' HBM over NVLink *inside* the fused
+  kernel (CUDA IPC mappings, ``rm_ring_mix_sgd_sharded_*``); D1D reduces local
+  column sums with an NCCL all-reduce pipelined against the local kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib, mixing
+
+
+def balanced_split(n: int, parts: int) -> list[tuple[int, int]]:
+    """[begin, end) of `parts` contiguous ranges covering range(n); the first
+    n % parts ranges get one extra element."""
+    if parts < 1:
+        raise ValueError("parts must be >= 1")
+    base, extra = divmod(n, parts)
+    out, b = [], 0
+    for p in range(parts):
+        e = b + base + (1 if p < extra else 0)
+        out.append((b, e))
+        b = e
+    return out
+
+
+@dataclass(frozen=True)
+class ShardLayout:
+    """Contiguous ownership of L learners by `world` ranks."""
+
+    L: int
+    world: int
+
+    @property
+    def bounds(self) -> list[tuple[int, int]]:
+        return balanced_split(self.L, self.world)
+
+    def rows(self, rank: int) -> tuple[int, int]:
+        return self.bounds[rank]
+
+    def owner(self, learner: int) -> int:
+        for r, (b, e) in enumerate(self.bounds):
+            if b <= learner < e:
+                return r
+        raise ValueError(f"learner {learner} out of range")
+
+    def local_index(self, learner: int) -> int:
+        return learner - self.bounds[self.owner(learner)][0]
+
+
+def plan_reference(left, right, row0: int, Lg: int):
+    """Host restatement of rm_shard_plan: (remote ids, staged triples) for the
+    rank owning [row0, row0+Lg).  Used by the tests to check the device planner."""
+    rem: list[int] = []
+
+    def staged(x: int) -> int:
+        if row0 <= x < row0 + Lg:
+            return x - row0
+        if x not in rem:
+            rem.append(x)
+        return Lg + rem.index(x)
+
+    tri = []
+    for j in range(Lg):
+        g = row0 + j
+        a, b, c = sorted((int(left[g]), g, int(right[g])))
+        tri.append((staged(a), staged(b), staged(c), j))
+    return rem, tri
+
+
+def exchange_objects(obj, group=None) -> list:
+    """all_gather_object wrapper (gloo or NCCL)."""
+    world = dist.get_world_size(group)
+    out = [None] * world
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+# ----------------------------------------------------------------------------
+# coordinate sharding
+# ----------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class CoordinateShards:
+    """Rank `rank` of `world` owns columns [c0, c1) of all L learners."""
+
+    d: int
+    world: int
+    rank: int
+
+    @property
+    def columns(self) -> tuple[int, int]:
+        return balanced_split(self.d, self.world)[self.rank]
+
+    @property
+    def width(self) -> int:
+        c0, c1 = self.columns
+        return c1 - c0
+
+
+# ----------------------------------------------------------------------------
+# learner sharding: IPC-mapped peer rows
+# ----------------------------------------------------------------------------
+
+class PeerMappedBuffers:
+    """Export local device buffers with CUDA IPC, import every peer's, and return
+    per-buffer base addresses for all ranks (own address for the local rank)."""
+
+    def __init__(self, tensors: list[torch.Tensor], group=None):
+        lib = _lib.load()
+        hsz = lib.rm_ipc_handle_size()
+        blobs = []
+        for t in tensors:
+            h = (ctypes.c_ubyte * hsz)()
+            off = ctypes.c_uint64(0)
+            _lib.check(lib.rm_ipc_get_handle(t.data_ptr(), ctypes.addressof(h),
+                                             ctypes.addressof(off)), "rm_ipc_get_handle")
+            blobs.append((bytes(h), int(off.value)))
+        allb = exchange_objects(blobs, group)
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self._opened: list[int] = []
+        self.bases: list[list[int]] = []   # [rank][buffer] -> device address
+        for r, rb in enumerate(allb):
+            row = []
+            for i, (hb, off) in enumerate(rb):
+                if r == self.rank:
+                    row.append(tensors[i].data_ptr())
+                    continue
+                h = (ctypes.c_ubyte * hsz).from_buffer_copy(hb)
+                p = ctypes.c_void_p()
+                _lib.check(lib.rm_ipc_open_handle(ctypes.addressof(h), ctypes.byref(p)),
+                           "rm_ipc_open_handle")
+                self._opened.append(p.value)
+                row.append(p.value + off)
+            self.bases.append(row)
+
+    def close(self):
+        lib = _lib.load()
+        for p in self._opened:
+            lib.rm_ipc_close_handle(ctypes.c_void_p(p))
+        self._opened = []
+
+
+class LearnerShardedRing:
+    """RAD / fixed-ring step with learners sharded over the ranks of `group`.
+
+    Holds the two W buffers (learner-major, this rank's Lg rows) and the
+    IPC row-pointer tables; `step(...)` runs plan -> fused mix -> step barrier.
+    """
+
+    def __init__(self, L: int, d: int, dtype=torch.float32, group=None, device=None):
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed must be initialised")
+        _lib.require_cuda()
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.L, self.d, self.dtype = L, d, dtype
+        self.layout = ShardLayout(L, self.world)
+        self.row0, row1 = self.layout.rows(self.rank)
+        self.Lg = row1 - self.row0
+        if self.Lg < 1:
+            raise ValueError(f"need at least one learner per rank (L={L}, world={self.world})")
+        self.device = torch.device(device if device is not None else
+                                   f"cuda:{torch.cuda.current_device()}")
+        self.W = [mixing.empty_learner_major(self.Lg, d, dtype, self.device) for _ in range(2)]
+        self.ld = self.W[0].stride(0)
+        self.peers = PeerMappedBuffers(self.W, group)
+        esz = torch.empty((), dtype=dtype).element_size()
+        self.row_ptrs = []
+        for parity in range(2):
+            ptrs = np.empty(L, dtype=np.uint64)
+            for r, (b, e) in enumerate(self.layout.bounds):
+                base = self.peers.bases[r][parity]
+                for i in range(e - b):
+                    ptrs[b + i] = base + i * self.ld * esz
+            self.row_ptrs.append(torch.from_numpy(ptrs.view(np.int64)).to(self.device))
+        self.plan = torch.empty(_lib.load().rm_shard_plan_ints(self.Lg), dtype=torch.int32,
+                                device=self.device)
+        self._token = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.cur = 0
+        self._fn = getattr(_lib.load(), f"rm_ring_mix_sgd_sharded_{mixing._suffix(self.W[0])}")
+
+    @property
+    def weights(self) -> torch.Tensor:
+        """This rank's learners, learner-major (Lg, d)."""
+        return self.W[self.cur]
+
+    def barrier(self):
+        """Stream-ordered step barrier: every rank's previous kernels are complete
+        (and their W' rows readable by peers) when this returns on the stream."""
+        dist.all_reduce(self._token, group=self.group)
+
+    def step(self, left: torch.Tensor, right: torch.Tensor, G: torch.Tensor | None, lr: float,
+             absmax: torch.Tensor | None = None, barrier: bool = True) -> torch.Tensor:
+        """One step: W[cur] -> W[1-cur].  left/right: device int32[L] global tables."""
+        lib = _lib.load()
+        s = _lib.stream_ptr()
+        _lib.check(lib.rm_shard_plan(left.data_ptr(), right.data_ptr(), self.L, self.row0,
+                                     self.Lg, self.plan.data_ptr(), s), "rm_shard_plan")
+        src, dst = self.W[self.cur], self.W[1 - self.cur]
+        if G is not None:
+            mixing._same(src, G, "G")
+        ldg = G.stride(0) if G is not None else self.ld
+        _lib.check(self._fn(self.row_ptrs[self.cur].data_ptr(), src.data_ptr(), _lib.ptr(G),
+                            dst.data_ptr(), self.L, self.row0, self.Lg, self.d, self.ld, ldg,
+                            dst.stride(0), self.plan.data_ptr(), float(lr), _lib.ptr(absmax), s),
+                   "rm_ring_mix_sgd_sharded")
+        self.cur = 1 - self.cur
+        if barrier:
+            self.barrier()
+        return dst
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        self.peers.close()
+
+
+class LearnerShardedD1D:
+    """D1D step with learners sharded: W' = sum_all(W)/L - lr*G, the global sum by an
+    NCCL all-reduce of fp64 column sums, pipelined in column chunks so the
+    all-reduce of chunk c overlaps the local kernels of chunks c+1 / c-1."""
+
+    def __init__(self, L: int, d: int, Lg: int, device, chunk_cols: int = 1 << 22, group=None):
+        self.L, self.d, self.Lg, self.group = L, d, Lg, group
+        self.device = torch.device(device)
+        self.chunks = [(b, e) for b, e in balanced_split(d, max(1, -(-d // chunk_cols)))]
+        self.S = torch.empty(d, dtype=torch.float64, device=self.device)
+        self.comm = torch.cuda.Stream(device=self.device)
+
+    def step(self, W: torch.Tensor, G: torch.Tensor | None, lr: float, out: torch.Tensor,
+             absmax: torch.Tensor | None = None) -> torch.Tensor:
+        lib = _lib.load()
+        sfx = mixing._suffix(W)
+        psum = getattr(lib, f"rm_partial_sum_{sfx}")
+        apply = getattr(lib, f"rm_apply_mean_sgd_{sfx}")
+        compute = torch.cuda.current_stream(self.device)
+        esz = W.element_size()
+        ready = []
+
+        def launch_partial(i):
+            b, e = self.chunks[i]
+            _lib.check(psum(W.data_ptr() + b * esz, self.Lg, e - b, W.stride(0),
+                            self.S.data_ptr() + b * 8, compute.cuda_stream), "rm_partial_sum")
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            self.comm.wait_event(ev)
+            with torch.cuda.stream(self.comm):
+                dist.all_reduce(self.S[b:e], group=self.group)
+                done = torch.cuda.Event()
+                done.record(self.comm)
+            ready.append(done)
+
+        def launch_apply(i):
+            b, e = self.chunks[i]
+            compute.wait_event(ready[i])
+            gp = 0 if G is None else G.data_ptr() + b * esz
+            _lib.check(apply(self.S.data_ptr() + b * 8, gp or None, out.data_ptr() + b * esz,
+                             self.Lg, self.L, e - b, G.stride(0) if G is not None else 0,
+                             out.stride(0), float(lr), _lib.ptr(absmax), compute.cuda_stream),
+                       "rm_apply_mean_sgd")
+
+        n = len(self.chunks)
+        for i in range(n):
+            launch_partial(i)
+            if i >= 1:
+                launch_apply(i - 1)
+        launch_apply(n - 1)
+        return out

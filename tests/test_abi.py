@@ -54,6 +54,5 @@ def test_last_error_is_a_string_without_cuda():
 
 
 def test_abi_uses_plain_c_types_only():
-    text = HEADER.read_text()
-    assert "torch" not in text.split("*/", 1)[1]
-    assert "at::" not in text and "Tensor" not in text
+    code = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    assert "torch" not in code and "at::" not in code and "Tensor" not in code

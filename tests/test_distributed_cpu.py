@@ -1,0 +1,98 @@
+"""Host-side logic of the multi-GPU layouts with a real world_size-2 gloo group
+(no GPU): ownership, splits, the shard planner restatement, object exchange."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import ringmix_oracle as O
+from paper_2002_01119_b200 import distributed as D
+
+
+def test_balanced_split_and_layout():
+    assert D.balanced_split(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    assert D.balanced_split(2, 4) == [(0, 1), (1, 2), (2, 2), (2, 2)]
+    lay = D.ShardLayout(64, 8)
+    assert lay.rows(3) == (24, 32)
+    assert all(lay.owner(l) == l // 8 for l in range(64))
+    assert lay.local_index(27) == 3
+    with pytest.raises(ValueError):
+        D.balanced_split(4, 0)
+
+
+def test_coordinate_shards_cover_all_columns():
+    d = 25_557_032
+    cols = [D.CoordinateShards(d, 8, r).columns for r in range(8)]
+    assert cols[0][0] == 0 and cols[-1][1] == d
+    assert all(a[1] == b[0] for a, b in zip(cols, cols[1:]))
+
+
+@pytest.mark.parametrize("L,world", [(64, 8), (16, 2), (128, 8), (10, 3)])
+def test_plan_reference_reconstructs_every_neighbourhood(L, world):
+    lay = D.ShardLayout(L, world)
+    for k in (0, 1, 7):
+        p = O.c_permutation(L, 12345, k)
+        _, left, right = O.neighbour_tables(p)
+        for r in range(world):
+            row0, row1 = lay.rows(r)
+            Lg = row1 - row0
+            rem, tri = D.plan_reference(left, right, row0, Lg)
+            assert len(set(rem)) == len(rem) <= 2 * Lg
+            assert all(lay.owner(x) != r for x in rem)
+
+            def gid(sx):
+                return row0 + sx if sx < Lg else rem[sx - Lg]
+            for j, (a, b, c, jj) in enumerate(tri):
+                g = row0 + j
+                assert jj == j
+                ids = [gid(a), gid(b), gid(c)]
+                assert ids == sorted({left[g], g, right[g]})  # ascending global order
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        got = D.exchange_objects({"rank": rank, "blob": bytes([rank]) * 64, "off": 4096 * rank})
+        lay = D.ShardLayout(16, world)
+        row0, row1 = lay.rows(rank)
+        p = O.c_permutation(16, 99, 3)
+        _, left, right = O.neighbour_tables(p)
+        rem, _ = D.plan_reference(left, right, row0, row1 - row0)
+        # every rank's remote requests are served by the owner's rows
+        reqs = D.exchange_objects(rem)
+        served = sorted(x for r in reqs for x in r if lay.owner(x) == rank)
+        q.put((rank, [g["rank"] for g in got], [g["off"] for g in got],
+               bytes(got[1 - rank]["blob"]) == bytes([1 - rank]) * 64, served))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_exchange_and_plans():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ranks, offs, blob_ok, served in res:
+        assert ranks == [0, 1] and offs == [0, 4096] and blob_ok
+        for x in served:
+            assert D.ShardLayout(16, 2).owner(x) == rank
