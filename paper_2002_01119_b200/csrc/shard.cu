@@ -225,12 +225,44 @@ __global__ void __launch_bounds__(kShThreads, 1)
 }
 
 // ---- D1D pieces ----
+// Column sums of the local rows (ascending learner order, fp64) and the apply
+// step.  Both stream HBM with 16-byte accesses and several rows in flight per
+// thread; the scalar tail handles d % VEC columns.
 template <typename T>
 __global__ void __launch_bounds__(256)
     partial_sum_kernel(const T* __restrict__ W, int Lg, long long d, long long ld,
                        double* __restrict__ S) {
   using E = Elem<T>;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
+  constexpr int VEC = E::VEC;
+  const long long nvec = d / VEC;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec;
+       v += (long long)gridDim.x * blockDim.x) {
+    double s[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; e++) s[e] = 0.0;
+    const T* p = W + v * VEC;
+    int l = 0;
+    for (; l + 4 <= Lg; l += 4) {
+      Vec<T> x[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        x[u].raw = __ldcs(reinterpret_cast<const uint4*>(p + (long long)(l + u) * ld));
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int e = 0; e < VEC; e++) s[e] = __dadd_rn(s[e], (double)E::ld(x[u].e(), e));
+    }
+    for (; l < Lg; l++) {
+      Vec<T> x;
+      x.raw = __ldcs(reinterpret_cast<const uint4*>(p + (long long)l * ld));
+#pragma unroll
+      for (int e = 0; e < VEC; e++) s[e] = __dadd_rn(s[e], (double)E::ld(x.e(), e));
+    }
+#pragma unroll
+    for (int e = 0; e < VEC; e++) S[v * VEC + e] = s[e];
+  }
+  // tail columns
+  for (long long c = nvec * VEC + blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
        c += (long long)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int l = 0; l < Lg; l++) s = __dadd_rn(s, (double)E::ld(W + l * ld + c, 0));
@@ -245,17 +277,30 @@ __global__ void __launch_bounds__(256)
                       unsigned long long* absmax) {
   using E = Elem<T>;
   using A = typename E::acc;
+  constexpr int VEC = E::VEC;
   typename E::amax_t amax = 0;
-  const long long total = (long long)Lg * d;
+  const long long nvec = (d + VEC - 1) / VEC;
+  const long long total = (long long)Lg * nvec;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(idx / d);
-    const long long c = idx - (long long)j * d;
-    A m = (A)__ddiv_rn(S[c], (double)L);
-    if (HAS_G) m = r_sub(m, r_mul((A)lr, (A)E::ld(G + j * ldg + c, 0)));
-    T y = E::st(m);
-    out[j * ldo + c] = y;
-    amax = E::amax_acc(amax, y);
+    const int j = (int)(idx / nvec);
+    const long long c = (idx - (long long)j * nvec) * VEC;
+    const bool full = c + VEC <= d;
+    Vec<T> g, y;
+    if (HAS_G && full) g.raw = __ldcs(reinterpret_cast<const uint4*>(G + j * ldg + c));
+#pragma unroll
+    for (int e = 0; e < VEC; e++) {
+      if (!full && c + e >= d) break;
+      A m = (A)__ddiv_rn(S[c + e], (double)L);
+      if (HAS_G) {
+        A gv = full ? (A)E::ld(g.e(), e) : (A)E::ld(G + j * ldg + c + e, 0);
+        m = r_sub(m, r_mul((A)lr, gv));
+      }
+      y.e()[e] = E::st(m);
+      amax = E::amax_acc(amax, y.e()[e]);
+      if (!full) out[j * ldo + c + e] = y.e()[e];
+    }
+    if (full) st_cs_v4(out + j * ldo + c, y.raw);
   }
   if (absmax) absmax_publish(absmax, E::amax_bits(amax));
 }
@@ -486,8 +531,9 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
   }                                                                                             \
   extern "C" int rm_partial_sum_##SUFFIX(const CT* W, int Lg, int64_t d, int64_t ld, double* S, \
                                          void* stream) {                                        \
-    if (W == nullptr || S == nullptr || Lg < 0 || d < 0 || ld < d) {                            \
-      set_error("invalid partial sum arguments");                                               \
+    if (W == nullptr || S == nullptr || Lg < 0 || d < 0 || ld < d ||                            \
+        ((reinterpret_cast<uintptr_t>(W) | (uintptr_t)(ld * sizeof(CT))) & 15)) {               \
+      set_error("invalid partial sum arguments (rows must be 16-byte aligned)");                \
       return RM_EINVAL;                                                                         \
     }                                                                                           \
     if (d == 0) return 0;                                                                       \
@@ -502,8 +548,10 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
                                             int L, int64_t d, int64_t ldg, int64_t ldo,         \
                                             double lr, unsigned long long* absmax_bits,         \
                                             void* stream) {                                     \
-    if (S == nullptr || out == nullptr || Lg < 0 || L < 1 || d < 0 || ldo < d) {                \
-      set_error("invalid apply-mean arguments");                                                \
+    if (S == nullptr || out == nullptr || Lg < 0 || L < 1 || d < 0 || ldo < d ||                \
+        ((reinterpret_cast<uintptr_t>(out) | (uintptr_t)(ldo * sizeof(CT)) |                    \
+          (G ? (reinterpret_cast<uintptr_t>(G) | (uintptr_t)(ldg * sizeof(CT))) : 0)) & 15)) {  \
+      set_error("invalid apply-mean arguments (rows must be 16-byte aligned)");                 \
       return RM_EINVAL;                                                                         \
     }                                                                                           \
     long long total = (long long)Lg * d;                                                        \

@@ -242,7 +242,9 @@ class LearnerShardedD1D:
     def __init__(self, L: int, d: int, Lg: int, device, chunk_cols: int = 1 << 22, group=None):
         self.L, self.d, self.Lg, self.group = L, d, Lg, group
         self.device = torch.device(device)
-        self.chunks = [(b, e) for b, e in balanced_split(d, max(1, -(-d // chunk_cols)))]
+        # chunk boundaries on 32-column (128 B) multiples keep every row 16 B aligned
+        step = max(32, (chunk_cols // 32) * 32)
+        self.chunks = [(b, min(b + step, d)) for b in range(0, d, step)]
         self.S = torch.empty(d, dtype=torch.float64, device=self.device)
         self.comm = torch.cuda.Stream(device=self.device)
 
