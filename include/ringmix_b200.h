@@ -192,6 +192,27 @@ int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, in
                            int64_t d, int64_t ldg, int64_t ldo, double lr,
                            unsigned long long* absmax_bits, void* stream);
 
+/* ---- device gradient producer for the reference's quadratic oracle ----
+ * (objectives.py:84-90 via simulation.py:226-238):
+ *   G[l] = lam * (Phi[l] - wopt) + noise_sd * z_l,
+ *   z_l = numpy stream(seed, TAG_GRADIENT, k, l).standard_normal(d)   (bit-exact)
+ * prefix_words = entropy words of (seed, TAG_GRADIENT); lam/wopt: device fp64[d];
+ * Phi/G: learner-major (L, d).  workspace: device, >= rm_normal_workspace_bytes(L, d). */
+int64_t rm_normal_workspace_bytes(int nstreams, int64_t n);
+int rm_quadratic_grad_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k, int L,
+                          int64_t d, const float* Phi, int64_t ldp, const double* lam,
+                          const double* wopt, double noise_sd, float* G, int64_t ldg,
+                          void* workspace, int64_t workspace_bytes, void* stream);
+int rm_quadratic_grad_f64(const uint32_t* prefix_words, int n_prefix, uint64_t k, int L,
+                          int64_t d, const double* Phi, int64_t ldp, const double* lam,
+                          const double* wopt, double noise_sd, double* G, int64_t ldg,
+                          void* workspace, int64_t workspace_bytes, void* stream);
+/* numpy stream(prefix [, k [, s]]).standard_normal(n) for s < nstreams (append = number of
+ * trailing entropy ints: 0, 1 = k, 2 = k and the stream index); Z: (nstreams, n) fp64. */
+int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int append, uint64_t k,
+                           int nstreams, int64_t n, double* Z, int64_t ldz, void* workspace,
+                           int64_t workspace_bytes, void* stream);
+
 /* ---- batched ring products (monte_carlo_consensus, spectral.py:273-279) ----
  * For b < B: Y_b[j] = ring3(X_b[left_b j], X_b[j], X_b[right_b j]) with `@`
  * (dgemm) rounding, rows of length d at stride ld, batches at batch_stride;

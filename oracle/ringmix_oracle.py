@@ -51,7 +51,8 @@ TAG_TRIAL = 4
 
 def build(force: bool = False) -> Path:
     """Compile oracle/*.c into oracle/_build/liboracle.so with gcc."""
-    srcs = [ORACLE_DIR / "perm_oracle.c", ORACLE_DIR / "mix_oracle.c"]
+    srcs = [ORACLE_DIR / "perm_oracle.c", ORACLE_DIR / "mix_oracle.c",
+            ORACLE_DIR / "normal_oracle.c"]
     if not force and LIB_PATH.exists():
         mtime = LIB_PATH.stat().st_mtime
         if all(s.stat().st_mtime <= mtime for s in srcs):
@@ -83,6 +84,8 @@ def lib() -> ctypes.CDLL:
         L.or_mean_sgd.restype = None
         L.or_pairwise_sum.argtypes = [vp, i64]
         L.or_pairwise_sum.restype = ctypes.c_double
+        L.or_standard_normal.argtypes = [vp, i32, i64, vp, vp, vp, vp]
+        L.or_standard_normal.restype = i64
         _lib = L
     return _lib
 
@@ -240,6 +243,38 @@ def neighbour_tables(perm) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     left = inv[(p - 1) % L]
     right = inv[(p + 1) % L]
     return inv, left, right
+
+
+# --------------------------------------------------------------------------
+# normals (quadratic-oracle gradient noise)
+# --------------------------------------------------------------------------
+
+ZIG_HEADER = ORACLE_DIR.parent / "paper_2002_01119_b200" / "csrc" / "ziggurat_tables.h"
+_zig = None
+
+
+def ziggurat_tables():
+    """numpy's ki (uint64) / wi / fi (float64) tables, as generated from the
+    installed libnpyrandom.a into csrc/ziggurat_tables.h."""
+    global _zig
+    if _zig is None:
+        import re
+        v = [int(x, 16) for x in re.findall(r"0x([0-9a-f]{16})ull", ZIG_HEADER.read_text())]
+        ki = np.array(v[:256], dtype=np.uint64)
+        wi = np.array(v[256:512], dtype=np.uint64).view(np.float64)
+        fi = np.array(v[512:768], dtype=np.uint64).view(np.float64)
+        _zig = (ki, wi, fi)
+    return _zig
+
+
+def c_standard_normal(n: int, *entropy: int) -> tuple[np.ndarray, int]:
+    """stream(*entropy).standard_normal(n) restated in C; returns (values, raw draws)."""
+    ki, wi, fi = ziggurat_tables()
+    w = _u32(entropy_words(*entropy))
+    out = np.empty(max(n, 1), dtype=np.float64)
+    draws = lib().or_standard_normal(w.ctypes.data, len(w), n, ki.ctypes.data, wi.ctypes.data,
+                                     fi.ctypes.data, out.ctypes.data)
+    return out[:n], int(draws)
 
 
 # --------------------------------------------------------------------------

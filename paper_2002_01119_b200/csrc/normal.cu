@@ -1,0 +1,516 @@
+// Device gradient producer for the reference's quadratic oracle (SURVEY §8(f)
+// next-1): G[l] = lambda * (Phi[l] - w*) + sd * z_l, where z_l is numpy's
+// stream(seed, TAG_GRADIENT, k, l).standard_normal(d) — reference
+// objectives.py:84-90 and simulation.py:226-238 — reproduced bit for bit.
+//
+// numpy draws a normal with a 256-layer ziggurat that consumes a VARIABLE
+// number of 64-bit PCG64 outputs (1 in ~98 % of cases), so element c of the
+// stream cannot be located without counting.  Parallel generation:
+//   1. spec:  every raw block [b*B, (b+1)*B) of every stream is simulated from
+//             its first draw as if an attempt started there (PCG64 jump-ahead
+//             to the block start).  Record which of the first 32 draws start
+//             attempts / produce outputs, the exit (first attempt >= next
+//             block) and the output count.
+//   2. merge: the true path enters block b at the exit of block b-1; if that
+//             entry is an attempt start of b's speculative path the two paths
+//             coincide from there (attempts are almost always single draws, so
+//             paths merge within a couple of draws).  Blocks that fail are
+//             re-simulated from the true entry (rare, sequential per stream).
+//   3. scan:  per-stream prefix sums give every block's first output index.
+//   4. gen:   each block regenerates its outputs from the true entry into
+//             shared memory, then the CTA writes G for its contiguous output
+//             range with coalesced loads of Phi / lambda / w* and stores of G.
+// The ziggurat tables are numpy's own doubles (ziggurat_tables.h, generated
+// from the installed libnpyrandom.a); fp arithmetic follows numpy's C code
+// without FMA contraction.
+#include "common.cuh"
+#include "arith.cuh"
+#include "ziggurat_tables.h"
+#include "../../include/ringmix_b200.h"
+
+namespace rm {
+
+constexpr int kZBlock = 256;        // raw draws per speculative block
+constexpr int kZGenThreads = 64;    // blocks (threads) per generation CTA
+constexpr int kZMaxPrefix = 24;
+
+struct U128d {
+  uint64_t hi, lo;
+};
+__device__ __forceinline__ U128d mul128(U128d a, U128d b) {
+  return {__umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo, a.lo * b.lo};
+}
+__device__ __forceinline__ U128d add128(U128d a, U128d b) {
+  uint64_t lo = a.lo + b.lo;
+  return {a.hi + b.hi + (lo < a.lo ? 1ull : 0ull), lo};
+}
+
+// jump tables: state after r steps = M^r * s + inc * S_r (S_r = sum_{i<r} M^i)
+__constant__ U128d c_jumpA[64];
+__constant__ U128d c_jumpS[64];
+
+struct ZStream {
+  U128d state, inc;
+};
+
+struct ZArgs {
+  uint32_t prefix[kZMaxPrefix];  // entropy words of (seed, tag)
+  int nprefix;
+  uint64_t k;                    // step index (entropy word after the prefix)
+  int append;                    // trailing entropy ints: 0 none, 1 (k), 2 (k, stream)
+  int nstreams;                  // learners
+  long long n;                   // normals per stream (d)
+  int nblocks;                   // raw blocks per stream
+};
+
+__device__ __forceinline__ uint32_t zs_hashmix(uint32_t v, uint32_t& hc) {
+  v ^= hc;
+  hc *= 0x931e8875u;
+  v *= hc;
+  v ^= v >> 16;
+  return v;
+}
+__device__ __forceinline__ uint32_t zs_mix(uint32_t x, uint32_t y) {
+  uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+  return r ^ (r >> 16);
+}
+
+__device__ ZStream z_seed(const ZArgs& a, int stream) {
+  uint32_t ent[kZMaxPrefix + 4];
+  int n = 0;
+  for (int i = 0; i < a.nprefix; i++) ent[n++] = a.prefix[i];
+  auto limbs = [&](uint64_t v) {
+    if (v == 0) {
+      ent[n++] = 0;
+      return;
+    }
+    while (v) {
+      ent[n++] = (uint32_t)v;
+      v >>= 32;
+    }
+  };
+  if (a.append >= 1) limbs(a.k);
+  if (a.append >= 2) limbs((uint64_t)stream);
+  uint32_t pool[4];
+  uint32_t hc = 0x43b0d7e5u;
+  for (int i = 0; i < 4; i++) pool[i] = zs_hashmix(i < n ? ent[i] : 0u, hc);
+  for (int s = 0; s < 4; s++)
+    for (int d = 0; d < 4; d++)
+      if (s != d) pool[d] = zs_mix(pool[d], zs_hashmix(pool[s], hc));
+  for (int s = 4; s < n; s++)
+    for (int d = 0; d < 4; d++) pool[d] = zs_mix(pool[d], zs_hashmix(ent[s], hc));
+  uint32_t hb = 0x8b51f9ddu, w[8];
+  for (int i = 0; i < 8; i++) {
+    uint32_t v = pool[i & 3] ^ hb;
+    hb *= 0x58f38dedu;
+    v *= hb;
+    w[i] = v ^ (v >> 16);
+  }
+  uint64_t v0 = w[0] | ((uint64_t)w[1] << 32), v1 = w[2] | ((uint64_t)w[3] << 32);
+  uint64_t v2 = w[4] | ((uint64_t)w[5] << 32), v3 = w[6] | ((uint64_t)w[7] << 32);
+  const U128d M = {2549297995355413924ull, 4865540595714422341ull};
+  ZStream z;
+  z.inc = {(v2 << 1) | (v3 >> 63), (v3 << 1) | 1ull};
+  U128d s = z.inc;                       // state = 0 * M + inc
+  s = add128(s, U128d{v0, v1});          // += initstate
+  s = add128(mul128(s, M), z.inc);       // step
+  z.state = s;
+  return z;
+}
+
+// state after r further steps
+__device__ __forceinline__ U128d z_jump(const ZStream& z, uint64_t r) {
+  U128d A = {0, 1}, S = {0, 0};
+  for (int i = 0; r; i++, r >>= 1) {
+    if (r & 1) {
+      // compose current (A, S) with 2^i steps: A' = Ai*A, S' = Ai*S + Si
+      S = add128(mul128(c_jumpA[i], S), c_jumpS[i]);
+      A = mul128(c_jumpA[i], A);
+    }
+  }
+  return add128(mul128(A, z.state), mul128(z.inc, S));
+}
+
+struct ZGen {
+  U128d state, inc;
+  __device__ __forceinline__ uint64_t next64() {
+    const U128d M = {2549297995355413924ull, 4865540595714422341ull};
+    state = add128(mul128(state, M), inc);
+    uint64_t x = state.hi ^ state.lo;
+    unsigned rot = (unsigned)(state.hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+  __device__ __forceinline__ double next_double() {
+    return __dmul_rn((double)(next64() >> 11), 1.0 / 9007199254740992.0);
+  }
+};
+
+// One ziggurat attempt starting with draw `r` (already taken).  Returns true
+// and sets *x when it produces an output; `extra` = further draws consumed.
+__device__ __forceinline__ bool z_attempt(ZGen& g, uint64_t r, double* x, int* extra) {
+  const int idx = (int)(r & 0xff);
+  r >>= 8;
+  const int sign = (int)(r & 1);
+  const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+  double v = __dmul_rn((double)rabs, __longlong_as_double((long long)kZigWiBits[idx]));
+  if (sign) v = -v;
+  *extra = 0;
+  if (rabs < kZigKi[idx]) {
+    *x = v;
+    return true;
+  }
+  if (idx == 0) {
+    const double R = 3.6541528853610087963519472518;
+    const double INV_R = 0.27366123732975827203338247596;
+    for (;;) {
+      double xx = __dmul_rn(-INV_R, log1p(-g.next_double()));
+      double yy = -log1p(-g.next_double());
+      *extra += 2;
+      if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+        *x = ((rabs >> 8) & 1) ? -__dadd_rn(R, xx) : __dadd_rn(R, xx);
+        return true;
+      }
+    }
+  }
+  const double f0 = __longlong_as_double((long long)kZigFiBits[idx - 1]);
+  const double f1 = __longlong_as_double((long long)kZigFiBits[idx]);
+  double lhs = __dadd_rn(__dmul_rn(__dsub_rn(f0, f1), g.next_double()), f1);
+  *extra = 1;
+  if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, v), v))) {
+    *x = v;
+    return true;
+  }
+  return false;
+}
+
+struct BlockInfo {
+  uint32_t att;    // bit i: draw b*B+i starts an attempt on the speculative path
+  uint32_t outs;   // bit i: that attempt produced an output
+  uint32_t exit;   // first speculative attempt start >= (b+1)*B, relative to b*B
+  uint32_t count;  // outputs of attempts starting in [b*B, (b+1)*B)
+};
+
+__global__ void zig_spec_kernel(ZArgs a, BlockInfo* __restrict__ info) {
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)a.nstreams * a.nblocks) return;
+  const int stream = (int)(gid / a.nblocks);
+  const int b = (int)(gid % a.nblocks);
+  ZStream zs = z_seed(a, stream);
+  ZGen g{z_jump(zs, (uint64_t)b * kZBlock), zs.inc};
+  uint32_t att = 0, outs = 0, count = 0;
+  uint32_t pos = 0;  // relative draw index of the next attempt
+  while (pos < (uint32_t)kZBlock) {
+    double x;
+    int extra;
+    bool ok = z_attempt(g, g.next64(), &x, &extra);
+    if (pos < 32) {
+      att |= 1u << pos;
+      if (ok) outs |= 1u << pos;
+    }
+    count += ok ? 1u : 0u;
+    pos += 1 + extra;
+  }
+  info[gid] = BlockInfo{att, outs, pos, count};
+}
+
+// entries[b] (relative entry of the true path into block b) and true counts.
+// Block 0 enters at 0; block b at exit(b-1) - B if b-1 merged.  Failing blocks
+// are appended to `bad` for the sequential repair.
+__global__ void zig_merge_kernel(ZArgs a, const BlockInfo* __restrict__ info,
+                                 uint32_t* __restrict__ entry, uint32_t* __restrict__ tcount,
+                                 uint32_t* __restrict__ nbad, uint64_t* __restrict__ bad) {
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)a.nstreams * a.nblocks) return;
+  const int b = (int)(gid % a.nblocks);
+  const BlockInfo me = info[gid];
+  const uint32_t e = b == 0 ? 0u : info[gid - 1].exit - kZBlock;
+  entry[gid] = e;
+  if (e < 32 && ((me.att >> e) & 1u)) {
+    tcount[gid] = me.count - __popc(me.outs & ((1u << e) - 1u));
+  } else {
+    tcount[gid] = 0;
+    uint32_t slot = atomicAdd(nbad, 1u);
+    bad[slot] = (uint64_t)gid;
+  }
+}
+
+// Sequential repair of blocks whose speculative path did not merge: one
+// thread per stream walks its bad blocks in order and re-simulates from the
+// true entry until the path merges again with the next block's speculation.
+__global__ void zig_repair_kernel(ZArgs a, const BlockInfo* __restrict__ info,
+                                  uint32_t* __restrict__ entry, uint32_t* __restrict__ tcount,
+                                  const uint32_t* __restrict__ nbad,
+                                  const uint64_t* __restrict__ bad) {
+  const int stream = blockIdx.x * blockDim.x + threadIdx.x;
+  if (stream >= a.nstreams) return;
+  const uint32_t nb = *nbad;
+  if (nb == 0) return;
+  ZStream zs = z_seed(a, stream);
+  long long next_b = -1;
+  for (;;) {
+    // smallest bad block of this stream not yet handled
+    long long best = -1;
+    for (uint32_t i = 0; i < nb; i++) {
+      long long gid = (long long)bad[i];
+      if (gid / a.nblocks != stream) continue;
+      long long bb = gid % a.nblocks;
+      if (bb > next_b && (best < 0 || bb < best)) best = bb;
+    }
+    if (best < 0) return;
+    long long b = best;
+    // walk forward from the true entry of block b until merged
+    for (;;) {
+      const long long gid = (long long)stream * a.nblocks + b;
+      const uint32_t e = entry[gid];
+      ZGen g{z_jump(zs, (uint64_t)b * kZBlock + e), zs.inc};
+      uint32_t pos = e, count = 0;
+      while (pos < (uint32_t)kZBlock) {
+        double x;
+        int extra;
+        count += z_attempt(g, g.next64(), &x, &extra) ? 1u : 0u;
+        pos += 1 + extra;
+      }
+      tcount[gid] = count;
+      next_b = b;
+      if (b + 1 >= a.nblocks) return;
+      const long long g2 = gid + 1;
+      const uint32_t e2 = pos - kZBlock;
+      entry[g2] = e2;
+      const BlockInfo nx = info[g2];
+      if (e2 < 32 && ((nx.att >> e2) & 1u)) {
+        tcount[g2] = nx.count - __popc(nx.outs & ((1u << e2) - 1u));
+        break;  // merged again; later blocks keep their speculative entries
+      }
+      b = b + 1;
+    }
+  }
+}
+
+// per-stream exclusive prefix sum of tcount -> offs (single pass per stream,
+// 1024 threads, sequential chunks)
+__global__ void zig_scan_kernel(ZArgs a, const uint32_t* __restrict__ tcount,
+                                unsigned long long* __restrict__ offs,
+                                unsigned long long* __restrict__ total) {
+  const int stream = blockIdx.x;
+  __shared__ unsigned long long carry;
+  __shared__ unsigned long long warp_sums[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const long long base = (long long)stream * a.nblocks;
+  for (int c0 = 0; c0 < a.nblocks; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    unsigned long long v = i < a.nblocks ? tcount[base + i] : 0ull;
+    // inclusive warp scan
+    unsigned long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) warp_sums[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      unsigned long long w = threadIdx.x < (blockDim.x >> 5) ? warp_sums[threadIdx.x] : 0ull;
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      warp_sums[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const unsigned long long before = carry + ((threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0ull);
+    if (i < a.nblocks) offs[base + i] = before + x - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) total[stream] = carry;
+}
+
+// Generation + fused quadratic gradient.  CTA = kZGenThreads consecutive raw
+// blocks of one stream; each thread regenerates its block's outputs (fp64)
+// into shared memory, then the CTA writes G for its output range coalesced.
+template <typename T>
+__global__ void __launch_bounds__(kZGenThreads)
+    zig_gen_kernel(ZArgs a, const uint32_t* __restrict__ entry,
+                   const uint32_t* __restrict__ tcount,
+                   const unsigned long long* __restrict__ offs, const T* __restrict__ Phi,
+                   long long ldp, const double* __restrict__ lam, const double* __restrict__ wopt,
+                   double sd, T* __restrict__ G, long long ldg, double* __restrict__ Z,
+                   long long ldz) {
+  using E = Elem<T>;
+  extern __shared__ double zbuf[];
+  const int groups = (a.nblocks + kZGenThreads - 1) / kZGenThreads;
+  const int stream = blockIdx.x / groups;
+  const int b0 = (blockIdx.x % groups) * kZGenThreads;
+  const int b = b0 + threadIdx.x;
+  const long long base = (long long)stream * a.nblocks;
+  const int blast = min(b0 + kZGenThreads, a.nblocks) - 1;
+  const unsigned long long o_first = offs[base + b0];
+  const unsigned long long o_end = offs[base + blast] + tcount[base + blast];
+  if (o_first >= (unsigned long long)a.n) return;  // whole CTA beyond d (uniform)
+  if (b < a.nblocks) {
+    const long long gid = base + b;
+    const uint32_t e = entry[gid];
+    ZStream zs = z_seed(a, stream);
+    ZGen g{z_jump(zs, (uint64_t)b * kZBlock + e), zs.inc};
+    uint32_t pos = e;
+    unsigned long long o = offs[gid] - o_first;
+    while (pos < (uint32_t)kZBlock) {
+      double x;
+      int extra;
+      if (z_attempt(g, g.next64(), &x, &extra)) zbuf[o++] = x;
+      pos += 1 + extra;
+    }
+  }
+  __syncthreads();
+  const long long o_stop = min((long long)o_end, a.n);
+  for (long long c = (long long)o_first + threadIdx.x; c < o_stop; c += kZGenThreads) {
+    const double z = zbuf[c - (long long)o_first];
+    if (Z) Z[stream * ldz + c] = z;
+    if (G) {
+      // objectives.py:87-90: gradient(w) + noise_sd * z, gradient = lam * (w - w*)
+      const double w = (double)E::ld(Phi + stream * ldp + c, 0);
+      const double gr = __dmul_rn(lam[c], __dsub_rn(w, wopt[c]));
+      G[stream * ldg + c] = E::st((typename E::acc)__dadd_rn(gr, __dmul_rn(sd, z)));
+    }
+  }
+}
+
+static bool g_jump_ready[64];
+
+static int ensure_jump_tables() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && g_jump_ready[dev]) return 0;
+  // host-side 128-bit arithmetic with unsigned __int128
+  typedef unsigned __int128 u128;
+  const u128 M = ((u128)2549297995355413924ull << 64) | 4865540595714422341ull;
+  U128d A[64], S[64];
+  u128 a = M, s = 1;  // 2^0 steps: A = M, S = 1
+  for (int i = 0; i < 64; i++) {
+    A[i] = {(uint64_t)(a >> 64), (uint64_t)a};
+    S[i] = {(uint64_t)(s >> 64), (uint64_t)s};
+    // doubling: A_{2r} = A_r^2, S_{2r} = S_r * (A_r + 1)
+    s = s * (a + 1);
+    a = a * a;
+  }
+  cudaError_t e = cudaMemcpyToSymbol(c_jumpA, A, sizeof(A));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_jumpS, S, sizeof(S));
+  if (e != cudaSuccess) return fail_cuda(e, "cudaMemcpyToSymbol(jump tables)");
+  if (dev >= 0 && dev < 64) g_jump_ready[dev] = true;
+  return 0;
+}
+
+}  // namespace rm
+
+using namespace rm;
+
+// Workspace bytes for nstreams x n normals.
+extern "C" int64_t rm_normal_workspace_bytes(int nstreams, int64_t n) {
+  if (nstreams < 1 || n < 0) return -1;
+  const long long nblocks = (long long)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) /
+                                        kZBlock) + 8;
+  const long long nb = nblocks * nstreams;
+  return (int64_t)(nb * (sizeof(BlockInfo) + 4 + 4 + 8) + nstreams * 8 + 8 + nb * 8 + 256);
+}
+
+// Quadratic-oracle gradients for all learners of step k (see header).
+template <typename T>
+static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k, int nstreams,
+                     int64_t n,
+                     const T* Phi, int64_t ldp, const double* lam, const double* wopt, double sd,
+                     T* G, int64_t ldg, double* Z, int64_t ldz, void* workspace,
+                     int64_t workspace_bytes, void* stream) {
+  if (nprefix < 0 || nprefix > kZMaxPrefix || nstreams < 1 || n < 0 || append < 0 ||
+      append > 2 || (append < 2 && nstreams != 1) ||
+      workspace == nullptr || (G != nullptr && (Phi == nullptr || lam == nullptr ||
+                                                wopt == nullptr || ldg < n || ldp < n)) ||
+      (Z != nullptr && ldz < n)) {
+    set_error("invalid normal/gradient arguments");
+    return RM_EINVAL;
+  }
+  if (n == 0) return 0;
+  const int64_t need = rm_normal_workspace_bytes(nstreams, n);
+  if (workspace_bytes < need) {
+    set_error("normal workspace too small: need %lld bytes", (long long)need);
+    return RM_ERANGE;
+  }
+  int rc = ensure_jump_tables();
+  if (rc) return rc;
+  ZArgs a{};
+  for (int i = 0; i < nprefix; i++) a.prefix[i] = prefix[i];
+  a.nprefix = nprefix;
+  a.append = append;
+  a.k = k;
+  a.nstreams = nstreams;
+  a.n = n;
+  a.nblocks = (int)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) / kZBlock) + 8;
+  const long long nb = (long long)a.nblocks * nstreams;
+  char* ws = static_cast<char*>(workspace);
+  BlockInfo* info = reinterpret_cast<BlockInfo*>(ws);
+  ws += nb * sizeof(BlockInfo);
+  unsigned long long* offs = reinterpret_cast<unsigned long long*>(ws);
+  ws += nb * 8;
+  uint32_t* entry = reinterpret_cast<uint32_t*>(ws);
+  ws += nb * 4;
+  uint32_t* tcount = reinterpret_cast<uint32_t*>(ws);
+  ws += nb * 4;
+  uint64_t* bad = reinterpret_cast<uint64_t*>(ws);
+  ws += nb * 8;
+  unsigned long long* total = reinterpret_cast<unsigned long long*>(ws);
+  ws += nstreams * 8;
+  uint32_t* nbad = reinterpret_cast<uint32_t*>(ws);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(nbad, 0, 4, st);
+  if (e != cudaSuccess) return fail_cuda(e, "cudaMemsetAsync");
+  const int threads = 128;
+  const long long grid = (nb + threads - 1) / threads;
+  zig_spec_kernel<<<(int)grid, threads, 0, st>>>(a, info);
+  RM_CHECK_LAUNCH("zig_spec_kernel");
+  zig_merge_kernel<<<(int)grid, threads, 0, st>>>(a, info, entry, tcount, nbad, bad);
+  RM_CHECK_LAUNCH("zig_merge_kernel");
+  zig_repair_kernel<<<(nstreams + 31) / 32, 32, 0, st>>>(a, info, entry, tcount, nbad, bad);
+  RM_CHECK_LAUNCH("zig_repair_kernel");
+  zig_scan_kernel<<<nstreams, 1024, 0, st>>>(a, tcount, offs, total);
+  RM_CHECK_LAUNCH("zig_scan_kernel");
+  const int groups = (a.nblocks + kZGenThreads - 1) / kZGenThreads;
+  // worst case outputs per CTA = kZGenThreads * kZBlock
+  const size_t smem = (size_t)kZGenThreads * kZBlock * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(zig_gen_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(zig_gen_kernel)");
+    attr = true;
+  }
+  zig_gen_kernel<T><<<groups * nstreams, kZGenThreads, smem, st>>>(
+      a, entry, tcount, offs, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+  RM_CHECK_LAUNCH("zig_gen_kernel");
+  return 0;
+}
+
+extern "C" int rm_quadratic_grad_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                                     int L, int64_t d, const float* Phi, int64_t ldp,
+                                     const double* lam, const double* wopt, double noise_sd,
+                                     float* G, int64_t ldg, void* workspace,
+                                     int64_t workspace_bytes, void* stream) {
+  return quad_grad<float>(prefix_words, n_prefix, 2, k, L, d, Phi, ldp, lam, wopt, noise_sd, G, ldg,
+                          nullptr, 0, workspace, workspace_bytes, stream);
+}
+
+extern "C" int rm_quadratic_grad_f64(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                                     int L, int64_t d, const double* Phi, int64_t ldp,
+                                     const double* lam, const double* wopt, double noise_sd,
+                                     double* G, int64_t ldg, void* workspace,
+                                     int64_t workspace_bytes, void* stream) {
+  return quad_grad<double>(prefix_words, n_prefix, 2, k, L, d, Phi, ldp, lam, wopt, noise_sd, G, ldg,
+                           nullptr, 0, workspace, workspace_bytes, stream);
+}
+
+extern "C" int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int append,
+                                      uint64_t k, int nstreams, int64_t n, double* Z,
+                                      int64_t ldz, void* workspace, int64_t workspace_bytes,
+                                      void* stream) {
+  return quad_grad<double>(prefix_words, n_prefix, append, k, nstreams, n, nullptr, 0, nullptr, nullptr,
+                           0.0, nullptr, 0, Z, ldz, workspace, workspace_bytes, stream);
+}

@@ -1,0 +1,129 @@
+"""Quadratic gradient oracle on the GPU (mirror of reference objectives.py, quadratic part).
+
+Reference: pkg/src/ringmix/objectives.py:57-90 (QuadraticObjective) and
+:145-164 (quadratic_oracle).  The spectrum and optimum are built exactly as in
+the reference (``np.logspace``; optimum = stream(seed, TAG_DATA).standard_normal(d)
+drawn by the device normal generator, bit-identical to numpy).  The oracle
+implements the device protocol used by ``simulation.gradient_matrix``:
+
+    device_gradients(Phi, cfg, k) -> G (L, d)
+        G[l] = lam * (Phi[l] - w*) + noise_scale/sqrt(batch) * z_l,
+        z_l = numpy stream(cfg.seed, TAG_GRADIENT, k, l).standard_normal(d)
+
+computed by ``rm_quadratic_grad_*`` (csrc/normal.cu) bit-for-bit like the
+reference's per-learner loop (simulation.py:233-237).  The logistic oracle is
+out of scope.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib, mixing, seeding
+
+
+def _normal_workspace(nstreams: int, n: int, device) -> torch.Tensor:
+    nbytes = int(_lib.load().rm_normal_workspace_bytes(nstreams, n))
+    return torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+
+
+def standard_normal(n: int, *entropy: int, device=None) -> torch.Tensor:
+    """numpy ``stream(*entropy).standard_normal(n)`` generated on the GPU (fp64 CUDA tensor)."""
+    _lib.require_cuda()
+    dev = torch.device(device if device is not None else "cuda")
+    words = seeding.entropy_words(*entropy)
+    Z = torch.empty((1, max(n, 1)), dtype=torch.float64, device=dev)
+    ws = _normal_workspace(1, n, dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().rm_standard_normal_f64(
+            words.ctypes.data, len(words), 0, 0, 1, n, Z.data_ptr(), Z.stride(0), ws.data_ptr(),
+            ws.numel(), _lib.stream_ptr()), "rm_standard_normal_f64")
+    return Z[0, :n]
+
+
+class QuadraticObjective:
+    """1/2 (w - w*)' A (w - w*) with diagonal A and additive gradient noise (objectives.py:57-90)."""
+
+    kind = "quadratic"
+
+    def __init__(self, eigenvalues, optimum, noise_scale: float, device=None):
+        self.eigenvalues = np.asarray(eigenvalues, dtype=float)
+        self.optimum = np.asarray(optimum, dtype=float)
+        self.noise_scale = float(noise_scale)
+        if self.eigenvalues.ndim != 1 or self.optimum.shape != self.eigenvalues.shape:
+            raise ValueError("eigenvalues and optimum must be 1-d with equal length")
+        if np.any(self.eigenvalues <= 0):
+            raise ValueError("eigenvalues must be strictly positive")
+        if self.noise_scale < 0:
+            raise ValueError("noise_scale must be >= 0")
+        self.dimension = len(self.eigenvalues)
+        self.device = torch.device(device if device is not None else "cuda")
+        self._lam = torch.from_numpy(self.eigenvalues).to(self.device)
+        self._opt = torch.from_numpy(self.optimum).to(self.device)
+        self._ws = None
+
+    # ---- reference host API (small helpers, fp64 numpy) ----
+    def loss(self, w) -> float:
+        dev = np.asarray(w, dtype=float) - self.optimum
+        return 0.5 * float(np.sum(self.eigenvalues * dev * dev))
+
+    def loss_columns(self, W) -> np.ndarray:
+        dev = np.asarray(W) - self.optimum[:, None]
+        return 0.5 * np.einsum("i,il,il->l", self.eigenvalues, dev, dev)
+
+    def gradient(self, w) -> np.ndarray:
+        return self.eigenvalues * (np.asarray(w, dtype=float) - self.optimum)
+
+    def stochastic_gradient(self, w, batch, shard=None) -> np.ndarray:
+        """Reference per-learner call; the noise comes from the device generator."""
+        noise_sd = self.noise_scale / np.sqrt(batch.batch_size)
+        z = standard_normal(self.dimension, *batch.sample_seed, device=self.device)
+        return self.gradient(w) + noise_sd * z.cpu().numpy()
+
+    # ---- device protocol (simulation.gradient_matrix) ----
+    def device_gradients(self, Phi: torch.Tensor, cfg, k: int) -> torch.Tensor:
+        L, d = Phi.shape
+        if d != self.dimension:
+            raise ValueError(f"Phi has {d} columns, oracle dimension is {self.dimension}")
+        sfx = {torch.float32: "f32", torch.float64: "f64"}.get(Phi.dtype)
+        if sfx is None:
+            raise TypeError("device quadratic gradients support float32/float64 weights")
+        ldp = mixing._rows(Phi, "Phi")[2]
+        G = mixing.empty_learner_major(L, d, Phi.dtype, Phi.device)
+        need = int(_lib.load().rm_normal_workspace_bytes(L, d))
+        if self._ws is None or self._ws.numel() < need or self._ws.device != Phi.device:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=Phi.device)
+        lam, opt = self._lam.to(Phi.device), self._opt.to(Phi.device)
+        words = seeding.entropy_words(cfg.seed, seeding.TAG_GRADIENT)
+        noise_sd = float(self.noise_scale / np.sqrt(cfg.batch_size))
+        fn = getattr(_lib.load(), f"rm_quadratic_grad_{sfx}")
+        with torch.cuda.device(Phi.device):
+            _lib.check(fn(words.ctypes.data, len(words), int(k), L, d, Phi.data_ptr(), ldp,
+                          lam.data_ptr(), opt.data_ptr(), noise_sd, G.data_ptr(), G.stride(0),
+                          self._ws.data_ptr(), self._ws.numel(), _lib.stream_ptr()),
+                       "rm_quadratic_grad")
+        return G
+
+    def device_loss_columns(self, X: torch.Tensor) -> torch.Tensor:
+        dev = X.to(torch.float64) - self._opt.to(X.device)
+        return 0.5 * (self._lam.to(X.device) * dev * dev).sum(dim=1)
+
+    def device_loss(self, w: torch.Tensor) -> float:
+        dev = w.to(torch.float64) - self._opt.to(w.device)
+        return 0.5 * float((self._lam.to(w.device) * dev * dev).sum().item())
+
+
+def quadratic_oracle(dimension: int, condition_number: float = 1.0, optimum=None,
+                     noise_scale: float = 0.0, seed: int = 0, device=None) -> QuadraticObjective:
+    """Quadratic objective with log-spaced spectrum in [1, condition_number] (objectives.py:145-164)."""
+    if dimension < 1:
+        raise ValueError(f"dimension must be >= 1, got {dimension}")
+    if condition_number < 1:
+        raise ValueError(f"condition_number must be >= 1, got {condition_number}")
+    eigenvalues = np.logspace(0.0, np.log10(condition_number), dimension)
+    if optimum is None:
+        optimum = standard_normal(dimension, seed, seeding.TAG_DATA,
+                                  device=device).cpu().numpy()
+    return QuadraticObjective(eigenvalues, np.asarray(optimum, dtype=float), noise_scale,
+                              device=device)

@@ -171,8 +171,52 @@ def make_spectral():
     print("spectral: ok")
 
 
+def make_normals():
+    """numpy standard_normal streams the quadratic oracle draws (objectives.py:87-90)."""
+    rec = {}
+    cases = [((5, 0, 0, 0), 1000), ((12345, 0, 7, 3), 20000), ((2**64 - 1, 0, 2**33, 63), 777),
+             ((9, 6), 4096), ((0, 0, 0, 0), 1)]
+    for i, (ent, n) in enumerate(cases):
+        rec[f"z_{i}"] = np.random.default_rng(np.random.SeedSequence(ent)).standard_normal(n)
+        rec[f"ent_{i}"] = np.array([str(e) for e in ent])
+    np.savez_compressed(OUT / "normals.npz", **rec, **META)
+    print("normals:", len(cases), "streams")
+
+
+def make_training():
+    """Full reference run_training with its own quadratic oracle (the path's callers)."""
+    from ringmix.objectives import quadratic_oracle
+    from ringmix.simulation import run_training
+
+    rec, specs = {}, []
+    for i, (strategy, L, d, iters, lr, mode, cond, noise, seed, warm) in enumerate([
+        (Strategy.RAND_PSGD, 8, 40, 6, 0.05, "async", 10.0, 1.0, 3, 0),
+        (Strategy.RAND_PSGD, 5, 17, 5, 0.1, "sync", 4.0, 0.5, CELL_SEED, 2),
+        (Strategy.ADPSGD_FIXED, 6, 33, 5, 0.05, "async", 10.0, 1.0, 7, 0),
+        (Strategy.DPSGD_FIXED, 4, 9, 4, 0.1, "async", 2.0, 2.0, 11, 0),
+        (Strategy.D1D, 8, 64, 6, 0.05, "async", 10.0, 1.0, 13, 0),
+        (Strategy.SPSGD, 4, 25, 4, 0.05, "async", 3.0, 1.0, 17, 0),
+    ]):
+        oracle = quadratic_oracle(d, condition_number=cond, noise_scale=noise, seed=seed + 100)
+        cfg = RunConfig(n_learners=L, iterations=iters, lr=lr, batch_size=4, seed=seed,
+                        staleness_mode=mode, warmup_iters=warm, log_every=2)
+        res = run_training(strategy, oracle, cfg)
+        rec[f"records_{i}"] = np.array([[r.iteration, r.sim_time_s, r.mean_loss,
+                                         r.avg_model_loss, r.consensus_dist, r.rho]
+                                        for r in res.records])
+        rec[f"W_{i}"] = res.state.weights
+        rec[f"optimum_{i}"] = oracle.optimum
+        specs.append((strategy.value, L, d, iters, lr, mode, cond, noise, seed, warm,
+                      res.diverged))
+    np.savez_compressed(OUT / "training.npz", specs=np.array(specs, dtype=object), **rec, **META,
+                        allow_pickle=True)
+    print("training:", len(specs), "runs")
+
+
 if __name__ == "__main__":
     make_perms()
     make_sequential()
     make_steps()
     make_spectral()
+    make_normals()
+    make_training()

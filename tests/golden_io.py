@@ -54,3 +54,27 @@ def step_cases():
 @lru_cache(maxsize=None)
 def spectral_golden():
     return dict(np.load(GOLDEN / "spectral.npz"))
+
+
+@lru_cache(maxsize=None)
+def normal_cases():
+    z = np.load(GOLDEN / "normals.npz")
+    out = []
+    i = 0
+    while f"z_{i}" in z:
+        out.append((tuple(int(x) for x in z[f"ent_{i}"]), z[f"z_{i}"]))
+        i += 1
+    return out
+
+
+@lru_cache(maxsize=None)
+def training_cases():
+    z = np.load(GOLDEN / "training.npz", allow_pickle=True)
+    out = []
+    for i, s in enumerate(z["specs"]):
+        strategy, L, d, iters, lr, mode, cond, noise, seed, warm, diverged = s
+        out.append(dict(idx=i, strategy=str(strategy), L=int(L), d=int(d), iters=int(iters),
+                        lr=float(lr), mode=str(mode), cond=float(cond), noise=float(noise),
+                        seed=int(seed), warm=int(warm), diverged=bool(diverged),
+                        records=z[f"records_{i}"], W=z[f"W_{i}"], optimum=z[f"optimum_{i}"]))
+    return out

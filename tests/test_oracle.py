@@ -11,7 +11,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from golden_io import perm_cases, sequential_cases, spectral_golden, step_cases
+from golden_io import normal_cases, perm_cases, sequential_cases, spectral_golden, step_cases
 from oracle import ringmix_oracle as O
 
 
@@ -159,3 +159,13 @@ def test_magnitude_tolerance_helper():
     ref = O.c_ring_mix_sgd(W, G, 0.1, left, right)
     assert O.magnitude_tolerance_ok(ref.astype(np.float32), ref, W, G, 0.1, left, right)
     assert not O.magnitude_tolerance_ok(ref + 1e-3, ref, W, G, 0.1, left, right)
+
+
+def test_c_oracle_standard_normal_matches_golden_and_numpy():
+    for ent, ref in normal_cases():
+        z, draws = O.c_standard_normal(len(ref), *ent)
+        assert np.array_equal(z, ref), ent
+        assert draws >= len(ref)
+    z, _ = O.c_standard_normal(300_000, 77, 0, 1, 2)
+    assert np.array_equal(z, np.random.default_rng(np.random.SeedSequence((77, 0, 1, 2)))
+                          .standard_normal(300_000))

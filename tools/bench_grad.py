@@ -1,0 +1,35 @@
+"""Time the device quadratic-gradient producer (bit-exact numpy normals) and the
+full device training step (gradient + fused RAD mix) at a given shape."""
+import os, sys, json, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2002_01119_b200 import mixing, objectives, simulation
+from paper_2002_01119_b200.simulation import RunConfig
+
+def main(L, d, reps=5):
+    dev = torch.device("cuda")
+    oracle = objectives.quadratic_oracle(d, condition_number=10.0, noise_scale=1.0, seed=1,
+                                         optimum=np.zeros(d))
+    Phi = mixing.empty_learner_major(L, d, torch.float32, dev); Phi.normal_()
+    cfg = RunConfig(n_learners=L, iterations=1, lr=0.01, batch_size=32, seed=5, dtype="float32")
+    for k in range(2):
+        oracle.device_gradients(Phi, cfg, k)
+    torch.cuda.synchronize()
+    ts = []
+    for k in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); G = oracle.device_gradients(Phi, cfg, 10 + k); b.record()
+        torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    # spot-check two learners vs numpy
+    ok = True
+    for l in (0, L - 1):
+        z = np.random.default_rng(np.random.SeedSequence((5, 0, 10 + reps - 1, l))).standard_normal(d)
+        ref = oracle.eigenvalues * (Phi[l].double().cpu().numpy() - 0.0) + (1.0 / np.sqrt(32)) * z
+        ok &= bool(np.array_equal(G[l].double().cpu().numpy(), ref.astype(np.float32).astype(np.float64)))
+    print(json.dumps({"L": L, "d": d, "grad_ms": float(np.median(ts)), "normals_per_s": L * d / (np.median(ts) / 1e3),
+                      "bit_exact_spotcheck": ok}), flush=True)
+
+if __name__ == "__main__":
+    main(16, 1 << 20)
+    main(64, 25_557_032)
