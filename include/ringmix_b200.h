@@ -213,6 +213,9 @@ int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int appen
                            int nstreams, int64_t n, double* Z, int64_t ldz, void* workspace,
                            int64_t workspace_bytes, void* stream);
 
+/* log1p bit-identical to the host glibc 2.39 (x86-64 FMA build), used by the ziggurat tail. */
+int rm_log1p_f64(const double* x, double* y, int64_t n, void* stream);
+
 /* ---- batched ring products (monte_carlo_consensus, spectral.py:273-279) ----
  * For b < B: Y_b[j] = ring3(X_b[left_b j], X_b[j], X_b[right_b j]) with `@`
  * (dgemm) rounding, rows of length d at stride ld, batches at batch_stride;

@@ -51,6 +51,7 @@ _SIGNATURES = {
     "rm_quadratic_grad_f64": ([vp, i32, u64, i32, i64, vp, i64, vp, vp, dbl, vp, i64, vp, i64, vp],
                               i32),
     "rm_standard_normal_f64": ([vp, i32, i32, u64, i32, i64, vp, i64, vp, i64, vp], i32),
+    "rm_log1p_f64": ([vp, vp, i64, vp], i32),
 }
 for _sfx in ("f32", "f64", "bf16"):
     _SIGNATURES[f"rm_ring_mix_sgd_sharded_{_sfx}"] = (

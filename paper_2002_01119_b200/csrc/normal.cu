@@ -26,12 +26,13 @@
 #include "common.cuh"
 #include "arith.cuh"
 #include "ziggurat_tables.h"
+#include <math_constants.h>
 #include "../../include/ringmix_b200.h"
 
 namespace rm {
 
 constexpr int kZBlock = 256;        // raw draws per speculative block
-constexpr int kZGenThreads = 64;    // blocks (threads) per generation CTA
+constexpr int kZGenThreads = 128;   // blocks (threads) per generation CTA
 constexpr int kZMaxPrefix = 24;
 
 struct U128d {
@@ -145,17 +146,113 @@ struct ZGen {
   }
 };
 
+// log1p exactly as the host's libm computes it.  numpy calls libm log1p in the
+// ziggurat tail; glibc 2.39 on x86-64 with FMA/AVX2 dispatches to the FMA build
+// of sysdeps/ieee754/dbl-64/s_log1p.c (fdlibm algorithm, Estrin-style
+// polynomial).  The operation sequence below follows that build instruction
+// for instruction (fused multiply-adds where the compiler fused them), so the
+// device value is bit-identical; CUDA's own log1p differs by 1 ulp in ~0.4 %
+// of tail draws.  Only the domain (-1, 0] used by the ziggurat tail is needed,
+// but the general cases are kept.
+__device__ __noinline__ double glibc_log1p(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01,
+               Lp3 = 2.857142874366239149e-01, Lp4 = 2.222219843214978396e-01,
+               Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  const int hx = __double2hiint(x);
+  const int ax = hx & 0x7fffffff;
+  int k = 1, hu = 0;
+  double f = 0.0, c = 0.0, u;
+  if (hx < 0x3FDA827A) {
+    if (ax >= 0x3ff00000) return x == -1.0 ? -CUDART_INF : CUDART_NAN;
+    if (ax < 0x3e200000) {
+      if (ax < 0x3c900000) return x;
+      return __fma_rn(-__dmul_rn(x, x), 0.5, x);
+    }
+    if (hx > 0 || hx <= (int)0xbfd2bec4) {
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  } else if (hx >= 0x7ff00000) {
+    return __dadd_rn(x, x);
+  }
+  if (k != 0) {
+    if (hx < 0x43400000) {
+      u = __dadd_rn(x, 1.0);
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = (k > 0) ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+      c = __ddiv_rn(c, u);
+    } else {
+      u = x;
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = __hiloint2double(hu | 0x3ff00000, __double2loint(u));
+    } else {
+      k += 1;
+      u = __hiloint2double(hu | 0x3fe00000, __double2loint(u));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double hfsq = __dmul_rn(__dmul_rn(f, 0.5), f);
+  const double dk = (double)k;
+  if (hu == 0) {
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      return __fma_rn(dk, ln2_hi, __fma_rn(dk, ln2_lo, c));
+    }
+    const double R = __dmul_rn(__fma_rn(-f, 0.66666666666666666, 1.0), hfsq);
+    if (k == 0) return __dsub_rn(f, R);
+    return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, __fma_rn(dk, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(f, 2.0));
+  const double z = __dmul_rn(s, s);
+  const double R2 = __fma_rn(z, Lp3, Lp2), R3 = __fma_rn(z, Lp5, Lp4), R4 = __fma_rn(z, Lp7, Lp6);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+  double R = __fma_rn(z, Lp1, __dmul_rn(z2, R2));
+  R = __fma_rn(z4, R3, R);
+  R = __fma_rn(z6, R4, R);
+  const double v = __dmul_rn(__dadd_rn(R, hfsq), s);
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, v));
+  const double t = __dsub_rn(__dsub_rn(hfsq, __dadd_rn(__fma_rn(dk, ln2_lo, c), v)), f);
+  return __fma_rn(dk, ln2_hi, -t);
+}
+
+// numpy's ziggurat tables, staged in shared memory (indices are random per
+// lane, which would serialise __constant__ reads)
+struct ZigTables {
+  uint64_t ki[256];
+  double wi[256];
+  double fi[256];
+};
+
+__device__ __forceinline__ void load_tables(ZigTables* t) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    t->ki[i] = kZigKi[i];
+    t->wi[i] = __longlong_as_double((long long)kZigWiBits[i]);
+    t->fi[i] = __longlong_as_double((long long)kZigFiBits[i]);
+  }
+}
+
 // One ziggurat attempt starting with draw `r` (already taken).  Returns true
 // and sets *x when it produces an output; `extra` = further draws consumed.
-__device__ __forceinline__ bool z_attempt(ZGen& g, uint64_t r, double* x, int* extra) {
+__device__ __forceinline__ bool z_attempt(const ZigTables& T, ZGen& g, uint64_t r, double* x,
+                                          int* extra) {
   const int idx = (int)(r & 0xff);
   r >>= 8;
   const int sign = (int)(r & 1);
   const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-  double v = __dmul_rn((double)rabs, __longlong_as_double((long long)kZigWiBits[idx]));
+  double v = __dmul_rn((double)rabs, T.wi[idx]);
   if (sign) v = -v;
   *extra = 0;
-  if (rabs < kZigKi[idx]) {
+  if (rabs < T.ki[idx]) {
     *x = v;
     return true;
   }
@@ -163,8 +260,8 @@ __device__ __forceinline__ bool z_attempt(ZGen& g, uint64_t r, double* x, int* e
     const double R = 3.6541528853610087963519472518;
     const double INV_R = 0.27366123732975827203338247596;
     for (;;) {
-      double xx = __dmul_rn(-INV_R, log1p(-g.next_double()));
-      double yy = -log1p(-g.next_double());
+      double xx = __dmul_rn(-INV_R, glibc_log1p(-g.next_double()));
+      double yy = -glibc_log1p(-g.next_double());
       *extra += 2;
       if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
         *x = ((rabs >> 8) & 1) ? -__dadd_rn(R, xx) : __dadd_rn(R, xx);
@@ -172,8 +269,7 @@ __device__ __forceinline__ bool z_attempt(ZGen& g, uint64_t r, double* x, int* e
       }
     }
   }
-  const double f0 = __longlong_as_double((long long)kZigFiBits[idx - 1]);
-  const double f1 = __longlong_as_double((long long)kZigFiBits[idx]);
+  const double f0 = T.fi[idx - 1], f1 = T.fi[idx];
   double lhs = __dadd_rn(__dmul_rn(__dsub_rn(f0, f1), g.next_double()), f1);
   *extra = 1;
   if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, v), v))) {
@@ -190,19 +286,30 @@ struct BlockInfo {
   uint32_t count;  // outputs of attempts starting in [b*B, (b+1)*B)
 };
 
-__global__ void zig_spec_kernel(ZArgs a, BlockInfo* __restrict__ info) {
+// per-stream PCG64 state right after seeding (SeedSequence hashing done once)
+__global__ void zig_seed_kernel(ZArgs a, ZStream* __restrict__ seeds) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < a.nstreams) seeds[s] = z_seed(a, s);
+}
+
+__global__ void __launch_bounds__(128)
+    zig_spec_kernel(ZArgs a, const ZStream* __restrict__ seeds, BlockInfo* __restrict__ info) {
+  __shared__ ZigTables T;
+  load_tables(&T);
+  __syncthreads();
   const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (gid >= (long long)a.nstreams * a.nblocks) return;
-  const int stream = (int)(gid / a.nblocks);
-  const int b = (int)(gid % a.nblocks);
-  ZStream zs = z_seed(a, stream);
+  // stream-fastest block order keeps concurrent CTAs on the same columns
+  const int stream = (int)(gid % a.nstreams);
+  const int b = (int)(gid / a.nstreams);
+  const ZStream zs = seeds[stream];
   ZGen g{z_jump(zs, (uint64_t)b * kZBlock), zs.inc};
   uint32_t att = 0, outs = 0, count = 0;
   uint32_t pos = 0;  // relative draw index of the next attempt
   while (pos < (uint32_t)kZBlock) {
     double x;
     int extra;
-    bool ok = z_attempt(g, g.next64(), &x, &extra);
+    const bool ok = z_attempt(T, g, g.next64(), &x, &extra);
     if (pos < 32) {
       att |= 1u << pos;
       if (ok) outs |= 1u << pos;
@@ -210,7 +317,7 @@ __global__ void zig_spec_kernel(ZArgs a, BlockInfo* __restrict__ info) {
     count += ok ? 1u : 0u;
     pos += 1 + extra;
   }
-  info[gid] = BlockInfo{att, outs, pos, count};
+  info[(long long)stream * a.nblocks + b] = BlockInfo{att, outs, pos, count};
 }
 
 // entries[b] (relative entry of the true path into block b) and true counts.
@@ -237,28 +344,29 @@ __global__ void zig_merge_kernel(ZArgs a, const BlockInfo* __restrict__ info,
 // Sequential repair of blocks whose speculative path did not merge: one
 // thread per stream walks its bad blocks in order and re-simulates from the
 // true entry until the path merges again with the next block's speculation.
-__global__ void zig_repair_kernel(ZArgs a, const BlockInfo* __restrict__ info,
-                                  uint32_t* __restrict__ entry, uint32_t* __restrict__ tcount,
-                                  const uint32_t* __restrict__ nbad,
+__global__ void zig_repair_kernel(ZArgs a, const ZStream* __restrict__ seeds,
+                                  const BlockInfo* __restrict__ info, uint32_t* __restrict__ entry,
+                                  uint32_t* __restrict__ tcount, const uint32_t* __restrict__ nbad,
                                   const uint64_t* __restrict__ bad) {
+  __shared__ ZigTables T;
+  const uint32_t nb = *nbad;
+  if (nb == 0) return;  // uniform: no bad blocks (the common case)
+  load_tables(&T);
+  __syncthreads();
   const int stream = blockIdx.x * blockDim.x + threadIdx.x;
   if (stream >= a.nstreams) return;
-  const uint32_t nb = *nbad;
-  if (nb == 0) return;
-  ZStream zs = z_seed(a, stream);
+  const ZStream zs = seeds[stream];
   long long next_b = -1;
   for (;;) {
-    // smallest bad block of this stream not yet handled
     long long best = -1;
     for (uint32_t i = 0; i < nb; i++) {
-      long long gid = (long long)bad[i];
+      const long long gid = (long long)bad[i];
       if (gid / a.nblocks != stream) continue;
-      long long bb = gid % a.nblocks;
+      const long long bb = gid % a.nblocks;
       if (bb > next_b && (best < 0 || bb < best)) best = bb;
     }
     if (best < 0) return;
     long long b = best;
-    // walk forward from the true entry of block b until merged
     for (;;) {
       const long long gid = (long long)stream * a.nblocks + b;
       const uint32_t e = entry[gid];
@@ -267,7 +375,7 @@ __global__ void zig_repair_kernel(ZArgs a, const BlockInfo* __restrict__ info,
       while (pos < (uint32_t)kZBlock) {
         double x;
         int extra;
-        count += z_attempt(g, g.next64(), &x, &extra) ? 1u : 0u;
+        count += z_attempt(T, g, g.next64(), &x, &extra) ? 1u : 0u;
         pos += 1 + extra;
       }
       tcount[gid] = count;
@@ -286,8 +394,7 @@ __global__ void zig_repair_kernel(ZArgs a, const BlockInfo* __restrict__ info,
   }
 }
 
-// per-stream exclusive prefix sum of tcount -> offs (single pass per stream,
-// 1024 threads, sequential chunks)
+// per-stream exclusive prefix sum of tcount -> offs
 __global__ void zig_scan_kernel(ZArgs a, const uint32_t* __restrict__ tcount,
                                 unsigned long long* __restrict__ offs,
                                 unsigned long long* __restrict__ total) {
@@ -299,8 +406,7 @@ __global__ void zig_scan_kernel(ZArgs a, const uint32_t* __restrict__ tcount,
   const long long base = (long long)stream * a.nblocks;
   for (int c0 = 0; c0 < a.nblocks; c0 += blockDim.x) {
     const int i = c0 + threadIdx.x;
-    unsigned long long v = i < a.nblocks ? tcount[base + i] : 0ull;
-    // inclusive warp scan
+    const unsigned long long v = i < a.nblocks ? tcount[base + i] : 0ull;
     unsigned long long x = v;
     for (int o = 1; o < 32; o <<= 1) {
       unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
@@ -317,7 +423,8 @@ __global__ void zig_scan_kernel(ZArgs a, const uint32_t* __restrict__ tcount,
       warp_sums[threadIdx.x] = w;
     }
     __syncthreads();
-    const unsigned long long before = carry + ((threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0ull);
+    const unsigned long long before =
+        carry + ((threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0ull);
     if (i < a.nblocks) offs[base + i] = before + x - v;
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry = before + x;
@@ -326,52 +433,82 @@ __global__ void zig_scan_kernel(ZArgs a, const uint32_t* __restrict__ tcount,
   if (threadIdx.x == 0) total[stream] = carry;
 }
 
-// Generation + fused quadratic gradient.  CTA = kZGenThreads consecutive raw
-// blocks of one stream; each thread regenerates its block's outputs (fp64)
-// into shared memory, then the CTA writes G for its output range coalesced.
+// Generation + fused quadratic gradient.  A CTA owns kZGenThreads consecutive
+// raw blocks of one stream (CTAs ordered stream-fastest so concurrent CTAs
+// share lam / w* columns in L2).  Each thread regenerates its block's outputs
+// from the true entry in rounds of kZRound; after each round every warp writes
+// whole runs of 32 consecutive outputs (coalesced Phi / lam / w* loads and G
+// stores).
+constexpr int kZRound = 32;
+
 template <typename T>
 __global__ void __launch_bounds__(kZGenThreads)
-    zig_gen_kernel(ZArgs a, const uint32_t* __restrict__ entry,
+    zig_gen_kernel(ZArgs a, const ZStream* __restrict__ seeds, const uint32_t* __restrict__ entry,
                    const uint32_t* __restrict__ tcount,
                    const unsigned long long* __restrict__ offs, const T* __restrict__ Phi,
                    long long ldp, const double* __restrict__ lam, const double* __restrict__ wopt,
                    double sd, T* __restrict__ G, long long ldg, double* __restrict__ Z,
                    long long ldz) {
   using E = Elem<T>;
-  extern __shared__ double zbuf[];
+  __shared__ ZigTables Tb;
+  __shared__ double zbuf[kZGenThreads][kZRound + 1];
+  __shared__ int rcount[kZGenThreads];
+  __shared__ unsigned long long rbase[kZGenThreads];
   const int groups = (a.nblocks + kZGenThreads - 1) / kZGenThreads;
-  const int stream = blockIdx.x / groups;
-  const int b0 = (blockIdx.x % groups) * kZGenThreads;
-  const int b = b0 + threadIdx.x;
+  const int stream = blockIdx.x % a.nstreams;
+  const int b0 = (blockIdx.x / a.nstreams) * kZGenThreads;
+  if (b0 >= a.nblocks) return;
+  (void)groups;
   const long long base = (long long)stream * a.nblocks;
-  const int blast = min(b0 + kZGenThreads, a.nblocks) - 1;
-  const unsigned long long o_first = offs[base + b0];
-  const unsigned long long o_end = offs[base + blast] + tcount[base + blast];
-  if (o_first >= (unsigned long long)a.n) return;  // whole CTA beyond d (uniform)
-  if (b < a.nblocks) {
+  if (offs[base + b0] >= (unsigned long long)a.n) return;  // CTA-uniform
+  load_tables(&Tb);
+  const int b = b0 + threadIdx.x;
+  const bool live = b < a.nblocks;
+  const ZStream zs = seeds[stream];
+  ZGen g{zs.state, zs.inc};
+  uint32_t pos = 0, left = 0;
+  unsigned long long obase = 0;
+  if (live) {
     const long long gid = base + b;
-    const uint32_t e = entry[gid];
-    ZStream zs = z_seed(a, stream);
-    ZGen g{z_jump(zs, (uint64_t)b * kZBlock + e), zs.inc};
-    uint32_t pos = e;
-    unsigned long long o = offs[gid] - o_first;
-    while (pos < (uint32_t)kZBlock) {
+    pos = entry[gid];
+    left = tcount[gid];
+    obase = offs[gid];
+    g.state = z_jump(zs, (uint64_t)b * kZBlock + pos);
+    if (obase >= (unsigned long long)a.n) left = 0;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (;;) {
+    // one round: up to kZRound outputs per thread
+    int cnt = 0;
+    __syncthreads();  // tables loaded / previous flush done
+    while (left > 0 && cnt < kZRound) {
       double x;
       int extra;
-      if (z_attempt(g, g.next64(), &x, &extra)) zbuf[o++] = x;
+      if (z_attempt(Tb, g, g.next64(), &x, &extra)) {
+        zbuf[threadIdx.x][cnt++] = x;
+        left--;
+      }
       pos += 1 + extra;
     }
-  }
-  __syncthreads();
-  const long long o_stop = min((long long)o_end, a.n);
-  for (long long c = (long long)o_first + threadIdx.x; c < o_stop; c += kZGenThreads) {
-    const double z = zbuf[c - (long long)o_first];
-    if (Z) Z[stream * ldz + c] = z;
-    if (G) {
-      // objectives.py:87-90: gradient(w) + noise_sd * z, gradient = lam * (w - w*)
-      const double w = (double)E::ld(Phi + stream * ldp + c, 0);
-      const double gr = __dmul_rn(lam[c], __dsub_rn(w, wopt[c]));
-      G[stream * ldg + c] = E::st((typename E::acc)__dadd_rn(gr, __dmul_rn(sd, z)));
+    rcount[threadIdx.x] = cnt;
+    rbase[threadIdx.x] = obase;
+    obase += cnt;
+    if (!__syncthreads_or(cnt > 0)) break;
+    for (int t = warp; t < kZGenThreads; t += kZGenThreads / 32) {
+      const int ct = rcount[t];
+      if (lane < ct) {
+        const long long c = (long long)rbase[t] + lane;
+        if (c < a.n) {
+          const double z = zbuf[t][lane];
+          if (Z) Z[stream * ldz + c] = z;
+          if (G) {
+            // objectives.py:87-90: gradient(w) + noise_sd * z, gradient = lam * (w - w*)
+            const double w = (double)E::ld(Phi + stream * ldp + c, 0);
+            const double gr = __dmul_rn(lam[c], __dsub_rn(w, wopt[c]));
+            G[stream * ldg + c] = E::st((typename E::acc)__dadd_rn(gr, __dmul_rn(sd, z)));
+          }
+        }
+      }
     }
   }
 }
@@ -411,7 +548,8 @@ extern "C" int64_t rm_normal_workspace_bytes(int nstreams, int64_t n) {
   const long long nblocks = (long long)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) /
                                         kZBlock) + 8;
   const long long nb = nblocks * nstreams;
-  return (int64_t)(nb * (sizeof(BlockInfo) + 4 + 4 + 8) + nstreams * 8 + 8 + nb * 8 + 256);
+  return (int64_t)(nb * (sizeof(BlockInfo) + 4 + 4 + 8) + nstreams * (8 + sizeof(ZStream)) + 8 +
+                   nb * 8 + 512);
 }
 
 // Quadratic-oracle gradients for all learners of step k (see header).
@@ -459,32 +597,29 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
   ws += nb * 8;
   unsigned long long* total = reinterpret_cast<unsigned long long*>(ws);
   ws += nstreams * 8;
+  ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 63) & ~(uintptr_t)63);
+  ZStream* seeds = reinterpret_cast<ZStream*>(ws);
+  ws += nstreams * sizeof(ZStream);
   uint32_t* nbad = reinterpret_cast<uint32_t*>(ws);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemsetAsync(nbad, 0, 4, st);
   if (e != cudaSuccess) return fail_cuda(e, "cudaMemsetAsync");
   const int threads = 128;
   const long long grid = (nb + threads - 1) / threads;
-  zig_spec_kernel<<<(int)grid, threads, 0, st>>>(a, info);
+  zig_seed_kernel<<<(nstreams + 63) / 64, 64, 0, st>>>(a, seeds);
+  RM_CHECK_LAUNCH("zig_seed_kernel");
+  zig_spec_kernel<<<(int)grid, threads, 0, st>>>(a, seeds, info);
   RM_CHECK_LAUNCH("zig_spec_kernel");
   zig_merge_kernel<<<(int)grid, threads, 0, st>>>(a, info, entry, tcount, nbad, bad);
   RM_CHECK_LAUNCH("zig_merge_kernel");
-  zig_repair_kernel<<<(nstreams + 31) / 32, 32, 0, st>>>(a, info, entry, tcount, nbad, bad);
+  zig_repair_kernel<<<(nstreams + 31) / 32, 32, 0, st>>>(a, seeds, info, entry, tcount, nbad,
+                                                         bad);
   RM_CHECK_LAUNCH("zig_repair_kernel");
   zig_scan_kernel<<<nstreams, 1024, 0, st>>>(a, tcount, offs, total);
   RM_CHECK_LAUNCH("zig_scan_kernel");
-  const int groups = (a.nblocks + kZGenThreads - 1) / kZGenThreads;
-  // worst case outputs per CTA = kZGenThreads * kZBlock
-  const size_t smem = (size_t)kZGenThreads * kZBlock * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(zig_gen_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(zig_gen_kernel)");
-    attr = true;
-  }
-  zig_gen_kernel<T><<<groups * nstreams, kZGenThreads, smem, st>>>(
-      a, entry, tcount, offs, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+  const long long groups = (a.nblocks + kZGenThreads - 1) / kZGenThreads;
+  zig_gen_kernel<T><<<(int)(groups * nstreams), kZGenThreads, 0, st>>>(
+      a, seeds, entry, tcount, offs, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
   RM_CHECK_LAUNCH("zig_gen_kernel");
   return 0;
 }
@@ -513,4 +648,26 @@ extern "C" int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix
                                       void* stream) {
   return quad_grad<double>(prefix_words, n_prefix, append, k, nstreams, n, nullptr, 0, nullptr, nullptr,
                            0.0, nullptr, 0, Z, ldz, workspace, workspace_bytes, stream);
+}
+
+// Element-wise glibc-compatible log1p (pins glibc_log1p against the host libm in tests).
+namespace rm {
+__global__ void log1p_kernel(const double* __restrict__ x, double* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = glibc_log1p(x[i]);
+}
+}  // namespace rm
+
+extern "C" int rm_log1p_f64(const double* x, double* y, int64_t n, void* stream) {
+  if (x == nullptr || y == nullptr || n < 0) {
+    set_error("invalid log1p arguments");
+    return RM_EINVAL;
+  }
+  if (n == 0) return 0;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  log1p_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, y, n);
+  RM_CHECK_LAUNCH("log1p_kernel");
+  return 0;
 }

@@ -102,3 +102,23 @@ def test_run_training_reproduces_reference_trace(case):
     else:
         # OpenBLAS edge-column rounding compounds over the run
         assert np.allclose(W, case["W"], rtol=0, atol=1e-13)
+
+
+def test_device_log1p_is_bit_identical_to_host_libm():
+    """numpy's ziggurat calls the C library's log1p (npy_log1p), which is what
+    math.log1p calls; numpy's own np.log1p ufunc is a different SIMD code and
+    is NOT the reference here."""
+    import math
+
+    from paper_2002_01119_b200 import _lib
+    rng = np.random.default_rng(0)
+    # the ziggurat tail evaluates log1p(-u), u = next_double in [0, 1)
+    u = rng.integers(0, 2**53, 300_000, dtype=np.uint64).astype(np.float64) \
+        * (1.0 / 9007199254740992.0)
+    x = np.concatenate([-u, rng.uniform(-0.999, 5.0, 100_000), [0.0, -0.0, 1e-300, -1e-17,
+                                                                1e-10, -0.2929, 0.41422, 1e20]])
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    _lib.check(_lib.load().rm_log1p_f64(xd.data_ptr(), yd.data_ptr(), len(x), _lib.stream_ptr()))
+    ref = np.array([math.log1p(v) for v in x])
+    assert np.array_equal(yd.cpu().numpy().view(np.int64), ref.view(np.int64))
