@@ -213,6 +213,21 @@ int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int appen
                            int nstreams, int64_t n, double* Z, int64_t ldz, void* workspace,
                            int64_t workspace_bytes, void* stream);
 
+/* ---- fused trace reductions (run_training's _record, simulation.py:398-409) ----
+ * One pass over W (L <= 128 learners, learner-major): cons_sq[l] += sum_c (W[l,c]-mean_c)^2
+ * (consensus_distance), and when lam != NULL: loss_col[l] += 0.5 sum_c lam_c (W[l,c]-wopt_c)^2,
+ * avg_loss += 0.5 sum_c lam_c (mean_c-wopt_c)^2.  Outputs are fp64 device accumulators the
+ * caller zeroes. */
+int rm_trace_stats_f32(const float* W, int L, int64_t d, int64_t ld, const double* lam,
+                       const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
+                       void* stream);
+int rm_trace_stats_f64(const double* W, int L, int64_t d, int64_t ld, const double* lam,
+                       const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
+                       void* stream);
+int rm_trace_stats_bf16(const uint16_t* W, int L, int64_t d, int64_t ld, const double* lam,
+                        const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
+                        void* stream);
+
 /* log1p bit-identical to the host glibc 2.39 (x86-64 FMA build), used by the ziggurat tail. */
 int rm_log1p_f64(const double* x, double* y, int64_t n, void* stream);
 

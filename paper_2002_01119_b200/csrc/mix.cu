@@ -213,29 +213,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(&full[s], parity);
 
     if (MODE != kRing) {
-      // numpy pairwise mean per column over the L staged rows; 8 lanes per
-      // column hold numpy's partial sums r[0..7] (8 <= n <= 128) and combine
-      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) with xor-shuffles (fp add is
-      // commutative, so the order inside each pair does not matter).
+      // numpy pairwise mean per column over the L staged rows: one thread per
+      // column keeps numpy's 8 partial sums r[0..7] (8 <= n <= 128) in
+      // registers (8 independent add chains) and combines them in numpy's
+      // order ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail.  Lanes
+      // read consecutive columns of one staged row: no bank conflicts.
       const T* src = (MODE == kMean) ? sW : sG;
       if (L <= 128 && L >= 8) {
         const int n8 = L - (L % 8);
-        for (int base0 = warp * 32; base0 < width * 8; base0 += kThreads) {
-          const int base = base0 + lane;
-          const bool active = base < width * 8;
-          const int col = base >> 3, k = base & 7;
-          A r = 0;
-          if (active) {
-            r = (A)E::ld(src, sidx(k, col));
-            for (int i = 8 + k; i < n8; i += 8) r = r_add(r, (A)E::ld(src, sidx(i, col)));
+        for (int col = tid; col < width; col += kThreads) {
+          A r[8];
+#pragma unroll
+          for (int k = 0; k < 8; k++) r[k] = (A)E::ld(src, sidx(k, col));
+          for (int i = 8; i < n8; i += 8) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) r[k] = r_add(r[k], (A)E::ld(src, sidx(i + k, col)));
           }
-          r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 1));
-          r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 2));
-          r = r_add(r, __shfl_xor_sync(0xffffffffu, r, 4));
-          if (active && k == 0) {
-            for (int i = n8; i < L; i++) r = r_add(r, (A)E::ld(src, sidx(i, col)));
-            s_mean[col] = (double)r_div(r, (A)L);
-          }
+          A res = r_add(r_add(r_add(r[0], r[1]), r_add(r[2], r[3])),
+                        r_add(r_add(r[4], r[5]), r_add(r[6], r[7])));
+          for (int i = n8; i < L; i++) res = r_add(res, (A)E::ld(src, sidx(i, col)));
+          s_mean[col] = (double)r_div(res, (A)L);
         }
       } else {
         for (int col = tid; col < width; col += kThreads) {

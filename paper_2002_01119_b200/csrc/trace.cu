@@ -1,0 +1,134 @@
+// Fused trace reductions for run_training's _record:
+//   cons_sq[l]  = sum_c (W[l,c] - mean_c)^2        consensus_distance (simulation.py:359-362)
+//   loss_col[l] = 0.5 * sum_c lam_c (W[l,c] - w*_c)^2   QuadraticObjective.loss_columns
+//                                                     (objectives.py:77-79)
+//   avg_loss    = 0.5 * sum_c lam_c (mean_c - w*_c)^2   loss(W.mean(axis=1)) (simulation.py:401)
+// in ONE pass over W (the reference makes three full passes plus temporaries).
+// mean_c uses numpy's pairwise order over the learners; the sums over columns
+// are parallel fp64 reductions (the reference sums sequentially), so they agree
+// to fp64 rounding, not bitwise.
+#include "common.cuh"
+#include "arith.cuh"
+#include "../../include/ringmix_b200.h"
+
+namespace rm {
+
+constexpr int kTrThreads = 256;
+constexpr int kTrMaxL = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(kTrThreads)
+    trace_stats_kernel(const T* __restrict__ W, int L, long long d, long long ld,
+                       const double* __restrict__ lam, const double* __restrict__ wopt,
+                       double* __restrict__ cons_sq, double* __restrict__ loss_col,
+                       double* __restrict__ avg_loss) {
+  using E = Elem<T>;
+  __shared__ double acc_c[kTrThreads / 32][kTrMaxL];
+  __shared__ double acc_l[kTrThreads / 32][kTrMaxL];
+  __shared__ double acc_a[kTrThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int l = lane; l < L; l += 32) {
+    acc_c[warp][l] = 0.0;
+    acc_l[warp][l] = 0.0;
+  }
+  if (lane == 0) acc_a[warp] = 0.0;
+  __syncwarp();
+  const bool has_obj = lam != nullptr;
+  double a_sum = 0.0;
+  // warp-uniform trip count (shuffles below need full warps)
+  const long long span = (long long)gridDim.x * kTrThreads;
+  const long long first = blockIdx.x * (long long)kTrThreads + warp * 32;
+  for (long long c0 = first; c0 < d; c0 += span) {
+    const long long c = c0 + lane;
+    const bool ok = c < d;
+    double mean = 0.0, lm = 0.0, wo = 0.0;
+    if (ok) {
+      auto get = [&](int i) { return (double)E::ld(W + (long long)i * ld + c, 0); };
+      mean = __ddiv_rn(pairwise_sum<double>(get, 0, L), (double)L);
+      if (has_obj) {
+        lm = lam[c];
+        wo = wopt[c];
+        const double dm = __dsub_rn(mean, wo);
+        a_sum += 0.5 * lm * dm * dm;
+      }
+    }
+    for (int l = 0; l < L; l++) {
+      double v = 0.0, q = 0.0;
+      if (ok) {
+        const double w = (double)E::ld(W + (long long)l * ld + c, 0);
+        const double dv = w - mean;
+        v = dv * dv;
+        if (has_obj) {
+          const double dw = w - wo;
+          q = lm * dw * dw;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (has_obj) q += __shfl_xor_sync(0xffffffffu, q, o);
+      }
+      if (lane == 0) {
+        acc_c[warp][l] += v;
+        if (has_obj) acc_l[warp][l] += q;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) a_sum += __shfl_xor_sync(0xffffffffu, a_sum, o);
+  if (lane == 0) acc_a[warp] = a_sum;
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += kTrThreads) {
+    double c = 0.0, q = 0.0;
+    for (int w = 0; w < kTrThreads / 32; w++) {
+      c += acc_c[w][l];
+      q += acc_l[w][l];
+    }
+    atomicAdd(&cons_sq[l], c);
+    if (has_obj) atomicAdd(&loss_col[l], 0.5 * q);
+  }
+  if (threadIdx.x == 0 && has_obj) {
+    double t = 0.0;
+    for (int w = 0; w < kTrThreads / 32; w++) t += acc_a[w];
+    atomicAdd(avg_loss, t);
+  }
+}
+
+template <typename T>
+static int trace_stats(const T* W, int L, int64_t d, int64_t ld, const double* lam,
+                       const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
+                       void* stream) {
+  if (W == nullptr || cons_sq == nullptr || L < 1 || L > kTrMaxL || d < 0 || ld < d ||
+      (lam != nullptr && (wopt == nullptr || loss_col == nullptr || avg_loss == nullptr))) {
+    set_error("invalid trace-stat arguments (L=%d, at most %d)", L, kTrMaxL);
+    return RM_EINVAL;
+  }
+  if (d == 0) return 0;
+  long long blocks = (d + kTrThreads - 1) / kTrThreads;
+  if (blocks > 4LL * sm_count(-1)) blocks = 4LL * sm_count(-1);
+  trace_stats_kernel<T><<<(int)blocks, kTrThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss);
+  RM_CHECK_LAUNCH("trace_stats_kernel");
+  return 0;
+}
+
+}  // namespace rm
+
+using namespace rm;
+
+extern "C" int rm_trace_stats_f32(const float* W, int L, int64_t d, int64_t ld, const double* lam,
+                                  const double* wopt, double* cons_sq, double* loss_col,
+                                  double* avg_loss, void* stream) {
+  return trace_stats<float>(W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss, stream);
+}
+
+extern "C" int rm_trace_stats_f64(const double* W, int L, int64_t d, int64_t ld, const double* lam,
+                                  const double* wopt, double* cons_sq, double* loss_col,
+                                  double* avg_loss, void* stream) {
+  return trace_stats<double>(W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss, stream);
+}
+
+extern "C" int rm_trace_stats_bf16(const uint16_t* W, int L, int64_t d, int64_t ld,
+                                   const double* lam, const double* wopt, double* cons_sq,
+                                   double* loss_col, double* avg_loss, void* stream) {
+  return trace_stats<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(W), L, d, ld, lam,
+                                    wopt, cons_sq, loss_col, avg_loss, stream);
+}

@@ -122,3 +122,20 @@ def test_device_log1p_is_bit_identical_to_host_libm():
     _lib.check(_lib.load().rm_log1p_f64(xd.data_ptr(), yd.data_ptr(), len(x), _lib.stream_ptr()))
     ref = np.array([math.log1p(v) for v in x])
     assert np.array_equal(yd.cpu().numpy().view(np.int64), ref.view(np.int64))
+
+
+@pytest.mark.parametrize("L,d,dtype", [(8, 1000, torch.float64), (64, 100_003, torch.float32),
+                                       (3, 17, torch.float64), (128, 5000, torch.bfloat16)])
+def test_fused_trace_stats_match_reference_formulas(L, d, dtype):
+    oracle = objectives.quadratic_oracle(d, condition_number=7.0, noise_scale=1.0, seed=2)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    X = mixing.empty_learner_major(L, d, dtype)
+    X.copy_(torch.randn((L, d), generator=g, device="cuda", dtype=torch.float64).to(dtype))
+    cons_sq, loss_col, avg = simulation.trace_stats(X.T, oracle)
+    W = X.double().cpu().numpy().T              # reference (d, L) layout
+    dev = W - W.mean(axis=1, keepdims=True)
+    assert np.allclose(cons_sq.cpu().numpy(), (dev * dev).sum(axis=0), rtol=1e-12)
+    assert np.allclose(loss_col.cpu().numpy(), oracle.loss_columns(W), rtol=1e-12)
+    assert np.isclose(float(avg), oracle.loss(W.mean(axis=1)), rtol=1e-12)
+    assert simulation.consensus_distance(X.T) == pytest.approx(
+        float(np.sqrt((dev * dev).sum(axis=0).max())), rel=1e-12)
