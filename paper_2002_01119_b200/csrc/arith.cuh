@@ -28,6 +28,13 @@ struct Elem<float> {
     return abs_bits((double)__uint_as_float(m));
   }
   __device__ static __forceinline__ double ld(const float* p, int i) { return (double)p[i]; }
+  // explicit shared-memory load (generic pointers into smem otherwise compile
+  // to generic LD.E)
+  __device__ static __forceinline__ double lds(const float* p) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
+    return (double)v;
+  }
   __device__ static __forceinline__ float st(double y) { return __double2float_rn(y); }
   __device__ static __forceinline__ double absd(float y) { return fabs((double)y); }
 };
@@ -45,6 +52,11 @@ struct Elem<double> {
     return m;
   }
   __device__ static __forceinline__ double ld(const double* p, int i) { return p[i]; }
+  __device__ static __forceinline__ double lds(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
+    return v;
+  }
   __device__ static __forceinline__ double st(double y) { return y; }
   __device__ static __forceinline__ double absd(double y) { return fabs(y); }
 };
@@ -62,6 +74,11 @@ struct Elem<__nv_bfloat16> {
   }
   __device__ static __forceinline__ float ld(const __nv_bfloat16* p, int i) {
     return __bfloat162float(p[i]);
+  }
+  __device__ static __forceinline__ float lds(const __nv_bfloat16* p) {
+    unsigned short v;
+    asm volatile("ld.shared.b16 %0, [%1];" : "=h"(v) : "r"(smem_u32(p)));
+    return __bfloat162float(__ushort_as_bfloat16(v));
   }
   __device__ static __forceinline__ __nv_bfloat16 st(float y) { return __float2bfloat16_rn(y); }
   __device__ static __forceinline__ double absd(__nv_bfloat16 y) {

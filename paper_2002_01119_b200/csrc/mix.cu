@@ -142,7 +142,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   int4* s_tri = reinterpret_cast<int4*>(smem + 128);
   unsigned char* stages = smem + 128 + ((L * 16 + 127) / 128) * 128;
   double* s_mean = nullptr;
-  if (MODE != kRing) s_mean = reinterpret_cast<double*>(stages + kStages * stage_bytes);
+  double* s_part = nullptr;  // [8][cw] partial sums (narrow tiles)
+  if (MODE != kRing) {
+    s_mean = reinterpret_cast<double*>(stages + kStages * stage_bytes);
+    s_part = s_mean + cw;
+  }
 
   T* out = static_cast<T*>(a.out);
   const int tid = threadIdx.x;
@@ -219,25 +223,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       // order ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail.  Lanes
       // read consecutive columns of one staged row: no bank conflicts.
       const T* src = (MODE == kMean) ? sW : sG;
-      if (L <= 128 && L >= 8) {
+      const int groups = cw <= kThreads / 2 ? min(8, kThreads / cw) : 1;
+      if (groups >= 2) {
+        // narrow tiles: split the 8 chains over `groups` threads per column so
+        // every warp works; partial sums meet in shared memory
+        const int n8 = L - (L % 8);
+        const int per = 8 / groups;
+        const int g = tid / cw, col = tid % cw;
+        if (g < groups && col < width) {
+          for (int q = 0; q < per; q++) {
+            const int k = g * per + q;
+            A r = (A)E::lds(src + sidx(k, col));
+            for (int i = 8 + k; i < n8; i += 8) r = r_add(r, (A)E::lds(src + sidx(i, col)));
+            s_part[k * cw + col] = (double)r;
+          }
+        }
+        __syncthreads();
+        if (tid < width) {
+          const double* pp = s_part + tid;
+          A res = r_add(r_add(r_add((A)pp[0], (A)pp[cw]), r_add((A)pp[2 * cw], (A)pp[3 * cw])),
+                        r_add(r_add((A)pp[4 * cw], (A)pp[5 * cw]),
+                              r_add((A)pp[6 * cw], (A)pp[7 * cw])));
+          for (int i = n8; i < L; i++) res = r_add(res, (A)E::lds(src + sidx(i, tid)));
+          s_mean[tid] = (double)r_div(res, (A)L);
+        }
+      } else {
+        // 8 <= L <= 128 here (launch_mix routes other L to the scalar kernel)
         const int n8 = L - (L % 8);
         for (int col = tid; col < width; col += kThreads) {
           A r[8];
 #pragma unroll
-          for (int k = 0; k < 8; k++) r[k] = (A)E::ld(src, sidx(k, col));
+          for (int k = 0; k < 8; k++) r[k] = (A)E::lds(src + sidx(k, col));
           for (int i = 8; i < n8; i += 8) {
 #pragma unroll
-            for (int k = 0; k < 8; k++) r[k] = r_add(r[k], (A)E::ld(src, sidx(i + k, col)));
+            for (int k = 0; k < 8; k++) r[k] = r_add(r[k], (A)E::lds(src + sidx(i + k, col)));
           }
           A res = r_add(r_add(r_add(r[0], r[1]), r_add(r[2], r[3])),
                         r_add(r_add(r[4], r[5]), r_add(r[6], r[7])));
-          for (int i = n8; i < L; i++) res = r_add(res, (A)E::ld(src, sidx(i, col)));
+          for (int i = n8; i < L; i++) res = r_add(res, (A)E::lds(src + sidx(i, col)));
           s_mean[col] = (double)r_div(res, (A)L);
-        }
-      } else {
-        for (int col = tid; col < width; col += kThreads) {
-          auto get = [&](int i) { return (A)E::ld(src, sidx(i, col)); };
-          s_mean[col] = (double)r_div(pairwise_sum<A>(get, 0, L), (A)L);
         }
       }
       __syncthreads();
@@ -330,7 +354,7 @@ static int launch_scalar(const MixArgs& a, long long c_begin, cudaStream_t st) {
 static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode) {
   size_t stage = (size_t)L * cw * elem * (stage_g ? 2 : 1);
   size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kStages * stage;
-  if (mode != kRing) bytes += (size_t)cw * sizeof(double);
+  if (mode != kRing) bytes += (size_t)cw * sizeof(double) * (cw <= kThreads / 2 ? 9 : 1);
   return bytes;
 }
 
@@ -396,7 +420,9 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
-  bool use_tma = aligned && a.L <= kMaxTmaL && a.d >= VEC && a.d < (1LL << 31) &&
+  // the tiled mean phase covers numpy's non-recursive pairwise case (8 <= L <= 128)
+  const bool mean_ok = MODE == kRing || (a.L >= 8 && a.L <= 128);
+  bool use_tma = aligned && mean_ok && a.L <= kMaxTmaL && a.d >= VEC && a.d < (1LL << 31) &&
                  encode_fn() != nullptr;
   int cw = 0;
   if (use_tma) {
