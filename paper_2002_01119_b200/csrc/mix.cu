@@ -233,16 +233,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (g < groups && col < width) {
           for (int q = 0; q < per; q++) {
             const int k = g * per + q;
-            // issue every load of the chain first (independent LDS), then add
-            // in numpy's order (n8 / 8 <= 16 for L <= 128)
-            A v[16];
-#pragma unroll
-            for (int t = 0; t < 16; t++)
-              if (8 * t + k < n8) v[t] = (A)E::lds(src + sidx(8 * t + k, col));
-            A r = v[0];
-#pragma unroll
-            for (int t = 1; t < 16; t++)
-              if (8 * t + k < n8) r = r_add(r, v[t]);
+            A r = (A)E::lds(src + sidx(k, col));
+            for (int i = 8 + k; i < n8; i += 8) r = r_add(r, (A)E::lds(src + sidx(i, col)));
             s_part[k * cw + col] = (double)r;
           }
         }
