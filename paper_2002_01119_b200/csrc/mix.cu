@@ -39,10 +39,12 @@ namespace rm {
 
 enum Mode { kRing = 0, kMean = 1, kSpsgd = 2 };
 
-constexpr int kThreads = 512;
+constexpr int kRingThreads = 512;   // ring tiles: one 512-thread CTA per SM
+constexpr int kMeanThreads = 256;   // mean tiles: two 256-thread CTAs per SM
 constexpr int kStages = 3;
 constexpr int kMaxTmaL = 256;   // one TMA row box per tile
-constexpr int kStageTarget = 64 * 1024;
+constexpr int kStageTarget = 64 * 1024;      // ring
+constexpr int kMeanStageTarget = 32 * 1024;  // mean (two CTAs per SM)
 
 struct MixArgs {
   const void* W;
@@ -122,10 +124,14 @@ __global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_
 // ----------------------------------------------------------------------------
 constexpr int kBox = 256;  // TMA box dimension limit (elements)
 
-template <typename T, int MODE, bool HAS_G>
-__global__ void __launch_bounds__(kThreads, 1)
+// NT threads per CTA: ring tiles run one 512-thread CTA per SM; mean tiles
+// (D1D / S-PSGD) run two 256-thread CTAs per SM, so one CTA's mean phase
+// overlaps the other's output phase.
+template <typename T, int MODE, bool HAS_G, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
     mix_tma_kernel(MixArgs a, const __grid_constant__ CUtensorMap tmW,
                    const __grid_constant__ CUtensorMap tmG) {
+  constexpr int kThreads = NT;
   using E = Elem<T>;
   using A = typename E::acc;
   constexpr int VEC = E::VEC;
@@ -352,6 +358,7 @@ static int launch_scalar(const MixArgs& a, long long c_begin, cudaStream_t st) {
 }
 
 static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode) {
+  const int kThreads = mode == kRing ? kRingThreads : kMeanThreads;
   size_t stage = (size_t)L * cw * elem * (stage_g ? 2 : 1);
   size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kStages * stage;
   if (mode != kRing) bytes += (size_t)cw * sizeof(double) * (cw <= kThreads / 2 ? 9 : 1);
@@ -405,6 +412,7 @@ static bool make_map(CUtensorMap* m, const void* base, long long d, int L, long 
 
 template <typename T, int MODE, bool HAS_G>
 static int launch_mix(MixArgs a, cudaStream_t st) {
+  constexpr int NT = MODE == kRing ? kRingThreads : kMeanThreads;
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const size_t esz = sizeof(T);
@@ -430,14 +438,16 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     // over every SM several times
     size_t per_col = (size_t)a.L * esz * (stage_g ? 2 : 1);
     cw = VEC;
-    while ((size_t)(cw * 2) * per_col <= (size_t)kStageTarget && cw * 2 <= 2048) cw *= 2;
+    const size_t target = MODE == kRing ? kStageTarget : kMeanStageTarget;
+    while ((size_t)(cw * 2) * per_col <= target && cw * 2 <= 2048) cw *= 2;
     const long long want_tiles = 4LL * sm_count(-1);
     while (cw > VEC && (a.d + cw - 1) / cw < want_tiles && cw * esz > 256) cw /= 2;
     if (const char* env = getenv("RINGMIX_TILE_COLS")) {  // tuning override
       int v = atoi(env);
       if (v >= VEC && (v & (v - 1)) == 0) cw = v;
     }
-    if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE) > (size_t)max_optin) use_tma = false;
+    const size_t cap = NT == kRingThreads ? (size_t)max_optin : (size_t)(max_optin / 2 - 1024);
+    if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE) > cap) use_tma = false;
   }
   if (!use_tma) return launch_scalar<T, MODE, HAS_G>(a, 0, st);
 
@@ -465,14 +475,14 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G>,
+    cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
     if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(mix_tma_kernel)");
     attr_set = true;
   }
-  long long grid = sm_count(-1);
+  long long grid = (long long)sm_count(-1) * (512 / NT);
   if (grid > a.ntiles) grid = a.ntiles;
-  mix_tma_kernel<T, MODE, HAS_G><<<(int)grid, kThreads, smem, st>>>(a, tmW, tmG);
+  mix_tma_kernel<T, MODE, HAS_G, NT><<<(int)grid, NT, smem, st>>>(a, tmW, tmG);
   RM_CHECK_LAUNCH("mix_tma_kernel");
   return RM_OK;
 }
