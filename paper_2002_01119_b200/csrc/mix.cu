@@ -79,12 +79,39 @@ __global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_
   const long long total = ncols * a.L;
   unsigned long long amax = 0;
   const A lr = (A)a.lr;
+  if (MODE != kRing) {
+    // one thread per column: the column mean once (numpy pairwise, any L),
+    // then every learner's output
+    for (long long cc = blockIdx.x * (long long)blockDim.x + threadIdx.x; cc < ncols;
+         cc += (long long)gridDim.x * blockDim.x) {
+      const long long c = c_begin + cc;
+      const T* src = MODE == kMean ? W : G;
+      const long long lds = MODE == kMean ? a.ldw : a.ldg;
+      auto get = [&](int i) { return (A)E::ld(src + i * lds + c, 0); };
+      const A m = r_div(pairwise_sum<A>(get, 0, a.L), (A)a.L);
+      for (int j = 0; j < a.L; j++) {
+        A y;
+        if (MODE == kMean) {
+          y = HAS_G ? r_sub(m, r_mul(lr, (A)E::ld(G + j * a.ldg + c, 0))) : m;
+        } else {  // kSpsgd: W - lr * mean_l(G)
+          if (a.mismatch && !(W[j * a.ldw + c] == W[c])) atomicOr(a.mismatch, 1u);
+          y = r_sub((A)E::ld(W + j * a.ldw + c, 0), r_mul(lr, m));
+        }
+        const T ys = E::st(y);
+        out[j * a.ldo + c] = ys;
+        const unsigned long long b = abs_bits((double)E::absd(ys));
+        amax = b > amax ? b : amax;
+      }
+    }
+    if (a.absmax) absmax_publish(a.absmax, amax);
+    return;
+  }
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int j = static_cast<int>(idx / ncols);
     const long long c = c_begin + idx % ncols;
     A y;
-    if (MODE == kRing) {
+    {
       int x0 = a.left[j], x1 = j, x2 = a.right[j], t;
       if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
       if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
@@ -92,16 +119,6 @@ __global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_
       y = ring3<A>(E::ld(W + x0 * a.ldw + c, 0), E::ld(W + x1 * a.ldw + c, 0),
                    E::ld(W + x2 * a.ldw + c, 0));
       if (HAS_G) y = r_sub(y, r_mul(lr, E::ld(G + j * a.ldg + c, 0)));
-    } else if (MODE == kMean) {
-      auto get = [&](int i) { return (A)E::ld(W + i * a.ldw + c, 0); };
-      A m = r_div(pairwise_sum<A>(get, 0, a.L), (A)a.L);
-      y = HAS_G ? r_sub(m, r_mul(lr, E::ld(G + j * a.ldg, c))) : m;
-    } else {  // kSpsgd: W - lr * mean_l(G)
-      auto get = [&](int i) { return (A)E::ld(G + i * a.ldg + c, 0); };
-      A m = r_div(pairwise_sum<A>(get, 0, a.L), (A)a.L);
-      A w = E::ld(W + j * a.ldw + c, 0);
-      if (a.mismatch && !(W[j * a.ldw + c] == W[c])) atomicOr(a.mismatch, 1u);
-      y = r_sub(w, r_mul(lr, m));
     }
     T ys = E::st(y);
     out[j * a.ldo + c] = ys;
