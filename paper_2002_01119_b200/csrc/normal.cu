@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(128)
 // are appended to `bad` for the sequential repair.
 __global__ void zig_merge_kernel(ZArgs a, const BlockInfo* __restrict__ info,
                                  uint32_t* __restrict__ entry, uint32_t* __restrict__ tcount,
-                                 uint32_t* __restrict__ nbad, uint64_t* __restrict__ bad) {
+                                 uint8_t* __restrict__ merged, uint32_t* __restrict__ nbad,
+                                 uint64_t* __restrict__ bad) {
   const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (gid >= (long long)a.nstreams * a.nblocks) return;
   const int b = (int)(gid % a.nblocks);
@@ -334,10 +335,60 @@ __global__ void zig_merge_kernel(ZArgs a, const BlockInfo* __restrict__ info,
   entry[gid] = e;
   if (e < 32 && ((me.att >> e) & 1u)) {
     tcount[gid] = me.count - __popc(me.outs & ((1u << e) - 1u));
+    merged[gid] = 1;
   } else {
     tcount[gid] = 0;
+    merged[gid] = 0;
     uint32_t slot = atomicAdd(nbad, 1u);
     bad[slot] = (uint64_t)gid;
+  }
+}
+
+// Parallel repair of isolated failures (predecessor merged, so the stored
+// entry is the true one): one thread per bad block re-simulates it, then
+// re-checks the successor against the corrected exit.  Failures whose
+// predecessor also failed (chains, very rare) go to `left` for the sequential
+// pass.
+__global__ void __launch_bounds__(128)
+    zig_repair_par_kernel(ZArgs a, const ZStream* __restrict__ seeds,
+                          const BlockInfo* __restrict__ info, uint32_t* __restrict__ entry,
+                          uint32_t* __restrict__ tcount, const uint8_t* __restrict__ merged,
+                          const uint32_t* __restrict__ nbad, const uint64_t* __restrict__ bad,
+                          uint32_t* __restrict__ nleft, uint64_t* __restrict__ left) {
+  __shared__ ZigTables T;
+  const uint32_t nb = *nbad;
+  if (blockIdx.x * blockDim.x >= nb) return;  // CTA-uniform
+  load_tables(&T);
+  __syncthreads();
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const long long gid = (long long)bad[i];
+  const int stream = (int)(gid / a.nblocks);
+  const int b = (int)(gid % a.nblocks);
+  if (b > 0 && !merged[gid - 1]) {
+    left[atomicAdd(nleft, 1u)] = (uint64_t)gid;  // chain: sequential pass
+    return;
+  }
+  const ZStream zs = seeds[stream];
+  const uint32_t e = entry[gid];
+  ZGen g{z_jump(zs, (uint64_t)b * kZBlock + e), zs.inc};
+  uint32_t pos = e, count = 0;
+  while (pos < (uint32_t)kZBlock) {
+    double x;
+    int extra;
+    count += z_attempt(T, g, g.next64(), &x, &extra) ? 1u : 0u;
+    pos += 1 + extra;
+  }
+  tcount[gid] = count;
+  if (b + 1 >= a.nblocks) return;
+  const uint32_t e2 = pos - kZBlock;
+  entry[gid + 1] = e2;
+  if (!merged[gid + 1]) return;  // successor is itself bad: the sequential pass owns it
+  const BlockInfo nx = info[gid + 1];
+  if (e2 < 32 && ((nx.att >> e2) & 1u)) {
+    tcount[gid + 1] = nx.count - __popc(nx.outs & ((1u << e2) - 1u));
+  } else {
+    left[atomicAdd(nleft, 1u)] = (uint64_t)(gid + 1);
   }
 }
 
@@ -350,7 +401,7 @@ __global__ void zig_repair_kernel(ZArgs a, const ZStream* __restrict__ seeds,
                                   const uint64_t* __restrict__ bad) {
   __shared__ ZigTables T;
   const uint32_t nb = *nbad;
-  if (nb == 0) return;  // uniform: no bad blocks (the common case)
+  if (nb == 0) return;  // uniform: no leftover blocks (the common case)
   load_tables(&T);
   __syncthreads();
   const int stream = blockIdx.x * blockDim.x + threadIdx.x;
@@ -494,19 +545,37 @@ __global__ void __launch_bounds__(kZGenThreads)
     rbase[threadIdx.x] = obase;
     obase += cnt;
     if (!__syncthreads_or(cnt > 0)) break;
-    for (int t = warp; t < kZGenThreads; t += kZGenThreads / 32) {
-      const int ct = rcount[t];
-      if (lane < ct) {
-        const long long c = (long long)rbase[t] + lane;
-        if (c < a.n) {
-          const double z = zbuf[t][lane];
-          if (Z) Z[stream * ldz + c] = z;
-          if (G) {
-            // objectives.py:87-90: gradient(w) + noise_sd * z, gradient = lam * (w - w*)
-            const double w = (double)E::ld(Phi + stream * ldp + c, 0);
-            const double gr = __dmul_rn(lam[c], __dsub_rn(w, wopt[c]));
-            G[stream * ldg + c] = E::st((typename E::acc)__dadd_rn(gr, __dmul_rn(sd, z)));
-          }
+    // each warp flushes the runs of threads warp, warp+4, ...; loads of 8 runs
+    // are issued before any is consumed (latency hiding)
+    constexpr int kBatch = 8;
+    for (int t0 = warp; t0 < kZGenThreads; t0 += kBatch * (kZGenThreads / 32)) {
+      long long cs[kBatch];
+      double w[kBatch], lm[kBatch], wo[kBatch];
+      bool on[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) {
+        const int t = t0 + u * (kZGenThreads / 32);
+        on[u] = false;
+        if (t < kZGenThreads && lane < rcount[t]) {
+          cs[u] = (long long)rbase[t] + lane;
+          on[u] = cs[u] < a.n;
+        }
+        if (on[u] && G) {
+          w[u] = (double)E::ld(Phi + stream * ldp + cs[u], 0);
+          lm[u] = lam[cs[u]];
+          wo[u] = wopt[cs[u]];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) {
+        if (!on[u]) continue;
+        const int t = t0 + u * (kZGenThreads / 32);
+        const double z = zbuf[t][lane];
+        if (Z) Z[stream * ldz + cs[u]] = z;
+        if (G) {
+          // objectives.py:87-90: gradient(w) + noise_sd * z, gradient = lam * (w - w*)
+          const double gr = __dmul_rn(lm[u], __dsub_rn(w[u], wo[u]));
+          G[stream * ldg + cs[u]] = E::st((typename E::acc)__dadd_rn(gr, __dmul_rn(sd, z)));
         }
       }
     }
@@ -548,8 +617,8 @@ extern "C" int64_t rm_normal_workspace_bytes(int nstreams, int64_t n) {
   const long long nblocks = (long long)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) /
                                         kZBlock) + 8;
   const long long nb = nblocks * nstreams;
-  return (int64_t)(nb * (sizeof(BlockInfo) + 4 + 4 + 8) + nstreams * (8 + sizeof(ZStream)) + 8 +
-                   nb * 8 + 512);
+  return (int64_t)(nb * (sizeof(BlockInfo) + 4 + 4 + 8 + 1 + 8) +
+                   nstreams * (8 + sizeof(ZStream)) + 16 + 1024);
 }
 
 // Quadratic-oracle gradients for all learners of step k (see header).
@@ -600,9 +669,15 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
   ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 63) & ~(uintptr_t)63);
   ZStream* seeds = reinterpret_cast<ZStream*>(ws);
   ws += nstreams * sizeof(ZStream);
+  uint64_t* left = reinterpret_cast<uint64_t*>(ws);
+  ws += nb * 8;
+  uint8_t* merged = reinterpret_cast<uint8_t*>(ws);
+  ws += nb;
+  ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 15) & ~(uintptr_t)15);
   uint32_t* nbad = reinterpret_cast<uint32_t*>(ws);
+  uint32_t* nleft = nbad + 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(nbad, 0, 4, st);
+  cudaError_t e = cudaMemsetAsync(nbad, 0, 8, st);
   if (e != cudaSuccess) return fail_cuda(e, "cudaMemsetAsync");
   const int threads = 128;
   const long long grid = (nb + threads - 1) / threads;
@@ -610,10 +685,14 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
   RM_CHECK_LAUNCH("zig_seed_kernel");
   zig_spec_kernel<<<(int)grid, threads, 0, st>>>(a, seeds, info);
   RM_CHECK_LAUNCH("zig_spec_kernel");
-  zig_merge_kernel<<<(int)grid, threads, 0, st>>>(a, info, entry, tcount, nbad, bad);
+  zig_merge_kernel<<<(int)grid, threads, 0, st>>>(a, info, entry, tcount, merged, nbad, bad);
   RM_CHECK_LAUNCH("zig_merge_kernel");
-  zig_repair_kernel<<<(nstreams + 31) / 32, 32, 0, st>>>(a, seeds, info, entry, tcount, nbad,
-                                                         bad);
+  // isolated failures in parallel (grid sized for the worst case; idle CTAs exit at once)
+  zig_repair_par_kernel<<<(int)grid, threads, 0, st>>>(a, seeds, info, entry, tcount, merged,
+                                                        nbad, bad, nleft, left);
+  RM_CHECK_LAUNCH("zig_repair_par_kernel");
+  zig_repair_kernel<<<(nstreams + 31) / 32, 32, 0, st>>>(a, seeds, info, entry, tcount, nleft,
+                                                         left);
   RM_CHECK_LAUNCH("zig_repair_kernel");
   zig_scan_kernel<<<nstreams, 1024, 0, st>>>(a, tcount, offs, total);
   RM_CHECK_LAUNCH("zig_scan_kernel");
