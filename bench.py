@@ -446,10 +446,18 @@ def run_ours(args):
     traffic = ncu_traffic(key) if key else None
 
     e2e = None
-    if not args.no_e2e and rank == 0 and args.dtype == "float32" and not uniform:
-        e2e = run_e2e(args, torch, mixing, dev)
+    want_e2e = not args.no_e2e and args.dtype == "float32" and not uniform
+    if want_e2e and (ws == 1 or wl.layout == "coord"):
+        # every rank drives its own column stripe through the host API (own PCIe link)
+        ms = run_e2e(args, torch, mixing, dev, cols=wl.cols)
         if ws > 1:
-            e2e["note"] = "host-buffer API measured on rank 0 for the whole problem"
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        e2e = e2e_line(args, ms, ws)
+    elif want_e2e and rank == 0:
+        e2e = e2e_line(args, run_e2e(args, torch, mixing, dev), 1)
+        e2e["note"] = "learner layout: host-buffer API measured on rank 0 for the whole problem"
     if ws > 1:
         dist.barrier()
     wl.close()
@@ -485,9 +493,13 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, torch, mixing, dev):
-    """Step through the host-buffer API (W, G pinned host -> W' host)."""
-    L, d = args.learners, args.dim
+def run_e2e(args, torch, mixing, dev, cols=None):
+    """Step through the host-buffer API (W, G pinned host -> W' host) for this
+    rank's column stripe (`cols`, default: the whole problem); returns ms/step."""
+    from paper_2002_01119_b200 import mixing as M
+
+    L = args.learners
+    d = args.dim if cols is None else cols
     Wh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
     Gh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
     Oh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
@@ -495,7 +507,6 @@ def run_e2e(args, torch, mixing, dev):
     Wh.normal_(generator=g)
     Gh.normal_(generator=g)
     ws_buf = mixing.host_workspace(L, 1 << 20, dev)
-    from paper_2002_01119_b200 import mixing as M
     tabs = M.permutation_tables(L, SEED, 0, args.e2e_steps + 1, dev)
     left = tabs.left.cpu()
     right = tabs.right.cpu()
@@ -512,12 +523,18 @@ def run_e2e(args, torch, mixing, dev):
         src, dst = dst, src
     b.record(stream)
     torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / args.e2e_steps
+    return a.elapsed_time(b) / args.e2e_steps
+
+
+def e2e_line(args, ms, ws):
+    L, d = args.learners, args.dim
     return {"value": L * d / (ms / 1e3), "unit": UNIT,
-            "h2d_bytes_per_step": 2 * L * d * 4 + 2 * L * 4, "d2h_bytes_per_step": L * d * 4,
+            "h2d_bytes_per_step": 2 * L * d * 4 + 2 * L * 4 * ws,
+            "d2h_bytes_per_step": L * d * 4,
             "ms_per_step": ms, "steps": args.e2e_steps,
             "path": "mixing.ring_mix_sgd_host -> rm_ring_mix_sgd_host_f32 (pinned host W, G; "
-                    "chunked H2D || kernel || D2H)"}
+                    "chunked H2D || kernel || D2H)" + (
+                        f"; every rank its column stripe, max over {ws} ranks" if ws > 1 else "")}
 
 
 def main():
