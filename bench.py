@@ -197,8 +197,17 @@ def cpu_reference_step_fn(L: int, d_sample: int, uniform: bool):
     return step
 
 
-def cpu_baseline(L: int, uniform: bool, seconds: float):
+def all_host_threads():
+    """OpenBLAS may have been initialised with 1 thread (torchrun exports
+    OMP_NUM_THREADS=1 for multi-process jobs); the CPU legs use every host core."""
+    from threadpoolctl import threadpool_limits
+
     cores = os.cpu_count() or 1
+    return threadpool_limits(limits=cores), cores
+
+
+def cpu_baseline(L: int, uniform: bool, seconds: float):
+    _limits, cores = all_host_threads()
     d_sample = 1 << 20
     step = cpu_reference_step_fn(L, d_sample, uniform)
     step()  # warm
@@ -213,7 +222,7 @@ def cpu_baseline(L: int, uniform: bool, seconds: float):
     med = statistics.median(times)
     return {"value": L * d_sample / med, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": (f"numpy fp64 apply_mixing(W,T) - lr*G on a (d=1,048,576 x L={L}) C-order "
-                       f"sample, OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', cores)}, "
+                       f"sample, OpenBLAS threads={cores}, "
                        f"median of {len(times)} steps ({sum(times):.1f} s)")}
 
 
@@ -224,6 +233,7 @@ def run_reference(args):
     L = args.learners
     uniform = args.strategy == "d1d"
     d_sample = 1 << 20
+    _limits, cores = all_host_threads()
     step = cpu_reference_step_fn(L, d_sample, uniform)
     for _ in range(args.warmup):
         step()
@@ -234,7 +244,6 @@ def run_reference(args):
         times.append(time.perf_counter() - t)
     total = sum(times)
     value = L * d_sample * args.steps / total
-    cores = os.cpu_count() or 1
     sample = (f"numpy fp64 apply_mixing(W,T) - lr*G (oracle port of simulation.py:267), "
               f"(d=1,048,576 x L={L}) C-order sample per step, all {cores} host threads")
     line = {
