@@ -43,7 +43,13 @@ import threading
 import time
 from pathlib import Path
 
-import numpy as np
+# The CPU legs (cpu_baseline, --impl reference) run on rank 0 with every host
+# core; torchrun exports OMP_NUM_THREADS=1 for multi-process jobs, which
+# OpenBLAS would otherwise honour at import.
+if os.environ.get("RANK", "0") == "0":
+    os.environ["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
+
+import numpy as np  # noqa: E402
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -198,12 +204,8 @@ def cpu_reference_step_fn(L: int, d_sample: int, uniform: bool):
 
 
 def all_host_threads():
-    """OpenBLAS may have been initialised with 1 thread (torchrun exports
-    OMP_NUM_THREADS=1 for multi-process jobs); the CPU legs use every host core."""
-    from threadpoolctl import threadpool_limits
-
-    cores = os.cpu_count() or 1
-    return threadpool_limits(limits=cores), cores
+    """Thread count of the CPU legs (OpenBLAS set to every core at import, rank 0)."""
+    return None, int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
 
 
 def cpu_baseline(L: int, uniform: bool, seconds: float):
