@@ -75,6 +75,7 @@ def parse():
     ap.add_argument("--strategy", choices=["rand_psgd", "adpsgd_fixed", "d1d"],
                     default="rand_psgd")
     ap.add_argument("--layout", choices=["coord", "learner"], default="coord")
+    ap.add_argument("--d1d-collective", choices=["auto", "nvls", "nccl"], default="auto")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -312,7 +313,17 @@ class Workload:
                 b, e = lay.rows(rank)
                 self.rows, self.cols = e - b, d
                 self.W = [synth(e - b, d), mixing.empty_learner_major(e - b, d, dtype, dev)]
-                self.d1d = D.LearnerShardedD1D(L, d, e - b, dev)
+                self.d1d = None
+                if args.d1d_collective in ("auto", "nvls"):
+                    try:
+                        self.d1d = D.LearnerShardedD1DNVLS(L, d, e - b, dev)
+                        self.d1d_kind = "nvls"
+                    except Exception:
+                        if args.d1d_collective == "nvls":
+                            raise
+                if self.d1d is None:
+                    self.d1d = D.LearnerShardedD1D(L, d, e - b, dev)
+                    self.d1d_kind = "nccl"
             else:
                 self.ring = D.LearnerShardedRing(L, d, dtype)
                 self.rows, self.cols = self.ring.Lg, d
@@ -379,8 +390,10 @@ class Workload:
             self.cur = 1 - self.cur
         if ev_pair is not None:
             ev_pair[1].record(stream)
-        self.launches["mix"] += (2 * len(self.d1d.chunks)
-                                 if self.layout == "learner" and self.uniform else 1)
+        if self.layout == "learner" and self.uniform:
+            self.launches["mix"] += 3 if self.d1d_kind == "nvls" else 2 * len(self.d1d.chunks)
+        else:
+            self.launches["mix"] += 1
         if self.layout == "learner" and not self.uniform:
             self.ring.barrier()              # next step reads this step's rows on peers
             self.launches["barrier_allreduce"] += 1

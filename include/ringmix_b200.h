@@ -192,6 +192,13 @@ int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, in
                            int64_t d, int64_t ldg, int64_t ldo, double lr,
                            unsigned long long* absmax_bits, void* stream);
 
+/* D1D across ranks through NVSwitch multicast: for columns [c0, c1) sum the
+ * ranks' fp64 partial sums in the switch (multimem.ld_reduce) and broadcast the
+ * sums to every rank (multimem.st).  P_mc / M_mc: multicast addresses of
+ * symmetric buffers (e.g. torch symmetric memory).  Caller orders it with
+ * cross-rank barriers. */
+int rm_nvls_sum_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1, void* stream);
+
 /* ---- device gradient producer for the reference's quadratic oracle ----
  * (objectives.py:84-90 via simulation.py:226-238):
  *   G[l] = lam * (Phi[l] - wopt) + noise_sd * z_l,

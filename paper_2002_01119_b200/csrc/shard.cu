@@ -572,3 +572,52 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
 RM_DEFINE_SHARD(f32, float, float)
 RM_DEFINE_SHARD(f64, double, double)
 RM_DEFINE_SHARD(bf16, uint16_t, __nv_bfloat16)
+
+// ---- D1D cross-GPU sum through NVSwitch multicast (NVLS) ----
+// P_mc / M_mc are multicast addresses of symmetric buffers (every rank maps the
+// same object).  For the caller's column shard [c0, c1): the switch sums the
+// ranks' partial column sums (multimem.ld_reduce.add.f64, in-network reduction)
+// and the result is broadcast into every rank's M (multimem.st).  Ordering
+// against the partial-sum writes and the readers of M is the caller's barrier.
+namespace rm {
+__global__ void __launch_bounds__(256)
+    nvls_sum_kernel(const double* __restrict__ P_mc, double* __restrict__ M_mc, long long c0,
+                    long long c1) {
+  constexpr int U = 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; c < c1;
+       c += U * stride) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const long long cc = c + u * stride;
+      if (cc < c1)
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];"
+                     : "=d"(v[u])
+                     : "l"(P_mc + cc)
+                     : "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const long long cc = c + u * stride;
+      if (cc < c1)
+        asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(M_mc + cc), "d"(v[u])
+                     : "memory");
+    }
+  }
+}
+}  // namespace rm
+
+extern "C" int rm_nvls_sum_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1,
+                               void* stream) {
+  if (P_mc == nullptr || M_mc == nullptr || c0 < 0 || c1 < c0) {
+    set_error("invalid NVLS reduction arguments");
+    return RM_EINVAL;
+  }
+  if (c1 == c0) return 0;
+  long long blocks = (c1 - c0 + 1023) / 1024;
+  if (blocks > 4LL * sm_count(-1)) blocks = 4LL * sm_count(-1);
+  nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(P_mc, M_mc, c0, c1);
+  RM_CHECK_LAUNCH("nvls_sum_kernel");
+  return 0;
+}

@@ -234,6 +234,55 @@ class LearnerShardedRing:
         self.peers.close()
 
 
+class LearnerShardedD1DNVLS:
+    """D1D step with learners sharded, the cross-GPU sum done by our own kernel in the
+    NVSwitch: every rank writes its fp64 column partial sums into a symmetric buffer;
+    for its 1/N column shard a rank sums all ranks' partials in the switch
+    (``multimem.ld_reduce``) and broadcasts the totals into every rank's copy
+    (``multimem.st``); then each rank applies mean - lr*G to its learners.  No NCCL
+    kernels; the two cross-rank barriers are symmetric-memory signal pads
+    (stream-ordered)."""
+
+    def __init__(self, L: int, d: int, Lg: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.L, self.d, self.Lg = L, d, Lg
+        self.device = torch.device(device)
+        self.group = group if group is not None else dist.group.WORLD
+        gname = self.group.group_name
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        self.P = symm_mem.empty(d, dtype=torch.float64, device=self.device)
+        self.M = symm_mem.empty(d, dtype=torch.float64, device=self.device)
+        self.hP = symm_mem.rendezvous(self.P, gname)
+        self.hM = symm_mem.rendezvous(self.M, gname)
+        if not self.hP.multicast_ptr or not self.hM.multicast_ptr:
+            raise RuntimeError("NVSwitch multicast (NVLS) is not available on this system")
+        # column shard reduced by this rank; 32-column aligned boundaries
+        step = -(-d // self.world)
+        step = ((step + 31) // 32) * 32
+        self.c0 = min(d, self.rank * step)
+        self.c1 = min(d, self.c0 + step)
+
+    def step(self, W: torch.Tensor, G: torch.Tensor | None, lr: float, out: torch.Tensor,
+             absmax: torch.Tensor | None = None) -> torch.Tensor:
+        lib = _lib.load()
+        sfx = mixing._suffix(W)
+        s = _lib.stream_ptr()
+        _lib.check(getattr(lib, f"rm_partial_sum_{sfx}")(W.data_ptr(), self.Lg, self.d,
+                                                         W.stride(0), self.P.data_ptr(), s),
+                   "rm_partial_sum")
+        self.hP.barrier(channel=0)
+        _lib.check(lib.rm_nvls_sum_f64(self.hP.multicast_ptr, self.hM.multicast_ptr, self.c0,
+                                       self.c1, s), "rm_nvls_sum_f64")
+        self.hM.barrier(channel=1)
+        _lib.check(getattr(lib, f"rm_apply_mean_sgd_{sfx}")(
+            self.M.data_ptr(), _lib.ptr(G), out.data_ptr(), self.Lg, self.L, self.d,
+            G.stride(0) if G is not None else 0, out.stride(0), float(lr), _lib.ptr(absmax), s),
+            "rm_apply_mean_sgd")
+        return out
+
+
 class LearnerShardedD1D:
     """D1D step with learners sharded: W' = sum_all(W)/L - lr*G, the global sum by an
     NCCL all-reduce of fp64 column sums, pipelined in column chunks so the

@@ -39,11 +39,23 @@ def main():
     torch.cuda.synchronize()
     dd = (out.double() - ref[b:e].double()).abs().max().item()
     ok_d1d = dd <= 2e-6
+    # NVSwitch multicast variant (our own in-switch reduction kernel)
+    try:
+        nv = D.LearnerShardedD1DNVLS(L, d, ring.Lg, dev)
+        out2 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
+        nv.step(ring.weights, Gl, 0.01, out2)
+        torch.cuda.synchronize()
+        dd2 = (out2.double() - ref[b:e].double()).abs().max().item()
+        ok_d1d = ok_d1d and dd2 <= 2e-6
+        nvls = True
+    except RuntimeError as exc:
+        nvls = str(exc)[:100]
     ring.close()
     res = torch.tensor([int(ok), int(ok_d1d)], device=dev)
     dist.all_reduce(res, op=dist.ReduceOp.MIN)
     if rank == 0:
-        print(json.dumps({"world": world, "rad_bit_identical": bool(res[0]), "d1d_ok": bool(res[1]), "d1d_maxdiff_rank0": dd}), flush=True)
+        print(json.dumps({"world": world, "rad_bit_identical": bool(res[0]), "d1d_ok": bool(res[1]),
+                          "d1d_maxdiff_rank0": dd, "nvls": nvls}), flush=True)
     dist.destroy_process_group()
 
 if __name__ == "__main__":
