@@ -194,10 +194,11 @@ int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, in
 
 /* D1D across ranks through NVSwitch multicast: for columns [c0, c1) sum the
  * ranks' fp64 partial sums in the switch (multimem.ld_reduce) and broadcast the
- * sums to every rank (multimem.st).  P_mc / M_mc: multicast addresses of
- * symmetric buffers (e.g. torch symmetric memory).  Caller orders it with
- * cross-rank barriers. */
-int rm_nvls_sum_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1, void* stream);
+ * means sum/L to every rank (multimem.st); apply with rm_apply_mean_sgd_*(L = 1).
+ * P_mc / M_mc: multicast addresses of symmetric buffers (e.g. torch symmetric
+ * memory).  Caller orders it with cross-rank barriers. */
+int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1, int L,
+                     void* stream);
 
 /* ---- device gradient producer for the reference's quadratic oracle ----
  * (objectives.py:84-90 via simulation.py:226-238):

@@ -270,37 +270,42 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// out[j][c] = S[c]/L - lr*G[j][c]; grid.y = local learner j, grid-stride over
+// 16-byte column vectors (no 64-bit division in the index math).  L == 1 means
+// S already holds the mean (the NVLS path divides once per column).
 template <typename T, bool HAS_G>
 __global__ void __launch_bounds__(256)
     apply_mean_kernel(const double* __restrict__ S, const T* __restrict__ G, T* __restrict__ out,
-                      int Lg, int L, long long d, long long ldg, long long ldo, double lr,
+                      int L, long long d, long long ldg, long long ldo, double lr,
                       unsigned long long* absmax) {
   using E = Elem<T>;
   using A = typename E::acc;
   constexpr int VEC = E::VEC;
   typename E::amax_t amax = 0;
+  const int j = blockIdx.y;
   const long long nvec = (d + VEC - 1) / VEC;
-  const long long total = (long long)Lg * nvec;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(idx / nvec);
-    const long long c = (idx - (long long)j * nvec) * VEC;
+  const T* g = HAS_G ? G + j * ldg : nullptr;
+  T* o = out + j * ldo;
+  const double invL = (double)L;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec;
+       v += (long long)gridDim.x * blockDim.x) {
+    const long long c = v * VEC;
     const bool full = c + VEC <= d;
-    Vec<T> g, y;
-    if (HAS_G && full) g.raw = __ldcs(reinterpret_cast<const uint4*>(G + j * ldg + c));
+    Vec<T> gv, y;
+    if (HAS_G && full) gv.raw = __ldcs(reinterpret_cast<const uint4*>(g + c));
 #pragma unroll
     for (int e = 0; e < VEC; e++) {
       if (!full && c + e >= d) break;
-      A m = (A)__ddiv_rn(S[c + e], (double)L);
+      A m = (A)(L == 1 ? S[c + e] : __ddiv_rn(S[c + e], invL));
       if (HAS_G) {
-        A gv = full ? (A)E::ld(g.e(), e) : (A)E::ld(G + j * ldg + c + e, 0);
-        m = r_sub(m, r_mul((A)lr, gv));
+        A gg = full ? (A)E::ld(gv.e(), e) : (A)E::ld(g + c + e, 0);
+        m = r_sub(m, r_mul((A)lr, gg));
       }
       y.e()[e] = E::st(m);
       amax = E::amax_acc(amax, y.e()[e]);
-      if (!full) out[j * ldo + c + e] = y.e()[e];
+      if (!full) o[c + e] = y.e()[e];
     }
-    if (full) st_cs_v4(out + j * ldo + c, y.raw);
+    if (full) st_cs_v4(o + c, y.raw);
   }
   if (absmax) absmax_publish(absmax, E::amax_bits(amax));
 }
@@ -554,17 +559,20 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
       set_error("invalid apply-mean arguments (rows must be 16-byte aligned)");                 \
       return RM_EINVAL;                                                                         \
     }                                                                                           \
-    long long total = (long long)Lg * d;                                                        \
-    if (total == 0) return 0;                                                                   \
-    long long blocks = (total + 255) / 256;                                                     \
-    if (blocks > 16LL * sm_count(-1)) blocks = 16LL * sm_count(-1);                             \
+    if ((long long)Lg * d == 0) return 0;                                                       \
+    long long nvec = (d + 15) / 16 + 1;                                                         \
+    long long bx = (nvec + 255) / 256;                                                          \
+    long long cap = (4LL * sm_count(-1) + Lg - 1) / (Lg > 0 ? Lg : 1);                          \
+    if (bx > cap) bx = cap;                                                                     \
+    if (bx < 1) bx = 1;                                                                         \
+    dim3 grid((unsigned)bx, (unsigned)Lg);                                                      \
     if (G)                                                                                      \
-      apply_mean_kernel<T, true><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(  \
-          S, reinterpret_cast<const T*>(G), reinterpret_cast<T*>(out), Lg, L, d, ldg, ldo, lr, \
+      apply_mean_kernel<T, true><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(          \
+          S, reinterpret_cast<const T*>(G), reinterpret_cast<T*>(out), L, d, ldg, ldo, lr,      \
           absmax_bits);                                                                         \
     else                                                                                        \
-      apply_mean_kernel<T, false><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>( \
-          S, nullptr, reinterpret_cast<T*>(out), Lg, L, d, ldg, ldo, lr, absmax_bits);         \
+      apply_mean_kernel<T, false><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(         \
+          S, nullptr, reinterpret_cast<T*>(out), L, d, ldg, ldo, lr, absmax_bits);              \
     RM_CHECK_LAUNCH("apply_mean_kernel");                                                       \
     return 0;                                                                                   \
   }
@@ -582,7 +590,7 @@ RM_DEFINE_SHARD(bf16, uint16_t, __nv_bfloat16)
 namespace rm {
 __global__ void __launch_bounds__(256)
     nvls_sum_kernel(const double* __restrict__ P_mc, double* __restrict__ M_mc, long long c0,
-                    long long c1) {
+                    long long c1, double L) {
   constexpr int U = 4;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; c < c1;
@@ -601,23 +609,25 @@ __global__ void __launch_bounds__(256)
     for (int u = 0; u < U; u++) {
       const long long cc = c + u * stride;
       if (cc < c1)
-        asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(M_mc + cc), "d"(v[u])
+        asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(M_mc + cc),
+                     "d"(__ddiv_rn(v[u], L))
                      : "memory");
     }
   }
 }
 }  // namespace rm
 
-extern "C" int rm_nvls_sum_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1,
-                               void* stream) {
-  if (P_mc == nullptr || M_mc == nullptr || c0 < 0 || c1 < c0) {
+extern "C" int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1,
+                                int L, void* stream) {
+  if (P_mc == nullptr || M_mc == nullptr || c0 < 0 || c1 < c0 || L < 1) {
     set_error("invalid NVLS reduction arguments");
     return RM_EINVAL;
   }
   if (c1 == c0) return 0;
   long long blocks = (c1 - c0 + 1023) / 1024;
   if (blocks > 4LL * sm_count(-1)) blocks = 4LL * sm_count(-1);
-  nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(P_mc, M_mc, c0, c1);
+  nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(P_mc, M_mc, c0, c1,
+                                                                             (double)L);
   RM_CHECK_LAUNCH("nvls_sum_kernel");
   return 0;
 }

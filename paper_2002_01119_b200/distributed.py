@@ -273,11 +273,12 @@ class LearnerShardedD1DNVLS:
                                                          W.stride(0), self.P.data_ptr(), s),
                    "rm_partial_sum")
         self.hP.barrier(channel=0)
-        _lib.check(lib.rm_nvls_sum_f64(self.hP.multicast_ptr, self.hM.multicast_ptr, self.c0,
-                                       self.c1, s), "rm_nvls_sum_f64")
+        _lib.check(lib.rm_nvls_mean_f64(self.hP.multicast_ptr, self.hM.multicast_ptr, self.c0,
+                                        self.c1, self.L, s), "rm_nvls_mean_f64")
         self.hM.barrier(channel=1)
+        # M holds the means already (L = 1: no per-learner division)
         _lib.check(getattr(lib, f"rm_apply_mean_sgd_{sfx}")(
-            self.M.data_ptr(), _lib.ptr(G), out.data_ptr(), self.Lg, self.L, self.d,
+            self.M.data_ptr(), _lib.ptr(G), out.data_ptr(), self.Lg, 1, self.d,
             G.stride(0) if G is not None else 0, out.stride(0), float(lr), _lib.ptr(absmax), s),
             "rm_apply_mean_sgd")
         return out
