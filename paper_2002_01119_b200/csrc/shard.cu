@@ -270,42 +270,59 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// out[j][c] = S[c]/L - lr*G[j][c]; grid.y = local learner j, grid-stride over
-// 16-byte column vectors (no 64-bit division in the index math).  L == 1 means
-// S already holds the mean (the NVLS path divides once per column).
+// out[j][c] = S[c]/L - lr*G[j][c] for the Lg local learners.  One thread per
+// 16-byte column vector reads S once and walks the rows (S is d fp64 values,
+// larger than L2, so per-row re-reads would cost Lg x d x 8 bytes).  L == 1
+// means S already holds the mean (the NVLS path divides once per column).
 template <typename T, bool HAS_G>
 __global__ void __launch_bounds__(256)
     apply_mean_kernel(const double* __restrict__ S, const T* __restrict__ G, T* __restrict__ out,
-                      int L, long long d, long long ldg, long long ldo, double lr,
+                      int Lg, int L, long long d, long long ldg, long long ldo, double lr,
                       unsigned long long* absmax) {
   using E = Elem<T>;
   using A = typename E::acc;
   constexpr int VEC = E::VEC;
   typename E::amax_t amax = 0;
-  const int j = blockIdx.y;
   const long long nvec = (d + VEC - 1) / VEC;
-  const T* g = HAS_G ? G + j * ldg : nullptr;
-  T* o = out + j * ldo;
-  const double invL = (double)L;
+  const double dL = (double)L;
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec;
        v += (long long)gridDim.x * blockDim.x) {
     const long long c = v * VEC;
     const bool full = c + VEC <= d;
-    Vec<T> gv, y;
-    if (HAS_G && full) gv.raw = __ldcs(reinterpret_cast<const uint4*>(g + c));
+    A m[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; e++) {
-      if (!full && c + e >= d) break;
-      A m = (A)(L == 1 ? S[c + e] : __ddiv_rn(S[c + e], invL));
-      if (HAS_G) {
-        A gg = full ? (A)E::ld(gv.e(), e) : (A)E::ld(g + c + e, 0);
-        m = r_sub(m, r_mul((A)lr, gg));
-      }
-      y.e()[e] = E::st(m);
-      amax = E::amax_acc(amax, y.e()[e]);
-      if (!full) o[c + e] = y.e()[e];
+      double sv = (full || c + e < d) ? S[c + e] : 0.0;
+      m[e] = (A)(L == 1 ? sv : __ddiv_rn(sv, dL));
     }
-    if (full) st_cs_v4(o + c, y.raw);
+#pragma unroll 4
+    for (int j = 0; j < Lg; j++) {
+      const T* g = HAS_G ? G + j * ldg : nullptr;
+      T* o = out + j * ldo;
+      Vec<T> gv, y;
+      if (HAS_G && full) gv.raw = __ldcs(reinterpret_cast<const uint4*>(g + c));
+#pragma unroll
+      for (int e = 0; e < VEC; e++) {
+        A r = m[e];
+        if (HAS_G) {
+          A gg = full ? (A)E::ld(gv.e(), e) : ((c + e < d) ? (A)E::ld(g + c + e, 0) : (A)0);
+          r = r_sub(r, r_mul((A)lr, gg));
+        }
+        y.e()[e] = E::st(r);
+      }
+      if (full) {
+#pragma unroll
+        for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
+        st_cs_v4(o + c, y.raw);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; e++)
+          if (c + e < d) {
+            amax = E::amax_acc(amax, y.e()[e]);
+            o[c + e] = y.e()[e];
+          }
+      }
+    }
   }
   if (absmax) absmax_publish(absmax, E::amax_bits(amax));
 }
@@ -560,19 +577,15 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
       return RM_EINVAL;                                                                         \
     }                                                                                           \
     if ((long long)Lg * d == 0) return 0;                                                       \
-    long long nvec = (d + 15) / 16 + 1;                                                         \
-    long long bx = (nvec + 255) / 256;                                                          \
-    long long cap = (4LL * sm_count(-1) + Lg - 1) / (Lg > 0 ? Lg : 1);                          \
-    if (bx > cap) bx = cap;                                                                     \
-    if (bx < 1) bx = 1;                                                                         \
-    dim3 grid((unsigned)bx, (unsigned)Lg);                                                      \
+    long long blocks = (d / 4 + 255) / 256 + 1;                                                 \
+    if (blocks > 8LL * sm_count(-1)) blocks = 8LL * sm_count(-1);                               \
     if (G)                                                                                      \
-      apply_mean_kernel<T, true><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(          \
-          S, reinterpret_cast<const T*>(G), reinterpret_cast<T*>(out), L, d, ldg, ldo, lr,      \
+      apply_mean_kernel<T, true><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(  \
+          S, reinterpret_cast<const T*>(G), reinterpret_cast<T*>(out), Lg, L, d, ldg, ldo, lr,  \
           absmax_bits);                                                                         \
     else                                                                                        \
-      apply_mean_kernel<T, false><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(         \
-          S, nullptr, reinterpret_cast<T*>(out), L, d, ldg, ldo, lr, absmax_bits);              \
+      apply_mean_kernel<T, false><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>( \
+          S, nullptr, reinterpret_cast<T*>(out), Lg, L, d, ldg, ldo, lr, absmax_bits);          \
     RM_CHECK_LAUNCH("apply_mean_kernel");                                                       \
     return 0;                                                                                   \
   }
