@@ -295,32 +295,44 @@ __global__ void __launch_bounds__(256)
       double sv = (full || c + e < d) ? S[c + e] : 0.0;
       m[e] = (A)(L == 1 ? sv : __ddiv_rn(sv, dL));
     }
-#pragma unroll 4
-    for (int j = 0; j < Lg; j++) {
-      const T* g = HAS_G ? G + j * ldg : nullptr;
-      T* o = out + j * ldo;
-      Vec<T> gv, y;
-      if (HAS_G && full) gv.raw = __ldcs(reinterpret_cast<const uint4*>(g + c));
+    // rows in batches of 8: all G loads of a batch are in flight before any use
+    constexpr int B = 8;
+    for (int j0 = 0; j0 < Lg; j0 += B) {
+      Vec<T> gv[B];
+      if (HAS_G && full) {
 #pragma unroll
-      for (int e = 0; e < VEC; e++) {
-        A r = m[e];
-        if (HAS_G) {
-          A gg = full ? (A)E::ld(gv.e(), e) : ((c + e < d) ? (A)E::ld(g + c + e, 0) : (A)0);
-          r = r_sub(r, r_mul((A)lr, gg));
-        }
-        y.e()[e] = E::st(r);
+        for (int u = 0; u < B; u++)
+          if (j0 + u < Lg)
+            gv[u].raw = __ldcs(reinterpret_cast<const uint4*>(G + (j0 + u) * ldg + c));
       }
-      if (full) {
 #pragma unroll
-        for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
-        st_cs_v4(o + c, y.raw);
-      } else {
+      for (int u = 0; u < B; u++) {
+        const int j = j0 + u;
+        if (j >= Lg) break;
+        T* o = out + j * ldo;
+        Vec<T> y;
 #pragma unroll
-        for (int e = 0; e < VEC; e++)
-          if (c + e < d) {
-            amax = E::amax_acc(amax, y.e()[e]);
-            o[c + e] = y.e()[e];
+        for (int e = 0; e < VEC; e++) {
+          A r = m[e];
+          if (HAS_G) {
+            A gg = full ? (A)E::ld(gv[u].e(), e)
+                        : ((c + e < d) ? (A)E::ld(G + j * ldg + c + e, 0) : (A)0);
+            r = r_sub(r, r_mul((A)lr, gg));
           }
+          y.e()[e] = E::st(r);
+        }
+        if (full) {
+#pragma unroll
+          for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
+          st_cs_v4(o + c, y.raw);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; e++)
+            if (c + e < d) {
+              amax = E::amax_acc(amax, y.e()[e]);
+              o[c + e] = y.e()[e];
+            }
+        }
       }
     }
   }
@@ -604,7 +616,7 @@ namespace rm {
 __global__ void __launch_bounds__(256)
     nvls_sum_kernel(const double* __restrict__ P_mc, double* __restrict__ M_mc, long long c0,
                     long long c1, double L) {
-  constexpr int U = 4;
+  constexpr int U = 8;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; c < c1;
        c += U * stride) {
@@ -637,8 +649,8 @@ extern "C" int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, in
     return RM_EINVAL;
   }
   if (c1 == c0) return 0;
-  long long blocks = (c1 - c0 + 1023) / 1024;
-  if (blocks > 4LL * sm_count(-1)) blocks = 4LL * sm_count(-1);
+  long long blocks = (c1 - c0 + 2047) / 2048;
+  if (blocks > 8LL * sm_count(-1)) blocks = 8LL * sm_count(-1);
   nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(P_mc, M_mc, c0, c1,
                                                                              (double)L);
   RM_CHECK_LAUNCH("nvls_sum_kernel");
