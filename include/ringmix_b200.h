@@ -236,6 +236,15 @@ int rm_trace_stats_bf16(const uint16_t* W, int L, int64_t d, int64_t ld, const d
                         const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
                         void* stream);
 
+/* Column means M[c] = (numpy pairwise sum over the L learners) / L, fp64, bit-identical
+ * to the mean of rm_mean_sgd_*.  With rm_apply_mean_sgd_*(M, G, out, L, 1, ...) it
+ * splits the D1D step so the average of W_k runs on a side stream while the
+ * gradient of W_{k-1} is produced (north-star (c)). */
+int rm_column_mean_f32(const float* W, int L, int64_t d, int64_t ld, double* M, void* stream);
+int rm_column_mean_f64(const double* W, int L, int64_t d, int64_t ld, double* M, void* stream);
+int rm_column_mean_bf16(const uint16_t* W, int L, int64_t d, int64_t ld, double* M,
+                        void* stream);
+
 /* log1p bit-identical to the host glibc 2.39 (x86-64 FMA build), used by the ziggurat tail. */
 int rm_log1p_f64(const double* x, double* y, int64_t n, void* stream);
 

@@ -56,6 +56,9 @@ _SIGNATURES = {
     "rm_trace_stats_f32": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp], i32),
     "rm_trace_stats_f64": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp], i32),
     "rm_trace_stats_bf16": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp], i32),
+    "rm_column_mean_f32": ([vp, i32, i64, i64, vp, vp], i32),
+    "rm_column_mean_f64": ([vp, i32, i64, i64, vp, vp], i32),
+    "rm_column_mean_bf16": ([vp, i32, i64, i64, vp, vp], i32),
 }
 for _sfx in ("f32", "f64", "bf16"):
     _SIGNATURES[f"rm_ring_mix_sgd_sharded_{_sfx}"] = (

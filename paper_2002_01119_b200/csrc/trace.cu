@@ -132,3 +132,59 @@ extern "C" int rm_trace_stats_bf16(const uint16_t* W, int L, int64_t d, int64_t 
   return trace_stats<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(W), L, d, ld, lam,
                                     wopt, cons_sq, loss_col, avg_loss, stream);
 }
+
+// ---- column mean (numpy pairwise order), the D1D average on its own ----
+// M[c] = pairwise_sum_l W[l, c] / L, bit-identical to the mean the fused
+// D1D tile computes.  Lets the average of W_k run on a side stream while the
+// gradient of W_{k-1} is produced (simulation.step_d1d; north-star (c)), after
+// which rm_apply_mean_sgd_*(M, G, L = 1) finishes the step.
+namespace rm {
+template <typename T>
+__global__ void __launch_bounds__(256)
+    column_mean_kernel(const T* __restrict__ W, int L, long long d, long long ld,
+                       double* __restrict__ M) {
+  using E = Elem<T>;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
+       c += (long long)gridDim.x * blockDim.x) {
+    const T* p = W + c;
+    double res;
+    if (L >= 8 && L <= 128) {
+      const int n8 = L - (L % 8);
+      double r[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) r[k] = (double)E::ld(p + (long long)k * ld, 0);
+      for (int i = 8; i < n8; i += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+          r[k] = __dadd_rn(r[k], (double)E::ld(p + (long long)(i + k) * ld, 0));
+      }
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (int i = n8; i < L; i++) res = __dadd_rn(res, (double)E::ld(p + (long long)i * ld, 0));
+    } else {
+      auto get = [&](int i) { return (double)E::ld(p + (long long)i * ld, 0); };
+      res = pairwise_sum<double>(get, 0, L);
+    }
+    M[c] = __ddiv_rn(res, (double)L);
+  }
+}
+}  // namespace rm
+
+#define RM_DEFINE_COLMEAN(SUFFIX, CT, T)                                                      \
+  extern "C" int rm_column_mean_##SUFFIX(const CT* W, int L, int64_t d, int64_t ld,          \
+                                         double* M, void* stream) {                           \
+    if (W == nullptr || M == nullptr || L < 1 || d < 0 || ld < d) {                           \
+      set_error("invalid column-mean arguments");                                             \
+      return RM_EINVAL;                                                                       \
+    }                                                                                         \
+    if (d == 0) return 0;                                                                     \
+    long long blocks = (d + 255) / 256;                                                       \
+    if (blocks > 16LL * sm_count(-1)) blocks = 16LL * sm_count(-1);                           \
+    column_mean_kernel<T><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(       \
+        reinterpret_cast<const T*>(W), L, d, ld, M);                                          \
+    RM_CHECK_LAUNCH("column_mean_kernel");                                                    \
+    return 0;                                                                                 \
+  }
+RM_DEFINE_COLMEAN(f32, float, float)
+RM_DEFINE_COLMEAN(f64, double, double)
+RM_DEFINE_COLMEAN(bf16, uint16_t, __nv_bfloat16)

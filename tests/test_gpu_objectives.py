@@ -139,3 +139,22 @@ def test_fused_trace_stats_match_reference_formulas(L, d, dtype):
     assert np.isclose(float(avg), oracle.loss(W.mean(axis=1)), rtol=1e-12)
     assert simulation.consensus_distance(X.T) == pytest.approx(
         float(np.sqrt((dev * dev).sum(axis=0).max())), rel=1e-12)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_overlapped_d1d_step_is_bit_identical_to_fused(dtype):
+    """step_d1d with a device oracle (mean of W_k on a side stream || gradient of
+    W_{k-1}) must equal the fused single-pass D1D kernel on the same inputs."""
+    L, d = 16, 50_001
+    oracle = objectives.quadratic_oracle(d, condition_number=5.0, noise_scale=1.0, seed=3)
+    cfg = RunConfig(n_learners=L, iterations=3, lr=0.05, batch_size=2, seed=4, dtype=dtype)
+    st = simulation.initial_state(oracle, cfg)
+    st.weights.copy_(st.weights + torch.randn_like(st.weights) * 0.1)
+    for _ in range(2):
+        new = simulation.step_d1d(st, oracle, cfg)
+        G = oracle.device_gradients(st.prev_weights.T, cfg, st.iteration)
+        ref = mixing.mean_mix_sgd(st.weights.T, G, simulation.learning_rate(cfg, st.iteration))
+        torch.cuda.synchronize()
+        assert torch.equal(new.weights.T, ref)
+        assert simulation.absmax_value(new.absmax_bits) == float(ref.abs().max())
+        st = new

@@ -30,6 +30,30 @@ def main(L, d, reps=5):
     print(json.dumps({"L": L, "d": d, "grad_ms": float(np.median(ts)), "normals_per_s": L * d / (np.median(ts) / 1e3),
                       "bit_exact_spotcheck": ok}), flush=True)
 
+def d1d_overlap(L, d, steps=5):
+    """D1D training step with the device quadratic oracle: sequential (gradient then
+    fused mean+SGD) vs overlapped (mean of W_k on a side stream || gradient of W_{k-1})."""
+    oracle = objectives.quadratic_oracle(d, condition_number=10.0, noise_scale=1.0, seed=1,
+                                         optimum=np.zeros(d))
+    cfg = RunConfig(n_learners=L, iterations=steps, lr=0.01, batch_size=32, seed=5,
+                    dtype="float32")
+    st = simulation.initial_state(oracle, cfg)
+    res = {}
+    for mode in ("sequential", "overlapped", "sequential", "overlapped"):
+        ts = []
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            if mode == "overlapped":
+                st = simulation.step_d1d(st, oracle, cfg)
+            else:
+                st = simulation._gossip_step(st, oracle, cfg, None, stale=True)
+            b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+        res[mode] = float(np.median(ts))
+    print(json.dumps({"L": L, "d": d, "d1d_step_ms": res}), flush=True)
+
+
 if __name__ == "__main__":
     main(16, 1 << 20)
     main(64, 25_557_032)
+    d1d_overlap(64, 25_557_032)
