@@ -374,8 +374,8 @@ static int launch_scalar(const MixArgs& a, long long c_begin, cudaStream_t st) {
   return RM_OK;
 }
 
-static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode) {
-  const int kThreads = mode == kRing ? kRingThreads : kMeanThreads;
+static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode,
+                             int kThreads) {
   size_t stage = (size_t)L * cw * elem * (stage_g ? 2 : 1);
   size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kStages * stage;
   if (mode != kRing) bytes += (size_t)cw * sizeof(double) * (cw <= kThreads / 2 ? 9 : 1);
@@ -427,9 +427,8 @@ static bool make_map(CUtensorMap* m, const void* base, long long d, int L, long 
   return r == CUDA_SUCCESS;
 }
 
-template <typename T, int MODE, bool HAS_G>
+template <typename T, int MODE, bool HAS_G, int NT>
 static int launch_mix(MixArgs a, cudaStream_t st) {
-  constexpr int NT = MODE == kRing ? kRingThreads : kMeanThreads;
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const size_t esz = sizeof(T);
@@ -455,7 +454,11 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     // over every SM several times
     size_t per_col = (size_t)a.L * esz * (stage_g ? 2 : 1);
     cw = VEC;
-    const size_t target = MODE == kRing ? kStageTarget : kMeanStageTarget;
+    size_t target = NT == kRingThreads ? kStageTarget : kMeanStageTarget;
+    if (const char* env = getenv("RINGMIX_STAGE_KB")) {  // tuning override
+      int kb = atoi(env);
+      if (kb >= 4 && kb <= 96) target = (size_t)kb * 1024;
+    }
     while ((size_t)(cw * 2) * per_col <= target && cw * 2 <= 2048) cw *= 2;
     const long long want_tiles = 4LL * sm_count(-1);
     while (cw > VEC && (a.d + cw - 1) / cw < want_tiles && cw * esz > 256) cw /= 2;
@@ -464,7 +467,7 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
       if (v >= VEC && (v & (v - 1)) == 0) cw = v;
     }
     const size_t cap = NT == kRingThreads ? (size_t)max_optin : (size_t)(max_optin / 2 - 1024);
-    if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE) > cap) use_tma = false;
+    if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT) > cap) use_tma = false;
   }
   if (!use_tma) return launch_scalar<T, MODE, HAS_G>(a, 0, st);
 
@@ -489,7 +492,7 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   } else {
     tmG = tmW;
   }
-  size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE);
+  size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT>,
@@ -556,8 +559,21 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
   a.absmax = absmax;
   a.mismatch = mismatch;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (MODE == kSpsgd || G != nullptr) return launch_mix<T, MODE, true>(a, st);
-  return launch_mix<T, MODE, false>(a, st);
+  // ring tiles: one 512-thread CTA per SM by default; RINGMIX_RING_NT=256 runs
+  // two 256-thread CTAs per SM (tuning experiments)
+  static int ring_nt = -1;
+  if (ring_nt < 0) {
+    const char* env = getenv("RINGMIX_RING_NT");
+    ring_nt = (env && atoi(env) == 256) ? 256 : 512;
+  }
+  const bool hg = MODE == kSpsgd || G != nullptr;
+  if (MODE != kRing)
+    return hg ? launch_mix<T, MODE, true, kMeanThreads>(a, st)
+              : launch_mix<T, MODE, false, kMeanThreads>(a, st);
+  if (ring_nt == 256)
+    return hg ? launch_mix<T, MODE, true, 256>(a, st) : launch_mix<T, MODE, false, 256>(a, st);
+  return hg ? launch_mix<T, MODE, true, kRingThreads>(a, st)
+            : launch_mix<T, MODE, false, kRingThreads>(a, st);
 }
 
 }  // namespace rm
