@@ -45,6 +45,7 @@ constexpr int kStages = 3;
 constexpr int kMaxTmaL = 256;   // one TMA row box per tile
 constexpr int kStageTarget = 64 * 1024;      // ring
 constexpr int kMeanStageTarget = 32 * 1024;  // mean (two CTAs per SM)
+constexpr int kSmallRingStageTarget = 24 * 1024;  // ring with L <= 32 (two CTAs per SM)
 
 struct MixArgs {
   const void* W;
@@ -454,7 +455,8 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     // over every SM several times
     size_t per_col = (size_t)a.L * esz * (stage_g ? 2 : 1);
     cw = VEC;
-    size_t target = NT == kRingThreads ? kStageTarget : kMeanStageTarget;
+    size_t target = NT == kRingThreads ? kStageTarget
+                                       : (MODE == kRing ? kSmallRingStageTarget : kMeanStageTarget);
     if (const char* env = getenv("RINGMIX_STAGE_KB")) {  // tuning override
       int kb = atoi(env);
       if (kb >= 4 && kb <= 96) target = (size_t)kb * 1024;
@@ -561,11 +563,16 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // ring tiles: one 512-thread CTA per SM by default; RINGMIX_RING_NT=256 runs
   // two 256-thread CTAs per SM (tuning experiments)
-  static int ring_nt = -1;
-  if (ring_nt < 0) {
+  // Measured on B200 (tools/sweep_ring.py): few learners (L <= 32) stream
+  // better with two 256-thread CTAs per SM and 24 KB stages (16 x 16.8 M fp32:
+  // 6.54 vs 5.87 TB/s); L = 64 / 128 prefer one 512-thread CTA with 64 KB stages.
+  static int ring_nt_env = -1;
+  if (ring_nt_env < 0) {
     const char* env = getenv("RINGMIX_RING_NT");
-    ring_nt = (env && atoi(env) == 256) ? 256 : 512;
+    ring_nt_env = env ? atoi(env) : 0;
   }
+  const int ring_nt = ring_nt_env == 256 || ring_nt_env == 512 ? ring_nt_env
+                                                               : (L <= 32 ? 256 : 512);
   const bool hg = MODE == kSpsgd || G != nullptr;
   if (MODE != kRing)
     return hg ? launch_mix<T, MODE, true, kMeanThreads>(a, st)

@@ -1,7 +1,9 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-SW_KB=0,48,80,96 timeout 300 python tools/sweep_ring.py > gpurun_out/sweep_ring.log 2>&1
-RINGMIX_RING_NT=256 SW_KB=24,32,48 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
-SW_L=16 SW_D=16777216 SW_KB=0,32 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
-SW_L=16 SW_D=16777216 RINGMIX_RING_NT=256 SW_KB=24,32 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
-SW_L=128 SW_D=10788736 SW_KB=0,96 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
-SW_L=128 SW_D=10788736 RINGMIX_RING_NT=256 SW_KB=32,48 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
+: > gpurun_out/sweep_ring.log
+for rep in 1 2 3; do
+SW_KB=48,64,32,48,64 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
+SW_L=16 SW_D=16777216 SW_KB=64,32,16,32 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
+SW_L=16 SW_D=16777216 RINGMIX_RING_NT=256 SW_KB=24,16,32 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
+SW_L=16 SW_D=1048576 SW_KB=64,32,16 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
+SW_L=16 SW_D=1048576 RINGMIX_RING_NT=256 SW_KB=24,16 timeout 300 python tools/sweep_ring.py >> gpurun_out/sweep_ring.log 2>&1
+done
