@@ -32,7 +32,6 @@
 #include "../../include/ringmix_b200.h"
 
 #include <stdlib.h>
-#include <string.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -362,148 +361,6 @@ __global__ void __launch_bounds__(NT, 512 / NT)
 }
 
 // ----------------------------------------------------------------------------
-// Ring tiles with G read straight from HBM (L > 32).
-//
-// Staging only W lets a 64 KB stage hold L x cw with cw = 16384 / L fp32
-// columns (1 KB row segments at L = 64 instead of 512 B when G is staged too).
-// G is used once per element, so it needs no shared memory: each thread loads
-// its G vectors for the NEXT tile into registers (kIpt x 16 B) before computing
-// the current one, hiding the HBM latency behind a whole tile.
-// ----------------------------------------------------------------------------
-constexpr int kIpt = 8;  // vector items per thread per tile
-
-template <typename T>
-__global__ void __launch_bounds__(kRingThreads, 1)
-    mix_ring_ldg_kernel(MixArgs a, const __grid_constant__ CUtensorMap tmW) {
-  using E = Elem<T>;
-  using A = typename E::acc;
-  constexpr int VEC = E::VEC;
-  constexpr int NT = kRingThreads;
-  extern __shared__ __align__(128) unsigned char smem[];
-
-  const int L = a.L;
-  const int cw = a.cw;
-  const int stage_bytes = L * cw * (int)sizeof(T);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  int4* s_tri = reinterpret_cast<int4*>(smem + 128);
-  unsigned char* stages = smem + 128 + ((L * 16 + 127) / 128) * 128;
-  const T* G = static_cast<const T*>(a.G);
-  T* out = static_cast<T*>(a.out);
-  const int tid = threadIdx.x;
-
-  if (tid == 0) {
-    tma_prefetch_desc(&tmW);
-    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  for (int j = tid; j < L; j += NT) {
-    int x0 = a.left[j], x1 = j, x2 = a.right[j], t;
-    if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
-    if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
-    if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
-    s_tri[j] = make_int4(x0, x1, x2, j);
-  }
-  __syncthreads();
-
-  const int box_c = cw < kBox ? cw : kBox;
-  const int lg_bc = __ffs(box_c) - 1;
-  const int box_stride = L << lg_bc;
-  auto sidx = [&](int r, int c) -> int {
-    return (c >> lg_bc) * box_stride + (r << lg_bc) + (c & (box_c - 1));
-  };
-  auto issue = [&](int s, long long t) {
-    const int c0 = (int)(t * cw);
-    unsigned char* st = stages + (size_t)s * stage_bytes;
-    mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
-    for (int cc = 0; cc < cw; cc += box_c)
-      tma_load_2d(st + cc * L * (int)sizeof(T), &tmW, c0 + cc, 0, &full[s]);
-  };
-  const long long first = blockIdx.x, stride = gridDim.x;
-  if (tid == 0) {
-    for (int s = 0; s < kStages; s++) {
-      const long long t = first + s * stride;
-      if (t < a.ntiles) issue(s, t);
-    }
-  }
-
-  const int log2_nv = a.log2_nv;
-  const int nv_full = 1 << log2_nv;
-  const int total = L << log2_nv;  // <= kIpt * NT
-  // G vectors of one tile for this thread (item k = tid + k * NT)
-  auto load_g = [&](long long t, uint4* g) {
-    const long long c0 = t * cw;
-    const int width = (int)min((long long)cw, a.d - c0);
-#pragma unroll
-    for (int k = 0; k < kIpt; k++) {
-      const int idx = tid + k * NT;
-      const int j = idx >> log2_nv, c = (idx & (nv_full - 1)) * VEC;
-      if (idx < total && c + VEC <= width)
-        g[k] = __ldcs(reinterpret_cast<const uint4*>(G + j * a.ldg + c0 + c));
-    }
-  };
-
-  typename E::amax_t amax = 0;
-  const A lr = (A)a.lr;
-  uint4 gnext[kIpt];
-  if (first < a.ntiles) load_g(first, gnext);
-  int it = 0;
-  for (long long t = first; t < a.ntiles; t += stride, ++it) {
-    uint4 gcur[kIpt];
-#pragma unroll
-    for (int k = 0; k < kIpt; k++) gcur[k] = gnext[k];
-    if (t + stride < a.ntiles) load_g(t + stride, gnext);  // in flight during this tile
-
-    const int s = it % kStages;
-    const uint32_t parity = (it / kStages) & 1;
-    const long long c0 = t * cw;
-    const int width = (int)min((long long)cw, a.d - c0);
-    const T* sW = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes);
-    mbar_wait(&full[s], parity);
-#pragma unroll
-    for (int k = 0; k < kIpt; k++) {
-      const int idx = tid + k * NT;
-      if (idx >= total) break;
-      const int j = idx >> log2_nv, c = (idx & (nv_full - 1)) * VEC;
-      if (c >= width) continue;
-      const int4 tri = s_tri[j];
-      Vec<T> va, vb, vc, vg, y;
-      va.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.x, c));
-      vb.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.y, c));
-      vc.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.z, c));
-      const bool fullv = c + VEC <= width;
-      vg.raw = gcur[k];
-      T* dst = out + j * a.ldo + c0 + c;
-#pragma unroll
-      for (int e = 0; e < VEC; e++) {
-        const A gval = fullv ? (A)E::ld(vg.e(), e)
-                             : ((c + e < width) ? (A)E::ld(G + j * a.ldg + c0 + c + e, 0) : (A)0);
-        A m = ring3<A>((A)E::ld(va.e(), e), (A)E::ld(vb.e(), e), (A)E::ld(vc.e(), e));
-        m = r_sub(m, r_mul(lr, gval));
-        y.e()[e] = E::st(m);
-      }
-      if (fullv) {
-#pragma unroll
-        for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
-        st_cs_v4(dst, y.raw);
-      } else {
-#pragma unroll
-        for (int e = 0; e < VEC; e++)
-          if (c + e < width) {
-            amax = E::amax_acc(amax, y.e()[e]);
-            dst[e] = y.e()[e];
-          }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const long long tn = t + (long long)kStages * stride;
-      if (tn < a.ntiles) issue(s, tn);
-    }
-  }
-  if (a.absmax) absmax_publish(a.absmax, E::amax_bits(amax));
-}
-
-// ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
 template <typename T, int MODE, bool HAS_G>
@@ -652,58 +509,6 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   return RM_OK;
 }
 
-template <typename T>
-static int launch_ring_ldg(MixArgs a, cudaStream_t st, bool* handled) {
-  using E = Elem<T>;
-  constexpr int VEC = E::VEC;
-  *handled = false;
-  const size_t esz = sizeof(T);
-  const uintptr_t al = reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.out) |
-                       reinterpret_cast<uintptr_t>(a.G) | (uintptr_t)(a.ldw * esz) |
-                       (uintptr_t)(a.ldo * esz) | (uintptr_t)(a.ldg * esz);
-  if ((al & 15) || a.L <= 32 || a.L > kMaxTmaL || a.d < VEC || a.d >= (1LL << 31) ||
-      encode_fn() == nullptr)
-    return RM_OK;
-  // cw: largest power of two with L * cw / VEC <= kIpt * threads
-  int cw = VEC;
-  while ((long long)a.L * (cw * 2) / VEC <= (long long)kIpt * kRingThreads) cw *= 2;
-  const long long want_tiles = 4LL * sm_count(-1);
-  while (cw > VEC && (a.d + cw - 1) / cw < want_tiles && cw * esz > 256) cw /= 2;
-  static int max_optin = -1;
-  if (max_optin < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  }
-  const size_t smem = 128 + ((size_t)(a.L * 16 + 127) / 128) * 128 +
-                      (size_t)kStages * a.L * cw * esz;
-  if (smem > (size_t)max_optin) return RM_OK;
-  a.cw = cw;
-  a.d_main = a.d;
-  int nv = cw / VEC, lg = 0;
-  while ((1 << lg) < nv) lg++;
-  a.log2_nv = lg;
-  a.ntiles = (a.d + cw - 1) / cw;
-  CUtensorMap tmW;
-  if (!make_map<T>(&tmW, a.W, a.d, a.L, a.ldw, cw < kBox ? cw : kBox, a.L)) {
-    set_error("cuTensorMapEncodeTiled failed for W");
-    return RM_EINVAL;
-  }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(mix_ring_ldg_kernel<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
-    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(mix_ring_ldg_kernel)");
-    attr_set = true;
-  }
-  long long grid = sm_count(-1);
-  if (grid > a.ntiles) grid = a.ntiles;
-  mix_ring_ldg_kernel<T><<<(int)grid, kRingThreads, smem, st>>>(a, tmW);
-  RM_CHECK_LAUNCH("mix_ring_ldg_kernel");
-  *handled = true;
-  return RM_OK;
-}
-
 template <typename T, int MODE>
 static int dispatch(const void* W, const void* G, void* out, int L, long long d, long long ldw,
                     long long ldg, long long ldo, const int32_t* left, const int32_t* right,
@@ -769,16 +574,6 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
   const int ring_nt = ring_nt_env == 256 || ring_nt_env == 512 ? ring_nt_env
                                                                : (L <= 32 ? 256 : 512);
   const bool hg = MODE == kSpsgd || G != nullptr;
-  static int ring_g = -1;  // 1: G by LDG (default for L > 32), 0: G staged (RINGMIX_RING_G=stage)
-  if (ring_g < 0) {
-    const char* env = getenv("RINGMIX_RING_G");
-    ring_g = (env && strcmp(env, "stage") == 0) ? 0 : 1;
-  }
-  if (MODE == kRing && hg && ring_g == 1) {
-    bool handled = false;
-    int rc = launch_ring_ldg<T>(a, st, &handled);
-    if (rc || handled) return rc;
-  }
   if (MODE != kRing)
     return hg ? launch_mix<T, MODE, true, kMeanThreads>(a, st)
               : launch_mix<T, MODE, false, kMeanThreads>(a, st);
