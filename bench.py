@@ -74,7 +74,7 @@ def parse():
     ap.add_argument("--dtype", choices=["float32", "bfloat16", "float64"], default="float32")
     ap.add_argument("--strategy", choices=["rand_psgd", "adpsgd_fixed", "d1d"],
                     default="rand_psgd")
-    ap.add_argument("--layout", choices=["coord", "learner"], default="coord")
+    ap.add_argument("--layout", choices=["coord", "learner", "position"], default="coord")
     ap.add_argument("--d1d-collective", choices=["auto", "nvls", "nccl"], default="auto")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -324,6 +324,14 @@ class Workload:
                 if self.d1d is None:
                     self.d1d = D.LearnerShardedD1D(L, d, e - b, dev)
                     self.d1d_kind = "nccl"
+            elif self.layout == "position":
+                self.pos = D.LearnerShardedRingPos(L, d, dtype)
+                self.rows, self.cols = self.pos.Lg, d
+                for r in range(self.pos.Lg):
+                    self.pos.W[0][r].copy_(torch.randn(d, generator=gen, device=dev,
+                                                       dtype=torch.float32).to(dtype))
+                ident = torch.arange(L, dtype=torch.int32, device=dev)
+                self.ident = ident
             else:
                 self.ring = D.LearnerShardedRing(L, d, dtype)
                 self.rows, self.cols = self.ring.Lg, d
@@ -339,7 +347,8 @@ class Workload:
         self.mean_fn = getattr(self.lib, f"rm_mean_sgd_{sfx}")
         self.words = seeding.entropy_words(SEED, 1)
         self.block = 64
-        self.tabs = [torch.empty((self.block, L), dtype=torch.int32, device=dev)
+        # block + 1 rows: the position layout also needs step k+1's permutation
+        self.tabs = [torch.empty((self.block + 1, L), dtype=torch.int32, device=dev)
                      for _ in range(4)]
         if args.strategy == "adpsgd_fixed":
             self.fixed = tuple(t.contiguous() for t in simulation.fixed_ring_tables(L, dev))
@@ -358,7 +367,7 @@ class Workload:
         if self.args.strategy == "rand_psgd" and (self.tab0 is None or
                                                   k >= self.tab0 + self.block):
             _lib.check(self.lib.rm_perm_tables(self.words.ctypes.data, len(self.words), k,
-                                               self.block, L,
+                                               self.block + 1, L,
                                                *(t.data_ptr() for t in self.tabs), sptr))
             self.tab0 = k
             self.launches["perm"] += 1
@@ -369,7 +378,13 @@ class Workload:
         if ev_pair is not None:
             ev_pair[0].record(stream)
         am = self.amax[k].data_ptr()
-        if self.layout == "learner":
+        if self.layout == "position":
+            if self.args.strategy == "rand_psgd":
+                ik, pn = self.tabs[1][k - self.tab0], self.tabs[0][k + 1 - self.tab0]
+            else:
+                ik = pn = self.ident
+            self.pos.step(ik, pn, self.G, LR, self.amax[k], barrier=False)
+        elif self.layout == "learner":
             if self.uniform:
                 src, dst = self.W[self.cur], self.W[1 - self.cur]
                 self.d1d.step(src, self.G, LR, dst, self.amax[k])
@@ -392,15 +407,18 @@ class Workload:
             ev_pair[1].record(stream)
         if self.layout == "learner" and self.uniform:
             self.launches["mix"] += 3 if self.d1d_kind == "nvls" else 2 * len(self.d1d.chunks)
-        else:
-            self.launches["mix"] += 1
-        if self.layout == "learner" and not self.uniform:
-            self.ring.barrier()              # next step reads this step's rows on peers
+        else:   # learner / position layouts launch a planner + the mix kernel
+            self.launches["mix"] += 2 if self.layout in ("learner", "position") else 1
+        if self.layout in ("learner", "position") and not self.uniform:
+            # next step reads this step's rows on peers
+            (self.ring if self.layout == "learner" else self.pos).barrier()
             self.launches["barrier_allreduce"] += 1
 
     def close(self):
         if self.layout == "learner" and not self.uniform:
             self.ring.close()
+        if self.layout == "position":
+            self.pos.close()
 
 
 def run_ours(args):
@@ -502,7 +520,7 @@ def run_ours(args):
             "config": config_dict(args, ws),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("mix_shard_kernel" if ws > 1 and args.layout == "learner"
+                         "kernel": ("mix_shard_kernel" if ws > 1 and args.layout != "coord"
                                     else "mix_tma_kernel") + f" ({args.strategy}, {args.dtype})",
                          "algorithmic_bytes_per_launch": algo_bytes,
                          "avg_launch_ms": kern_avg_s * 1e3, "peak_source": peak_src},

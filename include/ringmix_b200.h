@@ -176,6 +176,28 @@ int rm_ring_mix_sgd_sharded_bf16(const uint64_t* row_ptrs, const uint16_t* W_loc
                                  const int32_t* plan, double lr,
                                  unsigned long long* absmax_bits, void* stream);
 
+/* RAD in ring-position order ("push" layout): the rank owning positions [g0, g0+Lg)
+ * stores, in slot x, the learner at position x of step k (inv_k[x]).  rm_pos_plan
+ * builds the step's plan (boundary positions g0-1 and g0+Lg are the only remote
+ * reads) and dest[i] = address of learner inv_k[g0+i]'s slot for step k+1
+ * (next_slot_ptrs[perm_next[learner]], any rank).  rm_ring_mix_sgd_pos_* then mixes
+ * in position space (FMA chain in learner-id order: bit-identical to the
+ * single-GPU step) and writes every output straight to its next-step slot. */
+int rm_pos_plan(const int32_t* inv_k, const int32_t* perm_next, int L, int g0, int Lg,
+                const uint64_t* next_slot_ptrs, int32_t* plan, uint64_t* dest, void* stream);
+int rm_ring_mix_sgd_pos_f32(const uint64_t* slot_ptrs, const float* W_local, const float* G_local,
+                            int L, int g0, int Lg, int64_t d, int64_t ldw, int64_t ldg,
+                            const int32_t* plan, const uint64_t* dest, double lr,
+                            unsigned long long* absmax_bits, void* stream);
+int rm_ring_mix_sgd_pos_f64(const uint64_t* slot_ptrs, const double* W_local,
+                            const double* G_local, int L, int g0, int Lg, int64_t d, int64_t ldw,
+                            int64_t ldg, const int32_t* plan, const uint64_t* dest, double lr,
+                            unsigned long long* absmax_bits, void* stream);
+int rm_ring_mix_sgd_pos_bf16(const uint64_t* slot_ptrs, const uint16_t* W_local,
+                             const uint16_t* G_local, int L, int g0, int Lg, int64_t d,
+                             int64_t ldw, int64_t ldg, const int32_t* plan, const uint64_t* dest,
+                             double lr, unsigned long long* absmax_bits, void* stream);
+
 /* D1D across ranks: S[c] = sum of the local rows (fp64), all-reduced by the
  * caller (NCCL), then out[j] = S/L - lr*G[j]. */
 int rm_partial_sum_f32(const float* W, int Lg, int64_t d, int64_t ld, double* S, void* stream);

@@ -86,6 +86,7 @@ struct ShardArgs {
   const int32_t* plan;
   double lr;
   unsigned long long* absmax;
+  const uint64_t* dest;  // optional: output row j goes to dest[j] (local or peer address)
 };
 
 template <typename T, bool HAS_G>
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kShThreads, 1)
         if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
         y.e()[e] = E::st(m);
       }
-      T* dst = out + j * a.ldo + c0 + c;
+      T* dst = (a.dest ? reinterpret_cast<T*>(a.dest[j]) : out + j * a.ldo) + c0 + c;
       if (c + VEC <= width) {
 #pragma unroll
         for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
@@ -448,10 +449,12 @@ template <typename T>
 static int shard_dispatch(const uint64_t* row_ptrs, const T* W_local, const T* G_local, T* out,
                           int L, int row0, int Lg, long long d, long long ldw, long long ldg,
                           long long ldo, const int32_t* plan, double lr,
-                          unsigned long long* absmax, void* stream) {
+                          unsigned long long* absmax, void* stream,
+                          const uint64_t* dest = nullptr) {
   using E = Elem<T>;
   const size_t esz = sizeof(T);
-  if (row_ptrs == nullptr || W_local == nullptr || out == nullptr || plan == nullptr || L < 4 ||
+  if (row_ptrs == nullptr || W_local == nullptr || (out == nullptr && dest == nullptr) ||
+      plan == nullptr || L < 4 ||
       Lg < 1 || row0 < 0 || row0 + Lg > L || d < 1 || Lg > 256) {
     set_error("invalid sharded mix arguments (L=%d row0=%d Lg=%d)", L, row0, Lg);
     return RM_EINVAL;
@@ -473,9 +476,11 @@ static int shard_dispatch(const uint64_t* row_ptrs, const T* W_local, const T* G
   a.row0 = row0;
   a.Lg = Lg;
   a.Rmax = (2 * Lg < L - Lg) ? 2 * Lg : L - Lg;
+  if (dest != nullptr && a.Rmax > 2) a.Rmax = 2;  // position layout: two boundary rows
   a.plan = plan;
   a.lr = lr;
   a.absmax = absmax;
+  a.dest = dest;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (G_local) return launch_shard<T, true>(a, W_local, ldw, G_local, ldg, st);
   return launch_shard<T, false>(a, W_local, ldw, nullptr, ldw, st);
@@ -656,3 +661,78 @@ extern "C" int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, in
   RM_CHECK_LAUNCH("nvls_sum_kernel");
   return 0;
 }
+
+// ---- RAD in ring-position order ("push") ----
+// Storage slot x (owned by the rank with positions [g0, g0+Lg)) holds the
+// learner at ring position x of the CURRENT step's permutation: inv_k[x].
+// The mix of position x reads positions x-1, x, x+1 — all local except the
+// two boundary slots g0-1 and g0+Lg — and the output of learner l = inv_k[x]
+// is written straight to its slot for the NEXT step, p_{k+1}[l], on whichever
+// GPU owns it (P2P store in the epilogue).  The FMA chain still runs in
+// ascending learner id, so the step is bit-identical to the single-GPU step.
+namespace rm {
+__global__ void pos_plan_kernel(const int32_t* __restrict__ inv_k,
+                                const int32_t* __restrict__ perm_next, int L, int g0, int Lg,
+                                const uint64_t* __restrict__ next_slot_ptrs,
+                                int32_t* __restrict__ plan, uint64_t* __restrict__ dest) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int xl = (g0 - 1 + L) % L, xr = (g0 + Lg) % L;
+  const bool local_l = xl >= g0 && xl < g0 + Lg, local_r = xr >= g0 && xr < g0 + Lg;
+  if (i == 0) {
+    // remote boundary positions (0, 1 or 2 of them) in the plan's remote list
+    int R = 0;
+    if (!local_l) plan[1 + R++] = xl;
+    if (!local_r && xr != xl) plan[1 + R++] = xr;
+    plan[0] = R;
+  }
+  if (i >= Lg) return;
+  auto staged = [&](int y) -> int {
+    if (y >= g0 && y < g0 + Lg) return y - g0;
+    if (y == xl && !local_l) return Lg;
+    return Lg + (local_l ? 0 : 1);
+  };
+  const int x = g0 + i;
+  int p[3] = {(x - 1 + L) % L, x, (x + 1) % L};
+  int id[3] = {inv_k[p[0]], inv_k[p[1]], inv_k[p[2]]};
+  // sort by learner id (the reference's FMA order), carrying positions
+  for (int u = 0; u < 2; u++)
+    for (int v = 0; v < 2 - u; v++)
+      if (id[v + 1] < id[v]) {
+        int t = id[v]; id[v] = id[v + 1]; id[v + 1] = t;
+        t = p[v]; p[v] = p[v + 1]; p[v + 1] = t;
+      }
+  int32_t* tri = plan + 1 + 2 * Lg + 4 * i;
+  tri[0] = staged(p[0]);
+  tri[1] = staged(p[1]);
+  tri[2] = staged(p[2]);
+  tri[3] = i;
+  dest[i] = next_slot_ptrs[perm_next[inv_k[x]]];
+}
+}  // namespace rm
+
+extern "C" int rm_pos_plan(const int32_t* inv_k, const int32_t* perm_next, int L, int g0, int Lg,
+                           const uint64_t* next_slot_ptrs, int32_t* plan, uint64_t* dest,
+                           void* stream) {
+  if (inv_k == nullptr || perm_next == nullptr || next_slot_ptrs == nullptr || plan == nullptr ||
+      dest == nullptr || L < 4 || Lg < 1 || g0 < 0 || g0 + Lg > L) {
+    set_error("invalid position-plan arguments (L=%d g0=%d Lg=%d)", L, g0, Lg);
+    return RM_EINVAL;
+  }
+  pos_plan_kernel<<<(Lg + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      inv_k, perm_next, L, g0, Lg, next_slot_ptrs, plan, dest);
+  RM_CHECK_LAUNCH("pos_plan_kernel");
+  return 0;
+}
+
+#define RM_DEFINE_POS(SUFFIX, CT, T)                                                           \
+  extern "C" int rm_ring_mix_sgd_pos_##SUFFIX(                                                 \
+      const uint64_t* slot_ptrs, const CT* W_local, const CT* G_local, int L, int g0, int Lg,  \
+      int64_t d, int64_t ldw, int64_t ldg, const int32_t* plan, const uint64_t* dest,          \
+      double lr, unsigned long long* absmax_bits, void* stream) {                               \
+    return shard_dispatch<T>(slot_ptrs, reinterpret_cast<const T*>(W_local),                  \
+                             reinterpret_cast<const T*>(G_local), nullptr, L, g0, Lg, d, ldw,  \
+                             ldg, ldw, plan, lr, absmax_bits, stream, dest);                   \
+  }
+RM_DEFINE_POS(f32, float, float)
+RM_DEFINE_POS(f64, double, double)
+RM_DEFINE_POS(bf16, uint16_t, __nv_bfloat16)

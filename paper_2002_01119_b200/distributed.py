@@ -234,6 +234,92 @@ class LearnerShardedRing:
         self.peers.close()
 
 
+def _slot_table(layout: "ShardLayout", bases: list[int], ld: int, esz: int,
+                device) -> torch.Tensor:
+    """Device uint64[L]: address of slot/row x on its owning rank."""
+    ptrs = np.empty(layout.L, dtype=np.uint64)
+    for r, (b, e) in enumerate(layout.bounds):
+        for i in range(e - b):
+            ptrs[b + i] = bases[r] + i * ld * esz
+    return torch.from_numpy(ptrs.view(np.int64)).to(device)
+
+
+class LearnerShardedRingPos:
+    """RAD with learners stored in ring-POSITION order (SURVEY §8(e) "push").
+
+    Rank g owns ring positions [g0, g0+Lg); at step k its slot x holds the learner
+    at position x of p_k.  The mix reads only the two boundary slots from the
+    neighbouring ranks, and each output is stored straight into the learner's
+    slot for step k+1 (p_{k+1}[l]) on whichever rank owns it — so a step moves
+    ~Lg (n-1)/n + 2 rows over NVLink per rank instead of the ~2 Lg (n-1)/n the
+    learner-ordered pull needs.  Bit-identical to the single-GPU step.
+    """
+
+    def __init__(self, L: int, d: int, dtype=torch.float32, group=None, device=None):
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed must be initialised")
+        _lib.require_cuda()
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.L, self.d, self.dtype = L, d, dtype
+        self.layout = ShardLayout(L, self.world)
+        self.g0, g1 = self.layout.rows(self.rank)
+        self.Lg = g1 - self.g0
+        if self.Lg < 1 or L < 4:
+            raise ValueError(f"need L >= 4 and a position per rank (L={L}, world={self.world})")
+        self.device = torch.device(device if device is not None else
+                                   f"cuda:{torch.cuda.current_device()}")
+        self.W = [mixing.empty_learner_major(self.Lg, d, dtype, self.device) for _ in range(2)]
+        self.ld = self.W[0].stride(0)
+        self.peers = PeerMappedBuffers(self.W, group)
+        esz = torch.empty((), dtype=dtype).element_size()
+        self.slots = [_slot_table(self.layout, [self.peers.bases[r][p] for r in range(self.world)],
+                                  self.ld, esz, self.device) for p in range(2)]
+        lib = _lib.load()
+        self.plan = torch.empty(lib.rm_shard_plan_ints(self.Lg), dtype=torch.int32,
+                                device=self.device)
+        self.dest = torch.empty(self.Lg, dtype=torch.int64, device=self.device)
+        self._token = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.cur = 0
+        self._fn = getattr(lib, f"rm_ring_mix_sgd_pos_{mixing._suffix(self.W[0])}")
+
+    @property
+    def slots_local(self) -> torch.Tensor:
+        """This rank's slots (learner-major rows, ring-position order of the current step)."""
+        return self.W[self.cur]
+
+    def barrier(self):
+        dist.all_reduce(self._token, group=self.group)
+
+    def step(self, inv_k: torch.Tensor, perm_next: torch.Tensor, G: torch.Tensor | None,
+             lr: float, absmax: torch.Tensor | None = None, barrier: bool = True):
+        """inv_k: device int32[L] (learner at each position, step k); perm_next:
+        device int32[L] (position of each learner at step k+1); G: this rank's
+        gradients in slot order (Lg, d)."""
+        lib = _lib.load()
+        s = _lib.stream_ptr()
+        _lib.check(lib.rm_pos_plan(inv_k.data_ptr(), perm_next.data_ptr(), self.L, self.g0,
+                                   self.Lg, self.slots[1 - self.cur].data_ptr(),
+                                   self.plan.data_ptr(), self.dest.data_ptr(), s), "rm_pos_plan")
+        src = self.W[self.cur]
+        if G is not None:
+            mixing._same(src, G, "G")
+        _lib.check(self._fn(self.slots[self.cur].data_ptr(), src.data_ptr(), _lib.ptr(G), self.L,
+                            self.g0, self.Lg, self.d, self.ld,
+                            G.stride(0) if G is not None else self.ld, self.plan.data_ptr(),
+                            self.dest.data_ptr(), float(lr), _lib.ptr(absmax), s),
+                   "rm_ring_mix_sgd_pos")
+        self.cur = 1 - self.cur
+        if barrier:
+            self.barrier()
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        self.peers.close()
+
+
 class LearnerShardedD1DNVLS:
     """D1D step with learners sharded, the cross-GPU sum done by our own kernel in the
     NVSwitch: every rank writes its fp64 column partial sums into a symmetric buffer;

@@ -119,3 +119,55 @@ def test_d1d_partial_sum_and_apply_reproduce_mean_step(dtype):
     else:
         assert bool((diff <= 2.0**-23 * (ref.double().abs() + scale)).all())
         assert float((out != ref).double().mean()) < 1e-4
+
+
+@pytest.mark.parametrize("L,d,world", [(24, 3001, 4), (64, 2049, 8), (10, 77, 3), (16, 1000, 2)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_position_layout_steps_bit_identical_to_single_gpu(L, d, world, dtype):
+    """RAD in ring-position order, ranks emulated in one process: after every step the
+    slot of position x holds learner inv_{k+1}[x], equal to the single-GPU step."""
+    lay = D.ShardLayout(L, world)
+    g = torch.Generator(device="cuda").manual_seed(L + d)
+    full = mixing.empty_learner_major(L, d, dtype)
+    full.copy_(torch.randn((L, d), generator=g, device="cuda", dtype=torch.float64).to(dtype))
+    Gf = mixing.empty_learner_major(L, d, dtype)
+    Gf.copy_(torch.randn((L, d), generator=g, device="cuda", dtype=torch.float64).to(dtype))
+    K = 4
+    tabs = mixing.permutation_tables(L, 777, 0, K + 1)
+    inv = tabs.inv
+    bufs = [[mixing.empty_learner_major(e - b, d, dtype) for _ in range(2)]
+            for (b, e) in lay.bounds]
+    esz = full.element_size()
+    slots = [D._slot_table(lay, [bufs[r][p].data_ptr() for r in range(world)],
+                           bufs[0][0].stride(0), esz, "cuda") for p in range(2)]
+    inv0 = inv[0].long()
+    for r, (b, e) in enumerate(lay.bounds):
+        bufs[r][0].copy_(full[inv0[b:e]])
+    lib = _lib.load()
+    fn = getattr(lib, f"rm_ring_mix_sgd_pos_{mixing._suffix(full)}")
+    ref = full
+    cur = 0
+    for k in range(K):
+        ik = inv[k].contiguous()
+        pn = tabs.perm[k + 1].contiguous()
+        for r, (b, e) in enumerate(lay.bounds):
+            Lg = e - b
+            plan = torch.empty(lib.rm_shard_plan_ints(Lg), dtype=torch.int32, device="cuda")
+            dest = torch.empty(Lg, dtype=torch.int64, device="cuda")
+            _lib.check(lib.rm_pos_plan(ik.data_ptr(), pn.data_ptr(), L, b, Lg,
+                                       slots[1 - cur].data_ptr(), plan.data_ptr(),
+                                       dest.data_ptr(), _lib.stream_ptr()))
+            Gs = mixing.empty_learner_major(Lg, d, dtype)
+            Gs.copy_(Gf[ik[b:e].long()])          # gradient of the learner in each slot
+            src = bufs[r][cur]
+            _lib.check(fn(slots[cur].data_ptr(), src.data_ptr(), Gs.data_ptr(), L, b, Lg, d,
+                          src.stride(0), Gs.stride(0), plan.data_ptr(), dest.data_ptr(), 0.02,
+                          None, _lib.stream_ptr()))
+            torch.cuda.synchronize()
+        cur = 1 - cur
+        lt, rt = tabs.step(k)
+        ref = mixing.ring_mix_sgd(ref, Gf, 0.02, lt.contiguous(), rt.contiguous())
+        torch.cuda.synchronize()
+        nxt = inv[k + 1].long()
+        for r, (b, e) in enumerate(lay.bounds):
+            assert torch.equal(bufs[r][cur], ref[nxt[b:e]]), (k, r)

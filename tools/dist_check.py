@@ -51,6 +51,25 @@ def main():
     except RuntimeError as exc:
         nvls = str(exc)[:100]
     ring.close()
+    # RAD in ring-position order (push layout): 3 steps vs the single-GPU reference
+    pos = D.LearnerShardedRingPos(L, d, torch.float32)
+    tabs = mixing.permutation_tables(L, 12345, 0, 4, dev)
+    g0, g1 = pos.g0, pos.g0 + pos.Lg
+    pos.W[0].copy_(full[tabs.inv[0][g0:g1].long()])
+    Wr = mixing.empty_learner_major(L, d, torch.float32, dev); Wr.copy_(full)
+    Gfull = mixing.empty_learner_major(L, d, torch.float32, dev).copy_(Gf)
+    ok_pos = True
+    torch.cuda.synchronize(); dist.barrier()
+    for k in range(3):
+        Gs = mixing.empty_learner_major(pos.Lg, d, torch.float32, dev)
+        Gs.copy_(Gf[tabs.inv[k][g0:g1].long()])
+        pos.step(tabs.inv[k].contiguous(), tabs.perm[k + 1].contiguous(), Gs, 0.01)
+        lt, rt = tabs.step(k)
+        Wr = mixing.ring_mix_sgd(Wr, Gfull, 0.01, lt.contiguous(), rt.contiguous())
+        torch.cuda.synchronize()
+        ok_pos &= bool(torch.equal(pos.slots_local, Wr[tabs.inv[k + 1][g0:g1].long()]))
+    pos.close()
+    ok = ok and ok_pos
     res = torch.tensor([int(ok), int(ok_d1d)], device=dev)
     dist.all_reduce(res, op=dist.ReduceOp.MIN)
     if rank == 0:
