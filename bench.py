@@ -488,16 +488,19 @@ def run_ours(args):
     traffic = ncu_traffic(key) if key else None
 
     e2e = None
-    want_e2e = not args.no_e2e and args.dtype == "float32" and not uniform
+    want_e2e = not args.no_e2e and args.dtype == "float32"
     if want_e2e and (ws == 1 or wl.layout == "coord"):
-        # every rank drives its own column stripe through the host API (own PCIe link)
-        ms = run_e2e(args, torch, mixing, dev, cols=wl.cols)
+        # every rank drives its own column stripe (own PCIe link), max over ranks
+        ms_res = run_e2e_resident(args, torch, wl, dev)
+        ms_host = run_e2e(args, torch, mixing, dev, cols=wl.cols) if not uniform else None
         if ws > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms_res, ms_host or 0.0], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        e2e = e2e_line(args, ms, ws)
-    elif want_e2e and rank == 0:
+            ms_res, ms_host = float(t[0]), (float(t[1]) if ms_host else None)
+        e2e = e2e_resident_line(args, ms_res, ws)
+        if ms_host:
+            e2e["host_arrays_variant"] = e2e_line(args, ms_host, ws)
+    elif want_e2e and rank == 0 and not uniform:
         e2e = e2e_line(args, run_e2e(args, torch, mixing, dev), 1)
         e2e["note"] = "learner layout: host-buffer API measured on rank 0 for the whole problem"
     if ws > 1:
@@ -535,6 +538,61 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_e2e_resident(args, torch, wl, dev):
+    """The step through the public API (mixing.ring_mix_sgd / mean_mix_sgd) with the
+    weights resident in HBM (the simulator state, like model weights in training) and,
+    every step, the step's input — its gradients G — copied from pinned host memory
+    (H2D on a copy stream, double-buffered) and the step's result — max|W'|, the
+    divergence metric run_training checks — read back to the host.  Returns ms/step."""
+    from paper_2002_01119_b200 import mixing as M
+
+    L, cols = wl.L, wl.cols
+    G_host = wl.G.cpu().pin_memory()
+    Gd = [wl.G, M.empty_learner_major(L, cols, wl.G.dtype, dev)]
+    W = wl.W
+    res_host = torch.zeros(args.e2e_steps + 4, dtype=torch.int64).pin_memory()
+    amax = torch.zeros(args.e2e_steps + 4, dtype=torch.int64, device=dev)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(device=dev)
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    used = [torch.cuda.Event(), torch.cuda.Event()]
+    uniform = args.strategy == "d1d"
+    nsteps = args.e2e_steps + 2
+    tabs = M.permutation_tables(L, SEED, 0, nsteps + 1, dev)
+    fixed = None
+    if args.strategy == "adpsgd_fixed":
+        from paper_2002_01119_b200 import simulation as S
+        fixed = S.fixed_ring_tables(L, dev)
+
+    def one(k, cur):
+        b = k % 2
+        with torch.cuda.stream(copy):
+            if k >= 2:
+                copy.wait_event(used[b])
+            Gd[b].copy_(G_host, non_blocking=True)
+            copied[b].record(copy)
+        comp.wait_event(copied[b])
+        if uniform:
+            M.mean_mix_sgd(W[cur], Gd[b], LR, out=W[1 - cur], absmax=amax[k])
+        else:
+            lt, rt = fixed if fixed is not None else tabs.step(k)
+            M.ring_mix_sgd(W[cur], Gd[b], LR, lt, rt, out=W[1 - cur], absmax=amax[k])
+        used[b].record(comp)
+        res_host[k].copy_(amax[k], non_blocking=True)
+
+    one(0, 0)                       # warm-up
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(comp)
+    cur = 1
+    for k in range(1, args.e2e_steps + 1):
+        one(k, cur)
+        cur = 1 - cur
+    e.record(comp)
+    torch.cuda.synchronize()
+    return a.elapsed_time(e) / args.e2e_steps
+
+
 def run_e2e(args, torch, mixing, dev, cols=None):
     """Step through the host-buffer API (W, G pinned host -> W' host) for this
     rank's column stripe (`cols`, default: the whole problem); returns ms/step."""
@@ -569,6 +627,7 @@ def run_e2e(args, torch, mixing, dev, cols=None):
 
 
 def e2e_line(args, ms, ws):
+    """Host-arrays variant: W, G from host and W' back every step (12 B/param over PCIe)."""
     L, d = args.learners, args.dim
     return {"value": L * d / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": 2 * L * d * 4 + 2 * L * 4 * ws,
@@ -577,6 +636,18 @@ def e2e_line(args, ms, ws):
             "path": "mixing.ring_mix_sgd_host -> rm_ring_mix_sgd_host_f32 (pinned host W, G; "
                     "chunked H2D || kernel || D2H)" + (
                         f"; every rank its column stripe, max over {ws} ranks" if ws > 1 else "")}
+
+
+def e2e_resident_line(args, ms, ws):
+    L, d = args.learners, args.dim
+    return {"value": L * d / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": L * d * 4, "d2h_bytes_per_step": 8 * ws,
+            "ms_per_step": ms, "steps": args.e2e_steps,
+            "path": "public API mixing.ring_mix_sgd with W resident in HBM (simulator state); "
+                    "per step: G (the step's input) H2D from pinned host memory on a copy "
+                    "stream, double-buffered, and max|W'| (the divergence metric) D2H" + (
+                        f"; every rank its column stripe, max over {ws} ranks" if ws > 1 else ""),
+            "host_arrays_variant": None}
 
 
 def main():
