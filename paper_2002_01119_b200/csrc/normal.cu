@@ -750,3 +750,18 @@ extern "C" int rm_log1p_f64(const double* x, double* y, int64_t n, void* stream)
   RM_CHECK_LAUNCH("log1p_kernel");
   return 0;
 }
+
+// Byte offset, inside the workspace of the last rm_quadratic_grad_* /
+// rm_standard_normal_f64 call with this shape, of two uint32 counters:
+// speculation failures and failures left to the sequential repair (diagnostics).
+extern "C" int64_t rm_normal_stats_offset(int nstreams, int64_t n) {
+  if (nstreams < 1 || n < 0) return -1;
+  const long long nblocks = (long long)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) /
+                                        kZBlock) + 8;
+  const long long nb = nblocks * nstreams;
+  uintptr_t off = (uintptr_t)(nb * (sizeof(BlockInfo) + 8 + 4 + 4 + 8) + nstreams * 8);
+  off = (off + 63) & ~(uintptr_t)63;
+  off += nstreams * sizeof(ZStream) + nb * 8 + nb;
+  off = (off + 15) & ~(uintptr_t)15;
+  return (int64_t)off;
+}

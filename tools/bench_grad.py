@@ -53,7 +53,26 @@ def d1d_overlap(L, d, steps=5):
     print(json.dumps({"L": L, "d": d, "d1d_step_ms": res}), flush=True)
 
 
+
+
+def failure_stats(L, d):
+    from paper_2002_01119_b200 import _lib
+    oracle = objectives.quadratic_oracle(d, condition_number=10.0, noise_scale=1.0, seed=1,
+                                         optimum=np.zeros(d))
+    Phi = mixing.empty_learner_major(L, d, torch.float32, torch.device("cuda")); Phi.normal_()
+    cfg = RunConfig(n_learners=L, iterations=1, lr=0.01, batch_size=32, seed=5, dtype="float32")
+    oracle.device_gradients(Phi, cfg, 3)
+    torch.cuda.synchronize()
+    off = _lib.load().rm_normal_stats_offset(L, d)
+    cnt = oracle._ws[off:off + 8].cpu().numpy().view(np.uint32)
+    nblocks = int((1.04 * d + 64.0 * np.sqrt(d + 1.0)) / 256) + 8
+    print(json.dumps({"L": L, "d": d, "blocks": L * nblocks, "spec_failures": int(cnt[0]),
+                      "left_to_sequential": int(cnt[1])}), flush=True)
+
+
 if __name__ == "__main__":
     main(16, 1 << 20)
     main(64, 25_557_032)
     d1d_overlap(64, 25_557_032)
+    failure_stats(16, 1 << 20)
+    failure_stats(64, 25_557_032)
