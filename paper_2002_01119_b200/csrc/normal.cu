@@ -617,8 +617,10 @@ extern "C" int64_t rm_normal_workspace_bytes(int nstreams, int64_t n) {
   const long long nblocks = (long long)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) /
                                         kZBlock) + 8;
   const long long nb = nblocks * nstreams;
-  return (int64_t)(nb * (sizeof(BlockInfo) + 4 + 4 + 8 + 1 + 8) +
-                   nstreams * (8 + sizeof(ZStream)) + 16 + 1024);
+  // per block: info, offs (8), entry (4), tcount (4), bad (8), left (8), merged (1);
+  // per stream: total (8), seed; alignment padding and the two counters
+  return (int64_t)(nb * (sizeof(BlockInfo) + 8 + 4 + 4 + 8 + 8 + 1) +
+                   nstreams * (8 + sizeof(ZStream)) + 64 + 16 + 16 + 1024);
 }
 
 // Quadratic-oracle gradients for all learners of step k (see header).

@@ -158,3 +158,12 @@ def test_overlapped_d1d_step_is_bit_identical_to_fused(dtype):
         assert torch.equal(new.weights.T, ref)
         assert simulation.absmax_value(new.absmax_bits) == float(ref.abs().max())
         st = new
+
+
+def test_normal_workspace_covers_its_layout():
+    """The workspace size reported by the library covers every region the kernels
+    use (the counters sit at the end of the layout)."""
+    from paper_2002_01119_b200 import _lib
+    lib = _lib.load()
+    for L, d in [(1, 1), (3, 77), (16, 1 << 20), (64, 25_557_032)]:
+        assert lib.rm_normal_stats_offset(L, d) + 8 <= lib.rm_normal_workspace_bytes(L, d)
