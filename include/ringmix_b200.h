@@ -229,6 +229,13 @@ int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1, i
  * prefix_words = entropy words of (seed, TAG_GRADIENT); lam/wopt: device fp64[d];
  * Phi/G: learner-major (L, d).  workspace: device, >= rm_normal_workspace_bytes(L, d). */
 int64_t rm_normal_workspace_bytes(int nstreams, int64_t n);
+/* Larger workspace that also keeps the speculative ziggurat blocks (~8.4 B per
+ * normal): with it the output pass is a coalesced copy instead of a re-draw.
+ * Any workspace_bytes >= this selects that path; the bits are identical. */
+int64_t rm_normal_workspace_bytes_fast(int nstreams, int64_t n);
+/* Byte offset inside the workspace of the generator's repair counters
+ * (uint32 blocks_rejected_by_merge, uint32 blocks_left_for_sequential_repair). */
+int64_t rm_normal_stats_offset(int nstreams, int64_t n);
 int rm_quadratic_grad_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k, int L,
                           int64_t d, const float* Phi, int64_t ldp, const double* lam,
                           const double* wopt, double noise_sd, float* G, int64_t ldg,

@@ -46,6 +46,7 @@ _SIGNATURES = {
     "rm_shard_plan_ints": ([i32], i32),
     "rm_shard_plan": ([vp, vp, i32, i32, i32, vp, vp], i32),
     "rm_normal_workspace_bytes": ([i32, i64], i64),
+    "rm_normal_workspace_bytes_fast": ([i32, i64], i64),
     "rm_normal_stats_offset": ([i32, i64], i64),
     "rm_quadratic_grad_f32": ([vp, i32, u64, i32, i64, vp, i64, vp, vp, dbl, vp, i64, vp, i64, vp],
                               i32),

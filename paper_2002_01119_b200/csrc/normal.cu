@@ -293,7 +293,8 @@ __global__ void zig_seed_kernel(ZArgs a, ZStream* __restrict__ seeds) {
 }
 
 __global__ void __launch_bounds__(128)
-    zig_spec_kernel(ZArgs a, const ZStream* __restrict__ seeds, BlockInfo* __restrict__ info) {
+    zig_spec_kernel(ZArgs a, const ZStream* __restrict__ seeds, BlockInfo* __restrict__ info,
+                    double* __restrict__ scratch) {
   __shared__ ZigTables T;
   load_tables(&T);
   __syncthreads();
@@ -306,6 +307,9 @@ __global__ void __launch_bounds__(128)
   ZGen g{z_jump(zs, (uint64_t)b * kZBlock), zs.inc};
   uint32_t att = 0, outs = 0, count = 0;
   uint32_t pos = 0;  // relative draw index of the next attempt
+  // speculative outputs are kept (fast path): 16-byte stores of output pairs
+  double* slot = scratch ? scratch + ((long long)stream * a.nblocks + b) * kZBlock : nullptr;
+  double pend = 0.0;
   while (pos < (uint32_t)kZBlock) {
     double x;
     int extra;
@@ -314,9 +318,16 @@ __global__ void __launch_bounds__(128)
       att |= 1u << pos;
       if (ok) outs |= 1u << pos;
     }
+    if (ok && slot) {
+      if (count & 1u)
+        *reinterpret_cast<double2*>(slot + count - 1) = make_double2(pend, x);
+      else
+        pend = x;
+    }
     count += ok ? 1u : 0u;
     pos += 1 + extra;
   }
+  if (slot && (count & 1u)) slot[count - 1] = pend;
   info[(long long)stream * a.nblocks + b] = BlockInfo{att, outs, pos, count};
 }
 
@@ -353,6 +364,7 @@ __global__ void __launch_bounds__(128)
     zig_repair_par_kernel(ZArgs a, const ZStream* __restrict__ seeds,
                           const BlockInfo* __restrict__ info, uint32_t* __restrict__ entry,
                           uint32_t* __restrict__ tcount, const uint8_t* __restrict__ merged,
+                          uint8_t* __restrict__ valid,
                           const uint32_t* __restrict__ nbad, const uint64_t* __restrict__ bad,
                           uint32_t* __restrict__ nleft, uint64_t* __restrict__ left) {
   __shared__ ZigTables T;
@@ -388,6 +400,7 @@ __global__ void __launch_bounds__(128)
   if (e2 < 32 && ((nx.att >> e2) & 1u)) {
     tcount[gid + 1] = nx.count - __popc(nx.outs & ((1u << e2) - 1u));
   } else {
+    valid[gid + 1] = 0;
     left[atomicAdd(nleft, 1u)] = (uint64_t)(gid + 1);
   }
 }
@@ -397,7 +410,8 @@ __global__ void __launch_bounds__(128)
 // true entry until the path merges again with the next block's speculation.
 __global__ void zig_repair_kernel(ZArgs a, const ZStream* __restrict__ seeds,
                                   const BlockInfo* __restrict__ info, uint32_t* __restrict__ entry,
-                                  uint32_t* __restrict__ tcount, const uint32_t* __restrict__ nbad,
+                                  uint32_t* __restrict__ tcount, const uint8_t* __restrict__ merged,
+                                  uint8_t* __restrict__ valid, const uint32_t* __restrict__ nbad,
                                   const uint64_t* __restrict__ bad) {
   __shared__ ZigTables T;
   const uint32_t nb = *nbad;
@@ -430,14 +444,18 @@ __global__ void zig_repair_kernel(ZArgs a, const ZStream* __restrict__ seeds,
         pos += 1 + extra;
       }
       tcount[gid] = count;
+      valid[gid] = 0;
       next_b = b;
       if (b + 1 >= a.nblocks) return;
       const long long g2 = gid + 1;
       const uint32_t e2 = pos - kZBlock;
       entry[g2] = e2;
       const BlockInfo nx = info[g2];
-      if (e2 < 32 && ((nx.att >> e2) & 1u)) {
+      // stop only at a block the merge pass accepted (blocks it rejected may
+      // carry successor data from a parallel repair with a stale entry)
+      if (merged[g2] && e2 < 32 && ((nx.att >> e2) & 1u)) {
         tcount[g2] = nx.count - __popc(nx.outs & ((1u << e2) - 1u));
+        valid[g2] = 1;
         break;  // merged again; later blocks keep their speculative entries
       }
       b = b + 1;
@@ -582,6 +600,87 @@ __global__ void __launch_bounds__(kZGenThreads)
   }
 }
 
+// ---- fast path: the speculative outputs are kept in a scratch buffer ----
+// One warp per raw block copies its (merged) speculative outputs, skipping the
+// ones before the true entry, and writes G for them — coalesced reads of the
+// scratch and of Phi / lam / w*, coalesced G stores.  Blocks whose speculation
+// did not merge are regenerated by zig_fixup_kernel (~2e-4 of the blocks).
+template <typename T>
+__device__ __forceinline__ void emit_grad(const ZArgs& a, int stream, long long c, double z,
+                                          const T* __restrict__ Phi, long long ldp,
+                                          const double* __restrict__ lam,
+                                          const double* __restrict__ wopt, double sd,
+                                          T* __restrict__ G, long long ldg,
+                                          double* __restrict__ Z, long long ldz) {
+  using E = Elem<T>;
+  if (Z) Z[stream * ldz + c] = z;
+  if (G) {
+    // objectives.py:87-90: gradient(w) + noise_sd * z, gradient = lam * (w - w*)
+    const double w = (double)E::ld(Phi + stream * ldp + c, 0);
+    const double gr = __dmul_rn(lam[c], __dsub_rn(w, wopt[c]));
+    G[stream * ldg + c] = E::st((typename E::acc)__dadd_rn(gr, __dmul_rn(sd, z)));
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    zig_copy_kernel(ZArgs a, const BlockInfo* __restrict__ info,
+                    const uint32_t* __restrict__ entry, const uint32_t* __restrict__ tcount,
+                    const unsigned long long* __restrict__ offs, const uint8_t* __restrict__ valid,
+                    const double* __restrict__ scratch, const T* __restrict__ Phi, long long ldp,
+                    const double* __restrict__ lam, const double* __restrict__ wopt, double sd,
+                    T* __restrict__ G, long long ldg, double* __restrict__ Z, long long ldz) {
+  const long long gid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gid >= (long long)a.nstreams * a.nblocks) return;
+  if (!valid[gid]) return;
+  const unsigned long long base = offs[gid];
+  if (base >= (unsigned long long)a.n) return;
+  const int stream = (int)(gid / a.nblocks);
+  const uint32_t e = entry[gid];
+  const uint32_t skip = __popc(info[gid].outs & ((1u << e) - 1u));
+  const uint32_t cnt = tcount[gid];
+  const double* src = scratch + gid * kZBlock + skip;
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const long long c = (long long)base + i;
+    if (c < a.n) emit_grad<T>(a, stream, c, src[i], Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128)
+    zig_fixup_kernel(ZArgs a, const ZStream* __restrict__ seeds, const uint32_t* __restrict__ entry,
+                     const unsigned long long* __restrict__ offs, const uint8_t* __restrict__ valid,
+                     const uint32_t* __restrict__ nbad, const uint64_t* __restrict__ bad,
+                     const uint32_t* __restrict__ nleft, const uint64_t* __restrict__ left,
+                     const T* __restrict__ Phi, long long ldp, const double* __restrict__ lam,
+                     const double* __restrict__ wopt, double sd, T* __restrict__ G, long long ldg,
+                     double* __restrict__ Z, long long ldz) {
+  __shared__ ZigTables Tb;
+  const uint32_t n1 = *nbad, n2 = *nleft;
+  if (blockIdx.x * blockDim.x >= n1 + n2) return;  // CTA-uniform
+  load_tables(&Tb);
+  __syncthreads();
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n1 + n2) return;
+  const long long gid = (long long)(i < n1 ? bad[i] : left[i - n1]);
+  if (valid[gid]) return;
+  unsigned long long o = offs[gid];
+  if (o >= (unsigned long long)a.n) return;
+  const int stream = (int)(gid / a.nblocks);
+  const int b = (int)(gid % a.nblocks);
+  const ZStream zs = seeds[stream];
+  uint32_t pos = entry[gid];
+  ZGen g{z_jump(zs, (uint64_t)b * kZBlock + pos), zs.inc};
+  while (pos < (uint32_t)kZBlock && o < (unsigned long long)a.n) {
+    double x;
+    int extra;
+    if (z_attempt(Tb, g, g.next64(), &x, &extra))
+      emit_grad<T>(a, stream, (long long)o++, x, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+    pos += 1 + extra;
+  }
+}
+
 static bool g_jump_ready[64];
 
 static int ensure_jump_tables() {
@@ -619,8 +718,18 @@ extern "C" int64_t rm_normal_workspace_bytes(int nstreams, int64_t n) {
   const long long nb = nblocks * nstreams;
   // per block: info, offs (8), entry (4), tcount (4), bad (8), left (8), merged (1);
   // per stream: total (8), seed; alignment padding and the two counters
-  return (int64_t)(nb * (sizeof(BlockInfo) + 8 + 4 + 4 + 8 + 8 + 1) +
+  return (int64_t)(nb * (sizeof(BlockInfo) + 8 + 4 + 4 + 8 + 8 + 1 + 1) +
                    nstreams * (8 + sizeof(ZStream)) + 64 + 16 + 16 + 1024);
+}
+
+// Workspace for the fast path: the base layout plus the speculative outputs of
+// every raw block (kZBlock doubles each, ~8.4 bytes per normal).
+extern "C" int64_t rm_normal_workspace_bytes_fast(int nstreams, int64_t n) {
+  const int64_t base = rm_normal_workspace_bytes(nstreams, n);
+  if (base < 0) return base;
+  const long long nblocks = (long long)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) /
+                                        kZBlock) + 8;
+  return base + 256 + nblocks * nstreams * kZBlock * (int64_t)sizeof(double);
 }
 
 // Quadratic-oracle gradients for all learners of step k (see header).
@@ -678,6 +787,15 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
   ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 15) & ~(uintptr_t)15);
   uint32_t* nbad = reinterpret_cast<uint32_t*>(ws);
   uint32_t* nleft = nbad + 1;
+  ws += 16;
+  // validity of the speculative outputs per block (1 = merged at its true entry)
+  uint8_t* valid = reinterpret_cast<uint8_t*>(ws);
+  ws += nb;
+  double* scratch = nullptr;
+  if (workspace_bytes >= rm_normal_workspace_bytes_fast(nstreams, n)) {
+    ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255);
+    scratch = reinterpret_cast<double*>(ws);
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemsetAsync(nbad, 0, 8, st);
   if (e != cudaSuccess) return fail_cuda(e, "cudaMemsetAsync");
@@ -685,23 +803,35 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
   const long long grid = (nb + threads - 1) / threads;
   zig_seed_kernel<<<(nstreams + 63) / 64, 64, 0, st>>>(a, seeds);
   RM_CHECK_LAUNCH("zig_seed_kernel");
-  zig_spec_kernel<<<(int)grid, threads, 0, st>>>(a, seeds, info);
+  zig_spec_kernel<<<(int)grid, threads, 0, st>>>(a, seeds, info, scratch);
   RM_CHECK_LAUNCH("zig_spec_kernel");
   zig_merge_kernel<<<(int)grid, threads, 0, st>>>(a, info, entry, tcount, merged, nbad, bad);
   RM_CHECK_LAUNCH("zig_merge_kernel");
+  e = cudaMemcpyAsync(valid, merged, nb, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return fail_cuda(e, "cudaMemcpyAsync(valid)");
   // isolated failures in parallel (grid sized for the worst case; idle CTAs exit at once)
   zig_repair_par_kernel<<<(int)grid, threads, 0, st>>>(a, seeds, info, entry, tcount, merged,
-                                                        nbad, bad, nleft, left);
+                                                        valid, nbad, bad, nleft, left);
   RM_CHECK_LAUNCH("zig_repair_par_kernel");
-  zig_repair_kernel<<<(nstreams + 31) / 32, 32, 0, st>>>(a, seeds, info, entry, tcount, nleft,
-                                                         left);
+  zig_repair_kernel<<<(nstreams + 31) / 32, 32, 0, st>>>(a, seeds, info, entry, tcount, merged,
+                                                         valid, nleft, left);
   RM_CHECK_LAUNCH("zig_repair_kernel");
   zig_scan_kernel<<<nstreams, 1024, 0, st>>>(a, tcount, offs, total);
   RM_CHECK_LAUNCH("zig_scan_kernel");
-  const long long groups = (a.nblocks + kZGenThreads - 1) / kZGenThreads;
-  zig_gen_kernel<T><<<(int)(groups * nstreams), kZGenThreads, 0, st>>>(
-      a, seeds, entry, tcount, offs, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
-  RM_CHECK_LAUNCH("zig_gen_kernel");
+  if (scratch) {
+    zig_copy_kernel<T><<<(int)((nb * 32 + 255) / 256), 256, 0, st>>>(
+        a, info, entry, tcount, offs, valid, scratch, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+    RM_CHECK_LAUNCH("zig_copy_kernel");
+    zig_fixup_kernel<T><<<(int)((2 * nb + 127) / 128), 128, 0, st>>>(
+        a, seeds, entry, offs, valid, nbad, bad, nleft, left, Phi, ldp, lam, wopt, sd, G, ldg, Z,
+        ldz);
+    RM_CHECK_LAUNCH("zig_fixup_kernel");
+  } else {
+    const long long groups = (a.nblocks + kZGenThreads - 1) / kZGenThreads;
+    zig_gen_kernel<T><<<(int)(groups * nstreams), kZGenThreads, 0, st>>>(
+        a, seeds, entry, tcount, offs, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+    RM_CHECK_LAUNCH("zig_gen_kernel");
+  }
   return 0;
 }
 

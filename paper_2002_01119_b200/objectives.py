@@ -17,14 +17,35 @@ out of scope.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
 from . import _lib, mixing, seeding
 
 
+def normal_workspace_bytes(nstreams: int, n: int, device) -> int:
+    """Workspace size for the device normal generator.
+
+    The fast layout keeps every speculative ziggurat block (~8.4 B per normal) so
+    the output pass is a coalesced copy; it is used when it fits in a quarter of
+    the free HBM (``RINGMIX_NORMAL_FAST=0`` forces the compact layout, which
+    regenerates the draws in the output pass).  Both give identical bits.
+    """
+    lib = _lib.load()
+    base = int(lib.rm_normal_workspace_bytes(nstreams, n))
+    if os.environ.get("RINGMIX_NORMAL_FAST", "1") != "0":
+        fast = int(lib.rm_normal_workspace_bytes_fast(nstreams, n))
+        with torch.cuda.device(device):
+            free = torch.cuda.mem_get_info()[0]
+        if fast <= free // 4:
+            return fast
+    return base
+
+
 def _normal_workspace(nstreams: int, n: int, device) -> torch.Tensor:
-    nbytes = int(_lib.load().rm_normal_workspace_bytes(nstreams, n))
+    nbytes = normal_workspace_bytes(nstreams, n, device)
     return torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
 
 
@@ -93,6 +114,8 @@ class QuadraticObjective:
         G = mixing.empty_learner_major(L, d, Phi.dtype, Phi.device)
         need = int(_lib.load().rm_normal_workspace_bytes(L, d))
         if self._ws is None or self._ws.numel() < need or self._ws.device != Phi.device:
+            self._ws = None
+            need = normal_workspace_bytes(L, d, Phi.device)
             self._ws = torch.empty(need, dtype=torch.uint8, device=Phi.device)
         lam, opt = self._lam.to(Phi.device), self._opt.to(Phi.device)
         words = seeding.entropy_words(cfg.seed, seeding.TAG_GRADIENT)

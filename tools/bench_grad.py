@@ -70,7 +70,32 @@ def failure_stats(L, d):
                       "left_to_sequential": int(cnt[1])}), flush=True)
 
 
+def compare_paths(L, d, reps=3):
+    """Fast (scratch-copy) vs compact (re-draw) generator layouts: identical bits, timing."""
+    Phi = mixing.empty_learner_major(L, d, torch.float32, torch.device("cuda")); Phi.normal_()
+    cfg = RunConfig(n_learners=L, iterations=1, lr=0.01, batch_size=32, seed=5, dtype="float32")
+    out, ms = {}, {}
+    for mode in ("1", "0"):
+        os.environ["RINGMIX_NORMAL_FAST"] = mode
+        oracle = objectives.quadratic_oracle(d, condition_number=10.0, noise_scale=1.0, seed=1,
+                                             optimum=np.zeros(d))
+        oracle.device_gradients(Phi, cfg, 0)
+        ts = []
+        for k in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); G = oracle.device_gradients(Phi, cfg, 7); b.record()
+            torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+        out[mode], ms[mode] = G, float(np.median(ts))
+        del oracle
+        torch.cuda.empty_cache()
+    os.environ["RINGMIX_NORMAL_FAST"] = "1"
+    print(json.dumps({"L": L, "d": d, "fast_ms": ms["1"], "compact_ms": ms["0"],
+                      "identical": bool(torch.equal(out["1"], out["0"]))}), flush=True)
+
+
 if __name__ == "__main__":
+    compare_paths(16, 1 << 20)
+    compare_paths(64, 25_557_032)
     main(16, 1 << 20)
     main(64, 25_557_032)
     d1d_overlap(64, 25_557_032)
