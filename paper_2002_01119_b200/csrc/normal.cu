@@ -279,6 +279,42 @@ __device__ __forceinline__ bool z_attempt(const ZigTables& T, ZGen& g, uint64_t 
   return false;
 }
 
+// The slow part of a ziggurat attempt (the fast test `rabs < ki[idx]` failed):
+// `u0` is the next draw of the stream (already taken), further draws come from
+// g.  Same arithmetic as z_attempt; *extra = further draws consumed.
+__device__ __noinline__ bool z_slow(const ZigTables& T, ZGen& g, uint64_t u0, int idx,
+                                    uint64_t rabs, double* x, int* extra) {
+  const double v = *x;
+  if (idx == 0) {
+    const double R = 3.6541528853610087963519472518;
+    const double INV_R = 0.27366123732975827203338247596;
+    uint64_t u = u0;
+    *extra = 0;
+    for (;;) {
+      const double d0 = __dmul_rn((double)(u >> 11), 1.0 / 9007199254740992.0);
+      double xx = __dmul_rn(-INV_R, glibc_log1p(-d0));
+      double yy = -glibc_log1p(-g.next_double());
+      *extra += 2;
+      if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+        *x = ((rabs >> 8) & 1) ? -__dadd_rn(R, xx) : __dadd_rn(R, xx);
+        return true;
+      }
+      u = g.next64();
+    }
+  }
+  const double f0 = T.fi[idx - 1], f1 = T.fi[idx];
+  const double u = __dmul_rn((double)(u0 >> 11), 1.0 / 9007199254740992.0);
+  const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(f0, f1), u), f1);
+  *extra = 1;
+  return lhs < exp(__dmul_rn(__dmul_rn(-0.5, v), v));
+}
+
+__device__ __forceinline__ void st_v4_f64(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
+               : "memory");
+}
+
 struct BlockInfo {
   uint32_t att;    // bit i: draw b*B+i starts an attempt on the speculative path
   uint32_t outs;   // bit i: that attempt produced an output
@@ -292,7 +328,10 @@ __global__ void zig_seed_kernel(ZArgs a, ZStream* __restrict__ seeds) {
   if (s < a.nstreams) seeds[s] = z_seed(a, s);
 }
 
-__global__ void __launch_bounds__(128)
+#ifndef RM_ZSPEC_MINB
+#define RM_ZSPEC_MINB 1
+#endif
+__global__ void __launch_bounds__(128, RM_ZSPEC_MINB)
     zig_spec_kernel(ZArgs a, const ZStream* __restrict__ seeds, BlockInfo* __restrict__ info,
                     double* __restrict__ scratch) {
   __shared__ ZigTables T;
@@ -307,27 +346,54 @@ __global__ void __launch_bounds__(128)
   ZGen g{z_jump(zs, (uint64_t)b * kZBlock), zs.inc};
   uint32_t att = 0, outs = 0, count = 0;
   uint32_t pos = 0;  // relative draw index of the next attempt
-  // speculative outputs are kept (fast path): 16-byte stores of output pairs
+  // speculative outputs are kept (fast path): 32-byte stores of output quads
   double* slot = scratch ? scratch + ((long long)stream * a.nblocks + b) * kZBlock : nullptr;
-  double pend = 0.0;
+  double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+  // one-draw lookahead: the PCG step for draw pos+1 is independent of the table
+  // lookups for draw pos, so the two latencies overlap
+  uint64_t cur = g.next64();
   while (pos < (uint32_t)kZBlock) {
-    double x;
-    int extra;
-    const bool ok = z_attempt(T, g, g.next64(), &x, &extra);
+    const uint64_t nxt = g.next64();
+    const int idx = (int)(cur & 0xff);
+    const uint64_t rabs = (cur >> 9) & 0x000fffffffffffffull;
+    const uint64_t ki = T.ki[idx];
+    const double wi = T.wi[idx];
+    double x = __dmul_rn((double)rabs, wi);
+    if ((cur >> 8) & 1) x = -x;
+    bool ok;
+    uint32_t used;  // draws consumed by this attempt
+    if (rabs < ki) {
+      ok = true;
+      used = 1;
+      cur = nxt;
+    } else {
+      // slow path (about 1.2 % of draws): the further draws start at `nxt`
+      int extra;
+      ok = z_slow(T, g, nxt, idx, rabs, &x, &extra);
+      used = 1 + extra;
+      cur = g.next64();
+    }
     if (pos < 32) {
       att |= 1u << pos;
       if (ok) outs |= 1u << pos;
     }
     if (ok && slot) {
-      if (count & 1u)
-        *reinterpret_cast<double2*>(slot + count - 1) = make_double2(pend, x);
-      else
-        pend = x;
+      switch (count & 3u) {
+        case 0: q0 = x; break;
+        case 1: q1 = x; break;
+        case 2: q2 = x; break;
+        default: st_v4_f64(slot + count - 3, q0, q1, q2, x);
+      }
     }
     count += ok ? 1u : 0u;
-    pos += 1 + extra;
+    pos += used;
   }
-  if (slot && (count & 1u)) slot[count - 1] = pend;
+  if (slot) {
+    const uint32_t r = count & 3u, c0 = count - r;
+    if (r > 0) slot[c0] = q0;
+    if (r > 1) slot[c0 + 1] = q1;
+    if (r > 2) slot[c0 + 2] = q2;
+  }
   info[(long long)stream * a.nblocks + b] = BlockInfo{att, outs, pos, count};
 }
 
@@ -630,13 +696,16 @@ __global__ void __launch_bounds__(256)
                     const double* __restrict__ scratch, const T* __restrict__ Phi, long long ldp,
                     const double* __restrict__ lam, const double* __restrict__ wopt, double sd,
                     T* __restrict__ G, long long ldg, double* __restrict__ Z, long long ldz) {
-  const long long gid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  // stream-fastest warp order: concurrent warps cover the same columns, so
+  // lam / w* (fp64[d], read once per learner) are served from L2
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (gid >= (long long)a.nstreams * a.nblocks) return;
+  if (w >= (long long)a.nstreams * a.nblocks) return;
+  const int stream = (int)(w % a.nstreams);
+  const long long gid = (long long)stream * a.nblocks + w / a.nstreams;
   if (!valid[gid]) return;
   const unsigned long long base = offs[gid];
   if (base >= (unsigned long long)a.n) return;
-  const int stream = (int)(gid / a.nblocks);
   const uint32_t e = entry[gid];
   const uint32_t skip = __popc(info[gid].outs & ((1u << e) - 1u));
   const uint32_t cnt = tcount[gid];
