@@ -710,9 +710,18 @@ __global__ void __launch_bounds__(256)
   const uint32_t skip = __popc(info[gid].outs & ((1u << e) - 1u));
   const uint32_t cnt = tcount[gid];
   const double* src = scratch + gid * kZBlock + skip;
-  for (uint32_t i = lane; i < cnt; i += 32) {
-    const long long c = (long long)base + i;
-    if (c < a.n) emit_grad<T>(a, stream, c, src[i], Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+  // all loads of the block first (cnt <= kZBlock = 8 * 32), then the stores
+  const uint32_t lim = min((unsigned long long)cnt, (unsigned long long)a.n - base);
+  double z[kZBlock / 32];
+#pragma unroll
+  for (int j = 0; j < kZBlock / 32; ++j) {
+    const uint32_t i = lane + 32 * j;
+    z[j] = i < lim ? __ldcs(src + i) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < kZBlock / 32; ++j) {
+    const uint32_t i = lane + 32 * j;
+    if (i < lim) emit_grad<T>(a, stream, (long long)base + i, z[j], Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
   }
 }
 
