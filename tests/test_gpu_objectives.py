@@ -141,10 +141,12 @@ def test_fused_trace_stats_match_reference_formulas(L, d, dtype):
         float(np.sqrt((dev * dev).sum(axis=0).max())), rel=1e-12)
 
 
+@pytest.mark.parametrize("side_stream", [True, False])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
-def test_overlapped_d1d_step_is_bit_identical_to_fused(dtype):
+def test_overlapped_d1d_step_is_bit_identical_to_fused(dtype, side_stream, monkeypatch):
     """step_d1d with a device oracle (mean of W_k on a side stream || gradient of
     W_{k-1}) must equal the fused single-pass D1D kernel on the same inputs."""
+    monkeypatch.setattr(simulation, "D1D_SIDE_STREAM", side_stream)
     L, d = 16, 50_001
     oracle = objectives.quadratic_oracle(d, condition_number=5.0, noise_scale=1.0, seed=3)
     cfg = RunConfig(n_learners=L, iterations=3, lr=0.05, batch_size=2, seed=4, dtype=dtype)

@@ -45,7 +45,9 @@ def d1d_overlap(L, d, steps=5):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             if mode == "overlapped":
+                simulation.D1D_SIDE_STREAM = True
                 st = simulation.step_d1d(st, oracle, cfg)
+                simulation.D1D_SIDE_STREAM = False
             else:
                 st = simulation._gossip_step(st, oracle, cfg, None, stale=True)
             b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
