@@ -282,7 +282,7 @@ __device__ __forceinline__ bool z_attempt(const ZigTables& T, ZGen& g, uint64_t 
 // The slow part of a ziggurat attempt (the fast test `rabs < ki[idx]` failed):
 // `u0` is the next draw of the stream (already taken), further draws come from
 // g.  Same arithmetic as z_attempt; *extra = further draws consumed.
-__device__ __noinline__ bool z_slow(const ZigTables& T, ZGen& g, uint64_t u0, int idx,
+__device__ __forceinline__ bool z_slow(const ZigTables& T, ZGen& g, uint64_t u0, int idx,
                                     uint64_t rabs, double* x, int* extra) {
   const double v = *x;
   if (idx == 0) {
@@ -331,6 +331,49 @@ __global__ void zig_seed_kernel(ZArgs a, ZStream* __restrict__ seeds) {
 #ifndef RM_ZSPEC_MINB
 #define RM_ZSPEC_MINB 1
 #endif
+// One speculative attempt at relative draw `pos` whose first draw is `cur`;
+// `g` is positioned after draw pos+1 (= `nxt`, the one-draw lookahead).
+struct ZStep {
+  double x;
+  uint32_t used;  // draws consumed
+  bool ok;
+};
+__device__ __forceinline__ ZStep z_spec_step(const ZigTables& T, ZGen& g, uint64_t& cur) {
+  const uint64_t nxt = g.next64();
+  const int idx = (int)(cur & 0xff);
+  const uint64_t rabs = (cur >> 9) & 0x000fffffffffffffull;
+  const uint64_t ki = T.ki[idx];
+  const double wi = T.wi[idx];
+  double x = __dmul_rn((double)rabs, wi);
+  if ((cur >> 8) & 1) x = -x;
+  ZStep st;
+  if (rabs < ki) {
+    st.ok = true;
+    st.used = 1;
+    cur = nxt;
+  } else {
+    // slow path (about 1.2 % of draws): the further draws start at `nxt`
+    int extra;
+    st.ok = z_slow(T, g, nxt, idx, rabs, &x, &extra);
+    st.used = 1 + extra;
+    cur = g.next64();
+  }
+  st.x = x;
+  return st;
+}
+
+template <bool KEEP>
+__device__ __forceinline__ void z_keep(double* slot, uint32_t count, double x, double& q0,
+                                       double& q1, double& q2) {
+  if (!KEEP) return;
+  const uint32_t c = count & 3u;
+  if (c == 3u) st_v4_f64(slot + count - 3, q0, q1, q2, x);
+  q0 = c == 0u ? x : q0;
+  q1 = c == 1u ? x : q1;
+  q2 = c == 2u ? x : q2;
+}
+
+template <bool KEEP>
 __global__ void __launch_bounds__(128, RM_ZSPEC_MINB)
     zig_spec_kernel(ZArgs a, const ZStream* __restrict__ seeds, BlockInfo* __restrict__ info,
                     double* __restrict__ scratch) {
@@ -346,49 +389,27 @@ __global__ void __launch_bounds__(128, RM_ZSPEC_MINB)
   ZGen g{z_jump(zs, (uint64_t)b * kZBlock), zs.inc};
   uint32_t att = 0, outs = 0, count = 0;
   uint32_t pos = 0;  // relative draw index of the next attempt
-  // speculative outputs are kept (fast path): 32-byte stores of output quads
-  double* slot = scratch ? scratch + ((long long)stream * a.nblocks + b) * kZBlock : nullptr;
+  // KEEP: speculative outputs are kept in the scratch, 32-byte stores of quads
+  double* slot = KEEP ? scratch + ((long long)stream * a.nblocks + b) * kZBlock : nullptr;
   double q0 = 0.0, q1 = 0.0, q2 = 0.0;
   // one-draw lookahead: the PCG step for draw pos+1 is independent of the table
   // lookups for draw pos, so the two latencies overlap
   uint64_t cur = g.next64();
-  while (pos < (uint32_t)kZBlock) {
-    const uint64_t nxt = g.next64();
-    const int idx = (int)(cur & 0xff);
-    const uint64_t rabs = (cur >> 9) & 0x000fffffffffffffull;
-    const uint64_t ki = T.ki[idx];
-    const double wi = T.wi[idx];
-    double x = __dmul_rn((double)rabs, wi);
-    if ((cur >> 8) & 1) x = -x;
-    bool ok;
-    uint32_t used;  // draws consumed by this attempt
-    if (rabs < ki) {
-      ok = true;
-      used = 1;
-      cur = nxt;
-    } else {
-      // slow path (about 1.2 % of draws): the further draws start at `nxt`
-      int extra;
-      ok = z_slow(T, g, nxt, idx, rabs, &x, &extra);
-      used = 1 + extra;
-      cur = g.next64();
-    }
-    if (pos < 32) {
-      att |= 1u << pos;
-      if (ok) outs |= 1u << pos;
-    }
-    if (ok && slot) {
-      switch (count & 3u) {
-        case 0: q0 = x; break;
-        case 1: q1 = x; break;
-        case 2: q2 = x; break;
-        default: st_v4_f64(slot + count - 3, q0, q1, q2, x);
-      }
-    }
-    count += ok ? 1u : 0u;
-    pos += used;
+  while (pos < 32u) {  // attempts in the first 32 draws are recorded for the merge
+    const ZStep st = z_spec_step(T, g, cur);
+    att |= 1u << pos;
+    outs |= (st.ok ? 1u : 0u) << pos;
+    if (st.ok) z_keep<KEEP>(slot, count, st.x, q0, q1, q2);
+    count += st.ok ? 1u : 0u;
+    pos += st.used;
   }
-  if (slot) {
+  while (pos < (uint32_t)kZBlock) {
+    const ZStep st = z_spec_step(T, g, cur);
+    if (st.ok) z_keep<KEEP>(slot, count, st.x, q0, q1, q2);
+    count += st.ok ? 1u : 0u;
+    pos += st.used;
+  }
+  if (KEEP) {
     const uint32_t r = count & 3u, c0 = count - r;
     if (r > 0) slot[c0] = q0;
     if (r > 1) slot[c0 + 1] = q1;
@@ -881,7 +902,10 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
   const long long grid = (nb + threads - 1) / threads;
   zig_seed_kernel<<<(nstreams + 63) / 64, 64, 0, st>>>(a, seeds);
   RM_CHECK_LAUNCH("zig_seed_kernel");
-  zig_spec_kernel<<<(int)grid, threads, 0, st>>>(a, seeds, info, scratch);
+  if (scratch)
+    zig_spec_kernel<true><<<(int)grid, threads, 0, st>>>(a, seeds, info, scratch);
+  else
+    zig_spec_kernel<false><<<(int)grid, threads, 0, st>>>(a, seeds, info, scratch);
   RM_CHECK_LAUNCH("zig_spec_kernel");
   zig_merge_kernel<<<(int)grid, threads, 0, st>>>(a, info, entry, tcount, merged, nbad, bad);
   RM_CHECK_LAUNCH("zig_merge_kernel");
