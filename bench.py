@@ -76,6 +76,8 @@ def parse():
                     default="rand_psgd")
     ap.add_argument("--layout", choices=["coord", "learner", "position"], default="coord")
     ap.add_argument("--d1d-collective", choices=["auto", "nvls", "nccl"], default="auto")
+    ap.add_argument("--d1d-chunk-cols", type=int, default=1 << 22,
+                    help="learner-sharded D1D pipeline chunk (columns); 0 = one chunk")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -271,7 +273,9 @@ def config_dict(args, ws):
             "layout": args.layout if ws > 1 else "single-gpu",
             "parallelism": (f"{args.layout}-sharded over {ws} GPUs (strong scaling: the whole "
                             f"{args.learners} x {args.dim} problem)") if ws > 1 else "1 GPU",
-            "l2": "inputs (3 x L x d x 4 B) far larger than the 126 MB L2; no flush needed"}
+            "l2": "inputs (3 x L x d x 4 B) far larger than the 126 MB L2; no flush needed",
+            **({"d1d_collective": args.d1d_collective, "d1d_chunk_cols": args.d1d_chunk_cols}
+               if ws > 1 and args.strategy == "d1d" and args.layout == "learner" else {})}
 
 
 # ----------------------------------------------------------------------------
@@ -316,7 +320,8 @@ class Workload:
                 self.d1d = None
                 if args.d1d_collective in ("auto", "nvls"):
                     try:
-                        self.d1d = D.LearnerShardedD1DNVLS(L, d, e - b, dev)
+                        self.d1d = D.LearnerShardedD1DNVLS(
+                            L, d, e - b, dev, chunk_cols=args.d1d_chunk_cols or None)
                         self.d1d_kind = "nvls"
                     except Exception:
                         if args.d1d_collective == "nvls":
@@ -406,7 +411,7 @@ class Workload:
         if ev_pair is not None:
             ev_pair[1].record(stream)
         if self.layout == "learner" and self.uniform:
-            self.launches["mix"] += 3 if self.d1d_kind == "nvls" else 2 * len(self.d1d.chunks)
+            self.launches["mix"] += (3 if self.d1d_kind == "nvls" else 2) * len(self.d1d.chunks)
         else:   # learner / position layouts launch a planner + the mix kernel
             self.launches["mix"] += 2 if self.layout in ("learner", "position") else 1
         if self.layout in ("learner", "position") and not self.uniform:

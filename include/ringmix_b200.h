@@ -219,6 +219,11 @@ int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, in
  * means sum/L to every rank (multimem.st); apply with rm_apply_mean_sgd_*(L = 1).
  * P_mc / M_mc: multicast addresses of symmetric buffers (e.g. torch symmetric
  * memory).  Caller orders it with cross-rank barriers. */
+/* Caps, for the calling host thread, on the CTAs per SM launched by rm_partial_sum_*,
+ * rm_apply_mean_sgd_* and rm_nvls_mean_f64; 0 restores the defaults (16 / 8 / 8).  A chunk
+ * pipeline lowers them so the in-switch reduction of one chunk is co-resident (threads and
+ * registers) with the local kernels of its neighbours. */
+int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls);
 int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1, int L,
                      void* stream);
 

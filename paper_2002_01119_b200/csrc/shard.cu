@@ -559,6 +559,24 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
   return 0;
 }
 
+// Per-host-thread caps on the CTAs per SM of the D1D kernels (0 = defaults).  A
+// pipeline that runs the in-switch reduction concurrently with the local
+// partial-sum / apply kernels lowers them so the kernels can be co-resident.
+static thread_local int g_d1d_psum_cap = 0;
+static thread_local int g_d1d_apply_cap = 0;
+static thread_local int g_d1d_nvls_cap = 0;
+
+extern "C" int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls) {
+  if (partial_sum < 0 || partial_sum > 16 || apply < 0 || apply > 16 || nvls < 0 || nvls > 16) {
+    set_error("CTAs per SM must be in [0, 16] (0 = default)");
+    return RM_EINVAL;
+  }
+  g_d1d_psum_cap = partial_sum;
+  g_d1d_apply_cap = apply;
+  g_d1d_nvls_cap = nvls;
+  return 0;
+}
+
 #define RM_DEFINE_SHARD(SUFFIX, CT, T)                                                          \
   extern "C" int rm_ring_mix_sgd_sharded_##SUFFIX(                                              \
       const uint64_t* row_ptrs, const CT* W_local, const CT* G_local, CT* out, int L, int row0, \
@@ -577,7 +595,8 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
     }                                                                                           \
     if (d == 0) return 0;                                                                       \
     long long blocks = (d + 255) / 256;                                                         \
-    if (blocks > 16LL * sm_count(-1)) blocks = 16LL * sm_count(-1);                             \
+    const long long cap = (g_d1d_psum_cap ? g_d1d_psum_cap : 16) * (long long)sm_count(-1);     \
+    if (blocks > cap) blocks = cap;                                                             \
     partial_sum_kernel<T><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(         \
         reinterpret_cast<const T*>(W), Lg, d, ld, S);                                           \
     RM_CHECK_LAUNCH("partial_sum_kernel");                                                      \
@@ -595,7 +614,8 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
     }                                                                                           \
     if ((long long)Lg * d == 0) return 0;                                                       \
     long long blocks = (d / 4 + 255) / 256 + 1;                                                 \
-    if (blocks > 8LL * sm_count(-1)) blocks = 8LL * sm_count(-1);                               \
+    const long long cap = (g_d1d_apply_cap ? g_d1d_apply_cap : 8) * (long long)sm_count(-1);    \
+    if (blocks > cap) blocks = cap;                                                             \
     if (G)                                                                                      \
       apply_mean_kernel<T, true><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(  \
           S, reinterpret_cast<const T*>(G), reinterpret_cast<T*>(out), Lg, L, d, ldg, ldo, lr,  \
@@ -655,7 +675,8 @@ extern "C" int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, in
   }
   if (c1 == c0) return 0;
   long long blocks = (c1 - c0 + 2047) / 2048;
-  if (blocks > 8LL * sm_count(-1)) blocks = 8LL * sm_count(-1);
+  const long long cap = (g_d1d_nvls_cap ? g_d1d_nvls_cap : 8) * (long long)sm_count(-1);
+  if (blocks > cap) blocks = cap;
   nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(P_mc, M_mc, c0, c1,
                                                                              (double)L);
   RM_CHECK_LAUNCH("nvls_sum_kernel");

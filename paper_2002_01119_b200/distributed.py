@@ -17,6 +17,7 @@ a step barrier, and the D1D all-reduce).  Two layouts:
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -326,10 +327,17 @@ class LearnerShardedD1DNVLS:
     for its 1/N column shard a rank sums all ranks' partials in the switch
     (``multimem.ld_reduce``) and broadcasts the totals into every rank's copy
     (``multimem.st``); then each rank applies mean - lr*G to its learners.  No NCCL
-    kernels; the two cross-rank barriers are symmetric-memory signal pads
-    (stream-ordered)."""
+    kernels; the cross-rank barriers are symmetric-memory signal pads (stream-ordered).
 
-    def __init__(self, L: int, d: int, Lg: int, device, group=None):
+    The columns are cut into chunks (``chunk_cols``; None = one chunk) and pipelined
+    over two streams, so the in-switch reduction of chunk c (side stream) overlaps
+    the partial sums of chunk c+1 and the apply of chunk c-1 (compute stream) — the
+    D1D global average overlapped with the local update (north-star (c))."""
+
+    MAX_CHUNKS = 16   # barrier channels per handle: torch allows 32
+
+    def __init__(self, L: int, d: int, Lg: int, device, group=None,
+                 chunk_cols: int | None = 1 << 22):
         import torch.distributed._symmetric_memory as symm_mem
 
         self.L, self.d, self.Lg = L, d, Lg
@@ -344,29 +352,77 @@ class LearnerShardedD1DNVLS:
         self.hM = symm_mem.rendezvous(self.M, gname)
         if not self.hP.multicast_ptr or not self.hM.multicast_ptr:
             raise RuntimeError("NVSwitch multicast (NVLS) is not available on this system")
-        # column shard reduced by this rank; 32-column aligned boundaries
-        step = -(-d // self.world)
-        step = ((step + 31) // 32) * 32
-        self.c0 = min(d, self.rank * step)
-        self.c1 = min(d, self.c0 + step)
+        # chunk boundaries on multiples of 32*world columns; inside a chunk every rank
+        # reduces a 1/N slice with 32-column (256 B) aligned boundaries
+        quantum = 32 * self.world
+        want = d if chunk_cols is None else max(quantum, chunk_cols)
+        want = max(want, -(-d // self.MAX_CHUNKS))
+        step = -(-want // quantum) * quantum
+        self.chunks = [(c, min(c + step, d)) for c in range(0, d, step)] or [(0, 0)]
+        self.shards = []
+        for b, e in self.chunks:
+            sl = -(-(e - b) // self.world)
+            sl = -(-sl // 32) * 32
+            c0 = min(e, b + self.rank * sl)
+            self.shards.append((c0, min(e, c0 + sl)))
+        # kept for callers that read the single-chunk shard
+        self.c0, self.c1 = self.shards[0]
+        self.comm = torch.cuda.Stream(device=self.device)
+        # co-residency of the pipelined kernels: (local partial-sum/apply, in-switch)
+        # (partial sum, apply, in-switch reduce); apply needs 75 registers per thread
+        env = os.environ.get("RINGMIX_D1D_CTAS", "4,2,2").split(",")
+        self.ctas_per_sm = tuple(int(x) for x in env)
 
     def step(self, W: torch.Tensor, G: torch.Tensor | None, lr: float, out: torch.Tensor,
              absmax: torch.Tensor | None = None) -> torch.Tensor:
         lib = _lib.load()
         sfx = mixing._suffix(W)
-        s = _lib.stream_ptr()
-        _lib.check(getattr(lib, f"rm_partial_sum_{sfx}")(W.data_ptr(), self.Lg, self.d,
-                                                         W.stride(0), self.P.data_ptr(), s),
-                   "rm_partial_sum")
-        self.hP.barrier(channel=0)
-        _lib.check(lib.rm_nvls_mean_f64(self.hP.multicast_ptr, self.hM.multicast_ptr, self.c0,
-                                        self.c1, self.L, s), "rm_nvls_mean_f64")
-        self.hM.barrier(channel=1)
-        # M holds the means already (L = 1: no per-learner division)
-        _lib.check(getattr(lib, f"rm_apply_mean_sgd_{sfx}")(
-            self.M.data_ptr(), _lib.ptr(G), out.data_ptr(), self.Lg, 1, self.d,
-            G.stride(0) if G is not None else 0, out.stride(0), float(lr), _lib.ptr(absmax), s),
-            "rm_apply_mean_sgd")
+        psum = getattr(lib, f"rm_partial_sum_{sfx}")
+        apply = getattr(lib, f"rm_apply_mean_sgd_{sfx}")
+        compute = torch.cuda.current_stream(self.device)
+        esz = W.element_size()
+        ready: list[torch.cuda.Event] = []
+
+        def launch_partial(i):
+            b, e = self.chunks[i]
+            _lib.check(psum(W.data_ptr() + b * esz, self.Lg, e - b, W.stride(0),
+                            self.P.data_ptr() + b * 8, compute.cuda_stream), "rm_partial_sum")
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            self.comm.wait_event(ev)
+            c0, c1 = self.shards[i]
+            with torch.cuda.stream(self.comm):
+                self.hP.barrier(channel=i)          # every rank's partials of chunk i
+                _lib.check(lib.rm_nvls_mean_f64(self.hP.multicast_ptr, self.hM.multicast_ptr,
+                                                c0, c1, self.L, self.comm.cuda_stream),
+                           "rm_nvls_mean_f64")
+                self.hM.barrier(channel=i)          # every rank's means of chunk i
+                done = torch.cuda.Event()
+                done.record(self.comm)
+            ready.append(done)
+
+        def launch_apply(i):
+            b, e = self.chunks[i]
+            compute.wait_event(ready[i])
+            # M holds the means already (L = 1: no per-learner division)
+            gp = None if G is None else G.data_ptr() + b * esz
+            _lib.check(apply(self.M.data_ptr() + b * 8, gp, out.data_ptr() + b * esz, self.Lg,
+                             1, e - b, G.stride(0) if G is not None else 0, out.stride(0),
+                             float(lr), _lib.ptr(absmax), compute.cuda_stream),
+                       "rm_apply_mean_sgd")
+
+        n = len(self.chunks)
+        if n > 1:
+            _lib.check(lib.rm_set_d1d_ctas_per_sm(*self.ctas_per_sm), "rm_set_d1d_ctas_per_sm")
+        try:
+            launch_partial(0)
+            for i in range(n):
+                if i + 1 < n:
+                    launch_partial(i + 1)
+                launch_apply(i)
+        finally:
+            if n > 1:
+                lib.rm_set_d1d_ctas_per_sm(0, 0, 0)
         return out
 
 
@@ -383,6 +439,10 @@ class LearnerShardedD1D:
         self.chunks = [(b, min(b + step, d)) for b in range(0, d, step)]
         self.S = torch.empty(d, dtype=torch.float64, device=self.device)
         self.comm = torch.cuda.Stream(device=self.device)
+        # co-residency of the pipelined kernels: (local partial-sum/apply, in-switch)
+        # (partial sum, apply, in-switch reduce); apply needs 75 registers per thread
+        env = os.environ.get("RINGMIX_D1D_CTAS", "4,2,2").split(",")
+        self.ctas_per_sm = tuple(int(x) for x in env)
 
     def step(self, W: torch.Tensor, G: torch.Tensor | None, lr: float, out: torch.Tensor,
              absmax: torch.Tensor | None = None) -> torch.Tensor:

@@ -41,13 +41,18 @@ def main():
     ok_d1d = dd <= 2e-6
     # NVSwitch multicast variant (our own in-switch reduction kernel)
     try:
-        nv = D.LearnerShardedD1DNVLS(L, d, ring.Lg, dev)
-        out2 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
-        nv.step(ring.weights, Gl, 0.01, out2)
-        torch.cuda.synchronize()
-        dd2 = (out2.double() - ref[b:e].double()).abs().max().item()
-        ok_d1d = ok_d1d and dd2 <= 2e-6
-        nvls = True
+        outs = []
+        for cc in (None, 1 << 16):   # one chunk, and the chunk pipeline
+            nv = D.LearnerShardedD1DNVLS(L, d, ring.Lg, dev, chunk_cols=cc)
+            out2 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
+            for _ in range(2):
+                nv.step(ring.weights, Gl, 0.01, out2)
+            torch.cuda.synchronize()
+            dd2 = (out2.double() - ref[b:e].double()).abs().max().item()
+            ok_d1d = ok_d1d and dd2 <= 2e-6
+            outs.append(out2)
+        ok_d1d = ok_d1d and bool(torch.equal(outs[0], outs[1]))
+        nvls = len(nv.chunks)
     except RuntimeError as exc:
         nvls = str(exc)[:100]
     ring.close()
