@@ -145,7 +145,65 @@ constexpr int kBox = 256;  // TMA box dimension limit (elements)
 // NT threads per CTA: ring tiles run one 512-thread CTA per SM; mean tiles
 // (D1D / S-PSGD) run two 256-thread CTAs per SM, so one CTA's mean phase
 // overlaps the other's output phase.
-template <typename T, int MODE, bool HAS_G, int NT>
+// GDIRECT (mean mode with G): only W is staged (twice the tile width for the same
+// stage bytes, 512-byte row segments); each thread prefetches its G vectors for
+// the tile into registers before the mean phase, so their latency hides behind it.
+constexpr int kGPre = 8;  // G vectors prefetched per thread per tile
+
+__device__ __forceinline__ uint4 ldg_stream_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// The VEC column means of one output vector: 16-byte shared loads (lanes own
+// VEC consecutive columns, so scalar loads would be 2·VEC-way bank conflicts).
+template <int VEC>
+__device__ __forceinline__ void load_means(const double* s_mean, int c, double (&m)[VEC]) {
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(s_mean + c + e);
+    m[e] = t.x;
+    m[e + 1] = t.y;
+  }
+}
+
+// W' = mean - lr * g for one vector of a row (mean mode; same arithmetic as the
+// staged path).
+template <typename T>
+__device__ __forceinline__ void mean_emit(const Vec<T>& g, const double* s_mean, int c,
+                                          typename Elem<T>::acc lr, T* dst, int width,
+                                          typename Elem<T>::amax_t& amax) {
+  using E = Elem<T>;
+  using A = typename E::acc;
+  constexpr int VEC = E::VEC;
+  Vec<T> y;
+  double mv[VEC];
+  load_means<VEC>(s_mean, c, mv);
+#pragma unroll
+  for (int e = 0; e < VEC; e++) {
+    A m = (A)mv[e];
+    m = r_sub(m, r_mul(lr, (A)E::ld(g.e(), e)));
+    y.e()[e] = E::st(m);
+  }
+  if (c + VEC <= width) {
+#pragma unroll
+    for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
+    st_cs_v4(dst, y.raw);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; e++) {
+      if (c + e < width) {
+        amax = E::amax_acc(amax, y.e()[e]);
+        dst[e] = y.e()[e];
+      }
+    }
+  }
+}
+
+template <typename T, int MODE, bool HAS_G, int NT, bool GDIRECT = false>
 __global__ void __launch_bounds__(NT, 512 / NT)
     mix_tma_kernel(MixArgs a, const __grid_constant__ CUtensorMap tmW,
                    const __grid_constant__ CUtensorMap tmG) {
@@ -158,7 +216,8 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   const int L = a.L;
   const int cw = a.cw;
   const int w_bytes = L * cw * (int)sizeof(T);
-  constexpr bool stage_g = HAS_G || MODE == kSpsgd;
+  static_assert(!GDIRECT || (MODE == kMean && HAS_G), "GDIRECT is the mean mode with G");
+  constexpr bool stage_g = (HAS_G && !GDIRECT) || MODE == kSpsgd;
   const int stage_bytes = w_bytes * (stage_g ? 2 : 1);
 
   // layout: [mbarriers | tri table (L x int4) | stages | per-column mean]
@@ -238,6 +297,28 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     const T* sW = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes);
     const T* sG = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes + w_bytes);
 
+    const int nv = (width + VEC - 1) / VEC;
+    const int total = L << log2_nv;
+    Vec<T> gpre[GDIRECT ? kGPre : 1];
+    if (GDIRECT) {
+      const T* Gt = static_cast<const T*>(a.G) + c0;
+#pragma unroll
+      for (int k = 0; k < kGPre; k++) {
+        const int idx = tid + k * kThreads;
+        const int j = idx >> log2_nv;
+        const int c = (idx & (nv_full - 1)) * VEC;
+        if (idx < total && c < width) {
+          if (c + VEC <= width) {
+            gpre[k].raw = ldg_stream_v4(Gt + j * a.ldg + c);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; e++)
+              if (c + e < width) gpre[k].e()[e] = Gt[j * a.ldg + c + e];
+          }
+        }
+      }
+    }
+
     mbar_wait(&full[s], parity);
 
     if (MODE != kRing) {
@@ -291,10 +372,34 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       __syncthreads();
     }
 
-    const int nv = (width + VEC - 1) / VEC;
-    const int total = L << log2_nv;
+    if (GDIRECT) {
+      // the prefetched items, then (large tiles only) the rest with direct loads
+#pragma unroll
+      for (int k = 0; k < kGPre; k++) {
+        const int idx = tid + k * kThreads;
+        const int j = idx >> log2_nv;
+        const int c = (idx & (nv_full - 1)) * VEC;
+        if (idx < total && c < width)
+          mean_emit<T>(gpre[k], s_mean, c, lr, out + j * a.ldo + c0 + c, width, amax);
+      }
+      for (int idx = tid + kGPre * kThreads; idx < total; idx += kThreads) {
+        const int j = idx >> log2_nv;
+        const int c = (idx & (nv_full - 1)) * VEC;
+        if (c >= width) continue;
+        const T* gp = static_cast<const T*>(a.G) + j * a.ldg + c0 + c;
+        Vec<T> g;
+        if (c + VEC <= width) {
+          g.raw = ldg_stream_v4(gp);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; e++)
+            if (c + e < width) g.e()[e] = gp[e];
+        }
+        mean_emit<T>(g, s_mean, c, lr, out + j * a.ldo + c0 + c, width, amax);
+      }
+    }
 #pragma unroll 2
-    for (int idx = tid; idx < total; idx += kThreads) {
+    for (int idx = tid; idx < (GDIRECT ? 0 : total); idx += kThreads) {
       const int j = idx >> log2_nv;
       const int v = idx & (nv_full - 1);
       if (v >= nv) continue;
@@ -316,9 +421,11 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       } else if (MODE == kMean) {
         Vec<T> vg;
         if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
+        double mv[VEC];
+        load_means<VEC>(s_mean, c, mv);
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
-          A m = (A)s_mean[c + e];
+          A m = (A)mv[e];
           if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
           y.e()[e] = E::st(m);
         }
@@ -327,10 +434,12 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         vw.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
         w0.raw = *reinterpret_cast<const uint4*>(sW + sidx(0, c));
         bool diff = false;
+        double mv[VEC];
+        load_means<VEC>(s_mean, c, mv);
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
           if (c + e < width) diff |= !(vw.e()[e] == w0.e()[e]);
-          A m = (A)s_mean[c + e];
+          A m = (A)mv[e];
           y.e()[e] = E::st(r_sub((A)E::ld(vw.e(), e), r_mul(lr, m)));
         }
         if (diff && a.mismatch) atomicOr(a.mismatch, 1u);
@@ -373,6 +482,23 @@ static int launch_scalar(const MixArgs& a, long long c_begin, cudaStream_t st) {
   mix_scalar_kernel<T, MODE, HAS_G><<<(int)blocks, 256, 0, st>>>(a, c_begin);
   RM_CHECK_LAUNCH("mix_scalar_kernel");
   return RM_OK;
+}
+
+// mean mode with G: stage W and G (fp32 0.93, fp64 0.89 of HBM at C4), or stage
+// only W and prefetch G to registers (bf16: 0.71 vs 0.54 staged; the wider tile
+// halves the per-byte cost of the 2-byte mean-phase loads).  The env
+// RINGMIX_MEAN_STAGE_G=1/0 forces one variant (measurement).
+template <typename T>
+static bool mean_g_direct() {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("RINGMIX_MEAN_STAGE_G");
+    if (env && (atoi(env) == 0 || atoi(env) == 1))
+      v = atoi(env) == 1 ? 0 : 1;
+    else
+      v = sizeof(T) == 2 ? 1 : 0;
+  }
+  return v == 1;
 }
 
 static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode,
@@ -428,16 +554,16 @@ static bool make_map(CUtensorMap* m, const void* base, long long d, int L, long 
   return r == CUDA_SUCCESS;
 }
 
-template <typename T, int MODE, bool HAS_G, int NT>
+template <typename T, int MODE, bool HAS_G, int NT, bool GDIRECT = false>
 static int launch_mix(MixArgs a, cudaStream_t st) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const size_t esz = sizeof(T);
-  const bool stage_g = HAS_G || MODE == kSpsgd;
+  const bool stage_g = (HAS_G && !GDIRECT) || MODE == kSpsgd;
   const uintptr_t align_bits =
       reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.out) |
-      (stage_g ? reinterpret_cast<uintptr_t>(a.G) : 0) | (uintptr_t)(a.ldw * esz) |
-      (uintptr_t)(a.ldo * esz) | (stage_g ? (uintptr_t)(a.ldg * esz) : 0);
+      (HAS_G ? reinterpret_cast<uintptr_t>(a.G) : 0) | (uintptr_t)(a.ldw * esz) |
+      (uintptr_t)(a.ldo * esz) | (HAS_G ? (uintptr_t)(a.ldg * esz) : 0);
   const bool aligned = (align_bits & 15) == 0;
   static int max_optin = -1;
   if (max_optin < 0) {
@@ -497,14 +623,14 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT>,
+    cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT, GDIRECT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
     if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(mix_tma_kernel)");
     attr_set = true;
   }
   long long grid = (long long)sm_count(-1) * (512 / NT);
   if (grid > a.ntiles) grid = a.ntiles;
-  mix_tma_kernel<T, MODE, HAS_G, NT><<<(int)grid, NT, smem, st>>>(a, tmW, tmG);
+  mix_tma_kernel<T, MODE, HAS_G, NT, GDIRECT><<<(int)grid, NT, smem, st>>>(a, tmW, tmG);
   RM_CHECK_LAUNCH("mix_tma_kernel");
   return RM_OK;
 }
@@ -574,6 +700,8 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
   const int ring_nt = ring_nt_env == 256 || ring_nt_env == 512 ? ring_nt_env
                                                                : (L <= 32 ? 256 : 512);
   const bool hg = MODE == kSpsgd || G != nullptr;
+  if (MODE == kMean && hg && mean_g_direct<T>())
+    return launch_mix<T, kMean, true, kMeanThreads, true>(a, st);
   if (MODE != kRing)
     return hg ? launch_mix<T, MODE, true, kMeanThreads>(a, st)
               : launch_mix<T, MODE, false, kMeanThreads>(a, st);
