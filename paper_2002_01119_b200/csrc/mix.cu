@@ -145,17 +145,12 @@ constexpr int kBox = 256;  // TMA box dimension limit (elements)
 // NT threads per CTA: ring tiles run one 512-thread CTA per SM; mean tiles
 // (D1D / S-PSGD) run two 256-thread CTAs per SM, so one CTA's mean phase
 // overlaps the other's output phase.
-// GDIRECT (mean mode with G): only W is staged (twice the tile width for the same
-// stage bytes, 512-byte row segments); each thread prefetches its G vectors for
-// the tile into registers before the mean phase, so their latency hides behind it.
-constexpr int kGPre = 8;  // G vectors prefetched per thread per tile
-
-__device__ __forceinline__ uint4 ldg_stream_v4(const void* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
+// two adjacent bf16 columns of a staged row as floats (exact conversion)
+template <typename T>
+__device__ __forceinline__ float2 lds_pair(const T* p) {
+  uint32_t w;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(smem_u32(p)));
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
 
 // The VEC column means of one output vector: 16-byte shared loads (lanes own
@@ -170,40 +165,7 @@ __device__ __forceinline__ void load_means(const double* s_mean, int c, double (
   }
 }
 
-// W' = mean - lr * g for one vector of a row (mean mode; same arithmetic as the
-// staged path).
-template <typename T>
-__device__ __forceinline__ void mean_emit(const Vec<T>& g, const double* s_mean, int c,
-                                          typename Elem<T>::acc lr, T* dst, int width,
-                                          typename Elem<T>::amax_t& amax) {
-  using E = Elem<T>;
-  using A = typename E::acc;
-  constexpr int VEC = E::VEC;
-  Vec<T> y;
-  double mv[VEC];
-  load_means<VEC>(s_mean, c, mv);
-#pragma unroll
-  for (int e = 0; e < VEC; e++) {
-    A m = (A)mv[e];
-    m = r_sub(m, r_mul(lr, (A)E::ld(g.e(), e)));
-    y.e()[e] = E::st(m);
-  }
-  if (c + VEC <= width) {
-#pragma unroll
-    for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
-    st_cs_v4(dst, y.raw);
-  } else {
-#pragma unroll
-    for (int e = 0; e < VEC; e++) {
-      if (c + e < width) {
-        amax = E::amax_acc(amax, y.e()[e]);
-        dst[e] = y.e()[e];
-      }
-    }
-  }
-}
-
-template <typename T, int MODE, bool HAS_G, int NT, bool GDIRECT = false>
+template <typename T, int MODE, bool HAS_G, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT)
     mix_tma_kernel(MixArgs a, const __grid_constant__ CUtensorMap tmW,
                    const __grid_constant__ CUtensorMap tmG) {
@@ -216,8 +178,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   const int L = a.L;
   const int cw = a.cw;
   const int w_bytes = L * cw * (int)sizeof(T);
-  static_assert(!GDIRECT || (MODE == kMean && HAS_G), "GDIRECT is the mean mode with G");
-  constexpr bool stage_g = (HAS_G && !GDIRECT) || MODE == kSpsgd;
+  constexpr bool stage_g = HAS_G || MODE == kSpsgd;
   const int stage_bytes = w_bytes * (stage_g ? 2 : 1);
 
   // layout: [mbarriers | tri table (L x int4) | stages | per-column mean]
@@ -225,10 +186,10 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   int4* s_tri = reinterpret_cast<int4*>(smem + 128);
   unsigned char* stages = smem + 128 + ((L * 16 + 127) / 128) * 128;
   double* s_mean = nullptr;
-  double* s_part = nullptr;  // [8][cw] partial sums (narrow tiles)
+  A* s_part = nullptr;  // [8][cw] partial sums in the accumulation type (narrow tiles)
   if (MODE != kRing) {
     s_mean = reinterpret_cast<double*>(stages + kStages * stage_bytes);
-    s_part = s_mean + cw;
+    s_part = reinterpret_cast<A*>(s_mean + cw);
   }
 
   T* out = static_cast<T*>(a.out);
@@ -299,26 +260,6 @@ __global__ void __launch_bounds__(NT, 512 / NT)
 
     const int nv = (width + VEC - 1) / VEC;
     const int total = L << log2_nv;
-    Vec<T> gpre[GDIRECT ? kGPre : 1];
-    if (GDIRECT) {
-      const T* Gt = static_cast<const T*>(a.G) + c0;
-#pragma unroll
-      for (int k = 0; k < kGPre; k++) {
-        const int idx = tid + k * kThreads;
-        const int j = idx >> log2_nv;
-        const int c = (idx & (nv_full - 1)) * VEC;
-        if (idx < total && c < width) {
-          if (c + VEC <= width) {
-            gpre[k].raw = ldg_stream_v4(Gt + j * a.ldg + c);
-          } else {
-#pragma unroll
-            for (int e = 0; e < VEC; e++)
-              if (c + e < width) gpre[k].e()[e] = Gt[j * a.ldg + c + e];
-          }
-        }
-      }
-    }
-
     mbar_wait(&full[s], parity);
 
     if (MODE != kRing) {
@@ -329,7 +270,37 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       // read consecutive columns of one staged row: no bank conflicts.
       const T* src = (MODE == kMean) ? sW : sG;
       const int groups = cw <= kThreads / 2 ? min(8, kThreads / cw) : 1;
-      if (groups >= 2) {
+      // 2-byte elements: a thread owns a column pair (one 32-bit shared load
+      // feeds two columns' chains, full 128-byte wavefronts per warp)
+      const int pgroups = sizeof(T) == 2 ? min(8, kThreads / (cw / 2)) : 0;
+      if (sizeof(T) == 2 && pgroups >= 2 && cw >= 2) {
+        const int n8 = L - (L % 8);
+        const int per = 8 / pgroups;
+        const int ncp = cw / 2;
+        const int g = tid / ncp, col = 2 * (tid % ncp);
+        if (g < pgroups && col < width) {
+          for (int q = 0; q < per; q++) {
+            const int k = g * per + q;
+            float2 r = lds_pair(src + sidx(k, col));
+            for (int i = 8 + k; i < n8; i += 8) {
+              const float2 v = lds_pair(src + sidx(i, col));
+              r.x = __fadd_rn(r.x, v.x);
+              r.y = __fadd_rn(r.y, v.y);
+            }
+            s_part[k * cw + col] = r.x;
+            s_part[k * cw + col + 1] = r.y;
+          }
+        }
+        __syncthreads();
+        if (tid < width) {
+          const A* pp = s_part + tid;
+          A res = r_add(r_add(r_add((A)pp[0], (A)pp[cw]), r_add((A)pp[2 * cw], (A)pp[3 * cw])),
+                        r_add(r_add((A)pp[4 * cw], (A)pp[5 * cw]),
+                              r_add((A)pp[6 * cw], (A)pp[7 * cw])));
+          for (int i = n8; i < L; i++) res = r_add(res, (A)E::lds(src + sidx(i, tid)));
+          s_mean[tid] = (double)r_div(res, (A)L);
+        }
+      } else if (groups >= 2) {
         // narrow tiles: split the 8 chains over `groups` threads per column so
         // every warp works; partial sums meet in shared memory
         const int n8 = L - (L % 8);
@@ -340,12 +311,12 @@ __global__ void __launch_bounds__(NT, 512 / NT)
             const int k = g * per + q;
             A r = (A)E::lds(src + sidx(k, col));
             for (int i = 8 + k; i < n8; i += 8) r = r_add(r, (A)E::lds(src + sidx(i, col)));
-            s_part[k * cw + col] = (double)r;
+            s_part[k * cw + col] = r;
           }
         }
         __syncthreads();
         if (tid < width) {
-          const double* pp = s_part + tid;
+          const A* pp = s_part + tid;
           A res = r_add(r_add(r_add((A)pp[0], (A)pp[cw]), r_add((A)pp[2 * cw], (A)pp[3 * cw])),
                         r_add(r_add((A)pp[4 * cw], (A)pp[5 * cw]),
                               r_add((A)pp[6 * cw], (A)pp[7 * cw])));
@@ -372,34 +343,17 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       __syncthreads();
     }
 
-    if (GDIRECT) {
-      // the prefetched items, then (large tiles only) the rest with direct loads
+    // mean modes: a thread's column vector is the same for all its items (the
+    // host guarantees nv_full divides the CTA size), so its means are read once
+    A ma[VEC];
+    if (MODE != kRing) {
+      double mv[VEC];
+      load_means<VEC>(s_mean, (tid & (nv_full - 1)) * VEC, mv);
 #pragma unroll
-      for (int k = 0; k < kGPre; k++) {
-        const int idx = tid + k * kThreads;
-        const int j = idx >> log2_nv;
-        const int c = (idx & (nv_full - 1)) * VEC;
-        if (idx < total && c < width)
-          mean_emit<T>(gpre[k], s_mean, c, lr, out + j * a.ldo + c0 + c, width, amax);
-      }
-      for (int idx = tid + kGPre * kThreads; idx < total; idx += kThreads) {
-        const int j = idx >> log2_nv;
-        const int c = (idx & (nv_full - 1)) * VEC;
-        if (c >= width) continue;
-        const T* gp = static_cast<const T*>(a.G) + j * a.ldg + c0 + c;
-        Vec<T> g;
-        if (c + VEC <= width) {
-          g.raw = ldg_stream_v4(gp);
-        } else {
-#pragma unroll
-          for (int e = 0; e < VEC; e++)
-            if (c + e < width) g.e()[e] = gp[e];
-        }
-        mean_emit<T>(g, s_mean, c, lr, out + j * a.ldo + c0 + c, width, amax);
-      }
+      for (int e = 0; e < VEC; e++) ma[e] = (A)mv[e];
     }
 #pragma unroll 2
-    for (int idx = tid; idx < (GDIRECT ? 0 : total); idx += kThreads) {
+    for (int idx = tid; idx < total; idx += kThreads) {
       const int j = idx >> log2_nv;
       const int v = idx & (nv_full - 1);
       if (v >= nv) continue;
@@ -421,11 +375,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       } else if (MODE == kMean) {
         Vec<T> vg;
         if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
-        double mv[VEC];
-        load_means<VEC>(s_mean, c, mv);
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
-          A m = (A)mv[e];
+          A m = ma[e];
           if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
           y.e()[e] = E::st(m);
         }
@@ -434,12 +386,10 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         vw.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
         w0.raw = *reinterpret_cast<const uint4*>(sW + sidx(0, c));
         bool diff = false;
-        double mv[VEC];
-        load_means<VEC>(s_mean, c, mv);
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
           if (c + e < width) diff |= !(vw.e()[e] == w0.e()[e]);
-          A m = (A)mv[e];
+          A m = ma[e];
           y.e()[e] = E::st(r_sub((A)E::ld(vw.e(), e), r_mul(lr, m)));
         }
         if (diff && a.mismatch) atomicOr(a.mismatch, 1u);
@@ -484,28 +434,16 @@ static int launch_scalar(const MixArgs& a, long long c_begin, cudaStream_t st) {
   return RM_OK;
 }
 
-// mean mode with G: stage W and G (fp32 0.93, fp64 0.89 of HBM at C4), or stage
-// only W and prefetch G to registers (bf16: 0.71 vs 0.54 staged; the wider tile
-// halves the per-byte cost of the 2-byte mean-phase loads).  The env
-// RINGMIX_MEAN_STAGE_G=1/0 forces one variant (measurement).
-template <typename T>
-static bool mean_g_direct() {
-  static int v = -1;
-  if (v < 0) {
-    const char* env = getenv("RINGMIX_MEAN_STAGE_G");
-    if (env && (atoi(env) == 0 || atoi(env) == 1))
-      v = atoi(env) == 1 ? 0 : 1;
-    else
-      v = sizeof(T) == 2 ? 1 : 0;
-  }
-  return v == 1;
-}
-
 static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode,
                              int kThreads) {
   size_t stage = (size_t)L * cw * elem * (stage_g ? 2 : 1);
   size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kStages * stage;
-  if (mode != kRing) bytes += (size_t)cw * sizeof(double) * (cw <= kThreads / 2 ? 9 : 1);
+  // per-column means, plus [8][cw] partial sums when the mean phase splits a
+  // column's 8 chains over several threads (see the mean phase)
+  const bool split = cw <= kThreads / 2 || (elem == 2 && cw <= kThreads);
+  // (the partials are in the accumulation type: float for 2-byte elements)
+  const size_t acc = elem == 2 ? sizeof(float) : sizeof(double);
+  if (mode != kRing) bytes += (size_t)cw * sizeof(double) + (split ? 8 * cw * acc : 0);
   return bytes;
 }
 
@@ -554,16 +492,16 @@ static bool make_map(CUtensorMap* m, const void* base, long long d, int L, long 
   return r == CUDA_SUCCESS;
 }
 
-template <typename T, int MODE, bool HAS_G, int NT, bool GDIRECT = false>
+template <typename T, int MODE, bool HAS_G, int NT>
 static int launch_mix(MixArgs a, cudaStream_t st) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const size_t esz = sizeof(T);
-  const bool stage_g = (HAS_G && !GDIRECT) || MODE == kSpsgd;
+  const bool stage_g = HAS_G || MODE == kSpsgd;
   const uintptr_t align_bits =
       reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.out) |
-      (HAS_G ? reinterpret_cast<uintptr_t>(a.G) : 0) | (uintptr_t)(a.ldw * esz) |
-      (uintptr_t)(a.ldo * esz) | (HAS_G ? (uintptr_t)(a.ldg * esz) : 0);
+      (stage_g ? reinterpret_cast<uintptr_t>(a.G) : 0) | (uintptr_t)(a.ldw * esz) |
+      (uintptr_t)(a.ldo * esz) | (stage_g ? (uintptr_t)(a.ldg * esz) : 0);
   const bool aligned = (align_bits & 15) == 0;
   static int max_optin = -1;
   if (max_optin < 0) {
@@ -599,10 +537,12 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   }
   if (!use_tma) return launch_scalar<T, MODE, HAS_G>(a, 0, st);
 
-  a.cw = cw;
-  a.d_main = a.d;
   int nv = cw / VEC, lg = 0;
   while ((1 << lg) < nv) lg++;
+  // mean modes read a thread's column means once per tile (see the kernel)
+  if (MODE != kRing && (1 << lg) > NT) return launch_scalar<T, MODE, HAS_G>(a, 0, st);
+  a.cw = cw;
+  a.d_main = a.d;
   a.log2_nv = lg;
   a.ntiles = (a.d + cw - 1) / cw;
   const int box_c = cw < kBox ? cw : kBox;
@@ -623,14 +563,14 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT, GDIRECT>,
+    cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
     if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(mix_tma_kernel)");
     attr_set = true;
   }
   long long grid = (long long)sm_count(-1) * (512 / NT);
   if (grid > a.ntiles) grid = a.ntiles;
-  mix_tma_kernel<T, MODE, HAS_G, NT, GDIRECT><<<(int)grid, NT, smem, st>>>(a, tmW, tmG);
+  mix_tma_kernel<T, MODE, HAS_G, NT><<<(int)grid, NT, smem, st>>>(a, tmW, tmG);
   RM_CHECK_LAUNCH("mix_tma_kernel");
   return RM_OK;
 }
@@ -700,8 +640,6 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
   const int ring_nt = ring_nt_env == 256 || ring_nt_env == 512 ? ring_nt_env
                                                                : (L <= 32 ? 256 : 512);
   const bool hg = MODE == kSpsgd || G != nullptr;
-  if (MODE == kMean && hg && mean_g_direct<T>())
-    return launch_mix<T, kMean, true, kMeanThreads, true>(a, st);
   if (MODE != kRing)
     return hg ? launch_mix<T, MODE, true, kMeanThreads>(a, st)
               : launch_mix<T, MODE, false, kMeanThreads>(a, st);
