@@ -258,3 +258,36 @@ def test_full_size_c2_properties():
     Xs, Gs, Os = (t[:, cols.cuda()].contiguous() for t in (X, G, out))
     ref = O.c_ring_mix_sgd(_host_dL(Xs), _host_dL(Gs), 0.01, left, right)
     assert np.array_equal(_host_dL(Os), ref.astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64", "bf16"])
+def test_empty_parameter_vectors(dtype):
+    """d = 0 (the reference's (0, L) weight matrix): every kernel entry point returns
+    an empty result without launching, and the absmax stays at zero."""
+    L = 16
+    X = mixing.empty_learner_major(L, 0, DT[dtype], "cuda")
+    G = mixing.empty_learner_major(L, 0, DT[dtype], "cuda")
+    lt, rt, _, _ = _tables(L, 3, 0)
+    assert mixing.ring_mix_sgd(X, G, 0.1, lt, rt).shape == (L, 0)
+    assert mixing.mean_mix_sgd(X, G, 0.1).shape == (L, 0)
+    assert mixing.spsgd_update(X, G, 0.1).shape == (L, 0)
+    out = mixing.empty_learner_major(L, 0, DT[dtype], "cuda")
+    absmax = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _abi_ring(X, G, out, lt, rt, 0.1, absmax)
+    assert int(absmax.item()) == 0
+
+
+def test_single_column_and_ragged_tails_all_dtypes():
+    """d = 1 and d one past a vector multiple: the TMA tile path's ragged tail and the
+    scalar path agree with the oracle (fp64 bit-exact, fp32 rounded once)."""
+    for L, d in [(8, 1), (16, 5), (64, 129), (64, 4097)]:
+        X = _rand(L, d, torch.float64, 11 * L + d)
+        G = _rand(L, d, torch.float64, 5 * d + 3)
+        lt, rt, left, right = _tables(L, 99, d)
+        out = mixing.ring_mix_sgd(X, G, 0.02, lt, rt)
+        ref = O.c_ring_mix_sgd(_host_dL(X), _host_dL(G), 0.02, left, right)
+        assert np.array_equal(_host_dL(out), ref)
+        X32, G32 = X.float(), G.float()
+        out32 = mixing.ring_mix_sgd(X32, G32, 0.02, lt, rt)
+        ref32 = O.c_ring_mix_sgd(_host_dL(X32), _host_dL(G32), 0.02, left, right)
+        assert np.array_equal(_host_dL(out32), ref32.astype(np.float32).astype(np.float64))
