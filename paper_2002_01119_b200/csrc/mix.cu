@@ -579,7 +579,8 @@ template <typename T, int MODE>
 static int dispatch(const void* W, const void* G, void* out, int L, long long d, long long ldw,
                     long long ldg, long long ldo, const int32_t* left, const int32_t* right,
                     double lr, unsigned long long* absmax, unsigned int* mismatch, void* stream) {
-  if (L < 1 || d < 0 || W == nullptr || out == nullptr) {
+  // d == 0 (empty parameter vectors) is valid and may come with null buffers
+  if (L < 1 || d < 0 || (d > 0 && (W == nullptr || out == nullptr))) {
     set_error("invalid arguments: L=%d d=%lld", L, d);
     return RM_EINVAL;
   }
@@ -607,11 +608,11 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
     set_error("spsgd needs gradients");
     return RM_EINVAL;
   }
+  if (d == 0) return RM_OK;
   if (W == out) {
     set_error("in-place mixing is a read-after-write hazard across learners; use distinct buffers");
     return RM_EINVAL;
   }
-  if (d == 0) return RM_OK;
   MixArgs a{};
   a.W = W;
   a.G = G;

@@ -187,7 +187,7 @@ def _prep_out(W: torch.Tensor, out: torch.Tensor | None) -> torch.Tensor:
         out = empty_learner_major(L, d, W.dtype, W.device)
     _same(W, out, "out")
     _rows(out, "out")
-    if out.data_ptr() == W.data_ptr():
+    if W.numel() and out.data_ptr() == W.data_ptr():
         raise ValueError("in-place mixing is a read-after-write hazard across learners; "
                          "use distinct buffers")
     return out
