@@ -12,11 +12,12 @@ prints ONE JSON line on rank 0.
 * N = 1 workload: BASELINE.json configs[1] — RAD-PSGD, 64 learners x 25,557,032
   fp32 params (ResNet-50-sized flat vectors), synthetic N(0,1) weights and
   gradients, lr = 0.01.  3 x 6.54 GB buffers >> 126 MB L2, so no L2 flush.
-* N > 1 (torchrun, one process per GPU), strong scaling of the same C2
-  problem: `--layout coord` (default) gives every rank a column stripe of all
-  64 learners (rows of W are independent) and every rank derives
-  the same permutation from the shared seed: no data-path
-  collective.  `--layout learner` (north-star (d)) gives every rank 64/N
+* N > 1 (torchrun, one process per GPU): `--layout coord` (default) gives every
+  rank a column stripe of all 64 learners (rows of W are independent, SURVEY
+  §8(e)) and every rank derives the same permutation from the shared seed
+  (PAPER.md:131): no data-path collective.  Default `--scaling weak`: every rank
+  owns a full C2-width stripe (64 x 25,557,032) of a 64 x (N * 25,557,032)
+  problem, so per-GPU work is fixed; `--scaling strong` splits the C2 problem.  `--layout learner` (north-star (d)) gives every rank 64/N
   learners; the fused kernel pulls remote neighbour rows over NVLink (CUDA IPC)
   and a 4-byte NCCL all-reduce orders consecutive steps.
 * `value`: whole-job learner-params / s, device time (CUDA events), max over ranks.
@@ -75,6 +76,10 @@ def parse():
     ap.add_argument("--strategy", choices=["rand_psgd", "adpsgd_fixed", "d1d"],
                     default="rand_psgd")
     ap.add_argument("--layout", choices=["coord", "learner", "position"], default="coord")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="coord layout at N > 1: weak = every rank owns a full-width "
+                         "(L x dim) column stripe of an L x (N*dim) problem; strong = the "
+                         "L x dim problem split N ways")
     ap.add_argument("--d1d-collective", choices=["auto", "nvls", "nccl"], default="auto")
     ap.add_argument("--d1d-chunk-cols", type=int, default=1 << 22,
                     help="learner-sharded D1D pipeline chunk (columns); 0 = one chunk")
@@ -264,6 +269,25 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def host_pinned_budget() -> int:
+    """Bytes of pinned host memory the whole job may use for the e2e variants (a
+    quarter of the host's available RAM)."""
+    try:
+        import psutil
+        return int(psutil.virtual_memory().available) // 4
+    except Exception:
+        return 32 << 30
+
+
+def weak(args, ws):
+    """Weak scaling: coordinate stripes of fixed width per rank (no data-path collective)."""
+    return ws > 1 and args.layout == "coord" and args.scaling == "weak"
+
+
+def total_dim(args, ws):
+    return args.dim * ws if weak(args, ws) else args.dim
+
+
 def config_dict(args, ws):
     return {"workload": f"{args.strategy} mix+SGD step, {args.learners} learners x "
                         f"{args.dim} params/learner ({'ResNet-50-sized' if args.dim == D_DEFAULT else 'custom'}"
@@ -271,8 +295,12 @@ def config_dict(args, ws):
             "learners": args.learners, "params_per_learner": args.dim,
             "strategy": args.strategy, "lr": LR, "perm_seed": SEED,
             "layout": args.layout if ws > 1 else "single-gpu",
-            "parallelism": (f"{args.layout}-sharded over {ws} GPUs (strong scaling: the whole "
-                            f"{args.learners} x {args.dim} problem)") if ws > 1 else "1 GPU",
+            "parallelism": ((f"coord-sharded over {ws} GPUs (weak scaling: every rank owns a "
+                             f"{args.learners} x {args.dim} column stripe of the "
+                             f"{args.learners} x {args.dim * ws} problem; shared-seed "
+                             f"permutations, no data-path collective)") if weak(args, ws) else
+                            (f"{args.layout}-sharded over {ws} GPUs (strong scaling: the whole "
+                             f"{args.learners} x {args.dim} problem)")) if ws > 1 else "1 GPU",
             "l2": "inputs (3 x L x d x 4 B) far larger than the 126 MB L2; no flush needed",
             **({"d1d_collective": args.d1d_collective, "d1d_chunk_cols": args.d1d_chunk_cols}
                if ws > 1 and args.strategy == "d1d" and args.layout == "learner" else {})}
@@ -307,7 +335,10 @@ class Workload:
             return X
 
         if self.layout in ("single", "coord"):
-            cols = D.CoordinateShards(d, ws, rank).width if self.layout == "coord" else d
+            if self.layout == "coord":
+                cols = d if args.scaling == "weak" else D.CoordinateShards(d, ws, rank).width
+            else:
+                cols = d
             self.rows, self.cols = L, cols
             self.W = [synth(L, cols), mixing.empty_learner_major(L, cols, dtype, dev)]
             self.G = synth(L, cols)
@@ -482,7 +513,7 @@ def run_ours(args):
         elapsed_ms = float(t.item())
     clock_info = clocks.stop() if clocks else None
 
-    params_per_step = L * d                       # strong scaling: the whole C2 problem
+    params_per_step = L * total_dim(args, ws)     # all ranks' learner-params per step
     value = params_per_step * args.steps / (elapsed_ms / 1e3)
     kern_avg_s = statistics.mean(kern_ms) / 1e3
     bpp = BYTES_PER_PARAM[args.dtype]
@@ -495,9 +526,12 @@ def run_ours(args):
     e2e = None
     want_e2e = not args.no_e2e and args.dtype == "float32"
     if want_e2e and (ws == 1 or wl.layout == "coord"):
-        # every rank drives its own column stripe (own PCIe link), max over ranks
+        # every rank drives its own column stripe (own PCIe link), max over ranks.
+        # Pinned host memory per rank: G (L x cols) for the resident e2e, 3x that for
+        # the host-arrays variant — the variant only where the whole job stays small.
         ms_res = run_e2e_resident(args, torch, wl, dev)
-        ms_host = run_e2e(args, torch, mixing, dev, cols=wl.cols) if not uniform else None
+        host_ok = not uniform and 3 * wl.local_params * 4 * ws <= host_pinned_budget()
+        ms_host = run_e2e(args, torch, mixing, dev, cols=wl.cols) if host_ok else None
         if ws > 1:
             t = torch.tensor([ms_res, ms_host or 0.0], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -521,7 +555,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak" if weak(args, ws) else "strong",
+            "vs_baseline": None,
             "dtype": {"float32": "f32", "bfloat16": "bf16", "float64": "f64"}[args.dtype],
             "data": "synthetic: N(0,1) weights and gradients generated on device (torch "
                     "Generator), permutations from the device generator (seed 12345)",
@@ -552,7 +587,8 @@ def run_e2e_resident(args, torch, wl, dev):
     from paper_2002_01119_b200 import mixing as M
 
     L, cols = wl.L, wl.cols
-    G_host = wl.G.cpu().pin_memory()
+    G_host = torch.empty(wl.G.shape, dtype=wl.G.dtype, pin_memory=True)
+    G_host.copy_(wl.G)
     Gd = [wl.G, M.empty_learner_major(L, cols, wl.G.dtype, dev)]
     W = wl.W
     res_host = torch.zeros(args.e2e_steps + 4, dtype=torch.int64).pin_memory()
@@ -633,7 +669,7 @@ def run_e2e(args, torch, mixing, dev, cols=None):
 
 def e2e_line(args, ms, ws):
     """Host-arrays variant: W, G from host and W' back every step (12 B/param over PCIe)."""
-    L, d = args.learners, args.dim
+    L, d = args.learners, total_dim(args, ws)
     return {"value": L * d / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": 2 * L * d * 4 + 2 * L * 4 * ws,
             "d2h_bytes_per_step": L * d * 4,
@@ -644,7 +680,7 @@ def e2e_line(args, ms, ws):
 
 
 def e2e_resident_line(args, ms, ws):
-    L, d = args.learners, args.dim
+    L, d = args.learners, total_dim(args, ws)
     return {"value": L * d / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": L * d * 4, "d2h_bytes_per_step": 8 * ws,
             "ms_per_step": ms, "steps": args.e2e_steps,
