@@ -259,7 +259,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if weak(args, ws) else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic N(0,1) weights and gradients",
         "config": config_dict(args, ws),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
