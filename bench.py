@@ -270,6 +270,37 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def p2p_peaks():
+    p = ROOT / "profiles" / "p2p_peaks.json"
+    try:
+        z = json.loads(p.read_text())
+        return float(z["peer_read_gbs"]), float(z["peer_write_gbs"]), z["source"]
+    except Exception:
+        return 900.0, 900.0, "NVLink 5 nominal per direction (no measured file)"
+
+
+def nvlink_traffic(layout, L, d, esz, ws, perm, inv, left, right):
+    """Per-rank NVLink bytes per step of the learner-sharded RAD layouts, averaged over
+    the timed steps (host numpy on the device-generated tables; rows s = step k,
+    perm/inv have one extra row for step k+1).  Returns [(read, write)] per rank."""
+    from paper_2002_01119_b200.distributed import balanced_split
+    bounds = balanced_split(L, ws)
+    nsteps = left.shape[0]
+    out = []
+    for b, e in bounds:
+        rd = wr = 0
+        for s in range(nsteps):
+            if layout == "learner":      # pull: distinct remote neighbour rows
+                nb = set(left[s, b:e].tolist()) | set(right[s, b:e].tolist())
+                rd += sum(1 for x in nb if not b <= x < e)
+            else:                        # position: 2 boundary rows in, relabel stores out
+                rd += 2 if ws > 1 else 0
+                nxt = inv[s + 1][perm[s, b:e]]
+                wr += int(((nxt < b) | (nxt >= e)).sum())
+        out.append((rd * d * esz / nsteps, wr * d * esz / nsteps))
+    return out
+
+
 def host_pinned_budget() -> int:
     """Bytes of pinned host memory the whole job may use for the e2e variants (a
     quarter of the host's available RAM)."""
@@ -522,6 +553,25 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     achieved = algo_bytes / kern_avg_s / 1e9
     key = f"mix_{args.strategy}_{args.dtype}_L{L}_d{d}" if ws == 1 else None
+    nvlink = None
+    if ws > 1 and wl.layout in ("learner", "position") and not uniform and rank == 0:
+        k0 = args.warmup
+        tb = mixing.permutation_tables(L, SEED, k0, args.steps + 1, dev)
+        host = [t.cpu().numpy().astype(np.int64) for t in (tb.perm, tb.inv, tb.left, tb.right)]
+        per_rank = nvlink_traffic(wl.layout, L, d, bpp // 3, ws, host[0], host[1],
+                                  host[2][:-1], host[3][:-1])
+        prd, pwr, psrc = p2p_peaks()
+        rd = max(r for r, _ in per_rank)
+        wr = max(w for _, w in per_rank)
+        ach_rd, ach_wr = rd / kern_avg_s / 1e9, wr / kern_avg_s / 1e9
+        nvlink = {"bound": "nvlink", "unit": "GB/s",
+                  "read_bytes_per_step": rd, "write_bytes_per_step": wr,
+                  "achieved_read": ach_rd, "achieved_write": ach_wr,
+                  "peak_read": prd, "peak_write": pwr,
+                  "frac": max(ach_rd / prd, ach_wr / pwr),
+                  "note": "busiest rank's peer bytes per step (pull: distinct remote "
+                          "neighbour rows; position: 2 boundary rows read + relabel stores) "
+                          "over rank 0's mean kernel time", "peak_source": psrc}
     traffic = ncu_traffic(key) if key else None
 
     e2e = None
@@ -570,6 +620,7 @@ def run_ours(args):
                          "avg_launch_ms": kern_avg_s * 1e3, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            **({"nvlink": nvlink} if nvlink else {}),
             "gpu_launches": launches["perm"] + launches["mix"],
             "gpu_launches_detail": launches,
             "clocks": clock_info,

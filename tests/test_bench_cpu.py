@@ -1,0 +1,58 @@
+"""Host-side pieces of bench.py (no GPU): the NVLink traffic model of the
+learner-sharded layouts and the weak/strong scaling bookkeeping."""
+
+from __future__ import annotations
+
+import argparse
+import importlib.util
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", ROOT / "bench.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def _tables(perms):
+    perm = np.array(perms, dtype=np.int64)
+    inv = np.argsort(perm, axis=1)
+    L = perm.shape[1]
+    left = np.array([[inv[s][(perm[s][j] - 1) % L] for j in range(L)] for s in range(len(perm))])
+    right = np.array([[inv[s][(perm[s][j] + 1) % L] for j in range(L)] for s in range(len(perm))])
+    return perm, inv, left, right
+
+
+def test_nvlink_traffic_identity_ring():
+    b = _bench()
+    perm, inv, left, right = _tables([list(range(8))] * 2)
+    # pull: rank 0 owns learners 0..3, neighbours 7 and 4 are remote
+    pull = b.nvlink_traffic("learner", 8, 10, 4, 2, perm, inv, left[:1], right[:1])
+    assert pull == [(2 * 10 * 4, 0), (2 * 10 * 4, 0)]
+    # position layout, unchanged order: 2 boundary rows in, no relabel stores
+    pos = b.nvlink_traffic("position", 8, 10, 4, 2, perm, inv, left[:1], right[:1])
+    assert pos == [(2 * 10 * 4, 0), (2 * 10 * 4, 0)]
+
+
+def test_nvlink_traffic_reversal_moves_every_row():
+    b = _bench()
+    perm, inv, left, right = _tables([list(range(8)), list(range(7, -1, -1))])
+    pos = b.nvlink_traffic("position", 8, 1, 4, 2, perm, inv, left[:1], right[:1])
+    # learner at position x moves to position 7 - x: every output crosses ranks
+    assert pos == [(2 * 4, 4 * 4), (2 * 4, 4 * 4)]
+
+
+def test_weak_scaling_only_for_coordinate_stripes():
+    b = _bench()
+    a = argparse.Namespace(layout="coord", scaling="weak", dim=100, learners=4,
+                           strategy="rand_psgd", d1d_collective="auto", d1d_chunk_cols=0)
+    assert b.weak(a, 1) is False and b.total_dim(a, 1) == 100
+    assert b.weak(a, 4) is True and b.total_dim(a, 4) == 400
+    a.layout = "learner"
+    assert b.weak(a, 4) is False and b.total_dim(a, 4) == 100
+    assert "weak scaling" not in b.config_dict(a, 4)["parallelism"]
