@@ -193,7 +193,7 @@ class ClockSampler:
 
 def cpu_reference_step_fn(L: int, d_sample: int, uniform: bool):
     """The reference's step arithmetic on a (d_sample, L) fp64 C-order sample:
-    apply_mixing(W, T) - lr * G (simulation.py:267, mixing.py:143-162), restated
+    apply_mixing(W, T) - lr * G (simulation.py:267, mixing.py:106-125), restated
     by the oracle (oracle/ringmix_oracle.py numpy_gossip_step)."""
     from oracle import ringmix_oracle as O
 

@@ -5,22 +5,22 @@
  * no FFI; its plugin surface for this path is a set of Python functions.  Each
  * entry point below replaces one of them (file:line under /root/reference):
  *
- *   rm_perm_tables        <- mixing.permutation_for_step     pkg/src/ringmix/mixing.py:116-123
+ *   rm_perm_tables        <- mixing.permutation_for_step     pkg/src/ringmix/mixing.py:79-86
  *                            (+ the conjugation T0[p, p] of  simulation.py:299-300 /
- *                             mixing.conjugate_by_permutation mixing.py:126-140,
+ *                             mixing.conjugate_by_permutation mixing.py:89-103,
  *                             reduced to neighbour tables)
  *   rm_perm_sequential    <- seeding.stream + repeated        seeding.py:35-37,
- *                            mixing.sample_permutation        mixing.py:109-113
+ *                            mixing.sample_permutation        mixing.py:72-76
  *                            as drawn by monte_carlo_consensus spectral.py:273-277
  *   rm_pcg64_raw          <- numpy PCG64.random_raw under SeedSequence (pins the core)
  *   rm_ring_mix_sgd_*     <- simulation._gossip_step          simulation.py:263-268
- *                            = apply_mixing(W, T) - lr*G      mixing.py:143-162
+ *                            = apply_mixing(W, T) - lr*G      mixing.py:106-125
  *                            for T = ring or ring[p, p]       (step_rand_psgd :285-301,
  *                                                              step_dpsgd_fixed :271-273,
  *                                                              step_adpsgd_fixed :276-282)
  *                            with the fused _check_divergence  simulation.py:390-395
  *   rm_mean_sgd_*         <- step_d1d / uniform apply_mixing   simulation.py:304-312,
- *                                                              mixing.py:159-161
+ *                                                              mixing.py:122-124
  *   rm_spsgd_*            <- step_spsgd                        simulation.py:251-260
  *   rm_*_host_f32         <- the same step on HOST buffers (H2D, kernel, D2H pipelined)
  *   rm_ipc_* / rm_shard_* <- (no reference counterpart: the reference simulates all
@@ -89,7 +89,7 @@ int rm_pcg64_raw(const uint32_t* entropy_words, int n_words, int count, uint64_t
 
 /* ---- fused mix + SGD:  Wout[j] = (W[left j] + W[j] + W[right j])/3 - lr*G[j] ----
  * G may be NULL (pure apply_mixing).  L == 3 takes the exact column-mean path
- * like the reference (mixing.py:159-161).  fp32/fp64 compute in fp64 with the
+ * like the reference (mixing.py:122-124).  fp32/fp64 compute in fp64 with the
  * reference's rounding sequence; bf16 (uint16_t storage) computes in fp32. */
 int rm_ring_mix_sgd_f32(const float* W, const float* G, float* Wout, const int32_t* left,
                         const int32_t* right, int L, int64_t d, int64_t ldw, int64_t ldg,

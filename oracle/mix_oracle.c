@@ -5,7 +5,7 @@
  * rounding sequence is explicit and independent of which OpenBLAS kernel the
  * host CPU happens to select:
  *
- *  ring mix (reference mixing.py:143-162 `W @ T`, T = ring[p, p] from
+ *  ring mix (reference mixing.py:106-125 `W @ T`, T = ring[p, p] from
  *  simulation.py:299-300): each output column j has exactly three nonzero
  *  weights fl(1/3) at rows {left[j], j, right[j]}.  OpenBLAS dgemm accumulates
  *  the k-loop in ascending k with FMA (zero products add exactly), so
@@ -14,7 +14,7 @@
  *  numpy 2.3.5 / OpenBLAS 0.3.30 (Haswell kernel) on this host by
  *  tests/test_oracle.py.
  *
- *  uniform mix (mixing.py:159-161 `W.mean(axis=1)` then tile): numpy's
+ *  uniform mix (mixing.py:122-124 `W.mean(axis=1)` then tile): numpy's
  *  pairwise summation along the contiguous learner axis
  *  (numpy/_core/src/umath/loops_utils.h.src, DOUBLE_pairwise_sum), then
  *  true_divide by L.

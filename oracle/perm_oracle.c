@@ -5,8 +5,8 @@
  * only as the checker.
  *
  * Plain-C restatement of the integer chain behind the reference's
- * permutation_for_step (reference: pkg/src/ringmix/mixing.py:116-123) and
- * sample_permutation (mixing.py:109-113), whose randomness comes from
+ * permutation_for_step (reference: pkg/src/ringmix/mixing.py:79-86) and
+ * sample_permutation (mixing.py:72-76), whose randomness comes from
  * seeding.stream (pkg/src/ringmix/seeding.py:27-37):
  *
  *     np.random.default_rng(np.random.SeedSequence((seed, TAG, idx...)))

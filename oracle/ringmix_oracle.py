@@ -8,15 +8,15 @@ imports this module; its CUDA path fails loudly when its library is missing.
 What is restated, and where it comes from (paths under /root/reference):
 
 * permutation_for_step / sample_permutation / seeding.stream
-  (pkg/src/ringmix/mixing.py:109-123, seeding.py:27-37): numpy 2.3.5's
+  (pkg/src/ringmix/mixing.py:72-86, seeding.py:27-37): numpy 2.3.5's
   SeedSequence -> PCG64 -> Generator.permutation chain, restated twice:
   in plain C (oracle/perm_oracle.c, fast) and in pure Python below
   (`py_permutation`, small cases only).
 * neighbour tables of the conjugated ring T = ring[p, p]
-  (simulation.py:299-300, mixing.py:126-140): left[j] = inv[(p[j]-1) % L],
+  (simulation.py:299-300, mixing.py:89-103): left[j] = inv[(p[j]-1) % L],
   right[j] = inv[(p[j]+1) % L].
 * the step arithmetic (simulation.py:263-268 `apply_mixing(W, T) - lr*G`,
-  mixing.py:143-162): `numpy_*` functions perform the reference's own numpy
+  mixing.py:106-125): `numpy_*` functions perform the reference's own numpy
   operations on the reference's (d, L) fp64 layout; `c_*` functions are the
   scalar C restatement in oracle/mix_oracle.c with an explicit rounding
   sequence (FMA chain in ascending learner index for rings, numpy pairwise
@@ -282,7 +282,7 @@ def c_standard_normal(n: int, *entropy: int) -> tuple[np.ndarray, int]:
 # --------------------------------------------------------------------------
 
 def ring_matrix(L: int) -> np.ndarray:
-    """mixing.py:80-99 (1/3 on the diagonal and both ring neighbours)."""
+    """mixing.py:43-62 (1/3 on the diagonal and both ring neighbours)."""
     if L < 3:
         raise ValueError(f"degenerate ring topology: need at least 3 learners, got {L}")
     T = np.zeros((L, L))
@@ -294,7 +294,7 @@ def ring_matrix(L: int) -> np.ndarray:
 
 
 def numpy_apply_mixing(W_dL: np.ndarray, T: np.ndarray) -> np.ndarray:
-    """mixing.py:143-162, the reference's own numpy operations."""
+    """mixing.py:106-125, the reference's own numpy operations."""
     L = T.shape[0]
     if np.all(T == 1.0 / L):
         return np.tile(W_dL.mean(axis=1, keepdims=True), (1, L))

@@ -1,7 +1,7 @@
 // Fused learner-averaging kernels: gossip mix + SGD (RAD / AD / D-PSGD),
 // uniform mean + SGD (D1D), and S-PSGD — the reference's
 //   simulation._gossip_step (pkg/src/ringmix/simulation.py:263-268)
-//   W_next = apply_mixing(W, T) - lr * G        (mixing.py:143-162)
+//   W_next = apply_mixing(W, T) - lr * G        (mixing.py:106-125)
 // and step_spsgd (simulation.py:251-260), one HBM pass per step.
 //
 // HBM layout: learner-major (L, d) rows with leading dimension ld (elements);
@@ -589,7 +589,7 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
     return RM_EINVAL;
   }
   if (MODE == kRing && L == 3) {
-    // mixing.py:159-161: every entry of the 3-ring equals 1/L, so the
+    // mixing.py:122-124: every entry of the 3-ring equals 1/L, so the
     // reference takes the exact column-mean path.
     return dispatch<T, kMean>(W, G, out, L, d, ldw, ldg, ldo, nullptr, nullptr, lr, absmax,
                               nullptr, stream);

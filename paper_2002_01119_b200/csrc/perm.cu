@@ -1,5 +1,5 @@
 // On-device permutation generator, bit-exact with the reference's
-// permutation_for_step (pkg/src/ringmix/mixing.py:116-123) and the sequential
+// permutation_for_step (pkg/src/ringmix/mixing.py:79-86) and the sequential
 // draws of monte_carlo_consensus (spectral.py:273-277).
 //
 // The reference draws through numpy: SeedSequence(entropy) -> PCG64 (XSL-RR

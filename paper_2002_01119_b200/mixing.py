@@ -1,6 +1,6 @@
 """Mixing matrices, permutations and the fused mix kernels (mirror of mixing.py).
 
-Reference: pkg/src/ringmix/mixing.py:1-178.
+Reference: pkg/src/ringmix/mixing.py:1-141.
 
 L x L objects (ring/uniform matrices, conjugation, the stochasticity check)
 are host fp64 numpy exactly as in the reference: they are tiny and off the
@@ -33,7 +33,7 @@ _DT_SUFFIX = {torch.float32: "f32", torch.float64: "f64", torch.bfloat16: "bf16"
 
 @dataclass(frozen=True)
 class StochasticityReport:
-    """Result of `verify_doubly_stochastic`.  Reports, never raises (mixing.py:69-77)."""
+    """Result of `verify_doubly_stochastic`.  Reports, never raises (mixing.py:32-40)."""
 
     max_row_error: float
     max_col_error: float
@@ -43,7 +43,7 @@ class StochasticityReport:
 
 
 def build_ring_matrix(n_learners: int) -> np.ndarray:
-    """1/3-weighted ring (mixing.py:80-99); L < 3 is degenerate and rejected."""
+    """1/3-weighted ring (mixing.py:43-62); L < 3 is degenerate and rejected."""
     if n_learners < 3:
         raise ValueError(
             f"degenerate ring topology: need at least 3 learners, got {n_learners}")
@@ -56,14 +56,14 @@ def build_ring_matrix(n_learners: int) -> np.ndarray:
 
 
 def build_uniform_matrix(n_learners: int) -> np.ndarray:
-    """All entries 1/L (mixing.py:102-106)."""
+    """All entries 1/L (mixing.py:65-69)."""
     if n_learners < 1:
         raise ValueError(f"need at least 1 learner, got {n_learners}")
     return np.full((n_learners, n_learners), 1.0 / n_learners)
 
 
 def sample_permutation(n: int, rng: DeviceStream) -> np.ndarray:
-    """Uniform random permutation of range(n) drawn from a device stream (mixing.py:109-113)."""
+    """Uniform random permutation of range(n) drawn from a device stream (mixing.py:72-76)."""
     if n < 1:
         raise ValueError(f"need n >= 1, got {n}")
     if not isinstance(rng, DeviceStream):
@@ -111,13 +111,13 @@ def permutation_tables(n: int, shared_seed: int, step0: int = 0, nsteps: int = 1
 
 
 def permutation_for_step(n: int, shared_seed: int, step: int) -> np.ndarray:
-    """Permutation for iteration `step`, a pure function of (shared_seed, step) (mixing.py:116-123)."""
+    """Permutation for iteration `step`, a pure function of (shared_seed, step) (mixing.py:79-86)."""
     tabs = permutation_tables(n, shared_seed, step, 1)
     return tabs.perm[0].to(torch.int64).cpu().numpy()
 
 
 def conjugate_by_permutation(T: np.ndarray, perm) -> np.ndarray:
-    """Entry (i, j) = T[perm[i], perm[j]] (mixing.py:126-140)."""
+    """Entry (i, j) = T[perm[i], perm[j]] (mixing.py:89-103)."""
     perm = np.asarray(perm)
     n = T.shape[0]
     if T.shape != (n, n):
@@ -128,7 +128,7 @@ def conjugate_by_permutation(T: np.ndarray, perm) -> np.ndarray:
 
 
 def verify_doubly_stochastic(T, tol: float = 1e-12) -> StochasticityReport:
-    """Row/column sums and non-negativity to `tol`; never raises (mixing.py:165-178)."""
+    """Row/column sums and non-negativity to `tol`; never raises (mixing.py:128-141)."""
     T = np.asarray(T)
     if T.ndim != 2 or T.shape[0] != T.shape[1]:
         return StochasticityReport(np.inf, np.inf, -np.inf, tol, False)
@@ -199,7 +199,7 @@ def ring_mix_sgd(W: torch.Tensor, G: torch.Tensor | None, lr: float, left: torch
     """out[j] = (W[left j] + W[j] + W[right j]) / 3 - lr * G[j]   (one fused HBM pass).
 
     simulation._gossip_step with T = ring[p, p] (simulation.py:263-301).  L == 3
-    takes the reference's exact column-mean path (mixing.py:159-161).
+    takes the reference's exact column-mean path (mixing.py:122-124).
     `absmax` (optional int64 CUDA scalar, zeroed by the caller) receives the
     bit pattern of max|out| as a double (fused _check_divergence).
     """
@@ -321,7 +321,7 @@ def ring_structure(T: np.ndarray) -> tuple[np.ndarray, np.ndarray] | None:
 
 
 def apply_mixing(W, T):
-    """One averaging step W @ T, columns of W are learners (mixing.py:143-162).
+    """One averaging step W @ T, columns of W are learners (mixing.py:106-125).
 
     W: a (d, L) numpy array (promoted to float64, as `W @ T` does in the
     reference) or a (d, L) CUDA tensor (float32/float64/bfloat16; a `.T` view of
