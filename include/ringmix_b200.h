@@ -23,8 +23,20 @@
  *                                                              mixing.py:122-124
  *   rm_spsgd_*            <- step_spsgd                        simulation.py:251-260
  *   rm_*_host_f32         <- the same step on HOST buffers (H2D, kernel, D2H pipelined)
- *   rm_ipc_* / rm_shard_* <- (no reference counterpart: the reference simulates all
- *                            learners in one process; these shard them over GPUs)
+ *   rm_quadratic_grad_*   <- simulation.gradient_matrix with   simulation.py:226-238,
+ *                            QuadraticObjective.stochastic_   objectives.py:84-90
+ *                            gradient (bit-exact numpy normals)
+ *   rm_standard_normal_f64 <- seeding.stream(...).standard_normal  seeding.py:35-37
+ *   rm_trace_stats_*      <- run_training._record: consensus   simulation.py:398-409,
+ *                            distance + loss_columns + loss   :359-362, objectives.py:77-79
+ *   rm_column_mean_*      <- W.mean(axis=1) of step_d1d        mixing.py:122-124
+ *   rm_ring_mix_batched_f64 <- product @ T_k of                spectral.py:273-279
+ *                            monte_carlo_consensus
+ *   rm_ipc_* / rm_shard_* / rm_pos_* / rm_partial_sum_* / rm_apply_mean_sgd_* /
+ *   rm_nvls_mean_f64      <- (no reference counterpart: the reference simulates all
+ *                            learners in one process; these shard them over GPUs —
+ *                            the step they compute is still simulation.py:263-268 /
+ *                            :304-312)
  *
  * Conventions
  *   - All compute pointers are caller-owned DEVICE memory unless the name says
