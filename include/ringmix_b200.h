@@ -70,6 +70,11 @@ extern "C" {
 const char* rm_last_error(void);
 int rm_version(void);
 int rm_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+/* For FFI callers without a CUDA runtime of their own (the reference's numpy code through
+ * ctypes): a device buffer (e.g. the host-step workspace), and a stream synchronise. */
+int rm_device_alloc(int64_t bytes, void** ptr);
+int rm_device_free(void* ptr);
+int rm_stream_synchronize(void* stream);
 
 /* ---- permutations (bit-exact with numpy 2.3.5 SeedSequence/PCG64/permutation) ----
  * prefix_words: the entropy words of (seed, tag) — numpy's

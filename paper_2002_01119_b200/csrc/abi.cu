@@ -48,3 +48,30 @@ extern "C" int rm_device_info(int device, int* sms, int* major, int* minor) {
   if (minor) *minor = p.minor;
   return 0;
 }
+
+// ---- helpers for FFI callers without a CUDA runtime of their own (e.g. the
+// reference's numpy code through ctypes): device buffers and stream sync ----
+extern "C" int rm_device_alloc(int64_t bytes, void** ptr) {
+  if (ptr == nullptr || bytes < 0) {
+    rm::set_error("invalid allocation arguments");
+    return RM_EINVAL;
+  }
+  *ptr = nullptr;
+  if (bytes == 0) return 0;
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e != cudaSuccess) return rm::fail_cuda(e, "cudaMalloc");
+  return 0;
+}
+
+extern "C" int rm_device_free(void* ptr) {
+  if (ptr == nullptr) return 0;
+  cudaError_t e = cudaFree(ptr);
+  if (e != cudaSuccess) return rm::fail_cuda(e, "cudaFree");
+  return 0;
+}
+
+extern "C" int rm_stream_synchronize(void* stream) {
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return rm::fail_cuda(e, "cudaStreamSynchronize");
+  return 0;
+}

@@ -604,11 +604,11 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
       return RM_EINVAL;
     }
   }
+  if (d == 0) return RM_OK;
   if (MODE == kSpsgd && G == nullptr) {
     set_error("spsgd needs gradients");
     return RM_EINVAL;
   }
-  if (d == 0) return RM_OK;
   if (W == out) {
     set_error("in-place mixing is a read-after-write hazard across learners; use distinct buffers");
     return RM_EINVAL;

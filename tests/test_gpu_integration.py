@@ -1,0 +1,75 @@
+"""The reference-side ctypes binding shown in INTEGRATION.md, executed as written
+(only the library path is made absolute): a maintainer's copy of it must produce
+the same steps as the drop-in package and the oracle."""
+
+from __future__ import annotations
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ringmix_oracle as O
+from paper_2002_01119_b200 import _lib, mixing
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _binding():
+    text = (ROOT / "INTEGRATION.md").read_text()
+    sec = text[text.index("## 2. C-ABI"):text.index("## 3. Multi-GPU")]
+    code = "\n".join(re.findall(r"```python\n(.*?)```", sec, flags=re.S))
+    code = code.replace('"libringmix_b200.so"', repr(str(_lib.LIB_PATH)))
+    ns: dict = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    return ns
+
+
+def _tables(L, seed, k):
+    p = O.c_permutation(L, seed, k)
+    _, left, right = O.neighbour_tables(p)
+    return left.astype(np.int32), right.astype(np.int32)
+
+
+def test_host_buffer_binding_matches_oracle():
+    b = _binding()
+    L, d = 16, 100_003
+    rng = np.random.default_rng(3)
+    W = rng.standard_normal((L, d)).astype(np.float32)
+    G = rng.standard_normal((L, d)).astype(np.float32)
+    left, right = _tables(L, 77, 5)
+    ws = b["Workspace"](L, chunk_cols=1 << 14)
+    out = b["gossip_step_f32"](W, G, 0.05, left, right, ws)
+    ref = O.c_ring_mix_sgd(W.T.astype(np.float64), G.T.astype(np.float64), 0.05, left, right)
+    assert np.array_equal(out, ref.T.astype(np.float32))
+    with pytest.raises(ValueError):
+        b["gossip_step_f32"](W[:2], G[:2], 0.05, left[:2], right[:2], ws)   # L < 3
+
+
+def test_device_binding_matches_drop_in():
+    b = _binding()
+    L, d, seed, k = 64, 4099, 1234, 17
+    X = mixing.empty_learner_major(L, d, torch.float32, "cuda").normal_()
+    G = mixing.empty_learner_major(L, d, torch.float32, "cuda").normal_()
+    out = mixing.empty_learner_major(L, d, torch.float32, "cuda")
+
+    class T:
+        pass
+    t = T()
+    bufs = [torch.empty(L, dtype=torch.int32, device="cuda") for _ in range(4)]
+    t.perm, t.inv, t.left, t.right = (x.data_ptr() for x in bufs)
+    absmax = torch.zeros(1, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    b["rad_step"](X.data_ptr(), G.data_ptr(), out.data_ptr(), L, d, X.stride(0), 0.01, seed, k,
+                  t, absmax.data_ptr(), None)
+    torch.cuda.synchronize()
+    tabs = mixing.permutation_tables(L, seed, k, 1, "cuda")
+    lt, rt = tabs.step(k)
+    ref = mixing.ring_mix_sgd(X, G, 0.01, lt, rt)
+    torch.cuda.synchronize()
+    assert torch.equal(bufs[0].long(), tabs.perm[0].long())
+    assert torch.equal(out, ref)
+    assert absmax.item() > 0
