@@ -13,81 +13,111 @@
 
 namespace rm {
 
-constexpr int kTrThreads = 256;
+constexpr int kTrThreads = 256;  // = columns per tile
 constexpr int kTrMaxL = 128;
+constexpr int kTrWarps = kTrThreads / 32;
+constexpr int kTrPer = kTrMaxL / kTrWarps;  // learners per warp (at most)
 
+// numpy's pairwise sum of column c over the L learners (n < 8: in order; 8..128:
+// eight interleaved partial sums, combined in numpy's order, then the tail).
 template <typename T>
-__global__ void __launch_bounds__(kTrThreads)
+__device__ __forceinline__ double column_pairwise(const T* p, int L, long long ld) {
+  using E = Elem<T>;
+  if (L < 8) {
+    double res = -0.0;
+    for (int i = 0; i < L; i++) res = __dadd_rn(res, (double)E::ld(p + (long long)i * ld, 0));
+    return res;
+  }
+  const int n8 = L - (L % 8);
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) r[k] = (double)E::ld(p + (long long)k * ld, 0);
+  for (int i = 8; i < n8; i += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], (double)E::ld(p + (long long)(i + k) * ld, 0));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (int i = n8; i < L; i++) res = __dadd_rn(res, (double)E::ld(p + (long long)i * ld, 0));
+  return res;
+}
+
+// Per tile of 256 columns: (A) one thread per column computes the column mean
+// (coalesced row reads) and the average-model loss term; (B) warp w walks
+// learners w, w+8, ... over the tile (rows are L2-resident from phase A) and
+// accumulates that learner's consensus and loss sums in registers.  One pass
+// over W from HBM; per-learner totals leave with one atomicAdd per CTA.
+template <typename T>
+__global__ void __launch_bounds__(kTrThreads, 4)
     trace_stats_kernel(const T* __restrict__ W, int L, long long d, long long ld,
                        const double* __restrict__ lam, const double* __restrict__ wopt,
                        double* __restrict__ cons_sq, double* __restrict__ loss_col,
                        double* __restrict__ avg_loss) {
   using E = Elem<T>;
-  __shared__ double acc_c[kTrThreads / 32][kTrMaxL];
-  __shared__ double acc_l[kTrThreads / 32][kTrMaxL];
-  __shared__ double acc_a[kTrThreads / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int l = lane; l < L; l += 32) {
-    acc_c[warp][l] = 0.0;
-    acc_l[warp][l] = 0.0;
-  }
-  if (lane == 0) acc_a[warp] = 0.0;
-  __syncwarp();
+  __shared__ double s_mean[kTrThreads];
+  __shared__ double s_lm[kTrThreads];
+  __shared__ double s_wo[kTrThreads];
+  __shared__ double s_red[kTrWarps];
+  __shared__ double s_acc[kTrWarps][kTrPer][2];  // warp-private per-learner sums
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool has_obj = lam != nullptr;
+  if (lane < kTrPer) s_acc[warp][lane][0] = s_acc[warp][lane][1] = 0.0;
+  __syncwarp();
   double a_sum = 0.0;
-  // warp-uniform trip count (shuffles below need full warps)
-  const long long span = (long long)gridDim.x * kTrThreads;
-  const long long first = blockIdx.x * (long long)kTrThreads + warp * 32;
-  for (long long c0 = first; c0 < d; c0 += span) {
-    const long long c = c0 + lane;
-    const bool ok = c < d;
-    double mean = 0.0, lm = 0.0, wo = 0.0;
-    if (ok) {
-      auto get = [&](int i) { return (double)E::ld(W + (long long)i * ld + c, 0); };
-      mean = __ddiv_rn(pairwise_sum<double>(get, 0, L), (double)L);
+  for (long long c0 = blockIdx.x * (long long)kTrThreads; c0 < d;
+       c0 += (long long)gridDim.x * kTrThreads) {
+    const long long c = c0 + tid;
+    if (c < d) {
+      const double mean = __ddiv_rn(column_pairwise<T>(W + c, L, ld), (double)L);
+      s_mean[tid] = mean;
       if (has_obj) {
-        lm = lam[c];
-        wo = wopt[c];
+        const double lm = lam[c], wo = wopt[c];
+        s_lm[tid] = lm;
+        s_wo[tid] = wo;
         const double dm = __dsub_rn(mean, wo);
         a_sum += 0.5 * lm * dm * dm;
       }
     }
-    for (int l = 0; l < L; l++) {
+    __syncthreads();
+    const int width = (int)min((long long)kTrThreads, d - c0);
+    for (int j = 0; j < kTrPer; j++) {
+      const int l = warp + kTrWarps * j;
+      if (l >= L) break;
+      const T* row = W + (long long)l * ld + c0;
       double v = 0.0, q = 0.0;
-      if (ok) {
-        const double w = (double)E::ld(W + (long long)l * ld + c, 0);
-        const double dv = w - mean;
-        v = dv * dv;
+      for (int i = lane; i < width; i += 32) {
+        const double w = (double)E::ld(row + i, 0);
+        const double dv = w - s_mean[i];
+        v += dv * dv;
         if (has_obj) {
-          const double dw = w - wo;
-          q = lm * dw * dw;
+          const double dw = w - s_wo[i];
+          q += s_lm[i] * dw * dw;
         }
       }
       for (int o = 16; o > 0; o >>= 1) {
         v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (has_obj) q += __shfl_xor_sync(0xffffffffu, q, o);
+        q += __shfl_xor_sync(0xffffffffu, q, o);
       }
       if (lane == 0) {
-        acc_c[warp][l] += v;
-        if (has_obj) acc_l[warp][l] += q;
+        s_acc[warp][j][0] += v;
+        s_acc[warp][j][1] += q;
       }
+    }
+    __syncthreads();
+  }
+  if (lane < kTrPer) {
+    const int l = warp + kTrWarps * lane;
+    if (l < L) {
+      atomicAdd(&cons_sq[l], s_acc[warp][lane][0]);
+      if (has_obj) atomicAdd(&loss_col[l], 0.5 * s_acc[warp][lane][1]);
     }
   }
   for (int o = 16; o > 0; o >>= 1) a_sum += __shfl_xor_sync(0xffffffffu, a_sum, o);
-  if (lane == 0) acc_a[warp] = a_sum;
+  if (lane == 0) s_red[warp] = a_sum;
   __syncthreads();
-  for (int l = threadIdx.x; l < L; l += kTrThreads) {
-    double c = 0.0, q = 0.0;
-    for (int w = 0; w < kTrThreads / 32; w++) {
-      c += acc_c[w][l];
-      q += acc_l[w][l];
-    }
-    atomicAdd(&cons_sq[l], c);
-    if (has_obj) atomicAdd(&loss_col[l], 0.5 * q);
-  }
-  if (threadIdx.x == 0 && has_obj) {
+  if (tid == 0 && has_obj) {
     double t = 0.0;
-    for (int w = 0; w < kTrThreads / 32; w++) t += acc_a[w];
+    for (int w = 0; w < kTrWarps; w++) t += s_red[w];
     atomicAdd(avg_loss, t);
   }
 }
@@ -103,7 +133,7 @@ static int trace_stats(const T* W, int L, int64_t d, int64_t ld, const double* l
   }
   if (d == 0) return 0;
   long long blocks = (d + kTrThreads - 1) / kTrThreads;
-  if (blocks > 4LL * sm_count(-1)) blocks = 4LL * sm_count(-1);
+  if (blocks > 8LL * sm_count(-1)) blocks = 8LL * sm_count(-1);
   trace_stats_kernel<T><<<(int)blocks, kTrThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss);
   RM_CHECK_LAUNCH("trace_stats_kernel");
@@ -148,19 +178,8 @@ __global__ void __launch_bounds__(256)
        c += (long long)gridDim.x * blockDim.x) {
     const T* p = W + c;
     double res;
-    if (L >= 8 && L <= 128) {
-      const int n8 = L - (L % 8);
-      double r[8];
-#pragma unroll
-      for (int k = 0; k < 8; k++) r[k] = (double)E::ld(p + (long long)k * ld, 0);
-      for (int i = 8; i < n8; i += 8) {
-#pragma unroll
-        for (int k = 0; k < 8; k++)
-          r[k] = __dadd_rn(r[k], (double)E::ld(p + (long long)(i + k) * ld, 0));
-      }
-      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-      for (int i = n8; i < L; i++) res = __dadd_rn(res, (double)E::ld(p + (long long)i * ld, 0));
+    if (L <= kTrMaxL) {
+      res = column_pairwise<T>(p, L, ld);
     } else {
       auto get = [&](int i) { return (double)E::ld(p + (long long)i * ld, 0); };
       res = pairwise_sum<double>(get, 0, L);
