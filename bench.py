@@ -312,8 +312,9 @@ def host_pinned_budget() -> int:
 
 
 def weak(args, ws):
-    """Weak scaling: coordinate stripes of fixed width per rank (no data-path collective)."""
-    return ws > 1 and args.layout == "coord" and args.scaling == "weak"
+    """Weak scaling: coordinate stripes of fixed width per rank (no data-path collective);
+    at N = 1 it is the same single-GPU problem, labelled like the N > 1 runs."""
+    return args.layout == "coord" and args.scaling == "weak"
 
 
 def total_dim(args, ws):

@@ -51,7 +51,7 @@ def test_weak_scaling_only_for_coordinate_stripes():
     b = _bench()
     a = argparse.Namespace(layout="coord", scaling="weak", dim=100, learners=4,
                            strategy="rand_psgd", d1d_collective="auto", d1d_chunk_cols=0)
-    assert b.weak(a, 1) is False and b.total_dim(a, 1) == 100
+    assert b.weak(a, 1) is True and b.total_dim(a, 1) == 100
     assert b.weak(a, 4) is True and b.total_dim(a, 4) == 400
     a.layout = "learner"
     assert b.weak(a, 4) is False and b.total_dim(a, 4) == 100
