@@ -80,7 +80,8 @@ def parse():
                     help="coord layout at N > 1: weak = every rank owns a full-width "
                          "(L x dim) column stripe of an L x (N*dim) problem; strong = the "
                          "L x dim problem split N ways")
-    ap.add_argument("--d1d-collective", choices=["auto", "nvls", "nccl"], default="auto")
+    ap.add_argument("--d1d-collective", choices=["auto", "fused", "nvls", "nccl"],
+                    default="auto")
     ap.add_argument("--d1d-chunk-cols", type=int, default=1 << 22,
                     help="learner-sharded D1D pipeline chunk (columns); 0 = one chunk")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -382,7 +383,14 @@ class Workload:
                 self.rows, self.cols = e - b, d
                 self.W = [synth(e - b, d), mixing.empty_learner_major(e - b, d, dtype, dev)]
                 self.d1d = None
-                if args.d1d_collective in ("auto", "nvls"):
+                if args.d1d_collective in ("auto", "fused"):
+                    try:
+                        self.d1d = D.LearnerShardedD1DFused(L, d, e - b, dev)
+                        self.d1d_kind = "fused"
+                    except Exception:
+                        if args.d1d_collective == "fused":
+                            raise
+                if self.d1d is None and args.d1d_collective in ("auto", "nvls"):
                     try:
                         self.d1d = D.LearnerShardedD1DNVLS(
                             L, d, e - b, dev, chunk_cols=args.d1d_chunk_cols or None)
@@ -475,7 +483,8 @@ class Workload:
         if ev_pair is not None:
             ev_pair[1].record(stream)
         if self.layout == "learner" and self.uniform:
-            self.launches["mix"] += (3 if self.d1d_kind == "nvls" else 2) * len(self.d1d.chunks)
+            self.launches["mix"] += (1 if self.d1d_kind == "fused" else
+                                     (3 if self.d1d_kind == "nvls" else 2) * len(self.d1d.chunks))
         else:   # learner / position layouts launch a planner + the mix kernel
             self.launches["mix"] += 2 if self.layout in ("learner", "position") else 1
         if self.layout in ("learner", "position") and not self.uniform:

@@ -241,6 +241,37 @@ int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, in
  * pipeline lowers them so the in-switch reduction of one chunk is co-resident (threads and
  * registers) with the local kernels of its neighbours. */
 int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls);
+/* D1D across GPUs in ONE launch per rank (simulation.py:304-312 with the learners sharded):
+ * the CTAs split into partial-sum / in-switch-reduce / apply roles that walk the column
+ * chunks in order and hand chunks to each other (and to the other ranks) through flags.
+ *   P, M: symmetric fp64[d] buffers (local addresses) and their multicast addresses;
+ *   flags / flags_mc: symmetric uint32[2 * max_chunks], zeroed once on every rank before
+ *   the first call; counters: local device uint32[2 * max_chunks], zeroed once;
+ *   epoch: 1, 2, 3, ... (one per call, the same on every rank);
+ *   chunk_cols: a multiple of 32 * world; pct_partial / pct_reduce: share of the grid's
+ *   CTAs for those roles (the rest apply).  Every rank must call with the same d, L,
+ *   chunk_cols and epoch.  A wait that exceeds 20 s traps (no silent hang). */
+int rm_d1d_fused_nvls_f32(const float* W, const float* G, float* out, int Lg, int L, int64_t d,
+                          int64_t ldw, int64_t ldg, int64_t ldo, double lr,
+                          unsigned long long* absmax_bits, double* P, const double* P_mc,
+                          const double* M, double* M_mc, uint32_t* flags, uint32_t* flags_mc,
+                          uint32_t* counters, int rank, int world, int64_t chunk_cols,
+                          int max_chunks, uint32_t epoch, int pct_partial, int pct_reduce,
+                          void* stream);
+int rm_d1d_fused_nvls_f64(const double* W, const double* G, double* out, int Lg, int L,
+                          int64_t d, int64_t ldw, int64_t ldg, int64_t ldo, double lr,
+                          unsigned long long* absmax_bits, double* P, const double* P_mc,
+                          const double* M, double* M_mc, uint32_t* flags, uint32_t* flags_mc,
+                          uint32_t* counters, int rank, int world, int64_t chunk_cols,
+                          int max_chunks, uint32_t epoch, int pct_partial, int pct_reduce,
+                          void* stream);
+int rm_d1d_fused_nvls_bf16(const uint16_t* W, const uint16_t* G, uint16_t* out, int Lg, int L,
+                           int64_t d, int64_t ldw, int64_t ldg, int64_t ldo, double lr,
+                           unsigned long long* absmax_bits, double* P, const double* P_mc,
+                           const double* M, double* M_mc, uint32_t* flags, uint32_t* flags_mc,
+                           uint32_t* counters, int rank, int world, int64_t chunk_cols,
+                           int max_chunks, uint32_t epoch, int pct_partial, int pct_reduce,
+                           void* stream);
 int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1, int L,
                      void* stream);
 

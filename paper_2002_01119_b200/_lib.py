@@ -73,6 +73,9 @@ for _sfx in ("f32", "f64", "bf16"):
     _SIGNATURES[f"rm_ring_mix_sgd_sharded_{_sfx}"] = (
         [vp, vp, vp, vp, i32, i32, i32, i64, i64, i64, i64, vp, dbl, vp, vp], i32)
     _SIGNATURES[f"rm_partial_sum_{_sfx}"] = ([vp, i32, i64, i64, vp, vp], i32)
+    _SIGNATURES[f"rm_d1d_fused_nvls_{_sfx}"] = (
+        [vp, vp, vp, i32, i32, i64, i64, i64, i64, dbl, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32,
+         i64, i32, ctypes.c_uint32, i32, i32, vp], i32)
     _SIGNATURES[f"rm_apply_mean_sgd_{_sfx}"] = ([vp, vp, vp, i32, i32, i64, i64, i64, dbl, vp, vp],
                                                 i32)
     _SIGNATURES[f"rm_ring_mix_sgd_{_sfx}"] = (

@@ -228,16 +228,17 @@ __global__ void __launch_bounds__(kShThreads, 1)
 // ---- D1D pieces ----
 // Column sums of the local rows (ascending learner order, fp64) and the apply
 // step.  Both stream HBM with 16-byte accesses and several rows in flight per
-// thread; the scalar tail handles d % VEC columns.
+// thread; the scalar tail handles d % VEC columns.  The bodies are range
+// functions over (worker, nworkers) so the fused D1D kernel (below) can run them
+// on a subset of its CTAs.
 template <typename T>
-__global__ void __launch_bounds__(256)
-    partial_sum_kernel(const T* __restrict__ W, int Lg, long long d, long long ld,
-                       double* __restrict__ S) {
+__device__ __forceinline__ void partial_sum_range(const T* __restrict__ W, int Lg, long long d,
+                                                  long long ld, double* __restrict__ S,
+                                                  long long worker, long long nworkers) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const long long nvec = d / VEC;
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec;
-       v += (long long)gridDim.x * blockDim.x) {
+  for (long long v = worker; v < nvec; v += nworkers) {
     double s[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; e++) s[e] = 0.0;
@@ -263,12 +264,19 @@ __global__ void __launch_bounds__(256)
     for (int e = 0; e < VEC; e++) S[v * VEC + e] = s[e];
   }
   // tail columns
-  for (long long c = nvec * VEC + blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
-       c += (long long)gridDim.x * blockDim.x) {
+  for (long long c = nvec * VEC + worker; c < d; c += nworkers) {
     double s = 0.0;
     for (int l = 0; l < Lg; l++) s = __dadd_rn(s, (double)E::ld(W + l * ld + c, 0));
     S[c] = s;
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    partial_sum_kernel(const T* __restrict__ W, int Lg, long long d, long long ld,
+                       double* __restrict__ S) {
+  partial_sum_range<T>(W, Lg, d, ld, S, blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                       (long long)gridDim.x * blockDim.x);
 }
 
 // out[j][c] = S[c]/L - lr*G[j][c] for the Lg local learners.  One thread per
@@ -276,18 +284,17 @@ __global__ void __launch_bounds__(256)
 // larger than L2, so per-row re-reads would cost Lg x d x 8 bytes).  L == 1
 // means S already holds the mean (the NVLS path divides once per column).
 template <typename T, bool HAS_G>
-__global__ void __launch_bounds__(256)
-    apply_mean_kernel(const double* __restrict__ S, const T* __restrict__ G, T* __restrict__ out,
-                      int Lg, int L, long long d, long long ldg, long long ldo, double lr,
-                      unsigned long long* absmax) {
+__device__ __forceinline__ void apply_mean_range(const double* S, const T* __restrict__ G,
+                                                 T* __restrict__ out, int Lg, int L, long long d,
+                                                 long long ldg, long long ldo, double lr,
+                                                 typename Elem<T>::amax_t& amax, long long worker,
+                                                 long long nworkers) {
   using E = Elem<T>;
   using A = typename E::acc;
   constexpr int VEC = E::VEC;
-  typename E::amax_t amax = 0;
   const long long nvec = (d + VEC - 1) / VEC;
   const double dL = (double)L;
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec;
-       v += (long long)gridDim.x * blockDim.x) {
+  for (long long v = worker; v < nvec; v += nworkers) {
     const long long c = v * VEC;
     const bool full = c + VEC <= d;
     A m[VEC];
@@ -337,6 +344,18 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+}
+
+template <typename T, bool HAS_G>
+__global__ void __launch_bounds__(256)
+    apply_mean_kernel(const double* __restrict__ S, const T* __restrict__ G, T* __restrict__ out,
+                      int Lg, int L, long long d, long long ldg, long long ldo, double lr,
+                      unsigned long long* absmax) {
+  using E = Elem<T>;
+  typename E::amax_t amax = 0;
+  apply_mean_range<T, HAS_G>(S, G, out, Lg, L, d, ldg, ldo, lr, amax,
+                             blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                             (long long)gridDim.x * blockDim.x);
   if (absmax) absmax_publish(absmax, E::amax_bits(amax));
 }
 
@@ -638,17 +657,16 @@ RM_DEFINE_SHARD(bf16, uint16_t, __nv_bfloat16)
 // and the result is broadcast into every rank's M (multimem.st).  Ordering
 // against the partial-sum writes and the readers of M is the caller's barrier.
 namespace rm {
-__global__ void __launch_bounds__(256)
-    nvls_sum_kernel(const double* __restrict__ P_mc, double* __restrict__ M_mc, long long c0,
-                    long long c1, double L) {
+__device__ __forceinline__ void nvls_sum_range(const double* __restrict__ P_mc,
+                                               double* __restrict__ M_mc, long long c0,
+                                               long long c1, double L, long long worker,
+                                               long long nworkers) {
   constexpr int U = 8;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; c < c1;
-       c += U * stride) {
+  for (long long c = c0 + worker; c < c1; c += U * nworkers) {
     double v[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const long long cc = c + u * stride;
+      const long long cc = c + u * nworkers;
       if (cc < c1)
         asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];"
                      : "=d"(v[u])
@@ -657,13 +675,20 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const long long cc = c + u * stride;
+      const long long cc = c + u * nworkers;
       if (cc < c1)
         asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(M_mc + cc),
                      "d"(__ddiv_rn(v[u], L))
                      : "memory");
     }
   }
+}
+
+__global__ void __launch_bounds__(256)
+    nvls_sum_kernel(const double* __restrict__ P_mc, double* __restrict__ M_mc, long long c0,
+                    long long c1, double L) {
+  nvls_sum_range(P_mc, M_mc, c0, c1, L, blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                 (long long)gridDim.x * blockDim.x);
 }
 }  // namespace rm
 
@@ -682,6 +707,235 @@ extern "C" int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, in
   RM_CHECK_LAUNCH("nvls_sum_kernel");
   return 0;
 }
+
+// ---- D1D across GPUs in ONE kernel: partial sums, in-switch reduction, apply ----
+// The CTAs of a persistent grid take three roles and walk the column chunks in
+// order: partial-sum CTAs write the chunk's fp64 column sums of the local
+// learners into the symmetric buffer P and, when the last of them is done,
+// bump flagsA[c] on EVERY rank (multimem.red.release); reduce CTAs wait until
+// flagsA[c] shows all ranks, sum their 1/N slice of the chunk across ranks in
+// the switch (multimem.ld_reduce) and broadcast the means into every rank's M
+// (multimem.st), then bump flagsB[c] everywhere; apply CTAs wait on flagsB[c]
+// and write mean - lr*G for the local learners.  The in-switch reduction of
+// chunk c thus overlaps the partial sums of later chunks and the apply of
+// earlier ones inside one launch.  Flags and the per-role counters only grow
+// (targets world*epoch and n_role*epoch), so nothing is reset between steps.
+// All CTAs must be co-resident (the host sizes the grid by occupancy); waits
+// trap after 20 s instead of hanging.
+namespace rm {
+struct D1DFusedArgs {
+  const void* W;
+  const void* G;
+  void* out;
+  int Lg, L;
+  long long d, ldw, ldg, ldo;
+  double lr;
+  unsigned long long* absmax;
+  double* P;                 // this rank's partial sums (symmetric buffer, local address)
+  const double* P_mc;        // multicast address of P
+  const double* M;           // this rank's means (local address)
+  double* M_mc;              // multicast address of M
+  const uint32_t* flagsA;    // local: [nchunks] partial sums of chunk c ready (x world)
+  uint32_t* flagsA_mc;
+  const uint32_t* flagsB;    // local: [nchunks] means of chunk c ready (x world)
+  uint32_t* flagsB_mc;
+  uint32_t* cntP;            // local role counters [nchunks]
+  uint32_t* cntR;
+  int rank, world;
+  long long chunk;
+  int nchunks;
+  uint32_t epoch;
+  int nP, nR, nA;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void d1d_wait(const uint32_t* flag, uint32_t target) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = global_ns();
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(64);
+      if (global_ns() - t0 > 20000000000ull) __trap();
+    }
+    // the data arrives through the multicast alias of the same memory
+    asm volatile("fence.proxy.alias;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// every thread's writes of this chunk are made visible system-wide; the last CTA
+// of the role (counter reaches n_role * epoch) signals all ranks
+__device__ __forceinline__ void d1d_arrive(uint32_t* counter, uint32_t last, uint32_t* flag_mc) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t old = atomicAdd(counter, 1u);
+    if (old + 1u == last) {
+      __threadfence_system();
+      asm volatile("fence.proxy.alias;" ::: "memory");
+      asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag_mc) : "memory");
+    }
+  }
+}
+
+template <typename T, bool HAS_G, int MINB>
+__global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(D1DFusedArgs a) {
+  using E = Elem<T>;
+  const T* W = static_cast<const T*>(a.W);
+  const T* G = static_cast<const T*>(a.G);
+  T* out = static_cast<T*>(a.out);
+  const int bid = blockIdx.x;
+  const uint32_t all_ranks = (uint32_t)a.world * a.epoch;
+  if (bid < a.nP) {
+    const long long w = bid * (long long)blockDim.x + threadIdx.x;
+    const long long nw = (long long)a.nP * blockDim.x;
+    for (int c = 0; c < a.nchunks; c++) {
+      const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
+      partial_sum_range<T>(W + b, a.Lg, e - b, a.ldw, a.P + b, w, nw);
+      d1d_arrive(a.cntP + c, (uint32_t)a.nP * a.epoch, a.flagsA_mc + c);
+    }
+  } else if (bid < a.nP + a.nR) {
+    const long long w = (bid - a.nP) * (long long)blockDim.x + threadIdx.x;
+    const long long nw = (long long)a.nR * blockDim.x;
+    for (int c = 0; c < a.nchunks; c++) {
+      const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
+      long long sl = (e - b + a.world - 1) / a.world;
+      sl = (sl + 31) / 32 * 32;
+      const long long s0 = min(e, b + a.rank * sl), s1 = min(e, s0 + sl);
+      d1d_wait(a.flagsA + c, all_ranks);
+      nvls_sum_range(a.P_mc, a.M_mc, s0, s1, (double)a.L, w, nw);
+      d1d_arrive(a.cntR + c, (uint32_t)a.nR * a.epoch, a.flagsB_mc + c);
+    }
+  } else {
+    const long long w = (bid - a.nP - a.nR) * (long long)blockDim.x + threadIdx.x;
+    const long long nw = (long long)a.nA * blockDim.x;
+    typename E::amax_t amax = 0;
+    for (int c = 0; c < a.nchunks; c++) {
+      const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
+      d1d_wait(a.flagsB + c, all_ranks);
+      apply_mean_range<T, HAS_G>(a.M + b, HAS_G ? G + b : nullptr, out + b, a.Lg, 1, e - b,
+                                 a.ldg, a.ldo, a.lr, amax, w, nw);
+    }
+    if (a.absmax) absmax_publish(a.absmax, E::amax_bits(amax));
+  }
+}
+
+template <typename T>
+static int d1d_fused(const T* W, const T* G, T* out, int Lg, int L, int64_t d, int64_t ldw,
+                     int64_t ldg, int64_t ldo, double lr, unsigned long long* absmax, double* P,
+                     const double* P_mc, const double* M, double* M_mc, uint32_t* flags,
+                     uint32_t* flags_mc, uint32_t* counters, int rank, int world,
+                     int64_t chunk_cols, int max_chunks, uint32_t epoch, int pct_partial,
+                     int pct_reduce, void* stream) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  if (Lg < 1 || L < Lg || d < 0 || ldw < d || ldo < d || (G && ldg < d) || world < 1 ||
+      rank < 0 || rank >= world || epoch == 0 || max_chunks < 1 || W == nullptr ||
+      out == nullptr || P == nullptr || P_mc == nullptr || M == nullptr || M_mc == nullptr ||
+      flags == nullptr || flags_mc == nullptr || counters == nullptr || pct_partial < 1 ||
+      pct_reduce < 1 || pct_partial + pct_reduce > 98) {
+    set_error("invalid fused D1D arguments");
+    return RM_EINVAL;
+  }
+  if (chunk_cols < 32LL * world || chunk_cols % (32LL * world) != 0) {
+    set_error("chunk_cols must be a positive multiple of 32 * world");
+    return RM_EINVAL;
+  }
+  if (((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(out) |
+        (uintptr_t)(ldw * sizeof(T)) | (uintptr_t)(ldo * sizeof(T)) |
+        (G ? (reinterpret_cast<uintptr_t>(G) | (uintptr_t)(ldg * sizeof(T))) : 0)) & 15) ||
+      VEC * sizeof(T) != 16) {
+    set_error("fused D1D needs 16-byte aligned rows");
+    return RM_EINVAL;
+  }
+  if (d == 0) return 0;
+  const long long nchunks = (d + chunk_cols - 1) / chunk_cols;
+  if (nchunks > max_chunks) {
+    set_error("%lld chunks exceed the %d flag slots", nchunks, max_chunks);
+    return RM_ERANGE;
+  }
+  // CTAs per SM the kernel is compiled for (registers): more resident CTAs give the
+  // HBM-bound roles more loads in flight (RINGMIX_D1D_FUSED_OCC = 2 / 3 / 4)
+  static int occ_env = -1;
+  if (occ_env < 0) {
+    const char* env = getenv("RINGMIX_D1D_FUSED_OCC");
+    occ_env = env ? atoi(env) : 4;
+    if (occ_env < 2 || occ_env > 4) occ_env = 4;
+  }
+  auto kern = occ_env == 2 ? (G ? d1d_fused_kernel<T, true, 2> : d1d_fused_kernel<T, false, 2>)
+              : occ_env == 4 ? (G ? d1d_fused_kernel<T, true, 4> : d1d_fused_kernel<T, false, 4>)
+                             : (G ? d1d_fused_kernel<T, true, 3> : d1d_fused_kernel<T, false, 3>);
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+  if (e != cudaSuccess) return fail_cuda(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (occ < 1) {
+    set_error("fused D1D kernel cannot be resident");
+    return RM_EINVAL;
+  }
+  // every CTA must be resident at once (roles wait on each other)
+  const int grid = occ * sm_count(-1);
+  D1DFusedArgs a{};
+  a.W = W;
+  a.G = G;
+  a.out = out;
+  a.Lg = Lg;
+  a.L = L;
+  a.d = d;
+  a.ldw = ldw;
+  a.ldg = ldg;
+  a.ldo = ldo;
+  a.lr = lr;
+  a.absmax = absmax;
+  a.P = P;
+  a.P_mc = P_mc;
+  a.M = M;
+  a.M_mc = M_mc;
+  a.flagsA = flags;
+  a.flagsA_mc = flags_mc;
+  a.flagsB = flags + max_chunks;
+  a.flagsB_mc = flags_mc + max_chunks;
+  a.cntP = counters;
+  a.cntR = counters + max_chunks;
+  a.rank = rank;
+  a.world = world;
+  a.chunk = chunk_cols;
+  a.nchunks = (int)nchunks;
+  a.epoch = epoch;
+  a.nP = max(1, grid * pct_partial / 100);
+  a.nR = max(1, grid * pct_reduce / 100);
+  a.nA = grid - a.nP - a.nR;
+  if (a.nA < 1) {
+    set_error("fused D1D: no CTAs left for the apply role");
+    return RM_EINVAL;
+  }
+  kern<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  RM_CHECK_LAUNCH("d1d_fused_kernel");
+  return 0;
+}
+}  // namespace rm
+
+#define RM_DEFINE_D1D_FUSED(SUFFIX, CT, T)                                                      \
+  extern "C" int rm_d1d_fused_nvls_##SUFFIX(                                                    \
+      const CT* W, const CT* G, CT* out, int Lg, int L, int64_t d, int64_t ldw, int64_t ldg,    \
+      int64_t ldo, double lr, unsigned long long* absmax_bits, double* P, const double* P_mc,  \
+      const double* M, double* M_mc, uint32_t* flags, uint32_t* flags_mc, uint32_t* counters,  \
+      int rank, int world, int64_t chunk_cols, int max_chunks, uint32_t epoch, int pct_partial, \
+      int pct_reduce, void* stream) {                                                           \
+    return d1d_fused<T>(reinterpret_cast<const T*>(W), reinterpret_cast<const T*>(G),           \
+                        reinterpret_cast<T*>(out), Lg, L, d, ldw, ldg, ldo, lr, absmax_bits, P, \
+                        P_mc, M, M_mc, flags, flags_mc, counters, rank, world, chunk_cols,      \
+                        max_chunks, epoch, pct_partial, pct_reduce, stream);                    \
+  }
+RM_DEFINE_D1D_FUSED(f32, float, float)
+RM_DEFINE_D1D_FUSED(f64, double, double)
+RM_DEFINE_D1D_FUSED(bf16, uint16_t, __nv_bfloat16)
 
 // ---- RAD in ring-position order ("push") ----
 // Storage slot x (owned by the rank with positions [g0, g0+Lg)) holds the

@@ -426,6 +426,67 @@ class LearnerShardedD1DNVLS:
         return out
 
 
+class LearnerShardedD1DFused:
+    """D1D step with learners sharded, everything in ONE kernel launch per rank
+    (``rm_d1d_fused_nvls_*``): the CTAs split into partial-sum, in-switch-reduce and
+    apply roles that walk the column chunks in order and hand each chunk on — within
+    the GPU through counters, across GPUs through flags bumped on every rank with
+    ``multimem.red``.  The reduction of chunk c in the NVSwitch overlaps the partial
+    sums of later chunks and the apply of earlier ones without any host-side stream
+    choreography; the arithmetic is that of LearnerShardedD1DNVLS (same bits)."""
+
+    MAX_CHUNKS = 64
+
+    def __init__(self, L: int, d: int, Lg: int, device, group=None,
+                 chunk_cols: int = 1 << 21, split: tuple[int, int] | None = None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.L, self.d, self.Lg = L, d, Lg
+        self.device = torch.device(device)
+        self.group = group if group is not None else dist.group.WORLD
+        gname = self.group.group_name
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        self.P = symm_mem.empty(max(d, 1), dtype=torch.float64, device=self.device)
+        self.M = symm_mem.empty(max(d, 1), dtype=torch.float64, device=self.device)
+        self.F = symm_mem.empty(2 * self.MAX_CHUNKS, dtype=torch.int32, device=self.device)
+        self.F.zero_()
+        self.hP = symm_mem.rendezvous(self.P, gname)
+        self.hM = symm_mem.rendezvous(self.M, gname)
+        self.hF = symm_mem.rendezvous(self.F, gname)
+        if not (self.hP.multicast_ptr and self.hM.multicast_ptr and self.hF.multicast_ptr):
+            raise RuntimeError("NVSwitch multicast (NVLS) is not available on this system")
+        self.counters = torch.zeros(2 * self.MAX_CHUNKS, dtype=torch.int32, device=self.device)
+        quantum = 32 * self.world
+        chunk = max(chunk_cols, -(-d // self.MAX_CHUNKS), quantum)
+        self.chunk = -(-chunk // quantum) * quantum
+        if split is None:
+            env = os.environ.get("RINGMIX_D1D_FUSED_SPLIT", "30,10").split(",")
+            split = (int(env[0]), int(env[1]))
+        self.split = split
+        self.epoch = 0
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)     # every rank's flags are zero before any bump
+
+    @property
+    def chunks(self) -> list[tuple[int, int]]:
+        return [(b, min(b + self.chunk, self.d)) for b in range(0, self.d, self.chunk)]
+
+    def step(self, W: torch.Tensor, G: torch.Tensor | None, lr: float, out: torch.Tensor,
+             absmax: torch.Tensor | None = None) -> torch.Tensor:
+        lib = _lib.load()
+        fn = getattr(lib, f"rm_d1d_fused_nvls_{mixing._suffix(W)}")
+        self.epoch += 1
+        _lib.check(fn(W.data_ptr(), _lib.ptr(G), out.data_ptr(), self.Lg, self.L, self.d,
+                      W.stride(0), G.stride(0) if G is not None else 0, out.stride(0),
+                      float(lr), _lib.ptr(absmax), self.P.data_ptr(), self.hP.multicast_ptr,
+                      self.M.data_ptr(), self.hM.multicast_ptr, self.F.data_ptr(),
+                      self.hF.multicast_ptr, self.counters.data_ptr(), self.rank, self.world,
+                      self.chunk, self.MAX_CHUNKS, self.epoch, self.split[0], self.split[1],
+                      _lib.stream_ptr()), "rm_d1d_fused_nvls")
+        return out
+
+
 class LearnerShardedD1D:
     """D1D step with learners sharded: W' = sum_all(W)/L - lr*G, the global sum by an
     NCCL all-reduce of fp64 column sums, pipelined in column chunks so the

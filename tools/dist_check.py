@@ -53,6 +53,14 @@ def main():
             outs.append(out2)
         ok_d1d = ok_d1d and bool(torch.equal(outs[0], outs[1]))
         nvls = len(nv.chunks)
+        # one-kernel variant: same bits as the NVLS pipeline, over several epochs
+        fu = D.LearnerShardedD1DFused(L, d, ring.Lg, dev, chunk_cols=1 << 16)
+        out3 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
+        for _ in range(3):
+            fu.step(ring.weights, Gl, 0.01, out3)
+        torch.cuda.synchronize()
+        ok_d1d = ok_d1d and bool(torch.equal(out3, outs[0]))
+        nvls = f"{nvls} chunks; fused {len(fu.chunks)} chunks ok={bool(torch.equal(out3, outs[0]))}"
     except RuntimeError as exc:
         nvls = str(exc)[:100]
     ring.close()
