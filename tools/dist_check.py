@@ -61,6 +61,19 @@ def main():
         torch.cuda.synchronize()
         ok_d1d = ok_d1d and bool(torch.equal(out3, outs[0]))
         nvls = f"{nvls} chunks; fused {len(fu.chunks)} chunks ok={bool(torch.equal(out3, outs[0]))}"
+        # other storage types: the fused kernel against the single-GPU mean kernel
+        for dt, tol in ((torch.float64, 1e-13), (torch.bfloat16, 1e-2)):
+            Wd = mixing.empty_learner_major(ring.Lg, d, dt, dev).copy_(full[b:e].to(dt))
+            Gd = mixing.empty_learner_major(ring.Lg, d, dt, dev).copy_(Gf[b:e].to(dt))
+            od = mixing.empty_learner_major(ring.Lg, d, dt, dev)
+            fu.step(Wd, Gd, 0.01, od)
+            Fd = mixing.empty_learner_major(L, d, dt, dev).copy_(full.to(dt))
+            GFd = mixing.empty_learner_major(L, d, dt, dev).copy_(Gf.to(dt))
+            rd = mixing.mean_mix_sgd(Fd, GFd, 0.01)
+            torch.cuda.synchronize()
+            err = (od.double() - rd[b:e].double()).abs().max().item()
+            ok_d1d = ok_d1d and err <= tol
+            nvls += f"; {dt} maxdiff {err:.2e}"
     except RuntimeError as exc:
         nvls = str(exc)[:100]
     ring.close()
