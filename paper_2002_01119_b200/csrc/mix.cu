@@ -28,6 +28,7 @@
 // A fused epilogue publishes max|W'| (NaN sorts above inf) for the
 // reference's _check_divergence (simulation.py:390-395): zero extra bytes.
 #include "common.cuh"
+#include "tma_host.cuh"
 #include "arith.cuh"
 #include "../../include/ringmix_b200.h"
 
@@ -447,49 +448,10 @@ static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode,
   return bytes;
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-template <typename T>
-struct TmaType;
-template <>
-struct TmaType<float> {
-  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-};
-template <>
-struct TmaType<double> {
-  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-};
-template <>
-struct TmaType<__nv_bfloat16> {
-  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-};
-
 template <typename T>
 static bool make_map(CUtensorMap* m, const void* base, long long d, int L, long long ld, int box_c,
                      int box_r) {
-  auto fn = encode_fn();
-  if (fn == nullptr) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)L};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * sizeof(T))};
-  cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, TmaType<T>::v, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  return tma_map_2d<T>(m, base, d, L, ld, box_c, box_r);
 }
 
 template <typename T, int MODE, bool HAS_G, int NT>
@@ -512,7 +474,7 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   // the tiled mean phase covers numpy's non-recursive pairwise case (8 <= L <= 128)
   const bool mean_ok = MODE == kRing || (a.L >= 8 && a.L <= 128);
   bool use_tma = aligned && mean_ok && a.L <= kMaxTmaL && a.d >= VEC && a.d < (1LL << 31) &&
-                 encode_fn() != nullptr;
+                 tma_encode_fn() != nullptr;
   int cw = 0;
   if (use_tma) {
     // tile width: power of two, stage ~kStageTarget, enough tiles to spread

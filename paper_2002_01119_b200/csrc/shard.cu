@@ -19,6 +19,7 @@
 // D1D: rm_partial_sum (local column sums, fp64) -> NCCL all-reduce (host side,
 // chunk-pipelined on a side stream) -> rm_apply_mean_sgd.
 #include "common.cuh"
+#include "tma_host.cuh"
 #include "arith.cuh"
 #include "../../include/ringmix_b200.h"
 
@@ -359,43 +360,13 @@ __global__ void __launch_bounds__(256)
   if (absmax) absmax_publish(absmax, E::amax_bits(amax));
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 sh_encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-template <typename T>
-struct ShTmaType;
-template <>
-struct ShTmaType<float> {
-  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-};
-template <>
-struct ShTmaType<double> {
-  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-};
-template <>
-struct ShTmaType<__nv_bfloat16> {
-  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-};
-
 template <typename T, bool HAS_G>
 static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G_local,
                         long long ldg, cudaStream_t st) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const size_t esz = sizeof(T);
-  auto fn = sh_encode_fn();
+  auto fn = tma_encode_fn();
   if (fn == nullptr) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return RM_ENOSYS;
@@ -433,7 +404,7 @@ static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G
   cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)a.Lg};
   cuuint32_t estr[2] = {1, 1};
   cuuint64_t sw[1] = {(cuuint64_t)(ldw * esz)};
-  if (fn(&tmW, ShTmaType<T>::v, 2, const_cast<T*>(W_local), dims, sw, box, estr,
+  if (fn(&tmW, TmaType<T>::v, 2, const_cast<T*>(W_local), dims, sw, box, estr,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed for local W");
@@ -442,7 +413,7 @@ static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G
   tmG = tmW;
   if (HAS_G) {
     cuuint64_t sg[1] = {(cuuint64_t)(ldg * esz)};
-    if (fn(&tmG, ShTmaType<T>::v, 2, const_cast<T*>(G_local), dims, sg, box, estr,
+    if (fn(&tmG, TmaType<T>::v, 2, const_cast<T*>(G_local), dims, sg, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {

@@ -8,6 +8,7 @@
 // are parallel fp64 reductions (the reference sums sequentially), so they agree
 // to fp64 rounding, not bitwise.
 #include "common.cuh"
+#include "tma_host.cuh"
 #include "arith.cuh"
 #include "../../include/ringmix_b200.h"
 
@@ -122,6 +123,210 @@ __global__ void __launch_bounds__(kTrThreads, 4)
   }
 }
 
+// TMA-staged variant (16-byte aligned rows, L <= 128): tiles [L x cw] of W
+// arrive in a 3-stage shared-memory ring (one 2-D tensor-map load per tile);
+// phase A computes the tile's column means from shared memory, phase B has every
+// thread fold its fixed set of (row, 16-byte vector) items into per-row
+// register accumulators.  W crosses HBM exactly once, with no L2 re-reads.
+constexpr int kTrStages = 3;
+constexpr int kTrStageTarget = 32 * 1024;  // two 256-thread CTAs per SM
+constexpr int kTrItems = 8;                // (row, vector) items per thread per tile
+
+template <typename T>
+__global__ void __launch_bounds__(kTrThreads, 2)
+    trace_stats_tma_kernel(const __grid_constant__ CUtensorMap tmW, int L, long long d, int cw,
+                           int lg_nv, long long ntiles, const double* __restrict__ lam,
+                           const double* __restrict__ wopt, double* __restrict__ cons_sq,
+                           double* __restrict__ loss_col, double* __restrict__ avg_loss) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  double* s_mean = reinterpret_cast<double*>(smem + 128);
+  double* s_lm = s_mean + cw;
+  double* s_wo = s_lm + cw;
+  double* s_rows = s_wo + cw;  // [2][L] block totals
+  unsigned char* stages =
+      reinterpret_cast<unsigned char*>(s_rows + 2 * kTrMaxL) +
+      ((128 - (((uintptr_t)(s_rows + 2 * kTrMaxL)) & 127)) & 127);
+  const int tid = threadIdx.x;
+  const int stage_bytes = L * cw * (int)sizeof(T);
+  const bool has_obj = lam != nullptr;
+  const int box_c = cw < 256 ? cw : 256;
+  const int lg_bc = __ffs(box_c) - 1;
+  const int box_stride = L << lg_bc;
+  auto sidx = [&](int r, int c) -> int {
+    return (c >> lg_bc) * box_stride + (r << lg_bc) + (c & (box_c - 1));
+  };
+  if (tid == 0) {
+    tma_prefetch_desc(&tmW);
+    for (int st = 0; st < kTrStages; st++) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < 2 * kTrMaxL; i += kTrThreads) s_rows[i] = 0.0;
+  __syncthreads();
+  auto issue = [&](int st, long long t) {
+    mbar_arrive_expect_tx(&full[st], (uint32_t)stage_bytes);
+    T* dst = reinterpret_cast<T*>(stages + (size_t)st * stage_bytes);
+    for (int cc = 0; cc < cw; cc += box_c)
+      tma_load_2d(dst + sidx(0, cc), &tmW, (int)(t * cw + cc), 0, &full[st]);
+  };
+  const long long first = blockIdx.x, stride = gridDim.x;
+  if (tid == 0)
+    for (int st = 0; st < kTrStages; st++)
+      if (first + st * stride < ntiles) issue(st, first + st * stride);
+
+  // this thread's items: rows (tid >> lg_nv) + k * (kTrThreads >> lg_nv), vector v
+  const int nv_full = 1 << lg_nv;
+  const int v = tid & (nv_full - 1);
+  const int row0 = tid >> lg_nv, row_step = kTrThreads >> lg_nv;
+  double acc_c[kTrItems], acc_l[kTrItems];
+#pragma unroll
+  for (int k = 0; k < kTrItems; k++) acc_c[k] = acc_l[k] = 0.0;
+  double a_sum = 0.0;
+  int it = 0;
+  for (long long t = first; t < ntiles; t += stride, ++it) {
+    const int st = it % kTrStages;
+    const long long c0 = t * cw;
+    const int width = (int)min((long long)cw, d - c0);
+    const T* sW = reinterpret_cast<const T*>(stages + (size_t)st * stage_bytes);
+    mbar_wait(&full[st], (it / kTrStages) & 1);
+    // phase A: column means (numpy pairwise order) and the average-model loss
+    for (int col = tid; col < width; col += kTrThreads) {
+      double res;
+      if (L < 8) {
+        res = -0.0;
+        for (int i = 0; i < L; i++) res = __dadd_rn(res, (double)E::lds(sW + sidx(i, col)));
+      } else {
+        const int n8 = L - (L % 8);
+        double r[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) r[k] = (double)E::lds(sW + sidx(k, col));
+        for (int i = 8; i < n8; i += 8) {
+#pragma unroll
+          for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], (double)E::lds(sW + sidx(i + k, col)));
+        }
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (int i = n8; i < L; i++) res = __dadd_rn(res, (double)E::lds(sW + sidx(i, col)));
+      }
+      const double mean = __ddiv_rn(res, (double)L);
+      s_mean[col] = mean;
+      if (has_obj) {
+        const double lm = lam[c0 + col], wo = wopt[c0 + col];
+        s_lm[col] = lm;
+        s_wo[col] = wo;
+        const double dm = __dsub_rn(mean, wo);
+        a_sum += 0.5 * lm * dm * dm;
+      }
+    }
+    __syncthreads();
+    // phase B: this thread's rows over its vector of columns
+    const int c = v * VEC;
+    if (c < width) {
+      // 16-byte shared loads: a thread owns VEC consecutive columns (scalar loads
+      // would be 2*VEC-way bank conflicts); entries past `width` are never used
+      double m[VEC], lm[VEC], wo[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; e += 2) {
+        const double2 a2 = *reinterpret_cast<const double2*>(s_mean + c + e);
+        m[e] = a2.x;
+        m[e + 1] = a2.y;
+        if (has_obj) {
+          const double2 l2 = *reinterpret_cast<const double2*>(s_lm + c + e);
+          const double2 w2 = *reinterpret_cast<const double2*>(s_wo + c + e);
+          lm[e] = l2.x;
+          lm[e + 1] = l2.y;
+          wo[e] = w2.x;
+          wo[e + 1] = w2.y;
+        } else {
+          lm[e] = lm[e + 1] = wo[e] = wo[e + 1] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kTrItems; k++) {
+        const int j = row0 + k * row_step;
+        if (j < L) {
+          Vec<T> x;
+          x.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
+          double vv = 0.0, qq = 0.0;
+#pragma unroll
+          for (int e = 0; e < VEC; e++) {
+            if (c + e < width) {
+              const double w = (double)E::ld(x.e(), e);
+              const double dv = w - m[e];
+              vv += dv * dv;
+              const double dw = w - wo[e];
+              qq += lm[e] * dw * dw;
+            }
+          }
+          acc_c[k] += vv;
+          acc_l[k] += qq;
+        }
+      }
+    }
+    __syncthreads();  // stage consumed, means free
+    if (tid == 0) {
+      const long long tn = t + (long long)kTrStages * stride;
+      if (tn < ntiles) issue(st, tn);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kTrItems; k++) {
+    const int j = row0 + k * row_step;
+    if (j < L) {
+      atomicAdd(&s_rows[j], acc_c[k]);
+      atomicAdd(&s_rows[kTrMaxL + j], acc_l[k]);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) a_sum += __shfl_xor_sync(0xffffffffu, a_sum, o);
+  __syncthreads();
+  for (int j = tid; j < L; j += kTrThreads) {
+    atomicAdd(&cons_sq[j], s_rows[j]);
+    if (has_obj) atomicAdd(&loss_col[j], 0.5 * s_rows[kTrMaxL + j]);
+  }
+  if ((tid & 31) == 0 && has_obj) atomicAdd(avg_loss, a_sum);
+}
+
+// Returns 0 (launched), a CUDA error, or sets *covered = false for shapes the
+// tiled kernel does not handle (the caller then uses the generic kernel).
+template <typename T>
+static int trace_stats_tma(const T* W, int L, int64_t d, int64_t ld, const double* lam,
+                           const double* wopt, double* cons_sq, double* loss_col,
+                           double* avg_loss, cudaStream_t st, bool* covered) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  const size_t esz = sizeof(T);
+  // tile width: power of two, stage ~32 KB, exactly kTrItems items per thread
+  int cw = VEC;
+  while ((size_t)(cw * 2) * L * esz <= (size_t)kTrStageTarget && cw * 2 <= 2048) cw *= 2;
+  int nv = cw / VEC, lg = 0;
+  while ((1 << lg) < nv) lg++;
+  *covered = false;
+  if ((long long)L * nv > (long long)kTrItems * kTrThreads || nv > kTrThreads) return 0;
+  const int box_c = cw < 256 ? cw : 256;
+  CUtensorMap tm;
+  if (!tma_map_2d<T>(&tm, W, d, L, ld, box_c, L)) return 0;
+  const size_t smem = 128 + 3 * (size_t)cw * 8 + 2 * kTrMaxL * 8 + 128 +
+                      (size_t)kTrStages * L * cw * esz;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(trace_stats_tma_kernel<T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(trace_stats_tma_kernel)");
+    attr = true;
+  }
+  if (smem > 110 * 1024) return 0;
+  *covered = true;
+  const long long ntiles = (d + cw - 1) / cw;
+  long long grid = 2LL * sm_count(-1);
+  if (grid > ntiles) grid = ntiles;
+  trace_stats_tma_kernel<T><<<(int)grid, kTrThreads, smem, st>>>(
+      tm, L, d, cw, lg, ntiles, lam, wopt, cons_sq, loss_col, avg_loss);
+  RM_CHECK_LAUNCH("trace_stats_tma_kernel");
+  return 0;
+}
+
 template <typename T>
 static int trace_stats(const T* W, int L, int64_t d, int64_t ld, const double* lam,
                        const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
@@ -132,6 +337,15 @@ static int trace_stats(const T* W, int L, int64_t d, int64_t ld, const double* l
     return RM_EINVAL;
   }
   if (d == 0) return 0;
+  constexpr int VEC = Elem<T>::VEC;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(W) | (uintptr_t)(ld * sizeof(T))) & 15) == 0;
+  if (aligned && d >= VEC && d < (1LL << 31) && L <= 128 && tma_encode_fn() != nullptr &&
+      getenv("RINGMIX_TRACE_NO_TMA") == nullptr) {
+    bool covered = false;
+    const int rc = trace_stats_tma<T>(W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss,
+                                      static_cast<cudaStream_t>(stream), &covered);
+    if (rc != 0 || covered) return rc;
+  }
   long long blocks = (d + kTrThreads - 1) / kTrThreads;
   if (blocks > 8LL * sm_count(-1)) blocks = 8LL * sm_count(-1);
   trace_stats_kernel<T><<<(int)blocks, kTrThreads, 0, static_cast<cudaStream_t>(stream)>>>(

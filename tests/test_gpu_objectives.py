@@ -169,3 +169,26 @@ def test_normal_workspace_covers_its_layout():
     lib = _lib.load()
     for L, d in [(1, 1), (3, 77), (16, 1 << 20), (64, 25_557_032)]:
         assert lib.rm_normal_stats_offset(L, d) + 8 <= lib.rm_normal_workspace_bytes(L, d)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64, torch.bfloat16])
+def test_trace_stats_tiled_and_generic_kernels_agree(dtype, monkeypatch):
+    """The TMA-tiled trace reduction and the generic kernel (unaligned rows / other
+    shapes) give the same per-learner sums to fp64 rounding, on ragged shapes."""
+    for L, d in [(3, 7), (8, 1), (16, 1000), (33, 4099), (64, 100_003), (128, 2_049)]:
+        oracle = objectives.quadratic_oracle(d, condition_number=3.0, noise_scale=0.0, seed=L)
+        X = mixing.empty_learner_major(L, d, dtype, "cuda").normal_()
+        monkeypatch.delenv("RINGMIX_TRACE_NO_TMA", raising=False)
+        a = simulation.trace_stats(X.T, oracle)
+        monkeypatch.setenv("RINGMIX_TRACE_NO_TMA", "1")
+        b = simulation.trace_stats(X.T, oracle)
+        for x, y in zip(a, b):
+            assert torch.allclose(x, y, rtol=1e-12, atol=1e-12)
+        # and the reference's formulas on the host
+        W = X.double().cpu().numpy()
+        mean = W.mean(axis=0)
+        cons = ((W - mean) ** 2).sum(axis=1)
+        lam, opt = oracle.eigenvalues, oracle.optimum
+        loss_cols = 0.5 * (lam * (W - opt) ** 2).sum(axis=1)
+        np.testing.assert_allclose(a[0].cpu().numpy(), cons, rtol=1e-10)
+        np.testing.assert_allclose(a[1].cpu().numpy(), loss_cols, rtol=1e-10)
