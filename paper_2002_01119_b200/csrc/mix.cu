@@ -483,6 +483,9 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     cw = VEC;
     size_t target = NT == kRingThreads ? kStageTarget
                                        : (MODE == kRing ? kSmallRingStageTarget : kMeanStageTarget);
+    // bf16 ring tiles: 32 KB stages (128 columns at L = 64) measured 0.93 of HBM at C2
+    // against 0.84 with 64 KB (256 columns) — tools/gpu_bf16_sweep.sh
+    if (NT == kRingThreads && esz == 2) target = kStageTarget / 2;
     if (const char* env = getenv("RINGMIX_STAGE_KB")) {  // tuning override
       int kb = atoi(env);
       if (kb >= 4 && kb <= 96) target = (size_t)kb * 1024;
