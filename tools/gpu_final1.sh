@@ -18,4 +18,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:mix_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mix_tma -s 3 -c 1 -o $O/prof_c4_d1d python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --strategy d1d > $O/ncu_c4.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mix_tma -s 3 -c 1 -o $O/prof_c2_rad_bf16 python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --dtype bfloat16 > $O/ncu_c2bf.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:zig_ --csv --log-file $O/launches_normals_c2.csv python tools/grad_once.py 64 25557032 > $O/ncu_zig.log 2>&1
+timeout 600 python tools/bench_training.py > $O/bench_training.log 2>&1
+timeout 300 python tools/bench_trace.py > $O/bench_trace.log 2>&1
+timeout 300 python tools/bench_grad.py > $O/bench_grad.log 2>&1
 echo done > $O/done.txt
