@@ -291,3 +291,32 @@ def test_single_column_and_ragged_tails_all_dtypes():
         out32 = mixing.ring_mix_sgd(X32, G32, 0.02, lt, rt)
         ref32 = O.c_ring_mix_sgd(_host_dL(X32), _host_dL(G32), 0.02, left, right)
         assert np.array_equal(_host_dL(out32), ref32.astype(np.float32).astype(np.float64))
+
+
+def test_parameter_vectors_beyond_2_31_columns():
+    """Maximum sizes: d = 2^31 + 37 columns (past the 32-bit tile coordinates the TMA
+    path uses, so the 64-bit-indexed kernel takes over), L = 4, fp32, G = NULL:
+    ~69 GB of HBM.  Sampled columns, including both ends, are bit-exact vs the oracle,
+    and the divergence epilogue sees the whole matrix."""
+    free, _ = torch.cuda.mem_get_info()
+    L, d = 4, (1 << 31) + 37
+    if free < 2 * L * d * 4 + (8 << 30):
+        pytest.skip("needs ~77 GB of free HBM")
+    X = mixing.empty_learner_major(L, d, torch.float32, "cuda")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for r in range(L):
+        X[r].normal_(generator=g)
+    lt, rt, left, right = _tables(L, 99, 3)
+    amax = torch.zeros((), dtype=torch.int64, device="cuda")
+    out = mixing.ring_mix_sgd(X, None, 0.0, lt, rt, absmax=amax)
+    torch.cuda.synchronize()
+    cols = torch.randint(0, d, (4096,), generator=torch.Generator().manual_seed(1))
+    cols = torch.cat([cols, torch.arange(0, 64), torch.arange(d - 64, d),
+                      torch.arange((1 << 31) - 32, (1 << 31) + 32)]).cuda()
+    Xs, Os = X[:, cols].contiguous(), out[:, cols].contiguous()
+    ref = O.c_ring_mix_sgd(_host_dL(Xs), None, 0.0, left, right)
+    assert np.array_equal(_host_dL(Os), ref.astype(np.float32).astype(np.float64))
+    from paper_2002_01119_b200.simulation import absmax_value
+    assert absmax_value(amax) == float(max(out[r].abs().max().item() for r in range(L)))
+    del X, out
+    torch.cuda.empty_cache()
