@@ -566,8 +566,12 @@ def run_ours(args):
     nvlink = None
     if ws > 1 and wl.layout in ("learner", "position") and not uniform and rank == 0:
         k0 = args.warmup
-        tb = mixing.permutation_tables(L, SEED, k0, args.steps + 1, dev)
-        host = [t.cpu().numpy().astype(np.int64) for t in (tb.perm, tb.inv, tb.left, tb.right)]
+        if args.strategy == "adpsgd_fixed":      # the fixed ring: identity permutation
+            ident = np.tile(np.arange(L, dtype=np.int64), (args.steps + 1, 1))
+            host = [ident, ident, np.roll(ident, 1, axis=1), np.roll(ident, -1, axis=1)]
+        else:
+            tb = mixing.permutation_tables(L, SEED, k0, args.steps + 1, dev)
+            host = [t.cpu().numpy().astype(np.int64) for t in (tb.perm, tb.inv, tb.left, tb.right)]
         per_rank = nvlink_traffic(wl.layout, L, d, bpp // 3, ws, host[0], host[1],
                                   host[2][:-1], host[3][:-1])
         prd, pwr, psrc = p2p_peaks()

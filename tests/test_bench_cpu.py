@@ -56,3 +56,13 @@ def test_weak_scaling_only_for_coordinate_stripes():
     a.layout = "learner"
     assert b.weak(a, 4) is False and b.total_dim(a, 4) == 100
     assert "weak scaling" not in b.config_dict(a, 4)["parallelism"]
+
+
+def test_nvlink_traffic_fixed_ring_tables():
+    """The fixed ring's tables (left = j - 1, right = j + 1) cross ranks only at the
+    two shard boundaries."""
+    b = _bench()
+    ident = np.tile(np.arange(8, dtype=np.int64), (2, 1))
+    left, right = np.roll(ident, 1, axis=1), np.roll(ident, -1, axis=1)
+    pull = b.nvlink_traffic("learner", 8, 10, 4, 2, ident, ident, left[:1], right[:1])
+    assert pull == [(2 * 10 * 4, 0), (2 * 10 * 4, 0)]

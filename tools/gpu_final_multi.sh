@@ -20,8 +20,12 @@ for n in 2 4; do
   timeout 600 $TR --nproc-per-node $n --master-port $P bench.py --gpus $n --steps 50 --warmup 5 --no-cpu --no-e2e --layout learner --strategy adpsgd_fixed > $O/ad_learner_n$n.log 2>&1
   timeout 600 $TR --nproc-per-node $n --master-port $P bench.py --gpus $n --steps 50 --warmup 5 --no-cpu --no-e2e --layout learner > $O/rad_learner_n$n.log 2>&1
   timeout 600 $TR --nproc-per-node $n --master-port $P bench.py --gpus $n --steps 50 --warmup 5 --no-cpu --no-e2e --layout position > $O/rad_position_n$n.log 2>&1
-  timeout 600 $TR --nproc-per-node $n --master-port $P bench.py --gpus $n --steps 50 --warmup 5 --no-cpu --no-e2e --layout learner --strategy d1d > $O/d1d_nvls_n$n.log 2>&1
+  timeout 600 $TR --nproc-per-node $n --master-port $P bench.py --gpus $n --steps 50 --warmup 5 --no-cpu --no-e2e --layout learner --strategy d1d > $O/d1d_fused_n$n.log 2>&1
+  timeout 600 $TR --nproc-per-node $n --master-port $P bench.py --gpus $n --steps 50 --warmup 5 --no-cpu --no-e2e --layout learner --strategy d1d --d1d-collective nvls > $O/d1d_nvls_n$n.log 2>&1
   timeout 600 $TR --nproc-per-node $n --master-port $P bench.py --gpus $n --steps 50 --warmup 5 --no-cpu --no-e2e --layout learner --strategy d1d --d1d-chunk-cols 0 > $O/d1d_nvls1_n$n.log 2>&1
   timeout 600 $TR --nproc-per-node $n --master-port $P bench.py --gpus $n --steps 50 --warmup 5 --no-cpu --no-e2e --layout learner --strategy d1d --d1d-collective nccl > $O/d1d_nccl_n$n.log 2>&1
+done
+for SP in "35,10" "30,5" "25,10"; do
+  RINGMIX_D1D_FUSED_SPLIT=$SP timeout 600 $TR --nproc-per-node 4 --master-port 29950 bench.py --gpus 4 --steps 50 --warmup 5 --no-cpu --no-e2e --layout learner --strategy d1d > $O/d1d_fused_split_${SP/,/_}_n4.log 2>&1
 done
 echo done > $O/done.txt
