@@ -489,8 +489,10 @@ class Workload:
             self.launches["mix"] += 2 if self.layout in ("learner", "position") else 1
         if self.layout in ("learner", "position") and not self.uniform:
             # next step reads this step's rows on peers
-            (self.ring if self.layout == "learner" else self.pos).barrier()
-            self.launches["barrier_allreduce"] += 1
+            obj = self.ring if self.layout == "learner" else self.pos
+            obj.barrier()
+            if obj.sync is None:
+                self.launches["barrier_allreduce"] += 1
 
     def close(self):
         if self.layout == "learner" and not self.uniform:
@@ -563,6 +565,9 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     achieved = algo_bytes / kern_avg_s / 1e9
     key = f"mix_{args.strategy}_{args.dtype}_L{L}_d{d}" if ws == 1 else None
+    step_sync = None
+    if ws > 1 and wl.layout in ("learner", "position") and not uniform:
+        step_sync = (wl.ring if wl.layout == "learner" else wl.pos).sync is not None
     nvlink = None
     if ws > 1 and wl.layout in ("learner", "position") and not uniform and rank == 0:
         k0 = args.warmup
@@ -635,6 +640,9 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             **({"nvlink": nvlink} if nvlink else {}),
+            **({"step_ordering": "in-kernel flags (multimem.red), no collective"
+                if step_sync else "NCCL 4-byte all-reduce between steps"}
+               if step_sync is not None else {}),
             "gpu_launches": launches["perm"] + launches["mix"],
             "gpu_launches_detail": launches,
             "clocks": clock_info,

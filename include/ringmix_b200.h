@@ -164,6 +164,20 @@ int rm_ipc_get_handle(const void* dptr, void* handle_out, uint64_t* offset_out);
 int rm_ipc_open_handle(const void* handle, void** dptr_out);
 int rm_ipc_close_handle(void* dptr);
 
+/* Optional in-kernel step ordering for the learner-sharded step kernels, replacing a
+ * host-issued barrier between steps: the kernel of step `epoch` (1, 2, ...) waits until
+ * *done >= world * (epoch - 1) — every rank finished the previous step, whose rows it reads
+ * and whose buffers it overwrites — and at its end adds 1 to `done` on every rank through
+ * the multicast address done_mc (multimem.red.release).  done: symmetric uint32, zeroed on
+ * every rank before the first step; counter: local device uint32, zeroed once. */
+typedef struct {
+  const uint32_t* done;
+  uint32_t* done_mc;
+  uint32_t* counter;
+  uint32_t epoch;
+  int world;
+} rm_step_sync;
+
 /* Per-step plan for the rank owning learners [row0, row0+Lg): distinct remote
  * neighbour ids and each local learner's staged input indices in global-id
  * order.  plan: device int32[rm_shard_plan_ints(Lg)]; left/right: device
@@ -181,17 +195,20 @@ int rm_ring_mix_sgd_sharded_f32(const uint64_t* row_ptrs, const float* W_local,
                                 const float* G_local, float* out, int L, int row0, int Lg,
                                 int64_t d, int64_t ldw, int64_t ldg, int64_t ldo,
                                 const int32_t* plan, double lr, unsigned long long* absmax_bits,
-                                void* stream);
+                                void* stream,
+                                const rm_step_sync* sync);
 int rm_ring_mix_sgd_sharded_f64(const uint64_t* row_ptrs, const double* W_local,
                                 const double* G_local, double* out, int L, int row0, int Lg,
                                 int64_t d, int64_t ldw, int64_t ldg, int64_t ldo,
                                 const int32_t* plan, double lr, unsigned long long* absmax_bits,
-                                void* stream);
+                                void* stream,
+                                const rm_step_sync* sync);
 int rm_ring_mix_sgd_sharded_bf16(const uint64_t* row_ptrs, const uint16_t* W_local,
                                  const uint16_t* G_local, uint16_t* out, int L, int row0, int Lg,
                                  int64_t d, int64_t ldw, int64_t ldg, int64_t ldo,
                                  const int32_t* plan, double lr,
-                                 unsigned long long* absmax_bits, void* stream);
+                                 unsigned long long* absmax_bits, void* stream,
+                                const rm_step_sync* sync);
 
 /* RAD in ring-position order ("push" layout): the rank owning positions [g0, g0+Lg)
  * stores, in slot x, the learner at position x of step k (inv_k[x]).  rm_pos_plan
@@ -205,15 +222,18 @@ int rm_pos_plan(const int32_t* inv_k, const int32_t* perm_next, int L, int g0, i
 int rm_ring_mix_sgd_pos_f32(const uint64_t* slot_ptrs, const float* W_local, const float* G_local,
                             int L, int g0, int Lg, int64_t d, int64_t ldw, int64_t ldg,
                             const int32_t* plan, const uint64_t* dest, double lr,
-                            unsigned long long* absmax_bits, void* stream);
+                            unsigned long long* absmax_bits, void* stream,
+                                const rm_step_sync* sync);
 int rm_ring_mix_sgd_pos_f64(const uint64_t* slot_ptrs, const double* W_local,
                             const double* G_local, int L, int g0, int Lg, int64_t d, int64_t ldw,
                             int64_t ldg, const int32_t* plan, const uint64_t* dest, double lr,
-                            unsigned long long* absmax_bits, void* stream);
+                            unsigned long long* absmax_bits, void* stream,
+                                const rm_step_sync* sync);
 int rm_ring_mix_sgd_pos_bf16(const uint64_t* slot_ptrs, const uint16_t* W_local,
                              const uint16_t* G_local, int L, int g0, int Lg, int64_t d,
                              int64_t ldw, int64_t ldg, const int32_t* plan, const uint64_t* dest,
-                             double lr, unsigned long long* absmax_bits, void* stream);
+                             double lr, unsigned long long* absmax_bits, void* stream,
+                                const rm_step_sync* sync);
 
 /* D1D across ranks: S[c] = sum of the local rows (fp64), all-reduced by the
  * caller (NCCL), then out[j] = S/L - lr*G[j]. */

@@ -69,9 +69,9 @@ _SIGNATURES = {
 _SIGNATURES["rm_pos_plan"] = ([vp, vp, i32, i32, i32, vp, vp, vp, vp], i32)
 for _sfx in ("f32", "f64", "bf16"):
     _SIGNATURES[f"rm_ring_mix_sgd_pos_{_sfx}"] = (
-        [vp, vp, vp, i32, i32, i32, i64, i64, i64, vp, vp, dbl, vp, vp], i32)
+        [vp, vp, vp, i32, i32, i32, i64, i64, i64, vp, vp, dbl, vp, vp, vp], i32)
     _SIGNATURES[f"rm_ring_mix_sgd_sharded_{_sfx}"] = (
-        [vp, vp, vp, vp, i32, i32, i32, i64, i64, i64, i64, vp, dbl, vp, vp], i32)
+        [vp, vp, vp, vp, i32, i32, i32, i64, i64, i64, i64, vp, dbl, vp, vp, vp], i32)
     _SIGNATURES[f"rm_partial_sum_{_sfx}"] = ([vp, i32, i64, i64, vp, vp], i32)
     _SIGNATURES[f"rm_d1d_fused_nvls_{_sfx}"] = (
         [vp, vp, vp, i32, i32, i64, i64, i64, i64, dbl, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32,
@@ -84,6 +84,12 @@ for _sfx in ("f32", "f64", "bf16"):
     _SIGNATURES[f"rm_spsgd_{_sfx}"] = ([vp, vp, vp, i32, i64, i64, i64, i64, dbl, vp, vp, vp], i32)
 
 OPTIONAL_SIGNATURES: dict = {}
+
+
+class StepSyncArgs(ctypes.Structure):
+    """rm_step_sync (include/ringmix_b200.h)."""
+    _fields_ = [("done", vp), ("done_mc", vp), ("counter", vp), ("epoch", ctypes.c_uint32),
+                ("world", i32)]
 
 
 class RingmixError(RuntimeError):

@@ -99,4 +99,49 @@ __device__ __forceinline__ unsigned long long abs_bits(double y) {
   return static_cast<unsigned long long>(__double_as_longlong(y)) & 0x7fffffffffffffffULL;
 }
 
+// ---- cross-GPU step ordering through flags in symmetric memory ----
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Thread 0 spins (acquire, system scope) until *flag - target >= 0 (wraps), then
+// the CTA proceeds; traps after 20 s instead of hanging.  The data guarded by the
+// flag is read through another virtual alias (peer / multicast mapping), hence
+// the alias fence.
+__device__ __forceinline__ void xgpu_wait(const uint32_t* flag, uint32_t target) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = global_ns();
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(64);
+      if (global_ns() - t0 > 20000000000ull) __trap();
+    }
+    asm volatile("fence.proxy.alias;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// Every thread's writes so far are made visible system-wide; the CTA whose
+// arrival completes `last` arrivals on `counter` adds 1 to the flag on every
+// rank (multimem.red.release through the multicast address flag_mc).
+// reset: the last arriver zeroes the counter (for a counter private to one launch).
+__device__ __forceinline__ void xgpu_arrive(uint32_t* counter, uint32_t last, uint32_t* flag_mc,
+                                            bool reset = false) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t old = atomicAdd(counter, 1u);
+    if (old + 1u == last) {
+      if (reset) atomicExch(counter, 0u);
+      __threadfence_system();
+      asm volatile("fence.proxy.alias;" ::: "memory");
+      asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag_mc) : "memory");
+    }
+  }
+}
+
 }  // namespace rm

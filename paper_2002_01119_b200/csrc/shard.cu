@@ -88,6 +88,12 @@ struct ShardArgs {
   double lr;
   unsigned long long* absmax;
   const uint64_t* dest;  // optional: output row j goes to dest[j] (local or peer address)
+  // optional in-kernel step ordering (rm_step_sync): wait until every rank finished
+  // the previous step, signal this rank's completion to every rank at the end
+  const uint32_t* sync_done;
+  uint32_t* sync_done_mc;
+  uint32_t* sync_cnt;
+  uint32_t sync_target;
 };
 
 template <typename T, bool HAS_G>
@@ -127,6 +133,9 @@ __global__ void __launch_bounds__(kShThreads, 1)
   for (int i = tid; i < R; i += kShThreads)
     s_rptr[i] = reinterpret_cast<const T*>(a.row_ptrs[a.plan[1 + i]]);
   __syncthreads();
+  // peers' rows of this step (and the buffers this step overwrites) belong to the
+  // previous step of every rank: wait for all of them before the first load
+  if (a.sync_done) xgpu_wait(a.sync_done, a.sync_target);
 
   const int box_c = cw < 256 ? cw : 256;
   const int lg_bc = __ffs(box_c) - 1;
@@ -224,6 +233,11 @@ __global__ void __launch_bounds__(kShThreads, 1)
     if (tn < a.ntiles) issue(s, tn);
   }
   if (a.absmax) absmax_publish(a.absmax, E::amax_bits(amax));
+  if (a.sync_done) {
+    // the last CTA resets the counter (the next launch starts after this one on
+    // the stream) and bumps every rank's step flag
+    xgpu_arrive(a.sync_cnt, gridDim.x, a.sync_done_mc, true);
+  }
 }
 
 // ---- D1D pieces ----
@@ -440,7 +454,7 @@ static int shard_dispatch(const uint64_t* row_ptrs, const T* W_local, const T* G
                           int L, int row0, int Lg, long long d, long long ldw, long long ldg,
                           long long ldo, const int32_t* plan, double lr,
                           unsigned long long* absmax, void* stream,
-                          const uint64_t* dest = nullptr) {
+                          const uint64_t* dest = nullptr, const rm_step_sync* sync = nullptr) {
   using E = Elem<T>;
   const size_t esz = sizeof(T);
   if (row_ptrs == nullptr || W_local == nullptr || (out == nullptr && dest == nullptr) ||
@@ -471,6 +485,17 @@ static int shard_dispatch(const uint64_t* row_ptrs, const T* W_local, const T* G
   a.lr = lr;
   a.absmax = absmax;
   a.dest = dest;
+  if (sync != nullptr) {
+    if (sync->done == nullptr || sync->done_mc == nullptr || sync->counter == nullptr ||
+        sync->world < 1 || sync->epoch == 0) {
+      set_error("invalid step-sync arguments");
+      return RM_EINVAL;
+    }
+    a.sync_done = sync->done;
+    a.sync_done_mc = sync->done_mc;
+    a.sync_cnt = sync->counter;
+    a.sync_target = (uint32_t)sync->world * (sync->epoch - 1u);
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (G_local) return launch_shard<T, true>(a, W_local, ldw, G_local, ldg, st);
   return launch_shard<T, false>(a, W_local, ldw, nullptr, ldw, st);
@@ -571,10 +596,11 @@ extern "C" int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls) {
   extern "C" int rm_ring_mix_sgd_sharded_##SUFFIX(                                              \
       const uint64_t* row_ptrs, const CT* W_local, const CT* G_local, CT* out, int L, int row0, \
       int Lg, int64_t d, int64_t ldw, int64_t ldg, int64_t ldo, const int32_t* plan,           \
-      double lr, unsigned long long* absmax_bits, void* stream) {                               \
+      double lr, unsigned long long* absmax_bits, void* stream, const rm_step_sync* sync) {     \
     return shard_dispatch<T>(row_ptrs, reinterpret_cast<const T*>(W_local),                    \
                              reinterpret_cast<const T*>(G_local), reinterpret_cast<T*>(out), L, \
-                             row0, Lg, d, ldw, ldg, ldo, plan, lr, absmax_bits, stream);        \
+                             row0, Lg, d, ldw, ldg, ldo, plan, lr, absmax_bits, stream, nullptr, \
+                             sync);                                                             \
   }                                                                                             \
   extern "C" int rm_partial_sum_##SUFFIX(const CT* W, int Lg, int64_t d, int64_t ld, double* S, \
                                          void* stream) {                                        \
@@ -719,43 +745,6 @@ struct D1DFusedArgs {
   int nP, nR, nA;
 };
 
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ void d1d_wait(const uint32_t* flag, uint32_t target) {
-  if (threadIdx.x == 0) {
-    const unsigned long long t0 = global_ns();
-    for (;;) {
-      uint32_t v;
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-      if ((int)(v - target) >= 0) break;
-      __nanosleep(64);
-      if (global_ns() - t0 > 20000000000ull) __trap();
-    }
-    // the data arrives through the multicast alias of the same memory
-    asm volatile("fence.proxy.alias;" ::: "memory");
-  }
-  __syncthreads();
-}
-
-// every thread's writes of this chunk are made visible system-wide; the last CTA
-// of the role (counter reaches n_role * epoch) signals all ranks
-__device__ __forceinline__ void d1d_arrive(uint32_t* counter, uint32_t last, uint32_t* flag_mc) {
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t old = atomicAdd(counter, 1u);
-    if (old + 1u == last) {
-      __threadfence_system();
-      asm volatile("fence.proxy.alias;" ::: "memory");
-      asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag_mc) : "memory");
-    }
-  }
-}
-
 template <typename T, bool HAS_G, int MINB>
 __global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(D1DFusedArgs a) {
   using E = Elem<T>;
@@ -770,7 +759,7 @@ __global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(D1DFusedArgs a) {
     for (int c = 0; c < a.nchunks; c++) {
       const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
       partial_sum_range<T>(W + b, a.Lg, e - b, a.ldw, a.P + b, w, nw);
-      d1d_arrive(a.cntP + c, (uint32_t)a.nP * a.epoch, a.flagsA_mc + c);
+      xgpu_arrive(a.cntP + c, (uint32_t)a.nP * a.epoch, a.flagsA_mc + c);
     }
   } else if (bid < a.nP + a.nR) {
     const long long w = (bid - a.nP) * (long long)blockDim.x + threadIdx.x;
@@ -780,9 +769,9 @@ __global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(D1DFusedArgs a) {
       long long sl = (e - b + a.world - 1) / a.world;
       sl = (sl + 31) / 32 * 32;
       const long long s0 = min(e, b + a.rank * sl), s1 = min(e, s0 + sl);
-      d1d_wait(a.flagsA + c, all_ranks);
+      xgpu_wait(a.flagsA + c, all_ranks);
       nvls_sum_range(a.P_mc, a.M_mc, s0, s1, (double)a.L, w, nw);
-      d1d_arrive(a.cntR + c, (uint32_t)a.nR * a.epoch, a.flagsB_mc + c);
+      xgpu_arrive(a.cntR + c, (uint32_t)a.nR * a.epoch, a.flagsB_mc + c);
     }
   } else {
     const long long w = (bid - a.nP - a.nR) * (long long)blockDim.x + threadIdx.x;
@@ -790,7 +779,7 @@ __global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(D1DFusedArgs a) {
     typename E::amax_t amax = 0;
     for (int c = 0; c < a.nchunks; c++) {
       const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
-      d1d_wait(a.flagsB + c, all_ranks);
+      xgpu_wait(a.flagsB + c, all_ranks);
       apply_mean_range<T, HAS_G>(a.M + b, HAS_G ? G + b : nullptr, out + b, a.Lg, 1, e - b,
                                  a.ldg, a.ldo, a.lr, amax, w, nw);
     }
@@ -974,10 +963,10 @@ extern "C" int rm_pos_plan(const int32_t* inv_k, const int32_t* perm_next, int L
   extern "C" int rm_ring_mix_sgd_pos_##SUFFIX(                                                 \
       const uint64_t* slot_ptrs, const CT* W_local, const CT* G_local, int L, int g0, int Lg,  \
       int64_t d, int64_t ldw, int64_t ldg, const int32_t* plan, const uint64_t* dest,          \
-      double lr, unsigned long long* absmax_bits, void* stream) {                               \
+      double lr, unsigned long long* absmax_bits, void* stream, const rm_step_sync* sync) {     \
     return shard_dispatch<T>(slot_ptrs, reinterpret_cast<const T*>(W_local),                  \
                              reinterpret_cast<const T*>(G_local), nullptr, L, g0, Lg, d, ldw,  \
-                             ldg, ldw, plan, lr, absmax_bits, stream, dest);                   \
+                             ldg, ldw, plan, lr, absmax_bits, stream, dest, sync);             \
   }
 RM_DEFINE_POS(f32, float, float)
 RM_DEFINE_POS(f64, double, double)

@@ -159,6 +159,44 @@ class PeerMappedBuffers:
         self._opened = []
 
 
+class StepSync:
+    """In-kernel ordering of consecutive learner-sharded steps (rm_step_sync): a flag in
+    symmetric memory counts finished steps of all ranks; each step kernel waits for the
+    previous step of every rank and bumps every rank's flag when it is done (NVSwitch
+    multicast).  Replaces a host-issued barrier collective between steps.  Raises if
+    multicast is unavailable (callers fall back to the NCCL barrier)."""
+
+    def __init__(self, group, device):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.group = group if group is not None else dist.group.WORLD
+        self.device = device
+        self.world = dist.get_world_size(self.group)
+        self.flag = symm_mem.empty(4, dtype=torch.int32, device=device)
+        self.flag.zero_()
+        self.handle = symm_mem.rendezvous(self.flag, self.group.group_name)
+        if not self.handle.multicast_ptr:
+            raise RuntimeError("NVSwitch multicast (NVLS) is not available on this system")
+        self.counter = torch.zeros(4, dtype=torch.int32, device=device)
+        self.epoch = 0
+        torch.cuda.synchronize(device)
+        dist.barrier(group=self.group)   # every rank's flag is zero before any bump
+
+    def next(self) -> "_lib.StepSyncArgs":
+        self.epoch += 1
+        return _lib.StepSyncArgs(self.flag.data_ptr(), self.handle.multicast_ptr,
+                                 self.counter.data_ptr(), self.epoch, self.world)
+
+
+def _make_step_sync(group, device, enabled):
+    if not enabled or os.environ.get("RINGMIX_STEP_SYNC", "1") == "0":
+        return None
+    try:
+        return StepSync(group, device)
+    except Exception:
+        return None
+
+
 class LearnerShardedRing:
     """RAD / fixed-ring step with learners sharded over the ranks of `group`.
 
@@ -166,7 +204,8 @@ class LearnerShardedRing:
     IPC row-pointer tables; `step(...)` runs plan -> fused mix -> step barrier.
     """
 
-    def __init__(self, L: int, d: int, dtype=torch.float32, group=None, device=None):
+    def __init__(self, L: int, d: int, dtype=torch.float32, group=None, device=None,
+                 step_sync: bool = True):
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed must be initialised")
         _lib.require_cuda()
@@ -198,6 +237,8 @@ class LearnerShardedRing:
         self._token = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.cur = 0
         self._fn = getattr(_lib.load(), f"rm_ring_mix_sgd_sharded_{mixing._suffix(self.W[0])}")
+        # consecutive steps ordered inside the kernel when multicast is available
+        self.sync = _make_step_sync(group, self.device, step_sync)
 
     @property
     def weights(self) -> torch.Tensor:
@@ -206,8 +247,10 @@ class LearnerShardedRing:
 
     def barrier(self):
         """Stream-ordered step barrier: every rank's previous kernels are complete
-        (and their W' rows readable by peers) when this returns on the stream."""
-        dist.all_reduce(self._token, group=self.group)
+        (and their W' rows readable by peers) when this returns on the stream.  A
+        no-op when the step kernels order themselves (StepSync)."""
+        if self.sync is None:
+            dist.all_reduce(self._token, group=self.group)
 
     def step(self, left: torch.Tensor, right: torch.Tensor, G: torch.Tensor | None, lr: float,
              absmax: torch.Tensor | None = None, barrier: bool = True) -> torch.Tensor:
@@ -222,7 +265,8 @@ class LearnerShardedRing:
         ldg = G.stride(0) if G is not None else self.ld
         _lib.check(self._fn(self.row_ptrs[self.cur].data_ptr(), src.data_ptr(), _lib.ptr(G),
                             dst.data_ptr(), self.L, self.row0, self.Lg, self.d, self.ld, ldg,
-                            dst.stride(0), self.plan.data_ptr(), float(lr), _lib.ptr(absmax), s),
+                            dst.stride(0), self.plan.data_ptr(), float(lr), _lib.ptr(absmax), s,
+                            None if self.sync is None else ctypes.byref(self.sync.next())),
                    "rm_ring_mix_sgd_sharded")
         self.cur = 1 - self.cur
         if barrier:
@@ -256,7 +300,8 @@ class LearnerShardedRingPos:
     learner-ordered pull needs.  Bit-identical to the single-GPU step.
     """
 
-    def __init__(self, L: int, d: int, dtype=torch.float32, group=None, device=None):
+    def __init__(self, L: int, d: int, dtype=torch.float32, group=None, device=None,
+                 step_sync: bool = True):
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed must be initialised")
         _lib.require_cuda()
@@ -284,6 +329,7 @@ class LearnerShardedRingPos:
         self._token = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.cur = 0
         self._fn = getattr(lib, f"rm_ring_mix_sgd_pos_{mixing._suffix(self.W[0])}")
+        self.sync = _make_step_sync(group, self.device, step_sync)
 
     @property
     def slots_local(self) -> torch.Tensor:
@@ -291,7 +337,9 @@ class LearnerShardedRingPos:
         return self.W[self.cur]
 
     def barrier(self):
-        dist.all_reduce(self._token, group=self.group)
+        """Step barrier on the stream (a no-op when the kernels order themselves)."""
+        if self.sync is None:
+            dist.all_reduce(self._token, group=self.group)
 
     def step(self, inv_k: torch.Tensor, perm_next: torch.Tensor, G: torch.Tensor | None,
              lr: float, absmax: torch.Tensor | None = None, barrier: bool = True):
@@ -309,7 +357,8 @@ class LearnerShardedRingPos:
         _lib.check(self._fn(self.slots[self.cur].data_ptr(), src.data_ptr(), _lib.ptr(G), self.L,
                             self.g0, self.Lg, self.d, self.ld,
                             G.stride(0) if G is not None else self.ld, self.plan.data_ptr(),
-                            self.dest.data_ptr(), float(lr), _lib.ptr(absmax), s),
+                            self.dest.data_ptr(), float(lr), _lib.ptr(absmax), s,
+                            None if self.sync is None else ctypes.byref(self.sync.next())),
                    "rm_ring_mix_sgd_pos")
         self.cur = 1 - self.cur
         if barrier:

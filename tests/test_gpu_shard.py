@@ -65,7 +65,7 @@ def _emulate(L, d, world, dtype, k, with_g=True):
         amax = torch.zeros((), dtype=torch.int64, device="cuda")
         _lib.check(fn(row_ptrs.data_ptr(), X.data_ptr(), Gl.data_ptr() if with_g else None,
                       out.data_ptr(), L, b, Lg, d, X.stride(0), Gl.stride(0), out.stride(0),
-                      plan.data_ptr(), 0.03, amax.data_ptr(), _lib.stream_ptr()))
+                      plan.data_ptr(), 0.03, amax.data_ptr(), _lib.stream_ptr(), None))
         outs.append(out)
     torch.cuda.synchronize()
     return ref, torch.cat([o for o in outs], dim=0)
@@ -162,7 +162,7 @@ def test_position_layout_steps_bit_identical_to_single_gpu(L, d, world, dtype):
             src = bufs[r][cur]
             _lib.check(fn(slots[cur].data_ptr(), src.data_ptr(), Gs.data_ptr(), L, b, Lg, d,
                           src.stride(0), Gs.stride(0), plan.data_ptr(), dest.data_ptr(), 0.02,
-                          None, _lib.stream_ptr()))
+                          None, _lib.stream_ptr(), None))
             torch.cuda.synchronize()
         cur = 1 - cur
         lt, rt = tabs.step(k)
