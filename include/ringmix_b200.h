@@ -327,16 +327,19 @@ int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int appen
  * One pass over W (L <= 128 learners, learner-major): cons_sq[l] += sum_c (W[l,c]-mean_c)^2
  * (consensus_distance), and when lam != NULL: loss_col[l] += 0.5 sum_c lam_c (W[l,c]-wopt_c)^2,
  * avg_loss += 0.5 sum_c lam_c (mean_c-wopt_c)^2.  Outputs are fp64 device accumulators the
- * caller zeroes. */
+ * caller zeroes.  Deterministic: CTAs write partials into `workspace` (device,
+ * >= rm_trace_stats_workspace_bytes(L)) that a second kernel sums in a fixed order, so the
+ * same W gives the same bits on every run (the reference's CSVs are byte-stable). */
+int64_t rm_trace_stats_workspace_bytes(int L);
 int rm_trace_stats_f32(const float* W, int L, int64_t d, int64_t ld, const double* lam,
                        const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
-                       void* stream);
+                       void* workspace, int64_t workspace_bytes, void* stream);
 int rm_trace_stats_f64(const double* W, int L, int64_t d, int64_t ld, const double* lam,
                        const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
-                       void* stream);
+                       void* workspace, int64_t workspace_bytes, void* stream);
 int rm_trace_stats_bf16(const uint16_t* W, int L, int64_t d, int64_t ld, const double* lam,
                         const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
-                        void* stream);
+                        void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Column means M[c] = (numpy pairwise sum over the L learners) / L, fp64, bit-identical
  * to the mean of rm_mean_sgd_*.  With rm_apply_mean_sgd_*(M, G, out, L, 1, ...) it

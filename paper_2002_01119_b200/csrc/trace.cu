@@ -52,8 +52,7 @@ template <typename T>
 __global__ void __launch_bounds__(kTrThreads, 4)
     trace_stats_kernel(const T* __restrict__ W, int L, long long d, long long ld,
                        const double* __restrict__ lam, const double* __restrict__ wopt,
-                       double* __restrict__ cons_sq, double* __restrict__ loss_col,
-                       double* __restrict__ avg_loss) {
+                       double* __restrict__ part) {
   using E = Elem<T>;
   __shared__ double s_mean[kTrThreads];
   __shared__ double s_lm[kTrThreads];
@@ -106,21 +105,38 @@ __global__ void __launch_bounds__(kTrThreads, 4)
     }
     __syncthreads();
   }
+  // this CTA's partials, in a fixed order (trace_finalize_kernel sums the CTAs
+  // in index order: the result does not depend on scheduling)
+  double* out = part + (long long)blockIdx.x * (2 * L + 1);
   if (lane < kTrPer) {
     const int l = warp + kTrWarps * lane;
     if (l < L) {
-      atomicAdd(&cons_sq[l], s_acc[warp][lane][0]);
-      if (has_obj) atomicAdd(&loss_col[l], 0.5 * s_acc[warp][lane][1]);
+      out[l] = s_acc[warp][lane][0];
+      out[L + l] = has_obj ? 0.5 * s_acc[warp][lane][1] : 0.0;
     }
   }
   for (int o = 16; o > 0; o >>= 1) a_sum += __shfl_xor_sync(0xffffffffu, a_sum, o);
   if (lane == 0) s_red[warp] = a_sum;
   __syncthreads();
-  if (tid == 0 && has_obj) {
+  if (tid == 0) {
     double t = 0.0;
     for (int w = 0; w < kTrWarps; w++) t += s_red[w];
-    atomicAdd(avg_loss, t);
+    out[2 * L] = has_obj ? t : 0.0;
   }
+}
+
+// out[o] += sum over CTAs b (in index order) of part[b][o]
+__global__ void trace_finalize_kernel(const double* __restrict__ part, int nparts, int L,
+                                      double* __restrict__ cons_sq, double* __restrict__ loss_col,
+                                      double* __restrict__ avg_loss) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = 2 * L + 1;
+  if (o >= n) return;
+  double t = 0.0;
+  for (int b = 0; b < nparts; b++) t += part[(long long)b * n + o];
+  if (o < L) cons_sq[o] += t;
+  else if (o < 2 * L) { if (loss_col) loss_col[o - L] += t; }
+  else if (avg_loss) *avg_loss += t;
 }
 
 // TMA-staged variant (16-byte aligned rows, L <= 128): tiles [L x cw] of W
@@ -136,8 +152,7 @@ template <typename T>
 __global__ void __launch_bounds__(kTrThreads, 2)
     trace_stats_tma_kernel(const __grid_constant__ CUtensorMap tmW, int L, long long d, int cw,
                            int lg_nv, long long ntiles, const double* __restrict__ lam,
-                           const double* __restrict__ wopt, double* __restrict__ cons_sq,
-                           double* __restrict__ loss_col, double* __restrict__ avg_loss) {
+                           const double* __restrict__ wopt, double* __restrict__ part) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -271,29 +286,41 @@ __global__ void __launch_bounds__(kTrThreads, 2)
       if (tn < ntiles) issue(st, tn);
     }
   }
+  // deterministic in-CTA reduction: the (drained) stage buffers hold every
+  // thread's accumulators; thread j sums the owners of learner j in thread order
+  __syncthreads();
+  double* s_acc = reinterpret_cast<double*>(stages);  // [kTrThreads][kTrItems][2]
 #pragma unroll
   for (int k = 0; k < kTrItems; k++) {
-    const int j = row0 + k * row_step;
-    if (j < L) {
-      atomicAdd(&s_rows[j], acc_c[k]);
-      atomicAdd(&s_rows[kTrMaxL + j], acc_l[k]);
-    }
+    s_acc[(tid * kTrItems + k) * 2] = acc_c[k];
+    s_acc[(tid * kTrItems + k) * 2 + 1] = acc_l[k];
   }
   for (int o = 16; o > 0; o >>= 1) a_sum += __shfl_xor_sync(0xffffffffu, a_sum, o);
+  if ((tid & 31) == 0) s_rows[tid >> 5] = a_sum;
   __syncthreads();
+  double* out = part + (long long)blockIdx.x * (2 * L + 1);
   for (int j = tid; j < L; j += kTrThreads) {
-    atomicAdd(&cons_sq[j], s_rows[j]);
-    if (has_obj) atomicAdd(&loss_col[j], 0.5 * s_rows[kTrMaxL + j]);
+    const int k = j / row_step, r = j % row_step;
+    double c = 0.0, q = 0.0;
+    for (int vv = 0; vv < nv_full; vv++) {
+      const int owner = (r << lg_nv) | vv;
+      c += s_acc[(owner * kTrItems + k) * 2];
+      q += s_acc[(owner * kTrItems + k) * 2 + 1];
+    }
+    out[j] = c;
+    out[L + j] = has_obj ? 0.5 * q : 0.0;
   }
-  if ((tid & 31) == 0 && has_obj) atomicAdd(avg_loss, a_sum);
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kTrThreads / 32; w++) t += s_rows[w];
+    out[2 * L] = has_obj ? t : 0.0;
+  }
 }
 
-// Returns 0 (launched), a CUDA error, or sets *covered = false for shapes the
-// tiled kernel does not handle (the caller then uses the generic kernel).
 template <typename T>
 static int trace_stats_tma(const T* W, int L, int64_t d, int64_t ld, const double* lam,
-                           const double* wopt, double* cons_sq, double* loss_col,
-                           double* avg_loss, cudaStream_t st, bool* covered) {
+                           const double* wopt, double* part, int* nparts, cudaStream_t st,
+                           bool* covered) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const size_t esz = sizeof(T);
@@ -321,36 +348,54 @@ static int trace_stats_tma(const T* W, int L, int64_t d, int64_t ld, const doubl
   const long long ntiles = (d + cw - 1) / cw;
   long long grid = 2LL * sm_count(-1);
   if (grid > ntiles) grid = ntiles;
-  trace_stats_tma_kernel<T><<<(int)grid, kTrThreads, smem, st>>>(
-      tm, L, d, cw, lg, ntiles, lam, wopt, cons_sq, loss_col, avg_loss);
+  *nparts = (int)grid;
+  trace_stats_tma_kernel<T><<<(int)grid, kTrThreads, smem, st>>>(tm, L, d, cw, lg, ntiles, lam,
+                                                                 wopt, part);
   RM_CHECK_LAUNCH("trace_stats_tma_kernel");
   return 0;
+}
+
+// per-CTA partial sums: at most max(8, 2) CTAs per SM x (2L + 1) doubles
+static int64_t trace_workspace_bytes(int L) {
+  return (int64_t)8 * sm_count(-1) * (2 * (int64_t)L + 1) * (int64_t)sizeof(double);
 }
 
 template <typename T>
 static int trace_stats(const T* W, int L, int64_t d, int64_t ld, const double* lam,
                        const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
-                       void* stream) {
+                       void* workspace, int64_t workspace_bytes, void* stream) {
   if (W == nullptr || cons_sq == nullptr || L < 1 || L > kTrMaxL || d < 0 || ld < d ||
       (lam != nullptr && (wopt == nullptr || loss_col == nullptr || avg_loss == nullptr))) {
     set_error("invalid trace-stat arguments (L=%d, at most %d)", L, kTrMaxL);
     return RM_EINVAL;
   }
+  if (workspace == nullptr || workspace_bytes < trace_workspace_bytes(L)) {
+    set_error("trace-stat workspace too small (need %lld bytes)",
+              (long long)trace_workspace_bytes(L));
+    return RM_EINVAL;
+  }
   if (d == 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* part = static_cast<double*>(workspace);
+  int nparts = 0;
   constexpr int VEC = Elem<T>::VEC;
   const bool aligned = ((reinterpret_cast<uintptr_t>(W) | (uintptr_t)(ld * sizeof(T))) & 15) == 0;
+  bool covered = false;
   if (aligned && d >= VEC && d < (1LL << 31) && L <= 128 && tma_encode_fn() != nullptr &&
       getenv("RINGMIX_TRACE_NO_TMA") == nullptr) {
-    bool covered = false;
-    const int rc = trace_stats_tma<T>(W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss,
-                                      static_cast<cudaStream_t>(stream), &covered);
-    if (rc != 0 || covered) return rc;
+    const int rc = trace_stats_tma<T>(W, L, d, ld, lam, wopt, part, &nparts, st, &covered);
+    if (rc != 0) return rc;
   }
-  long long blocks = (d + kTrThreads - 1) / kTrThreads;
-  if (blocks > 8LL * sm_count(-1)) blocks = 8LL * sm_count(-1);
-  trace_stats_kernel<T><<<(int)blocks, kTrThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss);
-  RM_CHECK_LAUNCH("trace_stats_kernel");
+  if (!covered) {
+    long long blocks = (d + kTrThreads - 1) / kTrThreads;
+    if (blocks > 8LL * sm_count(-1)) blocks = 8LL * sm_count(-1);
+    nparts = (int)blocks;
+    trace_stats_kernel<T><<<(int)blocks, kTrThreads, 0, st>>>(W, L, d, ld, lam, wopt, part);
+    RM_CHECK_LAUNCH("trace_stats_kernel");
+  }
+  trace_finalize_kernel<<<(2 * L + 1 + 127) / 128, 128, 0, st>>>(
+      part, nparts, L, cons_sq, lam ? loss_col : nullptr, lam ? avg_loss : nullptr);
+  RM_CHECK_LAUNCH("trace_finalize_kernel");
   return 0;
 }
 
@@ -358,24 +403,23 @@ static int trace_stats(const T* W, int L, int64_t d, int64_t ld, const double* l
 
 using namespace rm;
 
-extern "C" int rm_trace_stats_f32(const float* W, int L, int64_t d, int64_t ld, const double* lam,
-                                  const double* wopt, double* cons_sq, double* loss_col,
-                                  double* avg_loss, void* stream) {
-  return trace_stats<float>(W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss, stream);
+extern "C" int64_t rm_trace_stats_workspace_bytes(int L) {
+  if (L < 1 || L > kTrMaxL) return -1;
+  return trace_workspace_bytes(L);
 }
 
-extern "C" int rm_trace_stats_f64(const double* W, int L, int64_t d, int64_t ld, const double* lam,
-                                  const double* wopt, double* cons_sq, double* loss_col,
-                                  double* avg_loss, void* stream) {
-  return trace_stats<double>(W, L, d, ld, lam, wopt, cons_sq, loss_col, avg_loss, stream);
-}
-
-extern "C" int rm_trace_stats_bf16(const uint16_t* W, int L, int64_t d, int64_t ld,
-                                   const double* lam, const double* wopt, double* cons_sq,
-                                   double* loss_col, double* avg_loss, void* stream) {
-  return trace_stats<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(W), L, d, ld, lam,
-                                    wopt, cons_sq, loss_col, avg_loss, stream);
-}
+#define RM_DEFINE_TRACE(SUFFIX, CT, T)                                                         \
+  extern "C" int rm_trace_stats_##SUFFIX(const CT* W, int L, int64_t d, int64_t ld,           \
+                                         const double* lam, const double* wopt,               \
+                                         double* cons_sq, double* loss_col, double* avg_loss,  \
+                                         void* workspace, int64_t workspace_bytes,             \
+                                         void* stream) {                                       \
+    return trace_stats<T>(reinterpret_cast<const T*>(W), L, d, ld, lam, wopt, cons_sq,        \
+                          loss_col, avg_loss, workspace, workspace_bytes, stream);             \
+  }
+RM_DEFINE_TRACE(f32, float, float)
+RM_DEFINE_TRACE(f64, double, double)
+RM_DEFINE_TRACE(bf16, uint16_t, __nv_bfloat16)
 
 // ---- column mean (numpy pairwise order), the D1D average on its own ----
 // M[c] = pairwise_sum_l W[l, c] / L, bit-identical to the mean the fused

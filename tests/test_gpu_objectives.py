@@ -192,3 +192,19 @@ def test_trace_stats_tiled_and_generic_kernels_agree(dtype, monkeypatch):
         loss_cols = 0.5 * (lam * (W - opt) ** 2).sum(axis=1)
         np.testing.assert_allclose(a[0].cpu().numpy(), cons, rtol=1e-10)
         np.testing.assert_allclose(a[1].cpu().numpy(), loss_cols, rtol=1e-10)
+
+
+@pytest.mark.parametrize("no_tma", ["", "1"])
+def test_trace_stats_are_deterministic(no_tma, monkeypatch):
+    """Per-CTA partials summed in a fixed order: repeated reductions of the same W give
+    identical bits (the reference's trace CSVs are byte-stable for a fixed config)."""
+    if no_tma:
+        monkeypatch.setenv("RINGMIX_TRACE_NO_TMA", "1")
+    L, d = 64, 3_000_017
+    oracle = objectives.quadratic_oracle(d, condition_number=7.0, noise_scale=0.0, seed=2)
+    X = mixing.empty_learner_major(L, d, torch.float32, "cuda").normal_()
+    first = simulation.trace_stats(X.T, oracle)
+    for _ in range(5):
+        again = simulation.trace_stats(X.T, oracle)
+        for x, y in zip(first, again):
+            assert torch.equal(x, y)
