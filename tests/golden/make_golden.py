@@ -4,7 +4,8 @@ Run in the build container, where /root/reference exists:
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
 
-Writes tests/golden/{perms,sequential,steps,spectral}.npz.  Each file records
+Writes tests/golden/{perms,sequential,steps,spectral,normals,training}.npz and
+tests/golden/sweep/*.csv (`make_golden.py sweep` regenerates only the sweep).  Each file records
 the numpy version it was produced under (the Generator stream is only
 guaranteed stable within a numpy version; these were frozen under 2.3.5 /
 OpenBLAS 0.3.30).  Nothing at test time reads /root/reference: the GPU box
@@ -213,10 +214,35 @@ def make_training():
     print("training:", len(specs), "runs")
 
 
+SWEEP_CFG = dict(learner_counts=(4, 8), iterations=6, trials=2, master_seed=7, lr=0.05,
+                 batch_mode="per-learner-fixed", batch_size=4, log_every=2, dimension=24,
+                 oracle_seed=3, condition_number=10.0, noise_scale=1.0, straggler_count=1,
+                 straggler_factor=3.0)
+
+
+def make_sweep():
+    """The reference's run_sweep artefacts (harness.py:192-234) for a small grid over all
+    five strategies: per-cell trace CSVs, summary.csv, aggregate.csv."""
+    import shutil
+    import tempfile
+    from ringmix.config import ExperimentConfig
+
+    cfg = ExperimentConfig(strategies=tuple(Strategy), **SWEEP_CFG)
+    dst = OUT / "sweep"
+    if dst.exists():
+        shutil.rmtree(dst)
+    with tempfile.TemporaryDirectory() as tmp:
+        harness.run_sweep(cfg, tmp, quiet=True)
+        dst.mkdir()
+        for f in sorted(Path(tmp).glob("*.csv")):
+            shutil.copy(f, dst / f.name)
+    print("sweep:", len(list(dst.glob("*.csv"))), "files")
+
+
+MAKERS = dict(perms=make_perms, sequential=make_sequential, steps=make_steps,
+              spectral=make_spectral, normals=make_normals, training=make_training,
+              sweep=make_sweep)
+
 if __name__ == "__main__":
-    make_perms()
-    make_sequential()
-    make_steps()
-    make_spectral()
-    make_normals()
-    make_training()
+    for name in (sys.argv[1:] or list(MAKERS)):
+        MAKERS[name]()

@@ -1,0 +1,52 @@
+"""run_sweep on the GPU vs the reference's own sweep artefacts (tests/golden/sweep/):
+same files, same rows, seeds / iterations / simulated times / rho exact, losses and
+consensus within fp64 rounding of the reference (parallel vs sequential sums over the
+parameters), and the device run is byte-stable run to run."""
+
+from __future__ import annotations
+
+import csv
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2002_01119_b200 import harness
+from paper_2002_01119_b200.simulation import Strategy
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden" / "sweep"
+CFG = harness.SweepConfig(strategies=tuple(Strategy), learner_counts=(4, 8), iterations=6,
+                          trials=2, master_seed=7, lr=0.05, batch_mode="per-learner-fixed",
+                          batch_size=4, log_every=2, dimension=24, oracle_seed=3,
+                          condition_number=10.0, noise_scale=1.0, straggler_count=1,
+                          straggler_factor=3.0)
+
+
+def _rows(path):
+    with open(path) as f:
+        return list(csv.DictReader(f))
+
+
+def test_sweep_matches_reference_artefacts(tmp_path):
+    res = harness.run_sweep(CFG, tmp_path / "a", quiet=True)
+    assert not res.any_diverged
+    ours = sorted(p.name for p in (tmp_path / "a").glob("*.csv"))
+    assert ours == sorted(p.name for p in GOLD.glob("*.csv"))
+    exact = {"iter", "sim_time_s", "rho", "strategy", "n_learners", "trial", "run_seed",
+             "csv_file", "status", "final_iter", "total_sim_time_s", "trials", "completed",
+             "median_total_sim_time_s"}
+    for name in ours:
+        a, b = _rows(tmp_path / "a" / name), _rows(GOLD / name)
+        assert len(a) == len(b) and list(a[0]) == list(b[0])
+        for ra, rb in zip(a, b):
+            for k in ra:
+                if k in exact:
+                    assert ra[k] == rb[k], (name, k)
+                else:
+                    np.testing.assert_allclose(float(ra[k]), float(rb[k]), rtol=1e-10,
+                                               atol=1e-12, err_msg=f"{name}:{k}")
+    # byte-stable: a second run writes the same bytes
+    harness.run_sweep(CFG, tmp_path / "b", quiet=True)
+    for name in ours:
+        assert (tmp_path / "a" / name).read_bytes() == (tmp_path / "b" / name).read_bytes()
