@@ -239,7 +239,16 @@ def make_sweep():
     print("sweep:", len(list(dst.glob("*.csv"))), "files")
 
 
-MAKERS = dict(perms=make_perms, sequential=make_sequential, steps=make_steps,
+def make_bounds():
+    """The reference's verify_bounds (harness.py:283-336) report and rows."""
+    rep = harness.verify_bounds(learner_counts=(3, 4, 8, 16, 33), k_max=8, trials=300, seed=5)
+    rows = np.array([[r.n_learners, r.rho, r.eig_gap, r.powering_excess, r.mc_fro_ratio,
+                      r.mc_spec_ratio] for r in rep.rows])
+    np.savez_compressed(OUT / "bounds.npz", rows=rows, render=np.array(rep.render()), **META)
+    print("bounds:", len(rep.rows), "rows")
+
+
+MAKERS = dict(bounds=make_bounds, perms=make_perms, sequential=make_sequential, steps=make_steps,
               spectral=make_spectral, normals=make_normals, training=make_training,
               sweep=make_sweep)
 

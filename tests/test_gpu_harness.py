@@ -50,3 +50,20 @@ def test_sweep_matches_reference_artefacts(tmp_path):
     harness.run_sweep(CFG, tmp_path / "b", quiet=True)
     for name in ours:
         assert (tmp_path / "a" / name).read_bytes() == (tmp_path / "b" / name).read_bytes()
+
+
+def test_verify_bounds_matches_reference_report():
+    """BASELINE config 5's caller (harness.py:283-336) with the Monte-Carlo trials on
+    the GPU: same rows as the reference's own report (tests/golden/bounds.npz)."""
+    z = np.load(GOLD.parent / "bounds.npz")
+    rep = harness.verify_bounds(learner_counts=(3, 4, 8, 16, 33), k_max=8, trials=300, seed=5)
+    rows = np.array([[r.n_learners, r.rho, r.eig_gap, r.powering_excess, r.mc_fro_ratio,
+                      r.mc_spec_ratio] for r in rep.rows])
+    ref = z["rows"]
+    assert np.array_equal(rows[:, :2], ref[:, :2])
+    np.testing.assert_allclose(rows[:, 2:4], ref[:, 2:4], rtol=0, atol=1e-14)
+    # the Frobenius ratio is |mean - closed| / (3 se): a difference of nearly equal
+    # numbers, so compare it (an O(1) quantity) to an absolute 1e-6
+    np.testing.assert_allclose(rows[:, 4:], ref[:, 4:], rtol=1e-6, atol=1e-6)
+    assert rep.ok and "overall: PASS" in str(z["render"])
+    assert rep.render().splitlines()[:2] == str(z["render"]).splitlines()[:2]
