@@ -1,9 +1,10 @@
 """The reference's acceptance criteria that exercise the learner-averaging path
 (pkg/tests/test_acceptance.py:144-268), run through the B200 drop-in with the same
 grids, seeds, tolerances and time budgets: the paper's claims reproduced on the GPU
-path.  Criterion 6 (randomized beats fixed), 7 (stale-ring loss grows with the
-learner count), 8 (exact averaging <= randomized ring <= fixed ring, the first two
-within 10 %), 9 (exact consensus after averaging, quadratic oracle)."""
+path.  Criterion 5 (Monte-Carlo consensus rate vs the closed forms), 6 (randomized
+beats fixed), 7 (stale-ring loss grows with the learner count), 8 (exact averaging <=
+randomized ring <= fixed ring, the first two within 10 %), 9 (exact consensus after
+averaging) and 11's mass conservation, all with the quadratic oracle."""
 
 from __future__ import annotations
 
@@ -81,3 +82,39 @@ def test_criterion_09_exact_consensus_after_averaging():
     recon = trace.state.weights + cfg.lr * trace.state.last_gradients
     worst = max(worst, simulation.consensus_distance(recon))
     assert worst <= 1e-12, f"worst post-averaging consensus {worst:.3e}"
+
+
+def test_criterion_05_randomized_consensus_rate():
+    from paper_2002_01119_b200.spectral import (randomized_consensus_bound,
+                                                 randomized_frobenius_expectation)
+    z95 = 1.959963984540054
+    t0 = time.monotonic()
+    for L in (4, 8, 16, 32):
+        fro = monte_carlo_consensus(L, 20, trials=1000, seed=2)
+        spec = monte_carlo_consensus(L, 20, trials=1000, seed=2, norm_kind="spectral")
+        for k in range(1, 21):
+            closed = randomized_frobenius_expectation(L, k)
+            tol = 3.0 * fro.squared_halfwidths[k - 1] / z95 + 1e-12 * max(1.0, closed)
+            assert abs(fro.squared_distances[k - 1] - closed) <= tol, (L, k)
+            assert spec.distances[k - 1] <= randomized_consensus_bound(L, k), (L, k)
+    assert time.monotonic() - t0 < 300.0
+
+
+def test_criterion_11_mass_conservation_every_strategy():
+    """Mixing moves the learner average only by the mean gradient (<= 1e-10), for
+    every step function, through the device kernels (fp64)."""
+    steps = {Strategy.SPSGD: simulation.step_spsgd, Strategy.DPSGD_FIXED: simulation.step_dpsgd_fixed,
+             Strategy.ADPSGD_FIXED: simulation.step_adpsgd_fixed,
+             Strategy.RAND_PSGD: simulation.step_rand_psgd, Strategy.D1D: simulation.step_d1d}
+    oracle = objectives.quadratic_oracle(dimension=8, condition_number=10.0, noise_scale=2.0,
+                                         seed=2)
+    worst = 0.0
+    for strategy, step in steps.items():
+        cfg = RunConfig(n_learners=8, iterations=60, lr=0.05, batch_size=4, seed=9)
+        state = simulation.initial_state(oracle, cfg)
+        for _ in range(cfg.iterations):
+            before = state.weights.mean(dim=1)
+            state = step(state, oracle, cfg)
+            expected = before - cfg.lr * state.last_gradients.mean(dim=1)
+            worst = max(worst, float((state.weights.mean(dim=1) - expected).abs().max()))
+    assert worst <= 1e-10, f"worst mean-drift {worst:.3e}"
