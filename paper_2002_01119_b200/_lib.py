@@ -135,16 +135,30 @@ def check(rc: int, what: str = "") -> None:
     raise RingmixError(f"{what}: {msg} (cuda error {rc})")
 
 
+_cuda_ok = False
+
+
 def require_cuda(t: torch.Tensor | None = None) -> None:
-    if not torch.cuda.is_available():
-        raise RuntimeError("ringmix_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+    global _cuda_ok
+    if not _cuda_ok:       # a positive answer is cached (the check costs ~5 us per call)
+        if not torch.cuda.is_available():
+            raise RuntimeError("ringmix_b200 needs a CUDA device (B200, sm_100a); "
+                               "no CPU fallback")
+        _cuda_ok = True
     if t is not None and not t.is_cuda:
         raise ValueError("expected a CUDA tensor")
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    """cudaStream_t of `stream`, default: the current stream of the current device."""
+    if stream is not None:
+        return int(stream.cuda_stream)
+    if _raw_stream is not None:          # same value, without building a Stream object
+        return int(_raw_stream(torch.cuda.current_device()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def ptr(t: torch.Tensor | None) -> int | None:
