@@ -507,6 +507,7 @@ class LearnerShardedD1DFused:
             raise RuntimeError("NVSwitch multicast (NVLS) is not available on this system")
         self.counters = torch.zeros(2 * self.MAX_CHUNKS, dtype=torch.int32, device=self.device)
         quantum = 32 * self.world
+        chunk_cols = int(os.environ.get("RINGMIX_D1D_FUSED_CHUNK", chunk_cols))
         chunk = max(chunk_cols, -(-d // self.MAX_CHUNKS), quantum)
         self.chunk = -(-chunk // quantum) * quantum
         if split is None:
