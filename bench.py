@@ -88,6 +88,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--event-every", type=int, default=4,
+                    help="bracket every N-th mix launch with CUDA events (roofline timing)")
     return ap.parse_args()
 
 
@@ -527,8 +529,10 @@ def run_ours(args):
     if clocks:
         clocks.start()
         time.sleep(0.3)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    # per-launch events bracket every `event_every`-th mix launch (1 = all of them)
+    sampled = [i for i in range(args.steps) if i % args.event_every == 0]
+    kev = {i: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for i in sampled}
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if ws > 1:
         dist.barrier()
@@ -539,14 +543,14 @@ def run_ours(args):
         clocks.mark(True)
     t_start.record(stream)
     for i in range(args.steps):
-        wl.step(k, kev[i])
+        wl.step(k, kev.get(i))
         k += 1
     t_stop.record(stream)
     torch.cuda.synchronize()
     if clocks:
         clocks.mark(False)
     elapsed_ms = t_start.elapsed_time(t_stop)
-    kern_ms = [a.elapsed_time(b) for a, b in kev]
+    kern_ms = [a.elapsed_time(b) for a, b in kev.values()]
     launches = dict(wl.launches)
     bits = wl.amax[:k].cpu().numpy().view(np.float64)
     if not np.all(np.isfinite(bits)):
