@@ -16,12 +16,18 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_learner_sharded_steps_on_all_visible_gpus():
+@pytest.mark.parametrize("L,d", [(64, 1_000_003), (67, 100_003), (5, 4_099)])
+def test_learner_sharded_steps_on_all_visible_gpus(L, d):
+    """Balanced and unbalanced learner shards, ragged widths: RAD (pull and position
+    layouts, in-kernel step ordering) bit-identical to one GPU; D1D (NCCL, NVLS pipeline,
+    fused kernel; fp32 / fp64 / bf16) within fp64 rounding of the sum."""
+    import os
     n = min(torch.cuda.device_count(), 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", "29517",
            str(ROOT / "tools" / "dist_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, CHK_L=str(L), CHK_D=str(d))
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [x for x in r.stdout.splitlines() if x.startswith("{")][-1]
     res = json.loads(line)
