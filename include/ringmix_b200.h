@@ -75,6 +75,9 @@ int rm_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 int rm_device_alloc(int64_t bytes, void** ptr);
 int rm_device_free(void* ptr);
 int rm_stream_synchronize(void* stream);
+/* Single-process multi-GPU: enable peer access between every pair of devices 0..ndev-1
+ * (already-enabled pairs are fine; RM_ENOSYS if a pair has no P2P path). */
+int rm_enable_peer_access(int ndev);
 
 /* ---- permutations (bit-exact with numpy 2.3.5 SeedSequence/PCG64/permutation) ----
  * prefix_words: the entropy words of (seed, tag) — numpy's

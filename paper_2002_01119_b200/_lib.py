@@ -34,6 +34,7 @@ _SIGNATURES = {
     "rm_device_alloc": ([i64, vp], i32),
     "rm_device_free": ([vp], i32),
     "rm_stream_synchronize": ([vp], i32),
+    "rm_enable_peer_access": ([i32], i32),
     "rm_perm_tables": ([vp, i32, u64, i32, i32, vp, vp, vp, vp, vp], i32),
     "rm_perm_sequential": ([vp, i32, u64, i32, i32, i32, vp, vp], i32),
     "rm_pcg64_raw": ([vp, i32, i32, vp, vp], i32),

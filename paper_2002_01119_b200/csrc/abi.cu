@@ -75,3 +75,43 @@ extern "C" int rm_stream_synchronize(void* stream) {
   if (e != cudaSuccess) return rm::fail_cuda(e, "cudaStreamSynchronize");
   return 0;
 }
+
+// single-process multi-GPU callers (one host thread driving several
+// GPUs) enable peer access between every pair of the first ndev devices; the
+// learner-sharded kernels then read / write peer rows through plain device
+// pointers.  Already-enabled pairs are not an error.  The current device is
+// restored.
+extern "C" int rm_enable_peer_access(int ndev) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess) return rm::fail_cuda(e, "cudaGetDeviceCount");
+  if (ndev < 1 || ndev > count) {
+    rm::set_error("ndev=%d outside [1, %d]", ndev, count);
+    return RM_EINVAL;
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int a = 0; a < ndev; a++) {
+    e = cudaSetDevice(a);
+    if (e != cudaSuccess) return rm::fail_cuda(e, "cudaSetDevice");
+    for (int b = 0; b < ndev; b++) {
+      if (a == b) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, a, b);
+      if (!can) {
+        cudaSetDevice(cur);
+        rm::set_error("device %d cannot access device %d", a, b);
+        return RM_ENOSYS;
+      }
+      e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();  // clear the sticky-free status
+      } else if (e != cudaSuccess) {
+        cudaSetDevice(cur);
+        return rm::fail_cuda(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  }
+  cudaSetDevice(cur);
+  return 0;
+}
