@@ -73,3 +73,14 @@ def test_device_binding_matches_drop_in():
     assert torch.equal(bufs[0].long(), tabs.perm[0].long())
     assert torch.equal(out, ref)
     assert absmax.item() > 0
+
+
+def test_enable_peer_access():
+    lib = _lib.load()
+    n = torch.cuda.device_count()
+    _lib.check(lib.rm_enable_peer_access(n))
+    _lib.check(lib.rm_enable_peer_access(n))          # idempotent
+    with pytest.raises(ValueError):
+        _lib.check(lib.rm_enable_peer_access(0))
+    with pytest.raises(ValueError):
+        _lib.check(lib.rm_enable_peer_access(n + 1))
