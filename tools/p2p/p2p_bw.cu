@@ -139,5 +139,55 @@ int main() {
     timeit("bulk st 512B x4", [&] { k_bulk_st<512><<<sms * 4, 32, 512>>>(src, bytes); }, bytes, w);
     timeit("cudaMemcpyPeer", [&] { cudaMemcpyPeerAsync(b0, 0, b1, 1, bytes); }, bytes, peer ? "peer" : "peer");
   }
+  // bidirectional: each GPU reads the other's memory at the same time (what two ranks of
+  // the learner-sharded pull kernel do), 16-byte loads, 4 CTAs/SM
+  {
+    CK(cudaSetDevice(1));
+    CK(cudaDeviceEnablePeerAccess(0, 0));
+    uint4* sink1; CK(cudaMalloc(&sink1, 64));
+    cudaStream_t s1; CK(cudaStreamCreate(&s1));
+    cudaEvent_t a1, b1e; CK(cudaEventCreate(&a1)); CK(cudaEventCreate(&b1e));
+    CK(cudaSetDevice(0));
+    cudaStream_t s0; CK(cudaStreamCreate(&s0));
+    for (int rep = 0; rep < 3; rep++) {
+      CK(cudaSetDevice(0));
+      cudaEventRecord(a, s0);
+      for (int r = 0; r < 5; r++) k_ld<<<sms * 4, 256, 0, s0>>>((const uint4*)b1, bytes / 16, sink);
+      cudaEventRecord(b, s0);
+      CK(cudaSetDevice(1));
+      cudaEventRecord(a1, s1);
+      for (int r = 0; r < 5; r++) k_ld<<<sms * 4, 256, 0, s1>>>((const uint4*)b0, bytes / 16, sink1);
+      cudaEventRecord(b1e, s1);
+      cudaEventSynchronize(b1e);
+      CK(cudaSetDevice(0));
+      cudaEventSynchronize(b);
+      float m0 = 0, m1 = 0;
+      cudaEventElapsedTime(&m0, a, b);
+      cudaEventElapsedTime(&m1, a1, b1e);
+      printf("%-28s %-6s %8.1f GB/s (GPU0 reads GPU1) %8.1f GB/s (GPU1 reads GPU0)\n",
+             "bidirectional ld16 x4", "peer", bytes * 5 / (m0 * 1e-3) / 1e9,
+             bytes * 5 / (m1 * 1e-3) / 1e9);
+    }
+    // bidirectional stores (what the ring-position layout's relabel stores do)
+    for (int rep = 0; rep < 3; rep++) {
+      CK(cudaSetDevice(0));
+      cudaEventRecord(a, s0);
+      for (int r = 0; r < 5; r++) k_st<<<sms * 4, 256, 0, s0>>>((uint4*)b1, bytes / 16);
+      cudaEventRecord(b, s0);
+      CK(cudaSetDevice(1));
+      cudaEventRecord(a1, s1);
+      for (int r = 0; r < 5; r++) k_st<<<sms * 4, 256, 0, s1>>>((uint4*)b0, bytes / 16);
+      cudaEventRecord(b1e, s1);
+      cudaEventSynchronize(b1e);
+      CK(cudaSetDevice(0));
+      cudaEventSynchronize(b);
+      float m0 = 0, m1 = 0;
+      cudaEventElapsedTime(&m0, a, b);
+      cudaEventElapsedTime(&m1, a1, b1e);
+      printf("%-28s %-6s %8.1f GB/s (GPU0 -> GPU1) %8.1f GB/s (GPU1 -> GPU0)\n",
+             "bidirectional st16 x4", "peer", bytes * 5 / (m0 * 1e-3) / 1e9,
+             bytes * 5 / (m1 * 1e-3) / 1e9);
+    }
+  }
   return 0;
 }
