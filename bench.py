@@ -621,7 +621,7 @@ def run_ours(args):
     wl.close()
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu:   # the CPU baseline is an N = 1 figure
         del wl
         cpu = cpu_baseline(L, uniform, args.cpu_seconds)
 
