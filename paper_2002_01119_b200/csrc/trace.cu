@@ -157,10 +157,10 @@ __global__ void __launch_bounds__(kTrThreads, 2)
   constexpr int VEC = E::VEC;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  double* s_mean = reinterpret_cast<double*>(smem + 128);
-  double* s_lm = s_mean + cw;
-  double* s_wo = s_lm + cw;
-  double* s_rows = s_wo + cw;  // [2][L] block totals
+  // column means / lam / w* of a tile, double-buffered: phase A of tile t+1 runs in
+  // the same barrier interval as phase B of tile t (one __syncthreads per tile)
+  double* s_cols = reinterpret_cast<double*>(smem + 128);  // [2][3][cw]
+  double* s_rows = s_cols + 6 * cw;                           // [2][L] block totals
   unsigned char* stages =
       reinterpret_cast<unsigned char*>(s_rows + 2 * kTrMaxL) +
       ((128 - (((uintptr_t)(s_rows + 2 * kTrMaxL)) & 127)) & 127);
@@ -199,14 +199,16 @@ __global__ void __launch_bounds__(kTrThreads, 2)
 #pragma unroll
   for (int k = 0; k < kTrItems; k++) acc_c[k] = acc_l[k] = 0.0;
   double a_sum = 0.0;
-  int it = 0;
-  for (long long t = first; t < ntiles; t += stride, ++it) {
+
+  // phase A of the tile in local slot `it`: wait for its stage, column means
+  // (numpy pairwise order) and the average-model loss into buffer it & 1
+  auto phase_a = [&](long long t, int it) {
     const int st = it % kTrStages;
     const long long c0 = t * cw;
     const int width = (int)min((long long)cw, d - c0);
     const T* sW = reinterpret_cast<const T*>(stages + (size_t)st * stage_bytes);
+    double* cm = s_cols + (it & 1) * 3 * cw;
     mbar_wait(&full[st], (it / kTrStages) & 1);
-    // phase A: column means (numpy pairwise order) and the average-model loss
     for (int col = tid; col < width; col += kTrThreads) {
       double res;
       if (L < 8) {
@@ -226,64 +228,76 @@ __global__ void __launch_bounds__(kTrThreads, 2)
         for (int i = n8; i < L; i++) res = __dadd_rn(res, (double)E::lds(sW + sidx(i, col)));
       }
       const double mean = __ddiv_rn(res, (double)L);
-      s_mean[col] = mean;
+      cm[col] = mean;
       if (has_obj) {
         const double lm = lam[c0 + col], wo = wopt[c0 + col];
-        s_lm[col] = lm;
-        s_wo[col] = wo;
+        cm[cw + col] = lm;
+        cm[2 * cw + col] = wo;
         const double dm = __dsub_rn(mean, wo);
         a_sum += 0.5 * lm * dm * dm;
       }
     }
-    __syncthreads();
-    // phase B: this thread's rows over its vector of columns
+  };
+  // phase B of the tile in slot `it`: this thread's rows over its vector of columns
+  auto phase_b = [&](long long t, int it) {
+    const int st = it % kTrStages;
+    const int width = (int)min((long long)cw, d - t * cw);
+    const T* sW = reinterpret_cast<const T*>(stages + (size_t)st * stage_bytes);
+    const double* cm = s_cols + (it & 1) * 3 * cw;
     const int c = v * VEC;
-    if (c < width) {
-      // 16-byte shared loads: a thread owns VEC consecutive columns (scalar loads
-      // would be 2*VEC-way bank conflicts); entries past `width` are never used
-      double m[VEC], lm[VEC], wo[VEC];
+    if (c >= width) return;
+    // 16-byte shared loads: a thread owns VEC consecutive columns (scalar loads
+    // would be 2*VEC-way bank conflicts); entries past `width` are never used
+    double m[VEC], lm[VEC], wo[VEC];
 #pragma unroll
-      for (int e = 0; e < VEC; e += 2) {
-        const double2 a2 = *reinterpret_cast<const double2*>(s_mean + c + e);
-        m[e] = a2.x;
-        m[e + 1] = a2.y;
-        if (has_obj) {
-          const double2 l2 = *reinterpret_cast<const double2*>(s_lm + c + e);
-          const double2 w2 = *reinterpret_cast<const double2*>(s_wo + c + e);
-          lm[e] = l2.x;
-          lm[e + 1] = l2.y;
-          wo[e] = w2.x;
-          wo[e + 1] = w2.y;
-        } else {
-          lm[e] = lm[e + 1] = wo[e] = wo[e + 1] = 0.0;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kTrItems; k++) {
-        const int j = row0 + k * row_step;
-        if (j < L) {
-          Vec<T> x;
-          x.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
-          double vv = 0.0, qq = 0.0;
-#pragma unroll
-          for (int e = 0; e < VEC; e++) {
-            if (c + e < width) {
-              const double w = (double)E::ld(x.e(), e);
-              const double dv = w - m[e];
-              vv += dv * dv;
-              const double dw = w - wo[e];
-              qq += lm[e] * dw * dw;
-            }
-          }
-          acc_c[k] += vv;
-          acc_l[k] += qq;
-        }
+    for (int e = 0; e < VEC; e += 2) {
+      const double2 a2 = *reinterpret_cast<const double2*>(cm + c + e);
+      m[e] = a2.x;
+      m[e + 1] = a2.y;
+      if (has_obj) {
+        const double2 l2 = *reinterpret_cast<const double2*>(cm + cw + c + e);
+        const double2 w2 = *reinterpret_cast<const double2*>(cm + 2 * cw + c + e);
+        lm[e] = l2.x;
+        lm[e + 1] = l2.y;
+        wo[e] = w2.x;
+        wo[e + 1] = w2.y;
+      } else {
+        lm[e] = lm[e + 1] = wo[e] = wo[e + 1] = 0.0;
       }
     }
-    __syncthreads();  // stage consumed, means free
+#pragma unroll
+    for (int k = 0; k < kTrItems; k++) {
+      const int j = row0 + k * row_step;
+      if (j < L) {
+        Vec<T> x;
+        x.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
+        double vv = 0.0, qq = 0.0;
+#pragma unroll
+        for (int e = 0; e < VEC; e++) {
+          if (c + e < width) {
+            const double w = (double)E::ld(x.e(), e);
+            const double dv = w - m[e];
+            vv += dv * dv;
+            const double dw = w - wo[e];
+            qq += lm[e] * dw * dw;
+          }
+        }
+        acc_c[k] += vv;
+        acc_l[k] += qq;
+      }
+    }
+  };
+
+  if (first < ntiles) phase_a(first, 0);
+  __syncthreads();
+  int it = 0;
+  for (long long t = first; t < ntiles; t += stride, ++it) {
+    if (t + stride < ntiles) phase_a(t + stride, it + 1);
+    phase_b(t, it);
+    __syncthreads();  // tile t's stage and mean buffer are free, tile t+1's means ready
     if (tid == 0) {
       const long long tn = t + (long long)kTrStages * stride;
-      if (tn < ntiles) issue(st, tn);
+      if (tn < ntiles) issue(it % kTrStages, tn);
     }
   }
   // deterministic in-CTA reduction: the (drained) stage buffers hold every
@@ -334,7 +348,7 @@ static int trace_stats_tma(const T* W, int L, int64_t d, int64_t ld, const doubl
   const int box_c = cw < 256 ? cw : 256;
   CUtensorMap tm;
   if (!tma_map_2d<T>(&tm, W, d, L, ld, box_c, L)) return 0;
-  const size_t smem = 128 + 3 * (size_t)cw * 8 + 2 * kTrMaxL * 8 + 128 +
+  const size_t smem = 128 + 6 * (size_t)cw * 8 + 2 * kTrMaxL * 8 + 128 +
                       (size_t)kTrStages * L * cw * esz;
   static bool attr = false;
   if (!attr) {
