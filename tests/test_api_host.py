@@ -165,3 +165,23 @@ def test_hot_path_requires_cuda_without_fallback():
         mixing.permutation_for_step(8, 42, 0)
     with pytest.raises(RuntimeError, match="CUDA"):
         mixing.apply_mixing(np.zeros((4, 5)), mixing.build_ring_matrix(5))
+
+
+@pytest.mark.parametrize("L", [4, 5])
+def test_expected_gram_matches_enumeration(L):
+    """E[T'T] over all relabellings of the ring equals the closed form (reference
+    test_spectral.py:71-79), and it is doubly stochastic with eigenvalues {1, a, ..., a}."""
+    import itertools
+    import math
+    T = mixing.build_ring_matrix(L)
+    total = np.zeros((L, L))
+    for perm in itertools.permutations(range(L)):
+        C = mixing.conjugate_by_permutation(T, np.array(perm))
+        total += C.T @ C
+    G = spectral.expected_gram(L)
+    assert np.allclose(total / math.factorial(L), G, atol=1e-14)
+    eig = np.sort(np.linalg.eigvalsh(G))
+    a = 1.0 / 3.0 - 2.0 / (3.0 * (L - 1))
+    assert np.allclose(eig, [a] * (L - 1) + [1.0], atol=1e-14)
+    with pytest.raises(ValueError):
+        spectral.expected_gram(2)
