@@ -150,3 +150,23 @@ def quadratic_oracle(dimension: int, condition_number: float = 1.0, optimum=None
                                   device=device).cpu().numpy()
     return QuadraticObjective(eigenvalues, np.asarray(optimum, dtype=float), noise_scale,
                               device=device)
+
+
+def evaluate_loss(oracle, w) -> float:
+    """Full-batch loss at w (objectives.py:192-194)."""
+    return oracle.loss(w)
+
+
+def gradient_check(oracle, w, step: float = 1e-5) -> float:
+    """Relative error ||fd - grad|| / max(||grad||, 1e-12) of the analytic gradient
+    against central differences of the loss (objectives.py:197-214); host fp64."""
+    if step <= 0:
+        raise ValueError(f"step must be > 0, got {step}")
+    w = np.asarray(w, dtype=float)
+    grad = np.asarray(oracle.gradient(w), dtype=float)
+    fd = np.empty_like(grad)
+    for i in range(len(w)):
+        bump = np.zeros_like(w)
+        bump[i] = step
+        fd[i] = (oracle.loss(w + bump) - oracle.loss(w - bump)) / (2.0 * step)
+    return float(np.linalg.norm(fd - grad)) / max(float(np.linalg.norm(grad)), 1e-12)

@@ -185,3 +185,20 @@ def test_expected_gram_matches_enumeration(L):
     assert np.allclose(eig, [a] * (L - 1) + [1.0], atol=1e-14)
     with pytest.raises(ValueError):
         spectral.expected_gram(2)
+
+
+def test_gradient_check_and_evaluate_loss_on_the_quadratic_oracle():
+    """Reference acceptance criterion 11's finite-difference half (test_acceptance.py:307-315)
+    on the quadratic oracle's host methods (no GPU needed)."""
+    from paper_2002_01119_b200.objectives import QuadraticObjective, evaluate_loss, gradient_check
+    lam = np.logspace(0.0, 1.0, 32)
+    opt = np.random.default_rng(0).standard_normal(32)
+    q = QuadraticObjective.__new__(QuadraticObjective)     # host methods only, no device
+    q.eigenvalues, q.optimum, q.noise_scale = lam, opt, 1.0
+    rng = np.random.default_rng(3)
+    for _ in range(5):
+        w = rng.standard_normal(32)
+        assert gradient_check(q, w) <= 1e-7
+        assert evaluate_loss(q, w) == q.loss(w)
+    with pytest.raises(ValueError):
+        gradient_check(q, w, step=0.0)
