@@ -146,6 +146,18 @@ constexpr int kBox = 256;  // TMA box dimension limit (elements)
 // NT threads per CTA: ring tiles run one 512-thread CTA per SM; mean tiles
 // (D1D / S-PSGD) run two 256-thread CTAs per SM, so one CTA's mean phase
 // overlaps the other's output phase.
+// element-wise round-to-nearest fp32 add of two pairs (FADD2 on sm_100; each lane of
+// the pair is an ordinary IEEE add, nothing is contracted)
+__device__ __forceinline__ float2 fadd2_rn(float2 a, float2 b) {
+  unsigned long long ra, rb, rc;
+  memcpy(&ra, &a, 8);
+  memcpy(&rb, &b, 8);
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rc) : "l"(ra), "l"(rb));
+  float2 c;
+  memcpy(&c, &rc, 8);
+  return c;
+}
+
 // two adjacent bf16 columns of a staged row as floats (exact conversion)
 template <typename T>
 __device__ __forceinline__ float2 lds_pair(const T* p) {
@@ -285,8 +297,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
             float2 r = lds_pair(src + sidx(k, col));
             for (int i = 8 + k; i < n8; i += 8) {
               const float2 v = lds_pair(src + sidx(i, col));
-              r.x = __fadd_rn(r.x, v.x);
-              r.y = __fadd_rn(r.y, v.y);
+              r = fadd2_rn(r, v);  // two independent IEEE adds in one instruction
             }
             s_part[k * cw + col] = r.x;
             s_part[k * cw + col + 1] = r.y;
