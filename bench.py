@@ -604,7 +604,9 @@ def run_ours(args):
         # Pinned host memory per rank: G (L x cols) for the resident e2e, 3x that for
         # the host-arrays variant — the variant only where the whole job stays small.
         ms_res = run_e2e_resident(args, torch, wl, dev)
-        host_ok = not uniform and 3 * wl.local_params * 4 * ws <= host_pinned_budget()
+        # (the variant only at N = 1: at N > 1 every rank would pin 3x its stripe)
+        host_ok = (not uniform and ws == 1
+                   and 3 * wl.local_params * 4 * ws <= host_pinned_budget())
         ms_host = run_e2e(args, torch, mixing, dev, cols=wl.cols) if host_ok else None
         if ws > 1:
             t = torch.tensor([ms_res, ms_host or 0.0], device=dev)
