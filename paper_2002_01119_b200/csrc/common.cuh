@@ -99,6 +99,21 @@ __device__ __forceinline__ unsigned long long abs_bits(double y) {
   return static_cast<unsigned long long>(__double_as_longlong(y)) & 0x7fffffffffffffffULL;
 }
 
+
+// Function attributes (e.g. the dynamic shared-memory opt-in) are per device: a
+// bit per device ordinal records where one has been set (re-setting is harmless,
+// so the unsynchronised update is benign).
+__host__ inline bool attr_needed(unsigned long long* mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 64 || !((*mask >> dev) & 1ull);
+}
+__host__ inline void attr_done(unsigned long long* mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64) *mask |= 1ull << dev;
+}
+
 // ---- cross-GPU step ordering through flags in symmetric memory ----
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;

@@ -537,12 +537,12 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     tmG = tmW;
   }
   size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set_mask = 0;
+  if (attr_needed(&attr_set_mask)) {
     cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
     if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(mix_tma_kernel)");
-    attr_set = true;
+    attr_done(&attr_set_mask);
   }
   long long grid = (long long)sm_count(-1) * (512 / NT);
   if (grid > a.ntiles) grid = a.ntiles;

@@ -435,12 +435,12 @@ static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G
       return RM_EINVAL;
     }
   }
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_mask = 0;
+  if (attr_needed(&attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(mix_shard_kernel<T, HAS_G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
     if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(mix_shard_kernel)");
-    attr = true;
+    attr_done(&attr_mask);
   }
   long long grid = sm_count(-1);
   if (grid > a.ntiles) grid = a.ntiles;

@@ -350,12 +350,12 @@ static int trace_stats_tma(const T* W, int L, int64_t d, int64_t ld, const doubl
   if (!tma_map_2d<T>(&tm, W, d, L, ld, box_c, L)) return 0;
   const size_t smem = 128 + 6 * (size_t)cw * 8 + 2 * kTrMaxL * 8 + 128 +
                       (size_t)kTrStages * L * cw * esz;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_mask = 0;
+  if (attr_needed(&attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(trace_stats_tma_kernel<T>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(trace_stats_tma_kernel)");
-    attr = true;
+    attr_done(&attr_mask);
   }
   if (smem > 110 * 1024) return 0;
   *covered = true;

@@ -84,3 +84,25 @@ def test_enable_peer_access():
         _lib.check(lib.rm_enable_peer_access(0))
     with pytest.raises(ValueError):
         _lib.check(lib.rm_enable_peer_access(n + 1))
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_one_process_drives_several_gpus():
+    """Kernel attributes (dynamic shared memory opt-in) are per device: the TMA mix and
+    trace kernels must work on every GPU one process drives, not only the first."""
+    from paper_2002_01119_b200 import simulation
+    L, d = 64, 100_003
+    outs = []
+    for dev in range(torch.cuda.device_count()):
+        with torch.cuda.device(dev):
+            g = torch.Generator(device=f"cuda:{dev}").manual_seed(1)
+            X = mixing.empty_learner_major(L, d, torch.float32, f"cuda:{dev}")
+            X.copy_(torch.randn((L, d), generator=g, device=f"cuda:{dev}"))
+            tabs = mixing.permutation_tables(L, 5, 0, 1, f"cuda:{dev}")
+            lt, rt = tabs.step(0)
+            out = mixing.ring_mix_sgd(X, X, 0.1, lt, rt)
+            cons = simulation.trace_stats(out.T)[0]
+            torch.cuda.synchronize()
+            outs.append((out.cpu(), cons.cpu()))
+    for o, c in outs[1:]:
+        assert torch.equal(o, outs[0][0]) and torch.equal(c, outs[0][1])
