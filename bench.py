@@ -731,9 +731,12 @@ def run_e2e(args, torch, mixing, dev, cols=None):
     Wh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
     Gh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
     Oh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
-    g = torch.Generator().manual_seed(7)
-    Wh.normal_(generator=g)
-    Gh.normal_(generator=g)
+    # synthetic host inputs, drawn on the device and copied once (a host RNG is ~100x
+    # slower and torchrun runs ranks single-threaded)
+    g = torch.Generator(device=dev).manual_seed(7)
+    for host in (Wh, Gh):
+        for r in range(L):
+            host[r].copy_(torch.randn(d, generator=g, device=dev))
     ws_buf = mixing.host_workspace(L, 1 << 20, dev)
     tabs = M.permutation_tables(L, SEED, 0, args.e2e_steps + 1, dev)
     left = tabs.left.cpu()
