@@ -66,3 +66,25 @@ def test_nvlink_traffic_fixed_ring_tables():
     left, right = np.roll(ident, 1, axis=1), np.roll(ident, -1, axis=1)
     pull = b.nvlink_traffic("learner", 8, 10, 4, 2, ident, ident, left[:1], right[:1])
     assert pull == [(2 * 10 * 4, 0), (2 * 10 * 4, 0)]
+
+
+def test_reference_arm_prints_the_contract_line():
+    """`bench.py --impl reference` (host only: the oracle port of the reference's numpy
+    arithmetic) prints one JSON line with the contract's keys."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "3", "--dim", "4096"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
