@@ -56,3 +56,16 @@ def test_last_error_is_a_string_without_cuda():
 def test_abi_uses_plain_c_types_only():
     code = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
     assert "torch" not in code and "at::" not in code and "Tensor" not in code
+
+
+def test_header_compiles_as_c_and_cpp(tmp_path):
+    """A cgo / JNI / plain-C caller includes the header as C99; a C++ caller as C++."""
+    import shutil
+    import subprocess
+    header = ROOT / "include" / "ringmix_b200.h"
+    for cc, lang, std in (("gcc", "c", "-std=c99"), ("g++", "c++", "-std=c++17")):
+        if shutil.which(cc) is None:
+            continue
+        r = subprocess.run([cc, "-fsyntax-only", "-Wall", "-Werror", "-x", lang, std, str(header)],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
