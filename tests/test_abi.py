@@ -69,3 +69,31 @@ def test_header_compiles_as_c_and_cpp(tmp_path):
         r = subprocess.run([cc, "-fsyntax-only", "-Wall", "-Werror", "-x", lang, std, str(header)],
                            capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
+
+
+def test_plain_c_program_links_and_calls_the_library(tmp_path):
+    """What a cgo / FFI binding does: a C program includes the header, links
+    libringmix_b200.so and calls host-side entry points (no GPU needed for these)."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        return
+    src = tmp_path / "caller.c"
+    src.write_text(
+        "#include <stdio.h>\n"
+        '#include "ringmix_b200.h"\n'
+        "int main(void) {\n"
+        "  int v = rm_version();\n"
+        "  long long ws = (long long)rm_normal_workspace_bytes(4, 1000);\n"
+        "  long long bad = (long long)rm_normal_workspace_bytes(0, 1000);\n"
+        '  printf("%d %lld %lld\\n", v, ws, bad);\n'
+        "  return (v > 0 && ws > 0 && bad < 0) ? 0 : 1;\n"
+        "}\n")
+    exe = tmp_path / "caller"
+    lib = ROOT / "paper_2002_01119_b200" / "lib"
+    r = subprocess.run(["gcc", "-std=c99", "-I", str(ROOT / "include"), str(src), "-L", str(lib),
+                        "-lringmix_b200", f"-Wl,-rpath,{lib}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, (r.stdout, r.stderr)
