@@ -7,14 +7,15 @@
 // HBM layout: learner-major (L, d) rows with leading dimension ld (elements);
 // the reference's (d, L) matrix is the transpose view.
 //
-// Design: a persistent kernel walks column tiles [c0, c0+CW)
-// of all L rows.  Per tile, one warp issues 1-D TMA bulk copies
-// (cp.async.bulk, one per row) of W[:, tile] and G[:, tile] into a shared
-// memory stage, completion tracked by an mbarrier (expect_tx).  NS stages
-// are in flight per CTA, so every W element crosses HBM exactly once although
-// it feeds three outputs (itself and its two ring neighbours), and the whole
-// chip keeps >= 35 KB/SM of loads in flight.  Consumers read the stage with
-// 16-byte shared loads and write W' with 16-byte streaming stores.
+// Design: a persistent kernel walks column tiles [c0, c0+cw)
+// of all L rows.  Per tile, one thread issues 2-D tensor-map TMA loads
+// (cp.async.bulk.tensor.2d, boxes of [L rows x <= 256 columns]) of W[:, tile]
+// and G[:, tile] into a shared-memory stage, completion tracked by an mbarrier
+// (expect_tx).  Three stages are in flight per CTA, so every W element crosses
+// HBM exactly once although it feeds three outputs (itself and its two ring
+// neighbours).  Consumers read the stage with 16-byte shared loads and write
+// W' with 16-byte streaming stores.  Mean tiles (D1D, S-PSGD) first reduce each
+// column in numpy's pairwise order, then apply the update.
 //
 // Arithmetic: fp32/fp64 storage computes in fp64 with the
 // reference's exact rounding sequence, so results are the reference's fp64
