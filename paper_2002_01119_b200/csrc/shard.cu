@@ -14,10 +14,14 @@
 // tile t+2 overlaps the HBM stream and the math of tile t, tile by tile.
 //
 // The arithmetic is the single-GPU kernel's (ascending *global* learner id FMA
-// chain), so a sharded step is bit-identical to the single-GPU step.
+// chain), so a sharded step is bit-identical to the single-GPU step.  With
+// `dest` the same kernel serves the ring-position layout (outputs stored to the
+// learner's next-step slot on any rank), and with an rm_step_sync it orders
+// consecutive steps itself through a multicast flag (no collective).
 //
-// D1D: rm_partial_sum (local column sums, fp64) -> NCCL all-reduce (host side,
-// chunk-pipelined on a side stream) -> rm_apply_mean_sgd.
+// D1D: rm_partial_sum (local column sums, fp64) -> cross-rank sum -> apply:
+// through NCCL (host side), through our in-NVSwitch kernel rm_nvls_mean_f64,
+// or all three phases fused into one launch per rank (rm_d1d_fused_nvls_*).
 #include "common.cuh"
 #include "tma_host.cuh"
 #include "arith.cuh"
