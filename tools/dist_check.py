@@ -61,6 +61,12 @@ def main():
         torch.cuda.synchronize()
         ok_d1d = ok_d1d and bool(torch.equal(out3, outs[0]))
         nvls = f"{nvls} chunks; fused {len(fu.chunks)} chunks ok={bool(torch.equal(out3, outs[0]))}"
+        # no gradients (apply_mixing semantics): the fused kernel's HAS_G = false path
+        out4 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
+        fu.step(ring.weights, None, 0.01, out4)
+        ref4 = mixing.mean_mix_sgd(Wref, None, 0.01)
+        torch.cuda.synchronize()
+        ok_d1d = ok_d1d and (out4.double() - ref4[b:e].double()).abs().max().item() <= 2e-6
         # other storage types: the fused kernel against the single-GPU mean kernel
         for dt, tol in ((torch.float64, 1e-13), (torch.bfloat16, 1e-2)):
             Wd = mixing.empty_learner_major(ring.Lg, d, dt, dev).copy_(full[b:e].to(dt))
