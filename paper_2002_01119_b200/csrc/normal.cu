@@ -137,9 +137,15 @@ struct ZGen {
   __device__ __forceinline__ uint64_t next64() {
     const U128d M = {2549297995355413924ull, 4865540595714422341ull};
     state = add128(mul128(state, M), inc);
-    uint64_t x = state.hi ^ state.lo;
-    unsigned rot = (unsigned)(state.hi >> 58);
-    return (x >> rot) | (x << ((64u - rot) & 63u));
+    // XSL-RR output: rotr64(hi ^ lo, hi >> 58), as two 32-bit funnel shifts after a
+    // conditional half swap (a rotation by >= 32 is a swap plus a rotation by rot & 31)
+    const uint64_t x = state.hi ^ state.lo;
+    const unsigned rot = (unsigned)(state.hi >> 58);
+    uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    const uint32_t sl = (rot & 32u) ? xh : xl, sh = (rot & 32u) ? xl : xh;
+    xl = __funnelshift_r(sl, sh, rot);
+    xh = __funnelshift_r(sh, sl, rot);
+    return ((uint64_t)xh << 32) | xl;
   }
   __device__ __forceinline__ double next_double() {
     return __dmul_rn((double)(next64() >> 11), 1.0 / 9007199254740992.0);
@@ -241,6 +247,27 @@ __device__ __forceinline__ void load_tables(ZigTables* t) {
   }
 }
 
+// Wedge test of a ziggurat attempt (strip idx >= 1, fast test failed) with its
+// second draw u: accept iff (f[idx-1] - f[idx]) * u + f[idx] < exp(-x^2 / 2).  An
+// fp32 exp (relative error < 2e-6 on the strips' range |x| < 3.66) decides unless
+// lhs lies within 2^-16 of it; only then is the fp64 exp evaluated, so the outcome
+// is that of the fp64 comparison.
+#ifndef RM_ZWEDGE_FAST
+#define RM_ZWEDGE_FAST 1
+#endif
+__device__ __forceinline__ bool z_wedge(const ZigTables& T, int idx, double x, uint64_t u) {
+  const double f0 = T.fi[idx - 1], f1 = T.fi[idx];
+  const double ud = __dmul_rn((double)(u >> 11), 1.0 / 9007199254740992.0);
+  const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(f0, f1), ud), f1);
+  const double t = __dmul_rn(__dmul_rn(-0.5, x), x);
+#if RM_ZWEDGE_FAST
+  const double e = (double)__expf((float)t);
+  if (lhs < e * (1.0 - 1.0 / 65536.0)) return true;
+  if (lhs > e * (1.0 + 1.0 / 65536.0)) return false;
+#endif
+  return lhs < exp(t);
+}
+
 // One ziggurat attempt starting with draw `r` (already taken).  Returns true
 // and sets *x when it produces an output; `extra` = further draws consumed.
 __device__ __forceinline__ bool z_attempt(const ZigTables& T, ZGen& g, uint64_t r, double* x,
@@ -269,10 +296,8 @@ __device__ __forceinline__ bool z_attempt(const ZigTables& T, ZGen& g, uint64_t 
       }
     }
   }
-  const double f0 = T.fi[idx - 1], f1 = T.fi[idx];
-  double lhs = __dadd_rn(__dmul_rn(__dsub_rn(f0, f1), g.next_double()), f1);
   *extra = 1;
-  if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, v), v))) {
+  if (z_wedge(T, idx, v, g.next64())) {
     *x = v;
     return true;
   }
@@ -302,11 +327,8 @@ __device__ __forceinline__ bool z_slow(const ZigTables& T, ZGen& g, uint64_t u0,
       u = g.next64();
     }
   }
-  const double f0 = T.fi[idx - 1], f1 = T.fi[idx];
-  const double u = __dmul_rn((double)(u0 >> 11), 1.0 / 9007199254740992.0);
-  const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(f0, f1), u), f1);
   *extra = 1;
-  return lhs < exp(__dmul_rn(__dmul_rn(-0.5, v), v));
+  return z_wedge(T, idx, v, u0);
 }
 
 __device__ __forceinline__ void st_v4_f64(double* p, double a, double b, double c, double d) {
@@ -344,8 +366,10 @@ __device__ __forceinline__ ZStep z_spec_step(const ZigTables& T, ZGen& g, uint64
   const uint64_t rabs = (cur >> 9) & 0x000fffffffffffffull;
   const uint64_t ki = T.ki[idx];
   const double wi = T.wi[idx];
+  // sign from bit 8: flip the product's sign bit (exact, as -x)
   double x = __dmul_rn((double)rabs, wi);
-  if ((cur >> 8) & 1) x = -x;
+  x = __hiloint2double(__double2hiint(x) ^ (int)(((uint32_t)cur & 0x100u) << 23),
+                       __double2loint(x));
   ZStep st;
   if (rabs < ki) {
     st.ok = true;
@@ -362,16 +386,32 @@ __device__ __forceinline__ ZStep z_spec_step(const ZigTables& T, ZGen& g, uint64
   return st;
 }
 
+#ifndef RM_ZKEEP
+#define RM_ZKEEP 0
+#endif
+// RM_ZKEEP 0: quads buffered in registers, 32-byte stores; 1: pairs, 16-byte stores;
+// 2: one 8-byte store per output
 template <bool KEEP>
 __device__ __forceinline__ void z_keep(double* slot, uint32_t count, double x, double& q0,
                                        double& q1, double& q2) {
   if (!KEEP) return;
+#if RM_ZKEEP == 2
+  slot[count] = x;
+#elif RM_ZKEEP == 1
+  if (count & 1u) {
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(slot + count - 1), "d"(q0), "d"(x)
+                 : "memory");
+  }
+  q0 = x;
+#else
   const uint32_t c = count & 3u;
   if (c == 3u) st_v4_f64(slot + count - 3, q0, q1, q2, x);
   q0 = c == 0u ? x : q0;
   q1 = c == 1u ? x : q1;
   q2 = c == 2u ? x : q2;
+#endif
 }
+
 
 template <bool KEEP>
 __global__ void __launch_bounds__(128, RM_ZSPEC_MINB)
@@ -410,10 +450,14 @@ __global__ void __launch_bounds__(128, RM_ZSPEC_MINB)
     pos += st.used;
   }
   if (KEEP) {
+#if RM_ZKEEP == 1
+    if (count & 1u) slot[count - 1] = q0;
+#elif RM_ZKEEP == 0
     const uint32_t r = count & 3u, c0 = count - r;
     if (r > 0) slot[c0] = q0;
     if (r > 1) slot[c0 + 1] = q1;
     if (r > 2) slot[c0 + 2] = q2;
+#endif
   }
   info[(long long)stream * a.nblocks + b] = BlockInfo{att, outs, pos, count};
 }
