@@ -33,7 +33,8 @@
  *   rm_ring_mix_batched_f64 <- product @ T_k of                spectral.py:273-279
  *                            monte_carlo_consensus
  *   rm_ipc_* / rm_shard_* / rm_pos_* / rm_partial_sum_* / rm_apply_mean_sgd_* /
- *   rm_nvls_mean_f64      <- (no reference counterpart: the reference simulates all
+ *   rm_nvls_mean_f64 / rm_step_sync_wait
+ *                         <- (no reference counterpart: the reference simulates all
  *                            learners in one process; these shard them over GPUs —
  *                            the step they compute is still simulation.py:263-268 /
  *                            :304-312)
@@ -180,6 +181,12 @@ typedef struct {
   uint32_t epoch;
   int world;
 } rm_step_sync;
+
+/* Stream-ordered wait until every rank finished step `sync->epoch` (*done >= world *
+ * epoch).  The next step kernel orders itself; any other consumer of a step's outputs
+ * in the ring-position layout (whose rows are written by every rank) calls this first.
+ * Returns 0 without launching when epoch == 0. */
+int rm_step_sync_wait(const rm_step_sync* sync, void* stream);
 
 /* Per-step plan for the rank owning learners [row0, row0+Lg): distinct remote
  * neighbour ids and each local learner's staged input indices in global-id

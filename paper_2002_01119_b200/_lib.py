@@ -69,6 +69,7 @@ _SIGNATURES = {
     "rm_column_mean_bf16": ([vp, i32, i64, i64, vp, vp], i32),
 }
 _SIGNATURES["rm_pos_plan"] = ([vp, vp, i32, i32, i32, vp, vp, vp, vp], i32)
+_SIGNATURES["rm_step_sync_wait"] = ([vp, vp], i32)
 for _sfx in ("f32", "f64", "bf16"):
     _SIGNATURES[f"rm_ring_mix_sgd_pos_{_sfx}"] = (
         [vp, vp, vp, i32, i32, i32, i64, i64, i64, vp, vp, dbl, vp, vp, vp], i32)

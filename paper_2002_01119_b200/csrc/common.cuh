@@ -136,6 +136,8 @@ __device__ __forceinline__ void xgpu_wait(const uint32_t* flag, uint32_t target)
       if (global_ns() - t0 > 20000000000ull) __trap();
     }
     asm volatile("fence.proxy.alias;" ::: "memory");
+    // the peers' generic-proxy stores are read next by TMA (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
   }
   __syncthreads();
 }

@@ -563,6 +563,26 @@ extern "C" int rm_ipc_close_handle(void* dptr) {
   return 0;
 }
 
+// Stream-ordered wait until every rank finished step `epoch` of an rm_step_sync
+// sequence (*done >= world * epoch): what a consumer of the step's outputs other
+// than the next step kernel (host reads, other kernels) needs in the push layout,
+// whose outputs land in this rank's buffers from every rank.
+__global__ void step_sync_wait_kernel(const uint32_t* done, uint32_t target) {
+  xgpu_wait(done, target);
+}
+
+extern "C" int rm_step_sync_wait(const rm_step_sync* sync, void* stream) {
+  if (sync == nullptr || sync->done == nullptr || sync->world < 1) {
+    set_error("invalid step-sync arguments");
+    return RM_EINVAL;
+  }
+  if (sync->epoch == 0) return 0;  // no step issued yet
+  step_sync_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      sync->done, (uint32_t)sync->world * sync->epoch);
+  RM_CHECK_LAUNCH("step_sync_wait_kernel");
+  return 0;
+}
+
 extern "C" int rm_shard_plan_ints(int Lg) { return plan_ints(Lg); }
 
 extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, int row0, int Lg,

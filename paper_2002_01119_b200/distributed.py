@@ -184,8 +184,17 @@ class StepSync:
 
     def next(self) -> "_lib.StepSyncArgs":
         self.epoch += 1
+        return self._args()
+
+    def _args(self) -> "_lib.StepSyncArgs":
         return _lib.StepSyncArgs(self.flag.data_ptr(), self.handle.multicast_ptr,
                                  self.counter.data_ptr(), self.epoch, self.world)
+
+    def wait_all(self) -> None:
+        """Stream-ordered: later work on the current stream starts once every rank
+        finished the latest step (rm_step_sync_wait)."""
+        _lib.check(_lib.load().rm_step_sync_wait(ctypes.byref(self._args()),
+                                                 _lib.stream_ptr()), "rm_step_sync_wait")
 
 
 def _make_step_sync(group, device, enabled):
@@ -333,8 +342,16 @@ class LearnerShardedRingPos:
 
     @property
     def slots_local(self) -> torch.Tensor:
-        """This rank's slots (learner-major rows, ring-position order of the current step)."""
+        """This rank's slots (learner-major rows, ring-position order of the current step).
+        Every rank writes into them, so with in-kernel step ordering the current stream
+        first waits for every rank's last step (`settle`)."""
+        self.settle()
         return self.W[self.cur]
+
+    def settle(self):
+        """Order later work on the current stream after every rank's last step."""
+        if self.sync is not None:   # (without it every step ends in a collective barrier)
+            self.sync.wait_all()
 
     def barrier(self):
         """Step barrier on the stream (a no-op when the kernels order themselves)."""

@@ -23,6 +23,7 @@ def main():
     Gl.copy_(Gf[b:e])
     torch.cuda.synchronize(); dist.barrier()
     ok = True
+    pull_steps = []
     # 3 RAD steps sharded vs single-GPU reference computed locally on full data
     Wref = mixing.empty_learner_major(L, d, torch.float32, dev); Wref.copy_(full)
     for k in range(3):
@@ -30,7 +31,9 @@ def main():
         out = ring.step(lt, rt, Gl, 0.01)
         Wref = mixing.ring_mix_sgd(Wref, mixing.empty_learner_major(L, d, torch.float32, dev).copy_(Gf), 0.01, lt, rt)
         torch.cuda.synchronize()
-        ok &= bool(torch.equal(out, Wref[b:e]))
+        same = bool(torch.equal(out, Wref[b:e]))
+        pull_steps.append(same)
+        ok &= same
     # D1D
     d1d = D.LearnerShardedD1D(L, d, ring.Lg, dev, chunk_cols=1 << 18)
     out = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
@@ -91,6 +94,7 @@ def main():
     Wr = mixing.empty_learner_major(L, d, torch.float32, dev); Wr.copy_(full)
     Gfull = mixing.empty_learner_major(L, d, torch.float32, dev).copy_(Gf)
     ok_pos = True
+    pos_steps = []
     torch.cuda.synchronize(); dist.barrier()
     for k in range(3):
         Gs = mixing.empty_learner_major(pos.Lg, d, torch.float32, dev)
@@ -99,14 +103,23 @@ def main():
         lt, rt = tabs.step(k)
         Wr = mixing.ring_mix_sgd(Wr, Gfull, 0.01, lt.contiguous(), rt.contiguous())
         torch.cuda.synchronize()
-        ok_pos &= bool(torch.equal(pos.slots_local, Wr[tabs.inv[k + 1][g0:g1].long()]))
+        same = bool(torch.equal(pos.slots_local, Wr[tabs.inv[k + 1][g0:g1].long()]))
+        pos_steps.append(same)
+        ok_pos &= same
     pos.close()
+    detail = torch.tensor([int(x) for x in pull_steps + pos_steps], device=dev)
+    all_detail = [torch.zeros_like(detail) for _ in range(world)]
+    dist.all_gather(all_detail, detail)
+    ok_pull = ok
     ok = ok and ok_pos
-    res = torch.tensor([int(ok), int(ok_d1d)], device=dev)
+    res = torch.tensor([int(ok), int(ok_d1d), int(ok_pull), int(ok_pos)], device=dev)
     dist.all_reduce(res, op=dist.ReduceOp.MIN)
     if rank == 0:
         print(json.dumps({"world": world, "rad_bit_identical": bool(res[0]), "d1d_ok": bool(res[1]),
-                          "d1d_maxdiff_rank0": dd, "nvls": nvls}), flush=True)
+                          "d1d_maxdiff_rank0": dd, "nvls": nvls, "pull_ok": bool(res[2]),
+                          "pos_ok": bool(res[3]),
+                          "per_rank_pull_pos_steps": [t.tolist() for t in all_detail]}),
+              flush=True)
     dist.destroy_process_group()
 
 if __name__ == "__main__":
