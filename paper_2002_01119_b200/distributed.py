@@ -261,6 +261,13 @@ class LearnerShardedRing:
         if self.sync is None:
             dist.all_reduce(self._token, group=self.group)
 
+    def settle(self):
+        """Order later work on the current stream after every rank's last step — needed
+        only before overwriting this rank's current W rows from outside the step (peers
+        may still be reading them); the outputs themselves are local."""
+        if self.sync is not None:
+            self.sync.wait_all()
+
     def step(self, left: torch.Tensor, right: torch.Tensor, G: torch.Tensor | None, lr: float,
              absmax: torch.Tensor | None = None, barrier: bool = True) -> torch.Tensor:
         """One step: W[cur] -> W[1-cur].  left/right: device int32[L] global tables."""
