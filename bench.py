@@ -3,29 +3,37 @@
 
 Contract (task README / DESIGN.md §6):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-prints ONE JSON line on rank 0.
+prints ONE JSON line on rank 0.  `--gpus N` without torchrun launches N ranks itself
+(torch.distributed.run, 127.0.0.1) and checks that WORLD_SIZE == N.
 
-* A step = one pass of the hot path over one batch: the device permutation
-  tables for step k (generated a block of 64 future steps per launch) and the
-  fused gossip-mix + SGD kernel over all learners (W' = ring[p,p]-mix(W) - lr G),
-  with the fused divergence epilogue.  W rotates between two HBM buffers.
-* N = 1 workload: BASELINE.json configs[1] — RAD-PSGD, 64 learners x 25,557,032
-  fp32 params (ResNet-50-sized flat vectors), synthetic N(0,1) weights and
-  gradients, lr = 0.01.  3 x 6.54 GB buffers >> 126 MB L2, so no L2 flush.
-* N > 1 (torchrun, one process per GPU): `--layout coord` (default) gives every
-  rank a column stripe of all 64 learners (rows of W are independent, SURVEY
-  §8(e)) and every rank derives the same permutation from the shared seed
-  (PAPER.md:131): no data-path collective.  Default `--scaling weak`: every rank
-  owns a full C2-width stripe (64 x 25,557,032) of a 64 x (N * 25,557,032)
-  problem, so per-GPU work is fixed; `--scaling strong` splits the C2 problem.  `--layout learner` (north-star (d)) gives every rank 64/N
-  learners; the fused kernel pulls remote neighbour rows over NVLink (CUDA IPC)
-  and a 4-byte NCCL all-reduce orders consecutive steps.
+* A step = one pass of the hot path over one batch: the device permutation tables
+  for step k (a block of 64 future steps per launch) and the fused gossip-mix + SGD
+  kernel over all learners (W' = ring[p,p]-mix(W) - lr G) with the fused divergence
+  epilogue.  W rotates between two HBM buffers.
+* N = 1: BASELINE.json configs[1] — RAD-PSGD, 64 learners x 25,557,032 fp32 params
+  (ResNet-50-sized flat vectors), synthetic N(0,1) weights and gradients, lr = 0.01.
+  `extras.c3_single_gpu` times configs[2] (128 x 43,154,944) on the same GPU: the
+  strong-scaling reference point of the N > 1 runs.
+* N > 1 (one process per GPU): strong scaling of BASELINE.json configs[2] — RAD-PSGD,
+  128 learners x 43,154,944 fp32 (LSTM acoustic model), learners sharded over the
+  ranks (north-star (d)) in ring-POSITION order (`--layout position`, the default):
+  each step mixes positions locally (2 boundary rows pulled over NVLink) and stores
+  every output straight into its learner's next-step slot on whichever GPU owns it;
+  consecutive steps order themselves inside the kernels (no collective).
+  `extras.learner_pull` times the learner-ordered pull layout on the same problem
+  and `extras.coord_weak` the zero-communication coordinate stripes (every rank a
+  64 x 25,557,032 stripe, weak scaling).  D1D (`--strategy d1d`) shards learners
+  with the fused partial-sum / cross-GPU-reduce / apply kernel.
 * `value`: whole-job learner-params / s, device time (CUDA events), max over ranks.
-* `e2e`: the same step through the public host-buffer API
-  (mixing.ring_mix_sgd_host -> rm_ring_mix_sgd_host_f32): W, G in pinned host
-  memory, H2D + kernel + D2H pipelined, timed on the device per step.
-* `roofline`: the mix kernel's algorithmic bytes (12 B per learner-param:
-  read W, read G, write W') / its CUDA-event duration vs measured HBM GB/s.
+* `e2e`: the same step through the public API with the step's inputs and results
+  crossing PCIe every step: N = 1 host buffers in and out (W, G -> W',
+  mixing.ring_mix_sgd_host); sharded layouts W resident, every rank's G H2D and
+  max|W'| D2H.
+* `roofline`: the mix kernel's algorithmic HBM bytes (12 B per learner-param) / its
+  CUDA-event duration vs the measured HBM GB/s.
+* `nvlink` (N > 1): NVML NVLink byte counters of every GPU over the timed region
+  (busiest rank), against 900 GB/s per direction and the measured peer peaks; the
+  traffic model is reported beside it.
 * `cpu_baseline`: the oracle port of the reference's arithmetic
   (numpy W @ T - lr G, fp64, (d, L) C-order) on a bounded sample, host cores.
 * `--impl reference`: that same CPU path as the timed arm (the reference is a
@@ -37,6 +45,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -57,26 +66,30 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "learner-params mixed/sec"
 UNIT = "learner-params/s"
-L_DEFAULT = 64
-D_DEFAULT = 25_557_032
+C2 = (64, 25_557_032)          # BASELINE.json configs[1] (and configs[3], D1D)
+C3 = (128, 43_154_944)         # BASELINE.json configs[2]
 LR = 0.01
 SEED = 12345
 BYTES_PER_PARAM = {"float32": 12, "bfloat16": 6, "float64": 24}
+NVLINK_NOMINAL_GBS = 900.0     # NVLink 5, per direction per GPU
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--learners", type=int, default=L_DEFAULT)
-    ap.add_argument("--dim", type=int, default=D_DEFAULT)
+    ap.add_argument("--learners", type=int, default=None,
+                    help="default: the BASELINE config of the run (64, or 128 at N > 1)")
+    ap.add_argument("--dim", type=int, default=None)
     ap.add_argument("--dtype", choices=["float32", "bfloat16", "float64"], default="float32")
     ap.add_argument("--strategy", choices=["rand_psgd", "adpsgd_fixed", "d1d"],
                     default="rand_psgd")
-    ap.add_argument("--layout", choices=["coord", "learner", "position"], default="coord")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+    ap.add_argument("--layout", choices=["auto", "coord", "learner", "position"],
+                    default="auto", help="N > 1: auto = position (RAD) / learner (fixed "
+                                         "ring, D1D)")
+    ap.add_argument("--scaling", choices=["auto", "weak", "strong"], default="auto",
                     help="coord layout at N > 1: weak = every rank owns a full-width "
                          "(L x dim) column stripe of an L x (N*dim) problem; strong = the "
                          "L x dim problem split N ways")
@@ -87,14 +100,18 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--rewarm-seconds", type=float, default=0.4,
+                    help="untimed steps right before the timed region (after the clock "
+                         "sampler started) so the GPU is at its load clocks")
     ap.add_argument("--event-every", type=int, default=4,
                     help="bracket every N-th mix launch with CUDA events (roofline timing)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ----------------------------------------------------------------------------
-# environment helpers
+# configuration
 # ----------------------------------------------------------------------------
 
 def dist_env():
@@ -102,6 +119,56 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def resolve(args, ws):
+    """Concrete layout / scaling / (L, d) / BASELINE config index of this run."""
+    r = argparse.Namespace(**vars(args))
+    if ws == 1:
+        r.layout = "coord"            # the whole problem on one GPU
+    elif args.layout == "auto":
+        r.layout = "position" if args.strategy == "rand_psgd" else "learner"
+    if args.scaling == "auto":
+        r.scaling = "weak" if (ws > 1 and r.layout == "coord") else "strong"
+    sharded = ws > 1 and r.layout in ("learner", "position")
+    big = sharded and args.strategy == "rand_psgd"
+    L, d = C3 if big else C2
+    r.learners = args.learners if args.learners is not None else L
+    r.dim = args.dim if args.dim is not None else d
+    r.config_index = 2 if big else (3 if args.strategy == "d1d" else 1)
+    return r
+
+
+def weak(args, ws):
+    """Weak scaling: coordinate stripes of fixed width per rank (no data-path collective)."""
+    return args.layout == "coord" and args.scaling == "weak"
+
+
+def total_dim(args, ws):
+    return args.dim * ws if weak(args, ws) else args.dim
+
+
+def config_name(L, d):
+    return {C2: "ResNet-50-sized", C3: "LSTM-acoustic-model-sized"}.get((L, d), "custom")
+
+
+def config_dict(args, ws):
+    idx = getattr(args, "config_index", 1)
+    return {"workload": f"{args.strategy} mix+SGD step, {args.learners} learners x "
+                        f"{args.dim} params/learner ({config_name(args.learners, args.dim)}), "
+                        f"BASELINE.json configs[{idx}]",
+            "learners": args.learners, "params_per_learner": args.dim,
+            "strategy": args.strategy, "lr": LR, "perm_seed": SEED,
+            "layout": args.layout if ws > 1 else "single-gpu",
+            "parallelism": ((f"coord-sharded over {ws} GPUs (weak scaling: every rank owns a "
+                             f"{args.learners} x {args.dim} column stripe of the "
+                             f"{args.learners} x {args.dim * ws} problem; shared-seed "
+                             f"permutations, no data-path collective)") if weak(args, ws) else
+                            (f"{args.layout}-sharded over {ws} GPUs (strong scaling: the whole "
+                             f"{args.learners} x {args.dim} problem)")) if ws > 1 else "1 GPU",
+            "l2": "inputs (3 x L x d x 4 B) far larger than the 126 MB L2; no flush needed",
+            **({"d1d_collective": args.d1d_collective, "d1d_chunk_cols": args.d1d_chunk_cols}
+               if ws > 1 and args.strategy == "d1d" and args.layout == "learner" else {})}
 
 
 def measured_peaks():
@@ -214,13 +281,13 @@ def cpu_reference_step_fn(L: int, d_sample: int, uniform: bool):
     return step
 
 
-def all_host_threads():
+def host_threads():
     """Thread count of the CPU legs (OpenBLAS set to every core at import, rank 0)."""
-    return None, int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    return int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
 
 
 def cpu_baseline(L: int, uniform: bool, seconds: float):
-    _limits, cores = all_host_threads()
+    cores = host_threads()
     d_sample = 1 << 20
     step = cpu_reference_step_fn(L, d_sample, uniform)
     step()  # warm
@@ -243,10 +310,12 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    L = args.learners
+    n = max(ws, args.gpus)
+    cfg = resolve(args, n)
+    L = cfg.learners
     uniform = args.strategy == "d1d"
     d_sample = 1 << 20
-    _limits, cores = all_host_threads()
+    cores = host_threads()
     step = cpu_reference_step_fn(L, d_sample, uniform)
     for _ in range(args.warmup):
         step()
@@ -260,12 +329,12 @@ def run_reference(args):
     sample = (f"numpy fp64 apply_mixing(W,T) - lr*G (oracle port of simulation.py:267), "
               f"(d=1,048,576 x L={L}) C-order sample per step, all {cores} host threads")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak" if weak(args, ws) else "strong",
+        "higher_is_better": True, "scaling": "weak" if weak(cfg, n) else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic N(0,1) weights and gradients",
-        "config": config_dict(args, ws),
+        "config": config_dict(cfg, n),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -273,13 +342,27 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------
+# NVLink: measured peaks, counters, traffic model
+# ----------------------------------------------------------------------------
+
 def p2p_peaks():
     p = ROOT / "profiles" / "p2p_peaks.json"
     try:
         z = json.loads(p.read_text())
         return float(z["peer_read_gbs"]), float(z["peer_write_gbs"]), z["source"]
     except Exception:
-        return 900.0, 900.0, "NVLink 5 nominal per direction (no measured file)"
+        return NVLINK_NOMINAL_GBS, NVLINK_NOMINAL_GBS, "NVLink 5 nominal per direction"
+
+
+def nvlink_counters(local):
+    try:
+        sys.path.insert(0, str(ROOT / "tools"))
+        from nvlink_counters import NvlinkCounters
+        c = NvlinkCounters(local)
+        return c if c.ok else None
+    except Exception:
+        return None
 
 
 def nvlink_traffic(layout, L, d, esz, ws, perm, inv, left, right):
@@ -314,112 +397,83 @@ def host_pinned_budget() -> int:
         return 32 << 30
 
 
-def weak(args, ws):
-    """Weak scaling: coordinate stripes of fixed width per rank (no data-path collective);
-    at N = 1 it is the same single-GPU problem, labelled like the N > 1 runs."""
-    return args.layout == "coord" and args.scaling == "weak"
-
-
-def total_dim(args, ws):
-    return args.dim * ws if weak(args, ws) else args.dim
-
-
-def config_dict(args, ws):
-    return {"workload": f"{args.strategy} mix+SGD step, {args.learners} learners x "
-                        f"{args.dim} params/learner ({'ResNet-50-sized' if args.dim == D_DEFAULT else 'custom'}"
-                        f"), BASELINE.json configs[1]",
-            "learners": args.learners, "params_per_learner": args.dim,
-            "strategy": args.strategy, "lr": LR, "perm_seed": SEED,
-            "layout": args.layout if ws > 1 else "single-gpu",
-            "parallelism": ((f"coord-sharded over {ws} GPUs (weak scaling: every rank owns a "
-                             f"{args.learners} x {args.dim} column stripe of the "
-                             f"{args.learners} x {args.dim * ws} problem; shared-seed "
-                             f"permutations, no data-path collective)") if weak(args, ws) else
-                            (f"{args.layout}-sharded over {ws} GPUs (strong scaling: the whole "
-                             f"{args.learners} x {args.dim} problem)")) if ws > 1 else "1 GPU",
-            "l2": "inputs (3 x L x d x 4 B) far larger than the 126 MB L2; no flush needed",
-            **({"d1d_collective": args.d1d_collective, "d1d_chunk_cols": args.d1d_chunk_cols}
-               if ws > 1 and args.strategy == "d1d" and args.layout == "learner" else {})}
-
-
 # ----------------------------------------------------------------------------
 # GPU arm
 # ----------------------------------------------------------------------------
 
 class Workload:
-    """One benchmark step for a layout: permutation tables (a block of 64 future
-    steps per launch) + the fused mix launch(es) for this rank's share."""
+    """One benchmark step for a layout: permutation tables (a block of 64 future steps
+    per launch) + the fused mix launch(es) for this rank's share.  `spec`: layout,
+    learners, dim, scaling, strategy, dtype, d1d options."""
 
-    def __init__(self, args, torch, dev, ws, rank):
+    def __init__(self, spec, torch, dev, ws, rank, nsteps):
         from paper_2002_01119_b200 import _lib, distributed as D, mixing, seeding, simulation
 
         self.torch, self._lib, self.mixing = torch, _lib, mixing
-        self.args, self.dev, self.ws, self.rank = args, dev, ws, rank
+        self.spec, self.dev, self.ws, self.rank = spec, dev, ws, rank
         dtype = {"float32": torch.float32, "bfloat16": torch.bfloat16,
-                 "float64": torch.float64}[args.dtype]
-        L, d = args.learners, args.dim
+                 "float64": torch.float64}[spec.dtype]
+        L, d = spec.learners, spec.dim
         self.L, self.d = L, d
-        self.layout = "single" if ws == 1 else args.layout
-        self.uniform = args.strategy == "d1d"
+        self.layout = "single" if ws == 1 else spec.layout
+        self.uniform = spec.strategy == "d1d"
         gen = torch.Generator(device=dev).manual_seed(1000 + rank)
 
-        def synth(rows, cols):
-            X = mixing.empty_learner_major(rows, cols, dtype, dev)
-            for r in range(rows):
-                X[r].copy_(torch.randn(cols, generator=gen, device=dev,
+        def fill(X):
+            for r in range(X.shape[0]):
+                X[r].copy_(torch.randn(X.shape[1], generator=gen, device=dev,
                                        dtype=torch.float32).to(dtype))
             return X
 
+        def synth(rows, cols):
+            return fill(mixing.empty_learner_major(rows, cols, dtype, dev))
+
+        self.sharded = None
         if self.layout in ("single", "coord"):
             if self.layout == "coord":
-                cols = d if args.scaling == "weak" else D.CoordinateShards(d, ws, rank).width
+                cols = d if spec.scaling == "weak" else D.CoordinateShards(d, ws, rank).width
             else:
                 cols = d
             self.rows, self.cols = L, cols
             self.W = [synth(L, cols), mixing.empty_learner_major(L, cols, dtype, dev)]
             self.G = synth(L, cols)
-        else:
-            if self.uniform:
-                lay = D.ShardLayout(L, ws)
-                b, e = lay.rows(rank)
-                self.rows, self.cols = e - b, d
-                self.W = [synth(e - b, d), mixing.empty_learner_major(e - b, d, dtype, dev)]
-                self.d1d = None
-                if args.d1d_collective in ("auto", "fused"):
-                    try:
-                        self.d1d = D.LearnerShardedD1DFused(L, d, e - b, dev)
-                        self.d1d_kind = "fused"
-                    except Exception:
-                        if args.d1d_collective == "fused":
-                            raise
-                if self.d1d is None and args.d1d_collective in ("auto", "nvls"):
-                    try:
-                        self.d1d = D.LearnerShardedD1DNVLS(
-                            L, d, e - b, dev, chunk_cols=args.d1d_chunk_cols or None)
-                        self.d1d_kind = "nvls"
-                    except Exception:
-                        if args.d1d_collective == "nvls":
-                            raise
-                if self.d1d is None:
-                    self.d1d = D.LearnerShardedD1D(L, d, e - b, dev)
-                    self.d1d_kind = "nccl"
-            elif self.layout == "position":
-                self.pos = D.LearnerShardedRingPos(L, d, dtype)
-                self.rows, self.cols = self.pos.Lg, d
-                for r in range(self.pos.Lg):
-                    self.pos.W[0][r].copy_(torch.randn(d, generator=gen, device=dev,
-                                                       dtype=torch.float32).to(dtype))
-                ident = torch.arange(L, dtype=torch.int32, device=dev)
-                self.ident = ident
-            else:
-                self.ring = D.LearnerShardedRing(L, d, dtype)
-                self.rows, self.cols = self.ring.Lg, d
-                for r in range(self.ring.Lg):
-                    self.ring.W[0][r].copy_(torch.randn(d, generator=gen, device=dev,
-                                                        dtype=torch.float32).to(dtype))
+        elif self.uniform:
+            lay = D.ShardLayout(L, ws)
+            b, e = lay.rows(rank)
+            self.rows, self.cols = e - b, d
+            self.W = [synth(e - b, d), mixing.empty_learner_major(e - b, d, dtype, dev)]
+            self.d1d = None
+            if spec.d1d_collective in ("auto", "fused"):
+                try:
+                    self.d1d = D.LearnerShardedD1DFused(L, d, e - b, dev)
+                    self.d1d_kind = "fused" + ("" if self.d1d.multicast else "-p2p")
+                except Exception:
+                    if spec.d1d_collective == "fused":
+                        raise
+            if self.d1d is None and spec.d1d_collective in ("auto", "nvls"):
+                try:
+                    self.d1d = D.LearnerShardedD1DNVLS(
+                        L, d, e - b, dev, chunk_cols=spec.d1d_chunk_cols or None)
+                    self.d1d_kind = "nvls"
+                except Exception:
+                    if spec.d1d_collective == "nvls":
+                        raise
+            if self.d1d is None:
+                self.d1d = D.LearnerShardedD1D(L, d, e - b, dev)
+                self.d1d_kind = "nccl"
             self.G = synth(self.rows, d)
+        else:
+            cls = D.LearnerShardedRingPos if self.layout == "position" else D.LearnerShardedRing
+            self.sharded = cls(L, d, dtype)
+            self.rows, self.cols = self.sharded.Lg, d
+            fill(self.sharded.W[0])
+            # the initial rows were written outside the step kernels: every rank's
+            # first step must wait for every rank's writes
+            self.sharded.publish()
+            self.G = synth(self.rows, d)
+            self.ident = torch.arange(L, dtype=torch.int32, device=dev)
         self.local_params = self.rows * self.cols
-        self.amax = torch.zeros(args.warmup + args.steps + 1, dtype=torch.int64, device=dev)
+        self.amax = torch.zeros(nsteps + 1, dtype=torch.int64, device=dev)
         self.lib = _lib.load()
         sfx = mixing._suffix(self.G)
         self.ring_fn = getattr(self.lib, f"rm_ring_mix_sgd_{sfx}")
@@ -429,7 +483,7 @@ class Workload:
         # block + 1 rows: the position layout also needs step k+1's permutation
         self.tabs = [torch.empty((self.block + 1, L), dtype=torch.int32, device=dev)
                      for _ in range(4)]
-        if args.strategy == "adpsgd_fixed":
+        if spec.strategy == "adpsgd_fixed":
             self.fixed = tuple(t.contiguous() for t in simulation.fixed_ring_tables(L, dev))
         self.tab0 = None
         self.launches = {"perm": 0, "mix": 0, "barrier_allreduce": 0}
@@ -438,69 +492,214 @@ class Workload:
     def reset_tables(self):
         self.tab0 = None
 
-    def step(self, k, ev_pair=None):
+    def step(self, k, ev_pair=None, G=None):
         torch, _lib = self.torch, self._lib
         stream = torch.cuda.current_stream()
         sptr = stream.cuda_stream
         L = self.L
-        if self.args.strategy == "rand_psgd" and (self.tab0 is None or
-                                                  k >= self.tab0 + self.block):
+        G = self.G if G is None else G
+        strat = self.spec.strategy
+        if strat == "rand_psgd" and (self.tab0 is None or k >= self.tab0 + self.block):
             _lib.check(self.lib.rm_perm_tables(self.words.ctypes.data, len(self.words), k,
                                                self.block + 1, L,
                                                *(t.data_ptr() for t in self.tabs), sptr))
             self.tab0 = k
             self.launches["perm"] += 1
-        if self.args.strategy == "rand_psgd":
+        if strat == "rand_psgd":
             lt, rt = self.tabs[2][k - self.tab0], self.tabs[3][k - self.tab0]
-        elif self.args.strategy == "adpsgd_fixed":
+        elif strat == "adpsgd_fixed":
             lt, rt = self.fixed
         if ev_pair is not None:
             ev_pair[0].record(stream)
         am = self.amax[k].data_ptr()
         if self.layout == "position":
-            if self.args.strategy == "rand_psgd":
+            if strat == "rand_psgd":
                 ik, pn = self.tabs[1][k - self.tab0], self.tabs[0][k + 1 - self.tab0]
             else:
                 ik = pn = self.ident
-            self.pos.step(ik, pn, self.G, LR, self.amax[k], barrier=False)
+            self.sharded.step(ik, pn, G, LR, self.amax[k], barrier=False)
         elif self.layout == "learner":
             if self.uniform:
                 src, dst = self.W[self.cur], self.W[1 - self.cur]
-                self.d1d.step(src, self.G, LR, dst, self.amax[k])
+                self.d1d.step(src, G, LR, dst, self.amax[k])
                 self.cur = 1 - self.cur
             else:
-                self.ring.step(lt, rt, self.G, LR, self.amax[k], barrier=False)
+                self.sharded.step(lt, rt, G, LR, self.amax[k], barrier=False)
         else:
             src, dst = self.W[self.cur], self.W[1 - self.cur]
             if self.uniform:
-                rc = self.mean_fn(src.data_ptr(), self.G.data_ptr(), dst.data_ptr(), L,
-                                  self.cols, src.stride(0), self.G.stride(0), dst.stride(0), LR,
+                rc = self.mean_fn(src.data_ptr(), G.data_ptr(), dst.data_ptr(), L,
+                                  self.cols, src.stride(0), G.stride(0), dst.stride(0), LR,
                                   am, sptr)
             else:
-                rc = self.ring_fn(src.data_ptr(), self.G.data_ptr(), dst.data_ptr(),
+                rc = self.ring_fn(src.data_ptr(), G.data_ptr(), dst.data_ptr(),
                                   lt.data_ptr(), rt.data_ptr(), L, self.cols, src.stride(0),
-                                  self.G.stride(0), dst.stride(0), LR, am, sptr)
+                                  G.stride(0), dst.stride(0), LR, am, sptr)
             _lib.check(rc, "mix")
             self.cur = 1 - self.cur
         if ev_pair is not None:
             ev_pair[1].record(stream)
         if self.layout == "learner" and self.uniform:
-            self.launches["mix"] += (1 if self.d1d_kind == "fused" else
+            self.launches["mix"] += (1 if self.d1d_kind.startswith("fused") else
                                      (3 if self.d1d_kind == "nvls" else 2) * len(self.d1d.chunks))
         else:   # learner / position layouts launch a planner + the mix kernel
-            self.launches["mix"] += 2 if self.layout in ("learner", "position") else 1
-        if self.layout in ("learner", "position") and not self.uniform:
-            # next step reads this step's rows on peers
-            obj = self.ring if self.layout == "learner" else self.pos
-            obj.barrier()
-            if obj.sync is None:
+            self.launches["mix"] += 2 if self.sharded is not None else 1
+        if self.sharded is not None:
+            # next step reads this step's rows on peers (a no-op with in-kernel ordering)
+            self.sharded.barrier()
+            if self.sharded.sync is None:
                 self.launches["barrier_allreduce"] += 1
 
     def close(self):
-        if self.layout == "learner" and not self.uniform:
-            self.ring.close()
-        if self.layout == "position":
-            self.pos.close()
+        if self.sharded is not None:
+            self.sharded.close()
+
+
+def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None):
+    """Warm-up, re-warm at load clocks, K timed steps.  Returns the measurement dict
+    (rank 0 gets the max-over-ranks numbers) and the workload (still open)."""
+    K, Wm = args.steps, args.warmup
+    nsteps = Wm + K + 4096          # amax slots: warm-up, re-warm (< 4000), timed, e2e
+    wl = Workload(spec, torch, dev, ws, rank, nsteps + args.e2e_steps + 64)
+    stream = torch.cuda.current_stream()
+    k = 0
+    for _ in range(Wm):
+        wl.step(k)
+        k += 1
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    # the sleep (nvidia-smi start-up) lets the clocks drop: bring them back to load
+    # levels with untimed steps right before the timed region (bounded by the amax slots)
+    t_end = time.perf_counter() + args.rewarm_seconds
+    rewarm = 0
+    while (time.perf_counter() < t_end or rewarm == 0) and rewarm < 3000:
+        wl.step(k)
+        k += 1
+        rewarm += 1
+        if rewarm % 8 == 0:
+            torch.cuda.synchronize()
+    if ws > 1:      # the same number of re-warm steps on every rank (ordered step epochs)
+        t = torch.tensor([rewarm], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        while rewarm < int(t.item()):
+            wl.step(k)
+            k += 1
+            rewarm += 1
+    sampled = [i for i in range(K) if i % args.event_every == 0]
+    kev = {i: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for i in sampled}
+    t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wl.launches = {key: 0 for key in wl.launches}
+    wl.reset_tables()   # the timed region generates its own tables
+    c0 = nvc.read() if nvc else None
+    if clocks:
+        clocks.mark(True)
+    k_first = k
+    t_start.record(stream)
+    for i in range(K):
+        wl.step(k, kev.get(i))
+        k += 1
+    t_stop.record(stream)
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.mark(False)
+    c1 = nvc.read() if nvc else None
+    elapsed_ms = t_start.elapsed_time(t_stop)
+    kern_ms = [a.elapsed_time(b) for a, b in kev.values()]
+    bits = wl.amax[:k].cpu().numpy().view(np.float64)
+    if not np.all(np.isfinite(bits)):
+        raise RuntimeError("non-finite weights in the benchmark run")
+    tx = rx = -1.0
+    if c0 is not None and c1 is not None:
+        tx, rx = float(c1[0] - c0[0]), float(c1[1] - c0[1])
+    if ws > 1:
+        t = torch.tensor([elapsed_ms, tx, rx], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, tx, rx = float(t[0]), float(t[1]), float(t[2])
+        lo = torch.tensor([min(tx, rx)], device=dev, dtype=torch.float64)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)     # any rank without counters -> none
+        if float(lo.item()) < 0:
+            tx = rx = -1.0
+    L = spec.learners
+    params_per_step = L * total_dim(spec, ws)
+    kern_avg_s = statistics.mean(kern_ms) / 1e3
+    bpp = BYTES_PER_PARAM[spec.dtype]
+    algo_bytes = bpp * wl.local_params
+    peak, peak_src = measured_peaks()
+    res = {
+        "value": params_per_step * K / (elapsed_ms / 1e3),
+        "ms_per_step": elapsed_ms / K,
+        "kern_avg_s": kern_avg_s,
+        "algo_bytes": algo_bytes,
+        "achieved": algo_bytes / kern_avg_s / 1e9,
+        "peak": peak, "peak_src": peak_src,
+        "launches": dict(wl.launches),
+        "rewarm_steps": rewarm,
+        "k_first": k_first,
+        "nvlink_counted": (tx, rx) if tx >= 0 else None,
+    }
+    return res, wl
+
+
+def nvlink_object(spec, res, wl, ws, dev, mixing):
+    """Measured NVLink bytes (NVML counters, busiest rank) per step over the step time,
+    with the traffic model and the peaks beside them.  Rank 0."""
+    K = spec.steps
+    L, d = spec.learners, spec.dim
+    esz = BYTES_PER_PARAM[spec.dtype] // 3
+    step_s = res["ms_per_step"] / 1e3
+    prd, pwr, psrc = p2p_peaks()
+    out = {"bound": "nvlink", "unit": "GB/s", "peak_nominal": NVLINK_NOMINAL_GBS,
+           "peak_measured_read": prd, "peak_measured_write": pwr, "peak_measured_source": psrc}
+    if res["nvlink_counted"] is not None:
+        tx, rx = res["nvlink_counted"]
+        tx_s, rx_s = tx / K, rx / K
+        a_tx, a_rx = tx_s / step_s / 1e9, rx_s / step_s / 1e9
+        out.update({"source": "NVML NVLink byte counters over the timed region (max over "
+                              "ranks; link-level bytes incl. protocol overhead)",
+                    "tx_bytes_per_step": tx_s, "rx_bytes_per_step": rx_s,
+                    "achieved_tx": a_tx, "achieved_rx": a_rx,
+                    "frac_nominal": max(a_tx, a_rx) / NVLINK_NOMINAL_GBS,
+                    "frac_measured_peak": max(a_tx / pwr, a_rx / prd)})
+    else:
+        out["source"] = "NVML NVLink counters unavailable on this system: traffic model only"
+    if not wl.uniform and spec.layout in ("learner", "position"):
+        k0 = res["k_first"]
+        if spec.strategy == "adpsgd_fixed":
+            ident = np.tile(np.arange(L, dtype=np.int64), (K + 1, 1))
+            host = [ident, ident, np.roll(ident, 1, axis=1), np.roll(ident, -1, axis=1)]
+        else:
+            tb = mixing.permutation_tables(L, SEED, k0, K + 1, dev)
+            host = [t.cpu().numpy().astype(np.int64) for t in (tb.perm, tb.inv, tb.left, tb.right)]
+        per_rank = nvlink_traffic(spec.layout, L, d, esz, ws, host[0], host[1], host[2][:-1],
+                                  host[3][:-1])
+        rd = max(r for r, _ in per_rank)
+        wr = max(w for _, w in per_rank)
+        out["model"] = {"read_bytes_per_step": rd, "write_bytes_per_step": wr,
+                        "achieved_read": rd / step_s / 1e9, "achieved_write": wr / step_s / 1e9,
+                        "note": "busiest rank's payload bytes per step (pull: distinct remote "
+                                "neighbour rows; position: 2 boundary rows read + relabel "
+                                "stores) over the step time"}
+        if "frac_nominal" not in out:
+            out["frac_nominal"] = max(rd, wr) / step_s / 1e9 / NVLINK_NOMINAL_GBS
+    return out
+
+
+def extra_line(spec, res, ws, dev, wl, mixing):
+    e = {"workload": config_dict(spec, ws)["workload"], "layout": spec.layout,
+         "scaling": "weak" if weak(spec, ws) else "strong",
+         "value": res["value"], "unit": UNIT, "ms_per_step": res["ms_per_step"],
+         "kernel_avg_ms": res["kern_avg_s"] * 1e3,
+         "hbm_frac": res["achieved"] / res["peak"]}
+    if ws > 1 and spec.layout in ("learner", "position"):
+        e["nvlink"] = nvlink_object(spec, res, wl, ws, dev, mixing)
+    return e
 
 
 def run_ours(args):
@@ -510,162 +709,150 @@ def run_ours(args):
     from paper_2002_01119_b200 import mixing
 
     ws, rank, local = dist_env()
+    if args.gpus != ws:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws} "
+                         f"(run without torchrun to let bench.py launch the ranks)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
-    L, d = args.learners, args.dim
-    uniform = args.strategy == "d1d"
-    wl = Workload(args, torch, dev, ws, rank)
-    stream = torch.cuda.current_stream()
-
-    k = 0
-    for _ in range(args.warmup):
-        wl.step(k)
-        k += 1
-    torch.cuda.synchronize()
-
+    spec = resolve(args, ws)
+    L = spec.learners
+    uniform = spec.strategy == "d1d"
     clocks = ClockSampler(local) if rank == 0 else None
-    if clocks:
-        clocks.start()
-        time.sleep(0.3)
-    # per-launch events bracket every `event_every`-th mix launch (1 = all of them)
-    sampled = [i for i in range(args.steps) if i % args.event_every == 0]
-    kev = {i: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for i in sampled}
-    t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    wl.launches = {key: 0 for key in wl.launches}
-    wl.reset_tables()   # the timed region generates its own tables
-    if clocks:
-        clocks.mark(True)
-    t_start.record(stream)
-    for i in range(args.steps):
-        wl.step(k, kev.get(i))
-        k += 1
-    t_stop.record(stream)
-    torch.cuda.synchronize()
-    if clocks:
-        clocks.mark(False)
-    elapsed_ms = t_start.elapsed_time(t_stop)
-    kern_ms = [a.elapsed_time(b) for a, b in kev.values()]
-    launches = dict(wl.launches)
-    bits = wl.amax[:k].cpu().numpy().view(np.float64)
-    if not np.all(np.isfinite(bits)):
-        raise RuntimeError("non-finite weights in the benchmark run")
-    if ws > 1:
-        t = torch.tensor([elapsed_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
-    clock_info = clocks.stop() if clocks else None
+    nvc = nvlink_counters(local) if ws > 1 else None
 
-    params_per_step = L * total_dim(args, ws)     # all ranks' learner-params per step
-    value = params_per_step * args.steps / (elapsed_ms / 1e3)
-    kern_avg_s = statistics.mean(kern_ms) / 1e3
-    bpp = BYTES_PER_PARAM[args.dtype]
-    algo_bytes = bpp * wl.local_params           # this rank's HBM bytes per launch
-    peak, peak_src = measured_peaks()
-    achieved = algo_bytes / kern_avg_s / 1e9
-    key = f"mix_{args.strategy}_{args.dtype}_L{L}_d{d}" if ws == 1 else None
-    step_sync = None
-    if ws > 1 and wl.layout in ("learner", "position") and not uniform:
-        step_sync = (wl.ring if wl.layout == "learner" else wl.pos).sync is not None
-    nvlink = None
-    if ws > 1 and wl.layout in ("learner", "position") and not uniform and rank == 0:
-        k0 = args.warmup
-        if args.strategy == "adpsgd_fixed":      # the fixed ring: identity permutation
-            ident = np.tile(np.arange(L, dtype=np.int64), (args.steps + 1, 1))
-            host = [ident, ident, np.roll(ident, 1, axis=1), np.roll(ident, -1, axis=1)]
-        else:
-            tb = mixing.permutation_tables(L, SEED, k0, args.steps + 1, dev)
-            host = [t.cpu().numpy().astype(np.int64) for t in (tb.perm, tb.inv, tb.left, tb.right)]
-        per_rank = nvlink_traffic(wl.layout, L, d, bpp // 3, ws, host[0], host[1],
-                                  host[2][:-1], host[3][:-1])
-        prd, pwr, psrc = p2p_peaks()
-        rd = max(r for r, _ in per_rank)
-        wr = max(w for _, w in per_rank)
-        ach_rd, ach_wr = rd / kern_avg_s / 1e9, wr / kern_avg_s / 1e9
-        nvlink = {"bound": "nvlink", "unit": "GB/s",
-                  "read_bytes_per_step": rd, "write_bytes_per_step": wr,
-                  "achieved_read": ach_rd, "achieved_write": ach_wr,
-                  "peak_read": prd, "peak_write": pwr,
-                  "frac": max(ach_rd / prd, ach_wr / pwr),
-                  "note": "busiest rank's peer bytes per step (pull: distinct remote "
-                          "neighbour rows; position: 2 boundary rows read + relabel stores) "
-                          "over rank 0's mean kernel time", "peak_source": psrc}
+    res, wl = measure(spec, torch, dist, dev, ws, rank, local, args, clocks=clocks, nvc=nvc)
+    clock_info = clocks.stop() if clocks else None
+    key = f"mix_{spec.strategy}_{spec.dtype}_L{L}_d{spec.dim}" if ws == 1 else None
     traffic = ncu_traffic(key) if key else None
+    step_sync = None
+    if wl.sharded is not None:
+        step_sync = wl.sharded.sync is not None
+    nvlink = None
+    if ws > 1 and spec.layout in ("learner", "position") and rank == 0:
+        nvlink = nvlink_object(spec, res, wl, ws, dev, mixing)
 
     e2e = None
-    want_e2e = not args.no_e2e and args.dtype == "float32"
-    if want_e2e and (ws == 1 or wl.layout == "coord"):
+    want_e2e = not args.no_e2e and spec.dtype == "float32"
+    if want_e2e and wl.sharded is None and (ws == 1 or spec.layout == "coord"):
         # every rank drives its own column stripe (own PCIe link), max over ranks.
         # e2e = the reference-facing call on HOST buffers (the reference's step takes and
         # returns host arrays): W, G pinned on the host, W' back, every step, through
-        # mixing.ring_mix_sgd_host -> rm_ring_mix_sgd_host_f32.  Pinned memory is 3 x the
-        # stripe, so each rank samples at most `cap` columns (the full C2 stripe at N = 1).
-        # The resident-W variant (only G crosses PCIe) is reported beside it.
-        ms_res = run_e2e_resident(args, torch, wl, dev)
+        # mixing.ring_mix_sgd_host -> rm_ring_mix_sgd_host_f32.  The resident-W variant
+        # (only G crosses PCIe) is reported beside it.
+        ms_res = run_e2e_resident(args, spec, torch, wl, dev)
         ms_host, e2e_cols = None, 0
         if not uniform:
             budget = min(24 << 30, host_pinned_budget() // ws)
             e2e_cols = min(wl.cols, max(32, (budget // (3 * L * 4)) // 32 * 32))
-            ms_host = run_e2e(args, torch, mixing, dev, cols=e2e_cols)
+            ms_host = run_e2e(args, spec, torch, dev, cols=e2e_cols)
         if ws > 1:
             t = torch.tensor([ms_res, ms_host or 0.0], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_res, ms_host = float(t[0]), (float(t[1]) if ms_host else None)
-        resident = e2e_resident_line(args, ms_res, ws)
+        resident = e2e_resident_line(args, spec, ms_res, ws, wl)
         if ms_host:
-            e2e = e2e_line(args, ms_host, ws, e2e_cols)
+            e2e = e2e_line(args, spec, ms_host, ws, e2e_cols)
             e2e["resident_variant"] = resident
         else:
             e2e = resident
-    elif want_e2e and rank == 0 and not uniform:
-        e2e = e2e_line(args, run_e2e(args, torch, mixing, dev), 1)
-        e2e["note"] = "learner layout: host-buffer API measured on rank 0 for the whole problem"
+    elif want_e2e:
+        # sharded layouts: W resident (sharded), every rank's G H2D + max|W'| D2H per step
+        ms_res = run_e2e_sharded(args, torch, wl, dev, res["k_first"] + args.steps + 8)
+        if ws > 1:
+            t = torch.tensor([ms_res], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_res = float(t.item())
+        e2e = e2e_resident_line(args, spec, ms_res, ws, wl)
     if ws > 1:
+        torch.cuda.synchronize()
         dist.barrier()
+    launches = res["launches"]
     wl.close()
+    del wl
+    torch.cuda.empty_cache()
+
+    extras = {}
+    if not args.no_extras and spec.strategy == "rand_psgd" and args.dtype == "float32" \
+            and args.learners is None and args.dim is None:
+        todo = []
+        if ws == 1:
+            todo.append(("c3_single_gpu", dict(layout="coord", learners=C3[0], dim=C3[1],
+                                               scaling="strong", config_index=2)))
+        else:
+            if spec.layout != "learner":
+                todo.append(("learner_pull", dict(layout="learner", learners=C3[0], dim=C3[1],
+                                                  scaling="strong", config_index=2)))
+            todo.append(("coord_weak", dict(layout="coord", learners=C2[0], dim=C2[1],
+                                            scaling="weak", config_index=1)))
+        for name, over in todo:
+            sp = argparse.Namespace(**{**vars(spec), **over})
+            free, _ = torch.cuda.mem_get_info(dev)
+            need = 3.3 * sp.learners * (sp.dim if sp.layout == "coord" else sp.dim / ws) * 4
+            ok = torch.tensor([1.0 if free > need else 0.0], device=dev)
+            if ws > 1:
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if float(ok.item()) < 1:
+                extras[name] = {"skipped": "not enough free HBM"}
+                continue
+            r2, w2 = measure(sp, torch, dist, dev, ws, rank, local, args, nvc=nvc)
+            if rank == 0:
+                extras[name] = extra_line(sp, r2, ws, dev, w2, mixing)
+            w2.close()
+            del w2
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:   # the CPU baseline is an N = 1 figure
-        del wl
         cpu = cpu_baseline(L, uniform, args.cpu_seconds)
 
     if rank == 0:
+        achieved = res["achieved"]
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak" if weak(args, ws) else "strong",
+            "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak" if weak(spec, ws) else "strong",
             "vs_baseline": None,
-            "dtype": {"float32": "f32", "bfloat16": "bf16", "float64": "f64"}[args.dtype],
+            "dtype": {"float32": "f32", "bfloat16": "bf16", "float64": "f64"}[spec.dtype],
             "data": "synthetic: N(0,1) weights and gradients generated on device (torch "
                     "Generator), permutations from the device generator (seed 12345)",
-            "config": config_dict(args, ws),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("mix_shard_kernel" if ws > 1 and args.layout != "coord"
-                                    else "mix_tma_kernel") + f" ({args.strategy}, {args.dtype})",
-                         "algorithmic_bytes_per_launch": algo_bytes,
-                         "avg_launch_ms": kern_avg_s * 1e3, "peak_source": peak_src},
+            "config": config_dict(spec, ws),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": res["peak"],
+                         "unit": "GB/s", "frac": achieved / res["peak"], "traffic": traffic,
+                         "kernel": (("mix_shard_kernel" if wl_kind(spec, ws) == "shard" else
+                                     "d1d_fused_kernel" if wl_kind(spec, ws) == "d1d" else
+                                     "mix_tma_kernel") + f" ({spec.strategy}, {spec.dtype})"),
+                         "algorithmic_bytes_per_launch": res["algo_bytes"],
+                         "avg_launch_ms": res["kern_avg_s"] * 1e3,
+                         "peak_source": res["peak_src"]},
             "cpu_baseline": cpu,
             "e2e": e2e,
             **({"nvlink": nvlink} if nvlink else {}),
-            **({"step_ordering": "in-kernel flags (multimem.red), no collective"
+            **({"step_ordering": "in-kernel flags (multimem.red / peer atomics), no collective"
                 if step_sync else "NCCL 4-byte all-reduce between steps"}
                if step_sync is not None else {}),
             "gpu_launches": launches["perm"] + launches["mix"],
             "gpu_launches_detail": launches,
+            "warmup_detail": {"warmup_steps": args.warmup,
+                              "rewarm_steps_before_timing": res["rewarm_steps"],
+                              "note": "untimed re-warm steps after the clock sampler started, "
+                                      "so the timed region starts at load clocks"},
             "clocks": clock_info,
+            **({"extras": extras} if extras else {}),
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
 
 
-def run_e2e_resident(args, torch, wl, dev):
+def wl_kind(spec, ws):
+    if ws == 1 or spec.layout == "coord":
+        return "tma"
+    return "d1d" if spec.strategy == "d1d" else "shard"
+
+
+def run_e2e_resident(args, spec, torch, wl, dev):
     """The step through the public API (mixing.ring_mix_sgd / mean_mix_sgd) with the
     weights resident in HBM (the simulator state, like model weights in training) and,
     every step, the step's input — its gradients G — copied from pinned host memory
@@ -684,11 +871,11 @@ def run_e2e_resident(args, torch, wl, dev):
     copy = torch.cuda.Stream(device=dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     used = [torch.cuda.Event(), torch.cuda.Event()]
-    uniform = args.strategy == "d1d"
+    uniform = spec.strategy == "d1d"
     nsteps = args.e2e_steps + 2
     tabs = M.permutation_tables(L, SEED, 0, nsteps + 1, dev)
     fixed = None
-    if args.strategy == "adpsgd_fixed":
+    if spec.strategy == "adpsgd_fixed":
         from paper_2002_01119_b200 import simulation as S
         fixed = S.fixed_ring_tables(L, dev)
 
@@ -721,13 +908,53 @@ def run_e2e_resident(args, torch, wl, dev):
     return a.elapsed_time(e) / args.e2e_steps
 
 
-def run_e2e(args, torch, mixing, dev, cols=None):
+def run_e2e_sharded(args, torch, wl, dev, k0):
+    """Sharded layouts through their public step API (distributed.LearnerShardedRingPos /
+    LearnerShardedRing / LearnerShardedD1DFused) with W resident: every step each rank
+    copies its learners' gradients from pinned host memory (copy stream, double-buffered)
+    and reads back max|W'|.  Returns this rank's ms/step."""
+    from paper_2002_01119_b200 import mixing as M
+
+    G_host = torch.empty(wl.G.shape, dtype=wl.G.dtype, pin_memory=True)
+    G_host.copy_(wl.G)
+    Gd = [wl.G, M.empty_learner_major(wl.rows, wl.cols, wl.G.dtype, dev)]
+    res_host = torch.zeros(args.e2e_steps + 4, dtype=torch.int64).pin_memory()
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(device=dev)
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    used = [torch.cuda.Event(), torch.cuda.Event()]
+    wl.reset_tables()
+
+    def one(i, k):
+        b = i % 2
+        with torch.cuda.stream(copy):
+            if i >= 2:
+                copy.wait_event(used[b])
+            Gd[b].copy_(G_host, non_blocking=True)
+            copied[b].record(copy)
+        comp.wait_event(copied[b])
+        wl.step(k, G=Gd[b])
+        used[b].record(comp)
+        res_host[i].copy_(wl.amax[k], non_blocking=True)
+
+    one(0, k0)
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(comp)
+    for i in range(1, args.e2e_steps + 1):
+        one(i, k0 + i)
+    e.record(comp)
+    torch.cuda.synchronize()
+    return a.elapsed_time(e) / args.e2e_steps
+
+
+def run_e2e(args, spec, torch, dev, cols=None):
     """Step through the host-buffer API (W, G pinned host -> W' host) for this
     rank's column stripe (`cols`, default: the whole problem); returns ms/step."""
     from paper_2002_01119_b200 import mixing as M
 
-    L = args.learners
-    d = args.dim if cols is None else cols
+    L = spec.learners
+    d = spec.dim if cols is None else cols
     Wh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
     Gh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
     Oh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
@@ -737,7 +964,7 @@ def run_e2e(args, torch, mixing, dev, cols=None):
     for host in (Wh, Gh):
         for r in range(L):
             host[r].copy_(torch.randn(d, generator=g, device=dev))
-    ws_buf = mixing.host_workspace(L, 1 << 20, dev)
+    ws_buf = M.host_workspace(L, 1 << 20, dev)
     tabs = M.permutation_tables(L, SEED, 0, args.e2e_steps + 1, dev)
     left = tabs.left.cpu()
     right = tabs.right.cpu()
@@ -757,13 +984,13 @@ def run_e2e(args, torch, mixing, dev, cols=None):
     return a.elapsed_time(b) / args.e2e_steps
 
 
-def e2e_line(args, ms, ws, cols=None):
+def e2e_line(args, spec, ms, ws, cols=None):
     """The step on host buffers: W, G from pinned host memory and W' back every step
     (12 B/param over PCIe); `cols` columns per rank (default: the whole problem)."""
-    L = args.learners
-    d = total_dim(args, ws) if cols is None else cols * ws
-    sample = None if cols is None or cols * ws == total_dim(args, ws) else (
-        f"{cols} of each rank's {total_dim(args, ws) // ws} columns (pinned-memory bound); "
+    L = spec.learners
+    d = total_dim(spec, ws) if cols is None else cols * ws
+    sample = None if cols is None or cols * ws == total_dim(spec, ws) else (
+        f"{cols} of each rank's {total_dim(spec, ws) // ws} columns (pinned-memory bound); "
         f"the rate is PCIe-bound, so it does not depend on the sample width")
     return {"value": L * d / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": 2 * L * d * 4 + 2 * L * 4 * ws,
@@ -776,15 +1003,38 @@ def e2e_line(args, ms, ws, cols=None):
             **({"sample": sample} if sample else {})}
 
 
-def e2e_resident_line(args, ms, ws):
-    L, d = args.learners, total_dim(args, ws)
+def e2e_resident_line(args, spec, ms, ws, wl):
+    L, d = spec.learners, total_dim(spec, ws)
+    sharded = wl.sharded is not None or (ws > 1 and spec.layout == "learner")
+    esz = BYTES_PER_PARAM[spec.dtype] // 3
     return {"value": L * d / (ms / 1e3), "unit": UNIT,
-            "h2d_bytes_per_step": L * d * 4, "d2h_bytes_per_step": 8 * ws,
+            "h2d_bytes_per_step": L * d * esz, "d2h_bytes_per_step": 8 * ws,
             "ms_per_step": ms, "steps": args.e2e_steps,
-            "path": "public API mixing.ring_mix_sgd with W resident in HBM (simulator state); "
-                    "per step: G (the step's input) H2D from pinned host memory on a copy "
-                    "stream, double-buffered, and max|W'| (the divergence metric) D2H" + (
-                        f"; every rank its column stripe, max over {ws} ranks" if ws > 1 else "")}
+            "path": ("public API (distributed.LearnerSharded* step) with W resident and "
+                     "sharded; per step every rank copies its learners' G from pinned host "
+                     "memory (copy stream, double-buffered) and reads back max|W'|; max over "
+                     f"{ws} ranks") if sharded else
+                    ("public API mixing.ring_mix_sgd with W resident in HBM (simulator state); "
+                     "per step: G (the step's input) H2D from pinned host memory on a copy "
+                     "stream, double-buffered, and max|W'| (the divergence metric) D2H" + (
+                         f"; every rank its column stripe, max over {ws} ranks"
+                         if ws > 1 else ""))}
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args) -> int:
+    """`--gpus N` without torchrun: launch N ranks (one per GPU) on 127.0.0.1."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -793,8 +1043,10 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -33,7 +33,8 @@
  *   rm_ring_mix_batched_f64 <- product @ T_k of                spectral.py:273-279
  *                            monte_carlo_consensus
  *   rm_ipc_* / rm_shard_* / rm_pos_* / rm_partial_sum_* / rm_apply_mean_sgd_* /
- *   rm_nvls_mean_f64 / rm_step_sync_wait
+ *   rm_nvls_mean_f64 / rm_p2p_mean_f64 / rm_d1d_fused_* / rm_step_sync_wait /
+ *   rm_xgpu_status
  *                         <- (no reference counterpart: the reference simulates all
  *                            learners in one process; these shard them over GPUs —
  *                            the step they compute is still simulation.py:263-268 /
@@ -173,20 +174,44 @@ int rm_ipc_close_handle(void* dptr);
  * *done >= world * (epoch - 1) — every rank finished the previous step, whose rows it reads
  * and whose buffers it overwrites — and at its end adds 1 to `done` on every rank through
  * the multicast address done_mc (multimem.red.release).  done: symmetric uint32, zeroed on
- * every rank before the first step; counter: local device uint32, zeroed once. */
+ * every rank before the first step; counter: local device uint32, zeroed once.
+ * Without NVSwitch multicast (done_mc == NULL) done_peers, a device uint64[world] table of
+ * every rank's `done` address (CUDA IPC / symmetric-memory peer pointers), is used instead:
+ * one red.release per rank.  With every rank's buffers on one GPU the same table drives a
+ * single-device emulation of the world (launch the ranks' steps in rank order per epoch).
+ * A wait longer than RINGMIX_XGPU_TIMEOUT_S (default 600 s) gives up instead of trapping
+ * and is reported by rm_xgpu_status(). */
 typedef struct {
   const uint32_t* done;
   uint32_t* done_mc;
   uint32_t* counter;
   uint32_t epoch;
   int world;
+  const uint64_t* done_peers;
 } rm_step_sync;
+
+/* Reads and clears the calling device's cross-rank wait status: bit 0 set = a cross-rank
+ * wait (step ordering, fused D1D) gave up after RINGMIX_XGPU_TIMEOUT_S; the step that
+ * saw it has unspecified contents. */
+int rm_xgpu_status(unsigned int* status);
+/* Sets the cross-rank wait bound of the current device (seconds; overrides the
+ * RINGMIX_XGPU_TIMEOUT_S default). */
+int rm_set_xgpu_timeout(double seconds);
 
 /* Stream-ordered wait until every rank finished step `sync->epoch` (*done >= world *
  * epoch).  The next step kernel orders itself; any other consumer of a step's outputs
  * in the ring-position layout (whose rows are written by every rank) calls this first.
  * Returns 0 without launching when epoch == 0. */
 int rm_step_sync_wait(const rm_step_sync* sync, void* stream);
+
+/* Stream-ordered publish of writes made outside the step kernels (initial weights,
+ * checkpoint restore, host edits of the current rows): adds 1 to `done` on every rank as a
+ * step's end would.  Collective: every rank calls it once, with sync->epoch = the epoch it
+ * occupies (last step + 1); the next step (epoch + 1) of every rank then waits for every
+ * rank's writes.  Readers of the position layout's slots call rm_step_sync_wait first;
+ * writers call rm_step_sync_wait (position layout: peers write into this rank's slots),
+ * write, then rm_step_sync_publish. */
+int rm_step_sync_publish(const rm_step_sync* sync, void* stream);
 
 /* Per-step plan for the rank owning learners [row0, row0+Lg): distinct remote
  * neighbour ids and each local learner's staged input indices in global-id
@@ -280,7 +305,8 @@ int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls);
  *   epoch: 1, 2, 3, ... (one per call, the same on every rank);
  *   chunk_cols: a multiple of 32 * world; pct_partial / pct_reduce: share of the grid's
  *   CTAs for those roles (the rest apply).  Every rank must call with the same d, L,
- *   chunk_cols and epoch.  A wait that exceeds 20 s traps (no silent hang). */
+ *   chunk_cols and epoch.  A wait longer than RINGMIX_XGPU_TIMEOUT_S gives up and is
+ *   reported by rm_xgpu_status(). */
 int rm_d1d_fused_nvls_f32(const float* W, const float* G, float* out, int Lg, int L, int64_t d,
                           int64_t ldw, int64_t ldg, int64_t ldo, double lr,
                           unsigned long long* absmax_bits, double* P, const double* P_mc,
@@ -304,6 +330,46 @@ int rm_d1d_fused_nvls_bf16(const uint16_t* W, const uint16_t* G, uint16_t* out, 
                            void* stream);
 int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, int64_t c1, int L,
                      void* stream);
+/* rm_nvls_mean_f64 without multicast: P_peers / M_peers are device uint64[world] tables of
+ * every rank's P / M; the cross-rank sum runs in ascending rank order (unicast NVLink
+ * loads), the means are stored to every rank. */
+int rm_p2p_mean_f64(const uint64_t* P_peers, const uint64_t* M_peers, int world, int64_t c0,
+                    int64_t c1, int L, void* stream);
+
+/* The fused D1D step without multicast (unicast NVLink P2P through peer tables), for
+ * `nlocal` ranks per launch: 1 in a one-process-per-GPU job on a system without NVSwitch
+ * multicast; `world` when every rank's buffers live on this GPU (single-device emulation
+ * of the whole world in one launch — what the one-GPU tests run).  ranks: host array of
+ * nlocal entries (device pointers inside); P_peers / M_peers / flags_peers: device
+ * uint64[world] tables of every rank's P / M / flags.  Cross-rank sums in ascending rank
+ * order.  Other arguments as rm_d1d_fused_nvls_*. */
+typedef struct {
+  const void* W;
+  const void* G;
+  void* out;
+  unsigned long long* absmax_bits;
+  double* P;
+  const double* M;
+  const uint32_t* flags;
+  uint32_t* counters;
+  int Lg;
+  int rank;
+} rm_d1d_rank;
+int rm_d1d_fused_p2p_f32(const rm_d1d_rank* ranks, int nlocal, int L, int64_t d, int64_t ldw,
+                         int64_t ldg, int64_t ldo, double lr, const uint64_t* P_peers,
+                         const uint64_t* M_peers, const uint64_t* flags_peers, int world,
+                         int64_t chunk_cols, int max_chunks, uint32_t epoch, int pct_partial,
+                         int pct_reduce, void* stream);
+int rm_d1d_fused_p2p_f64(const rm_d1d_rank* ranks, int nlocal, int L, int64_t d, int64_t ldw,
+                         int64_t ldg, int64_t ldo, double lr, const uint64_t* P_peers,
+                         const uint64_t* M_peers, const uint64_t* flags_peers, int world,
+                         int64_t chunk_cols, int max_chunks, uint32_t epoch, int pct_partial,
+                         int pct_reduce, void* stream);
+int rm_d1d_fused_p2p_bf16(const rm_d1d_rank* ranks, int nlocal, int L, int64_t d, int64_t ldw,
+                          int64_t ldg, int64_t ldo, double lr, const uint64_t* P_peers,
+                          const uint64_t* M_peers, const uint64_t* flags_peers, int world,
+                          int64_t chunk_cols, int max_chunks, uint32_t epoch, int pct_partial,
+                          int pct_reduce, void* stream);
 
 /* ---- device gradient producer for the reference's quadratic oracle ----
  * (objectives.py:84-90 via simulation.py:226-238):

@@ -70,6 +70,10 @@ _SIGNATURES = {
 }
 _SIGNATURES["rm_pos_plan"] = ([vp, vp, i32, i32, i32, vp, vp, vp, vp], i32)
 _SIGNATURES["rm_step_sync_wait"] = ([vp, vp], i32)
+_SIGNATURES["rm_xgpu_status"] = ([vp], i32)
+_SIGNATURES["rm_set_xgpu_timeout"] = ([dbl], i32)
+_SIGNATURES["rm_step_sync_publish"] = ([vp, vp], i32)
+_SIGNATURES["rm_p2p_mean_f64"] = ([vp, vp, i32, i64, i64, i32, vp], i32)
 for _sfx in ("f32", "f64", "bf16"):
     _SIGNATURES[f"rm_ring_mix_sgd_pos_{_sfx}"] = (
         [vp, vp, vp, i32, i32, i32, i64, i64, i64, vp, vp, dbl, vp, vp, vp], i32)
@@ -79,6 +83,9 @@ for _sfx in ("f32", "f64", "bf16"):
     _SIGNATURES[f"rm_d1d_fused_nvls_{_sfx}"] = (
         [vp, vp, vp, i32, i32, i64, i64, i64, i64, dbl, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32,
          i64, i32, ctypes.c_uint32, i32, i32, vp], i32)
+    _SIGNATURES[f"rm_d1d_fused_p2p_{_sfx}"] = (
+        [vp, i32, i32, i64, i64, i64, i64, dbl, vp, vp, vp, i32, i64, i32, ctypes.c_uint32, i32,
+         i32, vp], i32)
     _SIGNATURES[f"rm_apply_mean_sgd_{_sfx}"] = ([vp, vp, vp, i32, i32, i64, i64, i64, dbl, vp, vp],
                                                 i32)
     _SIGNATURES[f"rm_ring_mix_sgd_{_sfx}"] = (
@@ -92,7 +99,13 @@ OPTIONAL_SIGNATURES: dict = {}
 class StepSyncArgs(ctypes.Structure):
     """rm_step_sync (include/ringmix_b200.h)."""
     _fields_ = [("done", vp), ("done_mc", vp), ("counter", vp), ("epoch", ctypes.c_uint32),
-                ("world", i32)]
+                ("world", i32), ("done_peers", vp)]
+
+
+class D1DRank(ctypes.Structure):
+    """rm_d1d_rank (include/ringmix_b200.h): one rank's buffers of the fused D1D step."""
+    _fields_ = [("W", vp), ("G", vp), ("out", vp), ("absmax_bits", vp), ("P", vp), ("M", vp),
+                ("flags", vp), ("counters", vp), ("Lg", i32), ("rank", i32)]
 
 
 class RingmixError(RuntimeError):

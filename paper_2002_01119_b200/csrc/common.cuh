@@ -121,19 +121,31 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// Cross-rank waits are bounded: a rank whose host falls behind (checkpoint,
+// eval, module load, debugger) must not kill its peers' contexts, so the bound
+// is long (RINGMIX_XGPU_TIMEOUT_S, default 600 s, set per device by the host
+// launchers) and hitting it does not trap: the wait gives up, records the
+// timeout in g_xgpu_status (rm_xgpu_status() reads and clears it) and the step
+// completes with unspecified contents — the caller treats it as a failed step.
+static __device__ unsigned long long g_xgpu_timeout_ns = 600ull * 1000000000ull;
+static __device__ unsigned int g_xgpu_status = 0;
+
 // Thread 0 spins (acquire, system scope) until *flag - target >= 0 (wraps), then
-// the CTA proceeds; traps after 20 s instead of hanging.  The data guarded by the
-// flag is read through another virtual alias (peer / multicast mapping), hence
-// the alias fence.
+// the CTA proceeds.  The data guarded by the flag is read through another
+// virtual alias (peer / multicast mapping), hence the alias fence.
 __device__ __forceinline__ void xgpu_wait(const uint32_t* flag, uint32_t target) {
   if (threadIdx.x == 0) {
     const unsigned long long t0 = global_ns();
+    const unsigned long long limit = g_xgpu_timeout_ns;
     for (;;) {
       uint32_t v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
       if ((int)(v - target) >= 0) break;
       __nanosleep(64);
-      if (global_ns() - t0 > 20000000000ull) __trap();
+      if (global_ns() - t0 > limit) {
+        atomicOr(&g_xgpu_status, 1u);
+        break;
+      }
     }
     asm volatile("fence.proxy.alias;" ::: "memory");
     // the peers' generic-proxy stores are read next by TMA (async proxy)
@@ -142,12 +154,70 @@ __device__ __forceinline__ void xgpu_wait(const uint32_t* flag, uint32_t target)
   __syncthreads();
 }
 
+// A buffer that every rank of a learner-sharded job holds at the same offset
+// (symmetric memory), seen from one rank: either its NVSwitch multicast address
+// (mc != 0: one multimem instruction reaches every rank, reductions happen in
+// the switch) or a table of every rank's address of it (peers: unicast loads and
+// stores over NVLink P2P — or, with all "ranks" on one GPU, the single-device
+// emulation the tests run).  Element i is at byte offset i * sizeof(element).
+struct SymRef {
+  unsigned long long mc;
+  const unsigned long long* peers;  // device table [world] when mc == 0
+  int world;
+};
+
+// +1 on element i of every rank (release, system scope)
+__device__ __forceinline__ void sym_red_add_u32(const SymRef& s, long long i) {
+  if (s.mc) {
+    asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(s.mc + 4 * i)
+                 : "memory");
+  } else {
+    for (int r = 0; r < s.world; r++)
+      asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(s.peers[r] + 4 * i)
+                   : "memory");
+  }
+}
+
+// sum over ranks of element i (multicast: in-switch reduction; unicast: ascending rank)
+__device__ __forceinline__ double sym_ld_sum_f64(const SymRef& s, long long i) {
+  double v;
+  if (s.mc) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];"
+                 : "=d"(v)
+                 : "l"(s.mc + 8 * i)
+                 : "memory");
+  } else {
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(s.peers[0] + 8 * i)
+                 : "memory");
+    for (int r = 1; r < s.world; r++) {
+      double x;
+      asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(x) : "l"(s.peers[r] + 8 * i)
+                   : "memory");
+      v = __dadd_rn(v, x);
+    }
+  }
+  return v;
+}
+
+// element i := v on every rank
+__device__ __forceinline__ void sym_st_f64(const SymRef& s, long long i, double v) {
+  if (s.mc) {
+    asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(s.mc + 8 * i), "d"(v)
+                 : "memory");
+  } else {
+    for (int r = 0; r < s.world; r++)
+      asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(s.peers[r] + 8 * i), "d"(v)
+                   : "memory");
+  }
+}
+
 // Every thread's writes so far are made visible system-wide; the CTA whose
-// arrival completes `last` arrivals on `counter` adds 1 to the flag on every
-// rank (multimem.red.release through the multicast address flag_mc).
+// arrival completes `last` arrivals on `counter` adds 1 to element `i` of the
+// flag buffer on every rank (multimem.red.release through the multicast address,
+// or one red.release per rank in the peer-table form).
 // reset: the last arriver zeroes the counter (for a counter private to one launch).
-__device__ __forceinline__ void xgpu_arrive(uint32_t* counter, uint32_t last, uint32_t* flag_mc,
-                                            bool reset = false) {
+__device__ __forceinline__ void xgpu_arrive(uint32_t* counter, uint32_t last, const SymRef& flag,
+                                            long long i, bool reset = false) {
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -156,7 +226,7 @@ __device__ __forceinline__ void xgpu_arrive(uint32_t* counter, uint32_t last, ui
       if (reset) atomicExch(counter, 0u);
       __threadfence_system();
       asm volatile("fence.proxy.alias;" ::: "memory");
-      asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(flag_mc) : "memory");
+      sym_red_add_u32(flag, i);
     }
   }
 }

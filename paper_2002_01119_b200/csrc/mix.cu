@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         }
         if (diff && a.mismatch) atomicOr(a.mismatch, 1u);
       }
-      T* dst = out + j * a.ldo + c0 + c;
+      T* dst = out + (long long)j * a.ldo + c0 + c;
       if (c + VEC <= width) {
 #pragma unroll
         for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);

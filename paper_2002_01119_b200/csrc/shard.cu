@@ -33,6 +33,20 @@
 
 namespace rm {
 
+// Per device, once: the cross-rank wait bound of this module's kernels
+// (RINGMIX_XGPU_TIMEOUT_S seconds, default 600; see xgpu_wait).
+static unsigned long long g_xgpu_config_mask = 0;
+static void xgpu_config() {
+  if (!attr_needed(&g_xgpu_config_mask)) return;
+  unsigned long long ns = 600ull * 1000000000ull;
+  if (const char* env = getenv("RINGMIX_XGPU_TIMEOUT_S")) {
+    const double s = atof(env);
+    if (s > 0) ns = (unsigned long long)(s * 1e9);
+  }
+  if (cudaMemcpyToSymbol(g_xgpu_timeout_ns, &ns, sizeof(ns)) == cudaSuccess)
+    attr_done(&g_xgpu_config_mask);
+}
+
 constexpr int kShThreads = 512;
 constexpr int kShStages = 3;
 constexpr int kShStageTarget = 64 * 1024;
@@ -95,7 +109,7 @@ struct ShardArgs {
   // optional in-kernel step ordering (rm_step_sync): wait until every rank finished
   // the previous step, signal this rank's completion to every rank at the end
   const uint32_t* sync_done;
-  uint32_t* sync_done_mc;
+  SymRef sync_flag;  // `done` on every rank (multicast address or peer table)
   uint32_t* sync_cnt;
   uint32_t sync_target;
 };
@@ -240,7 +254,7 @@ __global__ void __launch_bounds__(kShThreads, 1)
   if (a.sync_done) {
     // the last CTA resets the counter (the next launch starts after this one on
     // the stream) and bumps every rank's step flag
-    xgpu_arrive(a.sync_cnt, gridDim.x, a.sync_done_mc, true);
+    xgpu_arrive(a.sync_cnt, gridDim.x, a.sync_flag, 0, true);
   }
 }
 
@@ -490,13 +504,16 @@ static int shard_dispatch(const uint64_t* row_ptrs, const T* W_local, const T* G
   a.absmax = absmax;
   a.dest = dest;
   if (sync != nullptr) {
-    if (sync->done == nullptr || sync->done_mc == nullptr || sync->counter == nullptr ||
-        sync->world < 1 || sync->epoch == 0) {
+    if (sync->done == nullptr || (sync->done_mc == nullptr && sync->done_peers == nullptr) ||
+        sync->counter == nullptr || sync->world < 1 || sync->epoch == 0) {
       set_error("invalid step-sync arguments");
       return RM_EINVAL;
     }
+    xgpu_config();
     a.sync_done = sync->done;
-    a.sync_done_mc = sync->done_mc;
+    a.sync_flag = SymRef{reinterpret_cast<unsigned long long>(sync->done_mc),
+                         reinterpret_cast<const unsigned long long*>(sync->done_peers),
+                         sync->world};
     a.sync_cnt = sync->counter;
     a.sync_target = (uint32_t)sync->world * (sync->epoch - 1u);
   }
@@ -577,9 +594,62 @@ extern "C" int rm_step_sync_wait(const rm_step_sync* sync, void* stream) {
     return RM_EINVAL;
   }
   if (sync->epoch == 0) return 0;  // no step issued yet
+  xgpu_config();
   step_sync_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
       sync->done, (uint32_t)sync->world * sync->epoch);
   RM_CHECK_LAUNCH("step_sync_wait_kernel");
+  return 0;
+}
+
+// Stream-ordered "publish": adds 1 to `done` on every rank, like the end of a step,
+// without a step.  Called collectively (every rank, same epoch) after writes to the
+// step buffers from outside the step kernels (initialisation, checkpoint restore,
+// host edits): the next step kernel of every rank then waits for them.
+__global__ void step_sync_publish_kernel(SymRef flag) {
+  __threadfence_system();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.alias;" ::: "memory");
+    sym_red_add_u32(flag, 0);
+  }
+}
+
+extern "C" int rm_step_sync_publish(const rm_step_sync* sync, void* stream) {
+  if (sync == nullptr || (sync->done_mc == nullptr && sync->done_peers == nullptr) ||
+      sync->world < 1) {
+    set_error("invalid step-sync arguments");
+    return RM_EINVAL;
+  }
+  step_sync_publish_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      SymRef{reinterpret_cast<unsigned long long>(sync->done_mc),
+             reinterpret_cast<const unsigned long long*>(sync->done_peers), sync->world});
+  RM_CHECK_LAUNCH("step_sync_publish_kernel");
+  return 0;
+}
+
+// Overrides the cross-rank wait bound of the current device (seconds > 0).
+extern "C" int rm_set_xgpu_timeout(double seconds) {
+  if (!(seconds > 0) || seconds > 1e6) {
+    set_error("timeout must be in (0, 1e6] seconds");
+    return RM_EINVAL;
+  }
+  const unsigned long long ns = (unsigned long long)(seconds * 1e9);
+  cudaError_t e = cudaMemcpyToSymbol(g_xgpu_timeout_ns, &ns, sizeof(ns));
+  if (e != cudaSuccess) return fail_cuda(e, "rm_set_xgpu_timeout");
+  attr_done(&g_xgpu_config_mask);
+  return 0;
+}
+
+// Reads and clears this device's cross-rank wait status: bit 0 = a wait gave up
+// after RINGMIX_XGPU_TIMEOUT_S (the steps that saw it have unspecified contents).
+extern "C" int rm_xgpu_status(unsigned int* status) {
+  if (status == nullptr) {
+    set_error("null pointer");
+    return RM_EINVAL;
+  }
+  unsigned int zero = 0;
+  cudaError_t e = cudaMemcpyFromSymbol(status, g_xgpu_status, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_xgpu_status, &zero, sizeof(zero));
+  if (e != cudaSuccess) return fail_cuda(e, "rm_xgpu_status");
   return 0;
 }
 
@@ -678,8 +748,7 @@ RM_DEFINE_SHARD(bf16, uint16_t, __nv_bfloat16)
 // and the result is broadcast into every rank's M (multimem.st).  Ordering
 // against the partial-sum writes and the readers of M is the caller's barrier.
 namespace rm {
-__device__ __forceinline__ void nvls_sum_range(const double* __restrict__ P_mc,
-                                               double* __restrict__ M_mc, long long c0,
+__device__ __forceinline__ void nvls_sum_range(const SymRef& P, const SymRef& M, long long c0,
                                                long long c1, double L, long long worker,
                                                long long nworkers) {
   constexpr int U = 8;
@@ -688,28 +757,32 @@ __device__ __forceinline__ void nvls_sum_range(const double* __restrict__ P_mc,
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const long long cc = c + u * nworkers;
-      if (cc < c1)
-        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];"
-                     : "=d"(v[u])
-                     : "l"(P_mc + cc)
-                     : "memory");
+      if (cc < c1) v[u] = sym_ld_sum_f64(P, cc);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const long long cc = c + u * nworkers;
-      if (cc < c1)
-        asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(M_mc + cc),
-                     "d"(__ddiv_rn(v[u], L))
-                     : "memory");
+      if (cc < c1) sym_st_f64(M, cc, __ddiv_rn(v[u], L));
     }
   }
 }
 
 __global__ void __launch_bounds__(256)
-    nvls_sum_kernel(const double* __restrict__ P_mc, double* __restrict__ M_mc, long long c0,
-                    long long c1, double L) {
-  nvls_sum_range(P_mc, M_mc, c0, c1, L, blockIdx.x * (long long)blockDim.x + threadIdx.x,
+    nvls_sum_kernel(SymRef P, SymRef M, long long c0, long long c1, double L) {
+  nvls_sum_range(P, M, c0, c1, L, blockIdx.x * (long long)blockDim.x + threadIdx.x,
                  (long long)gridDim.x * blockDim.x);
+}
+
+static int launch_sym_mean(const SymRef& P, const SymRef& M, int64_t c0, int64_t c1, int L,
+                           void* stream) {
+  if (c1 == c0) return 0;
+  long long blocks = (c1 - c0 + 2047) / 2048;
+  const long long cap = (g_d1d_nvls_cap ? g_d1d_nvls_cap : 8) * (long long)sm_count(-1);
+  if (blocks > cap) blocks = cap;
+  nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(P, M, c0, c1,
+                                                                             (double)L);
+  RM_CHECK_LAUNCH("nvls_sum_kernel");
+  return 0;
 }
 }  // namespace rm
 
@@ -719,14 +792,24 @@ extern "C" int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, in
     set_error("invalid NVLS reduction arguments");
     return RM_EINVAL;
   }
-  if (c1 == c0) return 0;
-  long long blocks = (c1 - c0 + 2047) / 2048;
-  const long long cap = (g_d1d_nvls_cap ? g_d1d_nvls_cap : 8) * (long long)sm_count(-1);
-  if (blocks > cap) blocks = cap;
-  nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(P_mc, M_mc, c0, c1,
-                                                                             (double)L);
-  RM_CHECK_LAUNCH("nvls_sum_kernel");
-  return 0;
+  return launch_sym_mean(SymRef{reinterpret_cast<unsigned long long>(P_mc), nullptr, 1},
+                         SymRef{reinterpret_cast<unsigned long long>(M_mc), nullptr, 1}, c0, c1,
+                         L, stream);
+}
+
+// Same reduction with peer tables instead of multicast addresses: P_peers /
+// M_peers are device uint64[world] tables of every rank's P / M (NVLink P2P
+// without NVSwitch multicast, or all ranks' buffers on one GPU).  The sum runs
+// in ascending rank order.
+extern "C" int rm_p2p_mean_f64(const uint64_t* P_peers, const uint64_t* M_peers, int world,
+                               int64_t c0, int64_t c1, int L, void* stream) {
+  if (P_peers == nullptr || M_peers == nullptr || world < 1 || c0 < 0 || c1 < c0 || L < 1) {
+    set_error("invalid peer-table reduction arguments");
+    return RM_EINVAL;
+  }
+  return launch_sym_mean(
+      SymRef{0, reinterpret_cast<const unsigned long long*>(P_peers), world},
+      SymRef{0, reinterpret_cast<const unsigned long long*>(M_peers), world}, c0, c1, L, stream);
 }
 
 // ---- D1D across GPUs in ONE kernel: partial sums, in-switch reduction, apply ----
@@ -744,46 +827,59 @@ extern "C" int rm_nvls_mean_f64(const double* P_mc, double* M_mc, int64_t c0, in
 // All CTAs must be co-resident (the host sizes the grid by occupancy); waits
 // trap after 20 s instead of hanging.
 namespace rm {
-struct D1DFusedArgs {
+// One rank's buffers of the fused D1D step (local addresses).  A launch drives
+// one rank (the normal multi-process case) or, with peer-table SymRefs, every
+// rank of a world whose buffers all live on this GPU (single-device emulation:
+// CTA block r * per_rank .. (r+1) * per_rank - 1 plays rank r).
+struct D1DRank {
   const void* W;
   const void* G;
   void* out;
-  int Lg, L;
+  unsigned long long* absmax;
+  double* P;                 // partial sums (symmetric buffer)
+  const double* M;           // means (symmetric buffer)
+  const uint32_t* flags;     // [2 * max_chunks]: A (partials of chunk c ready), B (means ready)
+  uint32_t* counters;        // [2 * max_chunks] role counters (local)
+  int Lg, rank;
+};
+
+constexpr int kD1DMaxLocalRanks = 8;
+
+struct D1DFusedArgs {
+  D1DRank r[kD1DMaxLocalRanks];
+  int nlocal, per_rank;
+  int L;
   long long d, ldw, ldg, ldo;
   double lr;
-  unsigned long long* absmax;
-  double* P;                 // this rank's partial sums (symmetric buffer, local address)
-  const double* P_mc;        // multicast address of P
-  const double* M;           // this rank's means (local address)
-  double* M_mc;              // multicast address of M
-  const uint32_t* flagsA;    // local: [nchunks] partial sums of chunk c ready (x world)
-  uint32_t* flagsA_mc;
-  const uint32_t* flagsB;    // local: [nchunks] means of chunk c ready (x world)
-  uint32_t* flagsB_mc;
-  uint32_t* cntP;            // local role counters [nchunks]
-  uint32_t* cntR;
-  int rank, world;
+  SymRef P, M, F;            // every rank's P / M / flags
+  int world;
   long long chunk;
-  int nchunks;
+  int nchunks, max_chunks;
   uint32_t epoch;
   int nP, nR, nA;
 };
 
 template <typename T, bool HAS_G, int MINB>
-__global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(D1DFusedArgs a) {
+__global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(const __grid_constant__ D1DFusedArgs a) {
   using E = Elem<T>;
-  const T* W = static_cast<const T*>(a.W);
-  const T* G = static_cast<const T*>(a.G);
-  T* out = static_cast<T*>(a.out);
-  const int bid = blockIdx.x;
+  const int lr_ = blockIdx.x / a.per_rank;
+  const int bid = blockIdx.x - lr_ * a.per_rank;
+  const D1DRank& R = a.r[lr_];
+  const T* W = static_cast<const T*>(R.W);
+  const T* G = static_cast<const T*>(R.G);
+  T* out = static_cast<T*>(R.out);
+  const uint32_t* flagsA = R.flags;
+  const uint32_t* flagsB = R.flags + a.max_chunks;
+  uint32_t* cntP = R.counters;
+  uint32_t* cntR = R.counters + a.max_chunks;
   const uint32_t all_ranks = (uint32_t)a.world * a.epoch;
   if (bid < a.nP) {
     const long long w = bid * (long long)blockDim.x + threadIdx.x;
     const long long nw = (long long)a.nP * blockDim.x;
     for (int c = 0; c < a.nchunks; c++) {
       const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
-      partial_sum_range<T>(W + b, a.Lg, e - b, a.ldw, a.P + b, w, nw);
-      xgpu_arrive(a.cntP + c, (uint32_t)a.nP * a.epoch, a.flagsA_mc + c);
+      partial_sum_range<T>(W + b, R.Lg, e - b, a.ldw, R.P + b, w, nw);
+      xgpu_arrive(cntP + c, (uint32_t)a.nP * a.epoch, a.F, c);
     }
   } else if (bid < a.nP + a.nR) {
     const long long w = (bid - a.nP) * (long long)blockDim.x + threadIdx.x;
@@ -792,10 +888,10 @@ __global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(D1DFusedArgs a) {
       const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
       long long sl = (e - b + a.world - 1) / a.world;
       sl = (sl + 31) / 32 * 32;
-      const long long s0 = min(e, b + a.rank * sl), s1 = min(e, s0 + sl);
-      xgpu_wait(a.flagsA + c, all_ranks);
-      nvls_sum_range(a.P_mc, a.M_mc, s0, s1, (double)a.L, w, nw);
-      xgpu_arrive(a.cntR + c, (uint32_t)a.nR * a.epoch, a.flagsB_mc + c);
+      const long long s0 = min(e, b + R.rank * sl), s1 = min(e, s0 + sl);
+      xgpu_wait(flagsA + c, all_ranks);
+      nvls_sum_range(a.P, a.M, s0, s1, (double)a.L, w, nw);
+      xgpu_arrive(cntR + c, (uint32_t)a.nR * a.epoch, a.F, a.max_chunks + c);
     }
   } else {
     const long long w = (bid - a.nP - a.nR) * (long long)blockDim.x + threadIdx.x;
@@ -803,40 +899,48 @@ __global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(D1DFusedArgs a) {
     typename E::amax_t amax = 0;
     for (int c = 0; c < a.nchunks; c++) {
       const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
-      xgpu_wait(a.flagsB + c, all_ranks);
-      apply_mean_range<T, HAS_G>(a.M + b, HAS_G ? G + b : nullptr, out + b, a.Lg, 1, e - b,
+      xgpu_wait(flagsB + c, all_ranks);
+      apply_mean_range<T, HAS_G>(R.M + b, HAS_G ? G + b : nullptr, out + b, R.Lg, 1, e - b,
                                  a.ldg, a.ldo, a.lr, amax, w, nw);
     }
-    if (a.absmax) absmax_publish(a.absmax, E::amax_bits(amax));
+    if (R.absmax) absmax_publish(R.absmax, E::amax_bits(amax));
   }
 }
 
+// ranks: nlocal entries (host array); P / M / F: every rank's symmetric buffers
 template <typename T>
-static int d1d_fused(const T* W, const T* G, T* out, int Lg, int L, int64_t d, int64_t ldw,
-                     int64_t ldg, int64_t ldo, double lr, unsigned long long* absmax, double* P,
-                     const double* P_mc, const double* M, double* M_mc, uint32_t* flags,
-                     uint32_t* flags_mc, uint32_t* counters, int rank, int world,
-                     int64_t chunk_cols, int max_chunks, uint32_t epoch, int pct_partial,
-                     int pct_reduce, void* stream) {
+static int d1d_fused(const D1DRank* ranks, int nlocal, int L, int64_t d, int64_t ldw, int64_t ldg,
+                     int64_t ldo, double lr, const SymRef& P, const SymRef& M, const SymRef& F,
+                     int world, int64_t chunk_cols, int max_chunks, uint32_t epoch,
+                     int pct_partial, int pct_reduce, void* stream) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
-  if (Lg < 1 || L < Lg || d < 0 || ldw < d || ldo < d || (G && ldg < d) || world < 1 ||
-      rank < 0 || rank >= world || epoch == 0 || max_chunks < 1 || W == nullptr ||
-      out == nullptr || P == nullptr || P_mc == nullptr || M == nullptr || M_mc == nullptr ||
-      flags == nullptr || flags_mc == nullptr || counters == nullptr || pct_partial < 1 ||
-      pct_reduce < 1 || pct_partial + pct_reduce > 98) {
+  if (nlocal < 1 || nlocal > kD1DMaxLocalRanks || nlocal > world || L < 1 || d < 0 ||
+      ldw < d || ldo < d || world < 1 || epoch == 0 || max_chunks < 1 || pct_partial < 1 ||
+      pct_reduce < 1 || pct_partial + pct_reduce > 98 || (!P.mc && !P.peers) ||
+      (!M.mc && !M.peers) || (!F.mc && !F.peers)) {
     set_error("invalid fused D1D arguments");
     return RM_EINVAL;
   }
+  const bool has_g = ranks[0].G != nullptr;
+  for (int i = 0; i < nlocal; i++) {
+    const D1DRank& r = ranks[i];
+    if (r.Lg < 1 || r.Lg > L || r.rank < 0 || r.rank >= world || r.W == nullptr ||
+        r.out == nullptr || r.P == nullptr || r.M == nullptr || r.flags == nullptr ||
+        r.counters == nullptr || (r.G != nullptr) != has_g || (has_g && ldg < d)) {
+      set_error("invalid fused D1D arguments (rank entry %d)", i);
+      return RM_EINVAL;
+    }
+    if (((reinterpret_cast<uintptr_t>(r.W) | reinterpret_cast<uintptr_t>(r.out) |
+          (uintptr_t)(ldw * sizeof(T)) | (uintptr_t)(ldo * sizeof(T)) |
+          (has_g ? (reinterpret_cast<uintptr_t>(r.G) | (uintptr_t)(ldg * sizeof(T))) : 0)) & 15) ||
+        VEC * sizeof(T) != 16) {
+      set_error("fused D1D needs 16-byte aligned rows");
+      return RM_EINVAL;
+    }
+  }
   if (chunk_cols < 32LL * world || chunk_cols % (32LL * world) != 0) {
     set_error("chunk_cols must be a positive multiple of 32 * world");
-    return RM_EINVAL;
-  }
-  if (((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(out) |
-        (uintptr_t)(ldw * sizeof(T)) | (uintptr_t)(ldo * sizeof(T)) |
-        (G ? (reinterpret_cast<uintptr_t>(G) | (uintptr_t)(ldg * sizeof(T))) : 0)) & 15) ||
-      VEC * sizeof(T) != 16) {
-    set_error("fused D1D needs 16-byte aligned rows");
     return RM_EINVAL;
   }
   if (d == 0) return 0;
@@ -845,6 +949,7 @@ static int d1d_fused(const T* W, const T* G, T* out, int Lg, int L, int64_t d, i
     set_error("%lld chunks exceed the %d flag slots", nchunks, max_chunks);
     return RM_ERANGE;
   }
+  xgpu_config();
   // CTAs per SM the kernel is compiled for (registers): more resident CTAs give the
   // HBM-bound roles more loads in flight (RINGMIX_D1D_FUSED_OCC = 2 / 3 / 4)
   static int occ_env = -1;
@@ -853,9 +958,9 @@ static int d1d_fused(const T* W, const T* G, T* out, int Lg, int L, int64_t d, i
     occ_env = env ? atoi(env) : 4;
     if (occ_env < 2 || occ_env > 4) occ_env = 4;
   }
-  auto kern = occ_env == 2 ? (G ? d1d_fused_kernel<T, true, 2> : d1d_fused_kernel<T, false, 2>)
-              : occ_env == 4 ? (G ? d1d_fused_kernel<T, true, 4> : d1d_fused_kernel<T, false, 4>)
-                             : (G ? d1d_fused_kernel<T, true, 3> : d1d_fused_kernel<T, false, 3>);
+  auto kern = occ_env == 2 ? (has_g ? d1d_fused_kernel<T, true, 2> : d1d_fused_kernel<T, false, 2>)
+              : occ_env == 4 ? (has_g ? d1d_fused_kernel<T, true, 4> : d1d_fused_kernel<T, false, 4>)
+                             : (has_g ? d1d_fused_kernel<T, true, 3> : d1d_fused_kernel<T, false, 3>);
   int occ = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (e != cudaSuccess) return fail_cuda(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
@@ -863,43 +968,35 @@ static int d1d_fused(const T* W, const T* G, T* out, int Lg, int L, int64_t d, i
     set_error("fused D1D kernel cannot be resident");
     return RM_EINVAL;
   }
-  // every CTA must be resident at once (roles wait on each other)
-  const int grid = occ * sm_count(-1);
+  // every CTA must be resident at once (roles wait on each other — across the
+  // local ranks too when several share this GPU)
+  const int per_rank = occ * sm_count(-1) / nlocal;
   D1DFusedArgs a{};
-  a.W = W;
-  a.G = G;
-  a.out = out;
-  a.Lg = Lg;
+  for (int i = 0; i < nlocal; i++) a.r[i] = ranks[i];
+  a.nlocal = nlocal;
+  a.per_rank = per_rank;
   a.L = L;
   a.d = d;
   a.ldw = ldw;
   a.ldg = ldg;
   a.ldo = ldo;
   a.lr = lr;
-  a.absmax = absmax;
   a.P = P;
-  a.P_mc = P_mc;
   a.M = M;
-  a.M_mc = M_mc;
-  a.flagsA = flags;
-  a.flagsA_mc = flags_mc;
-  a.flagsB = flags + max_chunks;
-  a.flagsB_mc = flags_mc + max_chunks;
-  a.cntP = counters;
-  a.cntR = counters + max_chunks;
-  a.rank = rank;
+  a.F = F;
   a.world = world;
   a.chunk = chunk_cols;
   a.nchunks = (int)nchunks;
+  a.max_chunks = max_chunks;
   a.epoch = epoch;
-  a.nP = max(1, grid * pct_partial / 100);
-  a.nR = max(1, grid * pct_reduce / 100);
-  a.nA = grid - a.nP - a.nR;
+  a.nP = max(1, per_rank * pct_partial / 100);
+  a.nR = max(1, per_rank * pct_reduce / 100);
+  a.nA = per_rank - a.nP - a.nR;
   if (a.nA < 1) {
     set_error("fused D1D: no CTAs left for the apply role");
     return RM_EINVAL;
   }
-  kern<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  kern<<<per_rank * nlocal, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
   RM_CHECK_LAUNCH("d1d_fused_kernel");
   return 0;
 }
@@ -912,10 +1009,37 @@ static int d1d_fused(const T* W, const T* G, T* out, int Lg, int L, int64_t d, i
       const double* M, double* M_mc, uint32_t* flags, uint32_t* flags_mc, uint32_t* counters,  \
       int rank, int world, int64_t chunk_cols, int max_chunks, uint32_t epoch, int pct_partial, \
       int pct_reduce, void* stream) {                                                           \
-    return d1d_fused<T>(reinterpret_cast<const T*>(W), reinterpret_cast<const T*>(G),           \
-                        reinterpret_cast<T*>(out), Lg, L, d, ldw, ldg, ldo, lr, absmax_bits, P, \
-                        P_mc, M, M_mc, flags, flags_mc, counters, rank, world, chunk_cols,      \
-                        max_chunks, epoch, pct_partial, pct_reduce, stream);                    \
+    if (P_mc == nullptr || M_mc == nullptr || flags_mc == nullptr) {                            \
+      set_error("invalid fused D1D arguments (multicast addresses)");                          \
+      return RM_EINVAL;                                                                         \
+    }                                                                                           \
+    D1DRank r{W, G, out, absmax_bits, P, M, flags, counters, Lg, rank};                         \
+    return d1d_fused<T>(&r, 1, L, d, ldw, ldg, ldo, lr,                                         \
+                        SymRef{reinterpret_cast<unsigned long long>(P_mc), nullptr, world},     \
+                        SymRef{reinterpret_cast<unsigned long long>(M_mc), nullptr, world},     \
+                        SymRef{reinterpret_cast<unsigned long long>(flags_mc), nullptr, world}, \
+                        world, chunk_cols, max_chunks, epoch, pct_partial, pct_reduce, stream); \
+  }                                                                                             \
+  extern "C" int rm_d1d_fused_p2p_##SUFFIX(                                                     \
+      const rm_d1d_rank* ranks, int nlocal, int L, int64_t d, int64_t ldw, int64_t ldg,         \
+      int64_t ldo, double lr, const uint64_t* P_peers, const uint64_t* M_peers,                 \
+      const uint64_t* flags_peers, int world, int64_t chunk_cols, int max_chunks,               \
+      uint32_t epoch, int pct_partial, int pct_reduce, void* stream) {                          \
+    if (ranks == nullptr || P_peers == nullptr || M_peers == nullptr || flags_peers == nullptr || \
+        nlocal < 1 || nlocal > kD1DMaxLocalRanks) {                                             \
+      set_error("invalid fused D1D arguments (peer tables / ranks)");                          \
+      return RM_EINVAL;                                                                         \
+    }                                                                                           \
+    D1DRank r[kD1DMaxLocalRanks];                                                               \
+    for (int i = 0; i < nlocal; i++)                                                            \
+      r[i] = D1DRank{ranks[i].W, ranks[i].G, ranks[i].out, ranks[i].absmax_bits, ranks[i].P,    \
+                     ranks[i].M, ranks[i].flags, ranks[i].counters, ranks[i].Lg, ranks[i].rank}; \
+    auto peer = [&](const uint64_t* t) {                                                        \
+      return SymRef{0, reinterpret_cast<const unsigned long long*>(t), world};                  \
+    };                                                                                          \
+    return d1d_fused<T>(r, nlocal, L, d, ldw, ldg, ldo, lr, peer(P_peers), peer(M_peers),       \
+                        peer(flags_peers), world, chunk_cols, max_chunks, epoch, pct_partial,   \
+                        pct_reduce, stream);                                                    \
   }
 RM_DEFINE_D1D_FUSED(f32, float, float)
 RM_DEFINE_D1D_FUSED(f64, double, double)

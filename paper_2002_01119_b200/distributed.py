@@ -159,12 +159,30 @@ class PeerMappedBuffers:
         self._opened = []
 
 
+def _peer_table(handle, device) -> torch.Tensor:
+    """Device uint64[world]: every rank's address of a symmetric buffer."""
+    off = int(getattr(handle, "offset", 0) or 0)
+    peers = np.array([int(p) + off for p in handle.buffer_ptrs], dtype=np.uint64)
+    return torch.from_numpy(peers.view(np.int64)).to(device)
+
+
+def _sym_addresses(handle, device) -> tuple[int, torch.Tensor | None]:
+    """(multicast address, None) when NVSwitch multicast is available, else
+    (0, peer table)."""
+    if handle.multicast_ptr:
+        return int(handle.multicast_ptr) + int(getattr(handle, "offset", 0) or 0), None
+    return 0, _peer_table(handle, device)
+
+
 class StepSync:
     """In-kernel ordering of consecutive learner-sharded steps (rm_step_sync): a flag in
     symmetric memory counts finished steps of all ranks; each step kernel waits for the
-    previous step of every rank and bumps every rank's flag when it is done (NVSwitch
-    multicast).  Replaces a host-issued barrier collective between steps.  Raises if
-    multicast is unavailable (callers fall back to the NCCL barrier)."""
+    previous step of every rank and bumps every rank's flag when it is done — through
+    NVSwitch multicast, or one unicast P2P atomic per rank (peer table) where multicast
+    is unavailable.  Replaces a host-issued barrier collective between steps.
+
+    Epochs advance only when a launch succeeded (`begin` / `commit`), so a rejected
+    launch does not leave every later wait target unreachable."""
 
     def __init__(self, group, device):
         import torch.distributed._symmetric_memory as symm_mem
@@ -175,26 +193,40 @@ class StepSync:
         self.flag = symm_mem.empty(4, dtype=torch.int32, device=device)
         self.flag.zero_()
         self.handle = symm_mem.rendezvous(self.flag, self.group.group_name)
-        if not self.handle.multicast_ptr:
-            raise RuntimeError("NVSwitch multicast (NVLS) is not available on this system")
+        self.mc, self.peers = _sym_addresses(self.handle, device)
         self.counter = torch.zeros(4, dtype=torch.int32, device=device)
         self.epoch = 0
         torch.cuda.synchronize(device)
         dist.barrier(group=self.group)   # every rank's flag is zero before any bump
 
-    def next(self) -> "_lib.StepSyncArgs":
-        self.epoch += 1
-        return self._args()
+    @property
+    def multicast(self) -> bool:
+        return bool(self.mc)
 
-    def _args(self) -> "_lib.StepSyncArgs":
-        return _lib.StepSyncArgs(self.flag.data_ptr(), self.handle.multicast_ptr,
-                                 self.counter.data_ptr(), self.epoch, self.world)
+    def begin(self) -> "_lib.StepSyncArgs":
+        """Arguments of the next step (epoch + 1); call `commit` once it launched."""
+        return self._args(self.epoch + 1)
+
+    def commit(self) -> None:
+        self.epoch += 1
+
+    def _args(self, epoch: int) -> "_lib.StepSyncArgs":
+        return _lib.StepSyncArgs(self.flag.data_ptr(), self.mc or None, self.counter.data_ptr(),
+                                 epoch, self.world,
+                                 None if self.peers is None else self.peers.data_ptr())
 
     def wait_all(self) -> None:
         """Stream-ordered: later work on the current stream starts once every rank
         finished the latest step (rm_step_sync_wait)."""
-        _lib.check(_lib.load().rm_step_sync_wait(ctypes.byref(self._args()),
+        _lib.check(_lib.load().rm_step_sync_wait(ctypes.byref(self._args(self.epoch)),
                                                  _lib.stream_ptr()), "rm_step_sync_wait")
+
+    def publish(self) -> None:
+        """Collective, stream-ordered: every rank's next step waits for the writes this
+        rank issued on the current stream before the call (rm_step_sync_publish)."""
+        _lib.check(_lib.load().rm_step_sync_publish(ctypes.byref(self.begin()),
+                                                    _lib.stream_ptr()), "rm_step_sync_publish")
+        self.commit()
 
 
 def _make_step_sync(group, device, enabled):
@@ -262,11 +294,19 @@ class LearnerShardedRing:
             dist.all_reduce(self._token, group=self.group)
 
     def settle(self):
-        """Order later work on the current stream after every rank's last step — needed
-        only before overwriting this rank's current W rows from outside the step (peers
-        may still be reading them); the outputs themselves are local."""
+        """Order later work on the current stream after every rank's last step (a reader
+        that must see the whole step of every rank; the local outputs alone need no
+        wait)."""
         if self.sync is not None:
             self.sync.wait_all()
+
+    def publish(self):
+        """Collective: call on every rank after writing this rank's current rows from
+        outside the step (initial weights, restore); the next step of every rank — whose
+        pulls read these rows — is ordered after the writes.  In-kernel ordering: a
+        stream-ordered flag bump (rm_step_sync_publish); otherwise a device sync and a
+        barrier."""
+        _publish(self)
 
     def step(self, left: torch.Tensor, right: torch.Tensor, G: torch.Tensor | None, lr: float,
              absmax: torch.Tensor | None = None, barrier: bool = True) -> torch.Tensor:
@@ -279,11 +319,14 @@ class LearnerShardedRing:
         if G is not None:
             mixing._same(src, G, "G")
         ldg = G.stride(0) if G is not None else self.ld
+        args = None if self.sync is None else self.sync.begin()
         _lib.check(self._fn(self.row_ptrs[self.cur].data_ptr(), src.data_ptr(), _lib.ptr(G),
                             dst.data_ptr(), self.L, self.row0, self.Lg, self.d, self.ld, ldg,
                             dst.stride(0), self.plan.data_ptr(), float(lr), _lib.ptr(absmax), s,
-                            None if self.sync is None else ctypes.byref(self.sync.next())),
+                            None if args is None else ctypes.byref(args)),
                    "rm_ring_mix_sgd_sharded")
+        if self.sync is not None:
+            self.sync.commit()
         self.cur = 1 - self.cur
         if barrier:
             self.barrier()
@@ -293,6 +336,14 @@ class LearnerShardedRing:
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)
         self.peers.close()
+
+
+def _publish(obj) -> None:
+    if obj.sync is not None:
+        obj.sync.publish()
+    else:
+        torch.cuda.synchronize(obj.device)
+        dist.barrier(group=obj.group)
 
 
 def _slot_table(layout: "ShardLayout", bases: list[int], ld: int, esz: int,
@@ -356,9 +407,17 @@ class LearnerShardedRingPos:
         return self.W[self.cur]
 
     def settle(self):
-        """Order later work on the current stream after every rank's last step."""
+        """Order later work on the current stream after every rank's last step (every rank
+        writes into this rank's slots): readers of the slots, and writers before they
+        overwrite them."""
         if self.sync is not None:   # (without it every step ends in a collective barrier)
             self.sync.wait_all()
+
+    def publish(self):
+        """Collective: after writing this rank's current slots from outside the step
+        (`settle` first), order every rank's next step — which reads the boundary slots —
+        after the writes."""
+        _publish(self)
 
     def barrier(self):
         """Step barrier on the stream (a no-op when the kernels order themselves)."""
@@ -378,12 +437,15 @@ class LearnerShardedRingPos:
         src = self.W[self.cur]
         if G is not None:
             mixing._same(src, G, "G")
+        args = None if self.sync is None else self.sync.begin()
         _lib.check(self._fn(self.slots[self.cur].data_ptr(), src.data_ptr(), _lib.ptr(G), self.L,
                             self.g0, self.Lg, self.d, self.ld,
                             G.stride(0) if G is not None else self.ld, self.plan.data_ptr(),
                             self.dest.data_ptr(), float(lr), _lib.ptr(absmax), s,
-                            None if self.sync is None else ctypes.byref(self.sync.next())),
+                            None if args is None else ctypes.byref(args)),
                    "rm_ring_mix_sgd_pos")
+        if self.sync is not None:
+            self.sync.commit()
         self.cur = 1 - self.cur
         if barrier:
             self.barrier()
@@ -527,8 +589,12 @@ class LearnerShardedD1DFused:
         self.hP = symm_mem.rendezvous(self.P, gname)
         self.hM = symm_mem.rendezvous(self.M, gname)
         self.hF = symm_mem.rendezvous(self.F, gname)
-        if not (self.hP.multicast_ptr and self.hM.multicast_ptr and self.hF.multicast_ptr):
-            raise RuntimeError("NVSwitch multicast (NVLS) is not available on this system")
+        # NVSwitch multicast when available (in-switch reduction), else peer tables
+        # (unicast NVLink loads / stores, rm_d1d_fused_p2p_*)
+        handles = (self.hP, self.hM, self.hF)
+        self.multicast = all(h.multicast_ptr for h in handles)
+        self._sym = [_sym_addresses(h, self.device) if self.multicast
+                     else (0, _peer_table(h, self.device)) for h in handles]
         self.counters = torch.zeros(2 * self.MAX_CHUNKS, dtype=torch.int32, device=self.device)
         quantum = 32 * self.world
         chunk_cols = int(os.environ.get("RINGMIX_D1D_FUSED_CHUNK", chunk_cols))
@@ -549,15 +615,28 @@ class LearnerShardedD1DFused:
     def step(self, W: torch.Tensor, G: torch.Tensor | None, lr: float, out: torch.Tensor,
              absmax: torch.Tensor | None = None) -> torch.Tensor:
         lib = _lib.load()
-        fn = getattr(lib, f"rm_d1d_fused_nvls_{mixing._suffix(W)}")
-        self.epoch += 1
-        _lib.check(fn(W.data_ptr(), _lib.ptr(G), out.data_ptr(), self.Lg, self.L, self.d,
-                      W.stride(0), G.stride(0) if G is not None else 0, out.stride(0),
-                      float(lr), _lib.ptr(absmax), self.P.data_ptr(), self.hP.multicast_ptr,
-                      self.M.data_ptr(), self.hM.multicast_ptr, self.F.data_ptr(),
-                      self.hF.multicast_ptr, self.counters.data_ptr(), self.rank, self.world,
-                      self.chunk, self.MAX_CHUNKS, self.epoch, self.split[0], self.split[1],
-                      _lib.stream_ptr()), "rm_d1d_fused_nvls")
+        sfx = mixing._suffix(W)
+        epoch = self.epoch + 1       # committed only once the launch succeeded
+        ldg = G.stride(0) if G is not None else 0
+        if self.multicast:
+            (pmc, _), (mmc, _), (fmc, _) = self._sym
+            _lib.check(getattr(lib, f"rm_d1d_fused_nvls_{sfx}")(
+                W.data_ptr(), _lib.ptr(G), out.data_ptr(), self.Lg, self.L, self.d, W.stride(0),
+                ldg, out.stride(0), float(lr), _lib.ptr(absmax), self.P.data_ptr(), pmc,
+                self.M.data_ptr(), mmc, self.F.data_ptr(), fmc, self.counters.data_ptr(),
+                self.rank, self.world, self.chunk, self.MAX_CHUNKS, epoch, self.split[0],
+                self.split[1], _lib.stream_ptr()), "rm_d1d_fused_nvls")
+        else:
+            r = _lib.D1DRank(W.data_ptr(), _lib.ptr(G), out.data_ptr(), _lib.ptr(absmax),
+                             self.P.data_ptr(), self.M.data_ptr(), self.F.data_ptr(),
+                             self.counters.data_ptr(), self.Lg, self.rank)
+            (_, pt), (_, mt), (_, ft) = self._sym
+            _lib.check(getattr(lib, f"rm_d1d_fused_p2p_{sfx}")(
+                ctypes.byref(r), 1, self.L, self.d, W.stride(0), ldg, out.stride(0), float(lr),
+                pt.data_ptr(), mt.data_ptr(), ft.data_ptr(), self.world, self.chunk,
+                self.MAX_CHUNKS, epoch, self.split[0], self.split[1], _lib.stream_ptr()),
+                "rm_d1d_fused_p2p")
+        self.epoch = epoch
         return out
 
 

@@ -6,8 +6,12 @@ Without a GPU those tests are skipped so `pytest tests/` stays green here.
 
 from __future__ import annotations
 
+import os
 import sys
 from pathlib import Path
+
+# a cross-rank wait that never completes (a test bug) gives up after 30 s, not 600 s
+os.environ.setdefault("RINGMIX_XGPU_TIMEOUT_S", "30")
 
 import pytest
 
