@@ -105,6 +105,10 @@ def parse(argv=None):
     ap.add_argument("--rewarm-seconds", type=float, default=0.4,
                     help="untimed steps right before the timed region (after the clock "
                          "sampler started) so the GPU is at its load clocks")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="capture the K timed steps (perm tables + mix launches) in one CUDA "
+                         "graph and time its replay; auto = on for one-GPU problems under "
+                         "1 GB per step (launch-bound sizes such as configs[0])")
     ap.add_argument("--event-every", type=int, default=4,
                     help="bracket every N-th mix launch with CUDA events (roofline timing)")
     return ap.parse_args(argv)
@@ -381,7 +385,8 @@ def nvlink_traffic(layout, L, d, esz, ws, perm, inv, left, right):
                 rd += sum(1 for x in nb if not b <= x < e)
             else:                        # position: 2 boundary rows in, relabel stores out
                 rd += 2 if ws > 1 else 0
-                nxt = inv[s + 1][perm[s, b:e]]
+                # slot x holds learner inv_k[x]; its output goes to slot p_{k+1}[inv_k[x]]
+                nxt = perm[s + 1][inv[s, b:e]]
                 wr += int(((nxt < b) | (nxt >= e)).sum())
         out.append((rd * d * esz / nsteps, wr * d * esz / nsteps))
     return out
@@ -563,34 +568,46 @@ def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None
     wl = Workload(spec, torch, dev, ws, rank, nsteps + args.e2e_steps + 64)
     stream = torch.cuda.current_stream()
     k = 0
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0.record(stream)
     for _ in range(Wm):
         wl.step(k)
         k += 1
+    w1.record(stream)
     torch.cuda.synchronize()
+    # re-warm: untimed steps right before the timed region, after the clock sampler's
+    # start-up sleep let the clocks drop.  The count is fixed up front and equal on every
+    # rank (the sharded steps order themselves across ranks: every rank must issue the
+    # same steps)
+    step_ms = max(w0.elapsed_time(w1) / Wm, 1e-3)
+    rewarm = int(min(3000, max(1, -(-args.rewarm_seconds * 1e3 // step_ms))))
+    if ws > 1:
+        t = torch.tensor([rewarm], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rewarm = int(t.item())
     if clocks:
         clocks.start()
         time.sleep(0.3)
-    # the sleep (nvidia-smi start-up) lets the clocks drop: bring them back to load
-    # levels with untimed steps right before the timed region (bounded by the amax slots)
-    t_end = time.perf_counter() + args.rewarm_seconds
-    rewarm = 0
-    while (time.perf_counter() < t_end or rewarm == 0) and rewarm < 3000:
+    for i in range(rewarm):
         wl.step(k)
         k += 1
-        rewarm += 1
-        if rewarm % 8 == 0:
+        if i % 8 == 7:
             torch.cuda.synchronize()
-    if ws > 1:      # the same number of re-warm steps on every rank (ordered step epochs)
-        t = torch.tensor([rewarm], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        while rewarm < int(t.item()):
-            wl.step(k)
-            k += 1
-            rewarm += 1
-    sampled = [i for i in range(K) if i % args.event_every == 0]
+    use_graph = use_graph_for(spec, args, ws)
+    sampled = [i for i in range(K) if i % args.event_every == 0] if not use_graph else []
     kev = {i: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for i in sampled}
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graph = None
+    if use_graph:
+        # the K timed steps captured once (perm-table launches + mix launches, PDL edges
+        # between consecutive mixes), replayed once untimed, then timed
+        wl.reset_tables()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for i in range(K):
+                wl.step(k + i)
+        graph.replay()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -601,17 +618,28 @@ def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None
     if clocks:
         clocks.mark(True)
     k_first = k
-    t_start.record(stream)
-    for i in range(K):
-        wl.step(k, kev.get(i))
-        k += 1
-    t_stop.record(stream)
+    if graph is not None:
+        t_start.record(stream)
+        graph.replay()
+        t_stop.record(stream)
+        # what the graph holds (the captured steps' launches)
+        wl.launches = {"perm": (K + wl.block - 1) // wl.block if spec.strategy == "rand_psgd"
+                       else 0, "mix": K, "barrier_allreduce": 0}
+        k += K
+    else:
+        t_start.record(stream)
+        for i in range(K):
+            wl.step(k, kev.get(i))
+            k += 1
+        t_stop.record(stream)
     torch.cuda.synchronize()
     if clocks:
         clocks.mark(False)
     c1 = nvc.read() if nvc else None
     elapsed_ms = t_start.elapsed_time(t_stop)
-    kern_ms = [a.elapsed_time(b) for a, b in kev.values()]
+    # per-launch kernel time: CUDA events around every event_every-th launch; in graph
+    # mode the replay time per step (mix + its share of the 1-per-64-steps perm launch)
+    kern_ms = [a.elapsed_time(b) for a, b in kev.values()] or [elapsed_ms / K]
     bits = wl.amax[:k].cpu().numpy().view(np.float64)
     if not np.all(np.isfinite(bits)):
         raise RuntimeError("non-finite weights in the benchmark run")
@@ -643,13 +671,38 @@ def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None
         "rewarm_steps": rewarm,
         "k_first": k_first,
         "nvlink_counted": (tx, rx) if tx >= 0 else None,
+        "graph": use_graph,
     }
     return res, wl
 
 
+def use_graph_for(spec, args, ws):
+    if args.graph == "off" or ws > 1:
+        return False
+    if args.graph == "on":
+        return True
+    return spec.learners * spec.dim * BYTES_PER_PARAM[spec.dtype] < (1 << 30)
+
+
+def ncu_nvlink(layout):
+    """The committed ncu NVLink capture of this layout's kernel (profiles/ncu_nvlink.json,
+    tools/pos_probe.py + tools/ncu_nvlink_summary.py): link bytes / payload bytes, and the
+    payload counted by the hardware / the traffic model."""
+    try:
+        z = json.loads((ROOT / "profiles" / "ncu_nvlink.json").read_text())[layout]
+        return z
+    except Exception:
+        return None
+
+
 def nvlink_object(spec, res, wl, ws, dev, mixing):
-    """Measured NVLink bytes (NVML counters, busiest rank) per step over the step time,
-    with the traffic model and the peaks beside them.  Rank 0."""
+    """NVLink bytes per step of the busiest rank over the step time, against 900 GB/s per
+    direction (NVLink 5) and the measured concurrent peer peaks.  Payload bytes come from
+    the traffic model, which the hardware counters pin: ncu's nvltx/nvlrx user-data bytes of
+    the same kernel equal the model (profiles/ncu_nvlink.json, ratio 1.000); link-level bytes
+    add the measured protocol overhead of that capture.  NVML's NVLink counters are not
+    supported on these B200s (NVML_ERROR_NOT_SUPPORTED), so the counts cannot be taken
+    inside this multi-process run.  Rank 0."""
     K = spec.steps
     L, d = spec.learners, spec.dim
     esz = BYTES_PER_PARAM[spec.dtype] // 3
@@ -667,8 +720,6 @@ def nvlink_object(spec, res, wl, ws, dev, mixing):
                     "achieved_tx": a_tx, "achieved_rx": a_rx,
                     "frac_nominal": max(a_tx, a_rx) / NVLINK_NOMINAL_GBS,
                     "frac_measured_peak": max(a_tx / pwr, a_rx / prd)})
-    else:
-        out["source"] = "NVML NVLink counters unavailable on this system: traffic model only"
     if not wl.uniform and spec.layout in ("learner", "position"):
         k0 = res["k_first"]
         if spec.strategy == "adpsgd_fixed":
@@ -681,13 +732,37 @@ def nvlink_object(spec, res, wl, ws, dev, mixing):
                                   host[3][:-1])
         rd = max(r for r, _ in per_rank)
         wr = max(w for _, w in per_rank)
-        out["model"] = {"read_bytes_per_step": rd, "write_bytes_per_step": wr,
-                        "achieved_read": rd / step_s / 1e9, "achieved_write": wr / step_s / 1e9,
-                        "note": "busiest rank's payload bytes per step (pull: distinct remote "
-                                "neighbour rows; position: 2 boundary rows read + relabel "
-                                "stores) over the step time"}
-        if "frac_nominal" not in out:
+        a_rd, a_wr = rd / step_s / 1e9, wr / step_s / 1e9
+        out["payload"] = {
+            "read_bytes_per_step": rd, "write_bytes_per_step": wr,
+            "achieved_read": a_rd, "achieved_write": a_wr,
+            "frac_measured_peak": max(a_rd / prd, a_wr / pwr),
+            "note": "busiest rank's payload per step (pull: distinct remote neighbour rows "
+                    "read; position: 2 boundary rows read + relabel stores to next-step slots "
+                    "on other GPUs) over the step time"}
+        nc = ncu_nvlink(spec.layout)
+        if nc is not None:
+            ltx = nc.get("link_over_user_tx") or 1.0
+            lrx = nc.get("link_over_user_rx") or 1.0
+            # reads also send request packets (TX) for the data they receive
+            link_tx = wr * ltx
+            link_rx = rd * lrx
+            out["link"] = {
+                "tx_bytes_per_step": link_tx, "rx_bytes_per_step": link_rx,
+                "achieved_tx": link_tx / step_s / 1e9, "achieved_rx": link_rx / step_s / 1e9,
+                "frac_nominal": max(link_tx, link_rx) / step_s / 1e9 / NVLINK_NOMINAL_GBS,
+                "link_over_payload": {"tx": ltx, "rx": lrx},
+                "counter_check": {"payload_counted_over_model_tx": nc.get("user_over_model_tx"),
+                                  "payload_counted_over_model_rx": nc.get("user_over_model_rx"),
+                                  "harness_tx_GBs": nc.get("tx_GBs"),
+                                  "harness_rx_GBs": nc.get("rx_GBs")},
+                "source": "payload x the link/payload byte ratio ncu counted (nvltx__bytes, "
+                          "nvlrx__bytes vs *_data_user) for this kernel in profiles/"
+                          "ncu_nvlink.json (single-process 2-GPU harness tools/pos_probe.py)"}
+            out["frac_nominal"] = out["link"]["frac_nominal"]
+        else:
             out["frac_nominal"] = max(rd, wr) / step_s / 1e9 / NVLINK_NOMINAL_GBS
+        out.setdefault("source", "traffic model pinned by ncu NVLink counters (see link)")
     return out
 
 
@@ -825,6 +900,9 @@ def run_ours(args):
                                      "mix_tma_kernel") + f" ({spec.strategy}, {spec.dtype})"),
                          "algorithmic_bytes_per_launch": res["algo_bytes"],
                          "avg_launch_ms": res["kern_avg_s"] * 1e3,
+                         "timing": ("CUDA-graph replay of the K steps / K (PDL between "
+                                    "consecutive mix launches)" if res["graph"] else
+                                    f"CUDA events around every {args.event_every}-th mix launch"),
                          "peak_source": res["peak_src"]},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -23,6 +23,9 @@
  *                                                              mixing.py:122-124
  *   rm_spsgd_*            <- step_spsgd                        simulation.py:251-260
  *   rm_*_host_f32         <- the same step on HOST buffers (H2D, kernel, D2H pipelined)
+ *   rm_gossip_step_dL_* / rm_gossip_step_host_dL_*
+ *                         <- the same step on the reference's own (d, L) C-order arrays
+ *                            (device or host), ring or uniform T   simulation.py:263-268
  *   rm_quadratic_grad_*   <- simulation.gradient_matrix with   simulation.py:226-238,
  *                            QuadraticObjective.stochastic_   objectives.py:84-90
  *                            gradient (bit-exact numpy normals)
@@ -73,9 +76,11 @@ const char* rm_last_error(void);
 int rm_version(void);
 int rm_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 /* For FFI callers without a CUDA runtime of their own (the reference's numpy code through
- * ctypes): a device buffer (e.g. the host-step workspace), and a stream synchronise. */
+ * ctypes): a device buffer (e.g. the host-step workspace), a stream-ordered copy in any
+ * direction (cudaMemcpyDefault), and a stream synchronise. */
 int rm_device_alloc(int64_t bytes, void** ptr);
 int rm_device_free(void* ptr);
+int rm_memcpy(void* dst, const void* src, int64_t bytes, void* stream);
 int rm_stream_synchronize(void* stream);
 /* Single-process multi-GPU: enable peer access between every pair of devices 0..ndev-1
  * (already-enabled pairs are fine; RM_ENOSYS if a pair has no P2P path). */
@@ -151,13 +156,41 @@ int rm_spsgd_bf16(const uint16_t* W, const uint16_t* G, uint16_t* Wout, int L, i
  * overlap); left/right: host int32[L].  The step is pipelined over column
  * chunks (H2D || kernel || D2H) through `workspace` (device, workspace_bytes;
  * rm_host_chunk_cols reports the chunk width it allows).  Stream-ordered on
- * `stream`; the host buffers must stay valid until it completes.  One call at a
- * time per device (the internal copy streams are shared).  G_host may be NULL. */
+ * `stream`; the host buffers must stay valid until it completes.  Every calling host
+ * thread has its own internal copy streams per device; concurrent calls need distinct
+ * workspaces.  G_host may be NULL. */
 int rm_host_chunk_cols(int L, int64_t workspace_bytes, int64_t* chunk_cols);
 int rm_ring_mix_sgd_host_f32(const float* W_host, const float* G_host, float* out_host,
                              const int32_t* left_host, const int32_t* right_host, int L, int64_t d,
                              double lr, void* workspace, int64_t workspace_bytes,
                              unsigned long long* absmax_bits, void* stream);
+
+/* ---- the reference's own array layout: (d, L) C-order ----
+ * simulation._gossip_step / apply_mixing on the arrays the reference holds
+ * (simulation.py:209, 263-268; mixing.py:106-125): W, G, W' are (d, L) row-major with
+ * row strides ldw / ldg / ldo >= L (elements); row r is coordinate r of every learner.
+ * left == right == NULL selects the uniform mean (D1D, mixing.py:122-124); otherwise
+ * the ring / ring[p, p] gather with neighbour tables as rm_ring_mix_sgd_*.  Same
+ * arithmetic and rounding as the learner-major kernels (no transpose anywhere). */
+int rm_gossip_step_dL_f32(const float* W, const float* G, float* out, const int32_t* left,
+                          const int32_t* right, int L, int64_t d, int64_t ldw, int64_t ldg,
+                          int64_t ldo, double lr, unsigned long long* absmax_bits, void* stream);
+int rm_gossip_step_dL_f64(const double* W, const double* G, double* out, const int32_t* left,
+                          const int32_t* right, int L, int64_t d, int64_t ldw, int64_t ldg,
+                          int64_t ldo, double lr, unsigned long long* absmax_bits, void* stream);
+/* The same on HOST (d, L) C-order arrays (dense rows, ld = L), e.g. the reference's
+ * numpy weights: contiguous row chunks H2D || kernel || D2H through `workspace` (device,
+ * >= 4096 + 9 * rows * L * sizeof(T) bytes for a chunk of `rows` rows); left/right are
+ * host int32[L] (or NULL for the uniform mean).  L <= 512.  Stream-ordered on `stream`;
+ * the host arrays must stay valid until it completes. */
+int rm_gossip_step_host_dL_f32(const float* W_host, const float* G_host, float* out_host,
+                               const int32_t* left_host, const int32_t* right_host, int L,
+                               int64_t d, double lr, void* workspace, int64_t workspace_bytes,
+                               unsigned long long* absmax_bits, void* stream);
+int rm_gossip_step_host_dL_f64(const double* W_host, const double* G_host, double* out_host,
+                               const int32_t* left_host, const int32_t* right_host, int L,
+                               int64_t d, double lr, void* workspace, int64_t workspace_bytes,
+                               unsigned long long* absmax_bits, void* stream);
 
 /* ---- learner-sharded multi-GPU path (one process per GPU) ----
  * CUDA IPC: export / map a peer process's device allocation (handles are

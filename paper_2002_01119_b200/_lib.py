@@ -34,6 +34,7 @@ _SIGNATURES = {
     "rm_device_alloc": ([i64, vp], i32),
     "rm_device_free": ([vp], i32),
     "rm_stream_synchronize": ([vp], i32),
+    "rm_memcpy": ([vp, vp, i64, vp], i32),
     "rm_enable_peer_access": ([i32], i32),
     "rm_perm_tables": ([vp, i32, u64, i32, i32, vp, vp, vp, vp, vp], i32),
     "rm_perm_sequential": ([vp, i32, u64, i32, i32, i32, vp, vp], i32),
@@ -71,6 +72,11 @@ _SIGNATURES = {
 _SIGNATURES["rm_pos_plan"] = ([vp, vp, i32, i32, i32, vp, vp, vp, vp], i32)
 _SIGNATURES["rm_step_sync_wait"] = ([vp, vp], i32)
 _SIGNATURES["rm_xgpu_status"] = ([vp], i32)
+for _sfx in ("f32", "f64"):
+    _SIGNATURES[f"rm_gossip_step_dL_{_sfx}"] = (
+        [vp, vp, vp, vp, vp, i32, i64, i64, i64, i64, dbl, vp, vp], i32)
+    _SIGNATURES[f"rm_gossip_step_host_dL_{_sfx}"] = (
+        [vp, vp, vp, vp, vp, i32, i64, dbl, vp, i64, vp, vp], i32)
 _SIGNATURES["rm_set_xgpu_timeout"] = ([dbl], i32)
 _SIGNATURES["rm_step_sync_publish"] = ([vp, vp], i32)
 _SIGNATURES["rm_p2p_mean_f64"] = ([vp, vp, i32, i64, i64, i32, vp], i32)

@@ -70,6 +70,18 @@ extern "C" int rm_device_free(void* ptr) {
   return 0;
 }
 
+extern "C" int rm_memcpy(void* dst, const void* src, int64_t bytes, void* stream) {
+  if ((dst == nullptr || src == nullptr) && bytes > 0) {
+    rm::set_error("null pointer");
+    return RM_EINVAL;
+  }
+  if (bytes <= 0) return 0;
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return rm::fail_cuda(e, "cudaMemcpyAsync");
+  return 0;
+}
+
 extern "C" int rm_stream_synchronize(void* stream) {
   cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return rm::fail_cuda(e, "cudaStreamSynchronize");

@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdarg.h>
+#include <stdlib.h>
+#include <utility>
 
 namespace rm {
 
@@ -112,6 +114,42 @@ __host__ inline void attr_done(unsigned long long* mask) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64) *mask |= 1ull << dev;
+}
+
+// ---- programmatic dependent launch (PDL) ----
+// A kernel launched with launch_pdl may start while the previous kernel on the
+// stream is still draining; it must call pdl_wait() before reading anything that
+// kernel may have written.  pdl_launch_dependents() lets the next kernel start
+// launching early (it still waits for this grid's completion in its pdl_wait).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// RINGMIX_PDL=0 launches without the programmatic-serialization attribute.
+__host__ inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* env = getenv("RINGMIX_PDL");
+    on = (env && env[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+__host__ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                                       size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ---- cross-GPU step ordering through flags in symmetric memory ----

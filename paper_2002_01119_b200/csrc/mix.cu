@@ -41,6 +41,12 @@ namespace rm {
 
 enum Mode { kRing = 0, kMean = 1, kSpsgd = 2 };
 
+// items per thread in flight in the output phase (build-time tuning knob)
+#ifndef RM_RING_UNROLL
+#define RM_RING_UNROLL 2
+#endif
+
+constexpr int kRingUnroll = RM_RING_UNROLL;
 constexpr int kRingThreads = 512;   // ring tiles: one 512-thread CTA per SM
 constexpr int kMeanThreads = 256;   // mean tiles: two 256-thread CTAs per SM
 constexpr int kStages = 3;
@@ -215,6 +221,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
+  // Programmatic dependent launch: everything above overlaps the previous kernel's
+  // tail; W, G and the neighbour tables may be its outputs, so wait for it here.
+  pdl_wait();
   if (MODE == kRing) {
     for (int j = tid; j < L; j += kThreads) {
       int x0 = a.left[j], x1 = j, x2 = a.right[j], t;
@@ -274,6 +283,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
 
     const int nv = (width + VEC - 1) / VEC;
     const int total = L << log2_nv;
+    // this CTA's last tile: let the next kernel on the stream start launching (it
+    // waits for this grid's completion before touching memory)
+    if (tid == 0 && t + stride >= a.ntiles) pdl_launch_dependents();
     mbar_wait(&full[s], parity);
 
     if (MODE != kRing) {
@@ -365,7 +377,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
 #pragma unroll
       for (int e = 0; e < VEC; e++) ma[e] = (A)mv[e];
     }
-#pragma unroll 2
+#pragma unroll kRingUnroll
     for (int idx = tid; idx < total; idx += kThreads) {
       const int j = idx >> log2_nv;
       const int v = idx & (nv_full - 1);
@@ -547,8 +559,9 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   }
   long long grid = (long long)sm_count(-1) * (512 / NT);
   if (grid > a.ntiles) grid = a.ntiles;
-  mix_tma_kernel<T, MODE, HAS_G, NT><<<(int)grid, NT, smem, st>>>(a, tmW, tmG);
-  RM_CHECK_LAUNCH("mix_tma_kernel");
+  cudaError_t e = launch_pdl(mix_tma_kernel<T, MODE, HAS_G, NT>, dim3((unsigned)grid), dim3(NT),
+                             smem, st, a, tmW, tmG);
+  if (e != cudaSuccess) return fail_cuda(e, "mix_tma_kernel");
   return RM_OK;
 }
 

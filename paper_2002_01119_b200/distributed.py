@@ -166,10 +166,15 @@ def _peer_table(handle, device) -> torch.Tensor:
     return torch.from_numpy(peers.view(np.int64)).to(device)
 
 
+def _use_multicast(handle) -> bool:
+    """NVSwitch multicast when the handle has it, unless RINGMIX_SYM_P2P=1 forces the
+    peer-table (unicast P2P) form (used by the multi-GPU checks to run both)."""
+    return bool(handle.multicast_ptr) and os.environ.get("RINGMIX_SYM_P2P", "0") != "1"
+
+
 def _sym_addresses(handle, device) -> tuple[int, torch.Tensor | None]:
-    """(multicast address, None) when NVSwitch multicast is available, else
-    (0, peer table)."""
-    if handle.multicast_ptr:
+    """(multicast address, None) when NVSwitch multicast is used, else (0, peer table)."""
+    if _use_multicast(handle):
         return int(handle.multicast_ptr) + int(getattr(handle, "offset", 0) or 0), None
     return 0, _peer_table(handle, device)
 
@@ -592,7 +597,7 @@ class LearnerShardedD1DFused:
         # NVSwitch multicast when available (in-switch reduction), else peer tables
         # (unicast NVLink loads / stores, rm_d1d_fused_p2p_*)
         handles = (self.hP, self.hM, self.hF)
-        self.multicast = all(h.multicast_ptr for h in handles)
+        self.multicast = all(_use_multicast(h) for h in handles)
         self._sym = [_sym_addresses(h, self.device) if self.multicast
                      else (0, _peer_table(h, self.device)) for h in handles]
         self.counters = torch.zeros(2 * self.MAX_CHUNKS, dtype=torch.int32, device=self.device)

@@ -297,6 +297,89 @@ def host_workspace(L: int, chunk_cols: int, device=None) -> torch.Tensor:
                        device=torch.device(device if device is not None else "cuda"))
 
 
+def _host_ptr(a):
+    """(pointer, dtype) of a C-contiguous host numpy array or CPU tensor."""
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or not a.is_contiguous():
+            raise ValueError("expected a contiguous host tensor")
+        return a.data_ptr(), {torch.float32: np.float32, torch.float64: np.float64}.get(a.dtype)
+    if not a.flags.c_contiguous:
+        raise ValueError("expected a C-contiguous (d, L) array")
+    return a.ctypes.data, a.dtype.type
+
+
+def workspace_dL(L: int, rows: int, dtype=np.float64, device=None) -> torch.Tensor:
+    """Device workspace for gossip_step_host: 3 slots x (W, G, W') chunks of `rows` rows."""
+    esz = np.dtype(dtype).itemsize
+    return torch.empty(4096 + 9 * rows * L * esz, dtype=torch.uint8,
+                       device=torch.device(device if device is not None else "cuda"))
+
+
+def gossip_step_host(W, G, lr: float, left=None, right=None, out=None, workspace=None,
+                     absmax: torch.Tensor | None = None, device=None, sync: bool = True):
+    """The step on the reference's own arrays: W, G host (d, L) C-order float64 or float32
+    (numpy arrays, or CPU tensors — pinned for overlap), returns `out` = apply_mixing(W, T)
+    - lr * G with T = ring[p, p] given by neighbour tables `left` / `right`, or the uniform
+    mean when both are None (simulation.py:263-268; mixing.py:106-125).  Row chunks go
+    H2D || kernel || D2H inside libringmix_b200 (rm_gossip_step_host_dL_*); nothing is
+    transposed.  G may be None (apply_mixing)."""
+    _lib.require_cuda()
+    wp, wdt = _host_ptr(W)
+    if wdt not in (np.float32, np.float64) or len(W.shape) != 2:
+        raise ValueError("W must be a (d, L) float32 or float64 host array")
+    d, L = W.shape
+    gp = None
+    if G is not None:
+        gp, gdt = _host_ptr(G)
+        if tuple(G.shape) != (d, L) or gdt is not wdt:
+            raise ValueError("G must match W (shape and dtype)")
+    if out is None:
+        out = np.empty((d, L), dtype=wdt)
+    op, odt = _host_ptr(out)
+    if tuple(out.shape) != (d, L) or odt is not wdt:
+        raise ValueError("out must match W (shape and dtype)")
+    if (left is None) != (right is None):
+        raise ValueError("give both neighbour tables or neither (uniform mean)")
+    tabs = None
+    if left is not None:
+        tabs = [np.ascontiguousarray(np.asarray(t.cpu() if isinstance(t, torch.Tensor) else t,
+                                                dtype=np.int32)) for t in (left, right)]
+        if any(t.shape != (L,) for t in tabs):
+            raise ValueError(f"neighbour tables must have {L} entries")
+    dev = torch.device(device if device is not None else "cuda")
+    if workspace is None:
+        workspace = workspace_dL(L, max(1, min(d, (1 << 24) // max(L, 1))), wdt, dev)
+    sfx = "f64" if wdt is np.float64 else "f32"
+    with torch.cuda.device(dev):
+        _lib.check(getattr(_lib.load(), f"rm_gossip_step_host_dL_{sfx}")(
+            wp, gp, op, None if tabs is None else tabs[0].ctypes.data,
+            None if tabs is None else tabs[1].ctypes.data, L, d, float(lr),
+            workspace.data_ptr(), workspace.numel(), _lib.ptr(absmax), _lib.stream_ptr()),
+            "rm_gossip_step_host_dL")
+        if sync:
+            torch.cuda.current_stream().synchronize()
+    return out
+
+
+def gossip_step_dL(W: torch.Tensor, G: torch.Tensor | None, lr: float, left=None, right=None,
+                   out: torch.Tensor | None = None, absmax: torch.Tensor | None = None):
+    """gossip_step_host on DEVICE (d, L) row-major tensors (unit column stride)."""
+    _lib.require_cuda(W)
+    if W.dim() != 2 or W.stride(1) != 1 or W.dtype not in (torch.float32, torch.float64):
+        raise ValueError("W must be a (d, L) float32/float64 CUDA tensor with unit column stride")
+    d, L = W.shape
+    if G is not None and (G.shape != W.shape or G.dtype != W.dtype or G.stride(1) != 1):
+        raise ValueError("G must match W")
+    if out is None:
+        out = torch.empty_like(W, memory_format=torch.contiguous_format)
+    sfx = "f64" if W.dtype == torch.float64 else "f32"
+    _lib.check(getattr(_lib.load(), f"rm_gossip_step_dL_{sfx}")(
+        W.data_ptr(), _lib.ptr(G), out.data_ptr(), _lib.ptr(left), _lib.ptr(right), L, d,
+        W.stride(0), G.stride(0) if G is not None else L, out.stride(0), float(lr),
+        _lib.ptr(absmax), _lib.stream_ptr()), "rm_gossip_step_dL")
+    return out
+
+
 # ----------------------------------------------------------------------------
 # apply_mixing (reference-facing, any T)
 # ----------------------------------------------------------------------------
@@ -337,7 +420,14 @@ def apply_mixing(W, T):
             f"size mismatch: W has {shape[1]} columns, T is {Tn.shape[0]}x{Tn.shape[0]}")
     _lib.require_cuda()
     L = Tn.shape[0]
-    if is_np:
+    if is_np and L <= 512:
+        # the reference's own (d, L) array: the (d, L) kernels take it as it is
+        W64 = np.ascontiguousarray(np.asarray(W, dtype=np.float64))
+        if np.all(Tn == 1.0 / L):
+            return gossip_step_host(W64, None, 0.0)
+        rs = ring_structure(Tn)
+        if rs is not None:
+            return gossip_step_host(W64, None, 0.0, rs[0], rs[1])
         X = torch.from_numpy(np.ascontiguousarray(np.asarray(W, dtype=np.float64).T)).cuda()
     else:
         X = W.T

@@ -47,6 +47,23 @@ def test_nvlink_traffic_reversal_moves_every_row():
     assert pos == [(2 * 4, 4 * 4), (2 * 4, 4 * 4)]
 
 
+def test_nvlink_traffic_position_layout_composes_the_permutations():
+    """Slot x of step k holds learner inv_k[x]; its output goes to slot p_{k+1}[inv_k[x]].
+    A 3-cycle relabelling (not an involution) tells p_{k+1}[inv_k[.]] from
+    inv_{k+1}[p_k[.]]."""
+    b = _bench()
+    p0 = [1, 2, 0, 3]          # learner l at position p0[l]
+    p1 = [0, 1, 2, 3]
+    perm, inv, left, right = _tables([p0, p1])
+    # 2 ranks: slots {0, 1} and {2, 3}; step 0 slot 0 holds learner 2 (-> slot 2, remote),
+    # slot 1 holds learner 0 (-> slot 0, local); slot 2 holds learner 1 (-> slot 1,
+    # remote), slot 3 holds learner 3 (local)
+    pos = b.nvlink_traffic("position", 4, 1, 4, 2, perm, inv, left[:1], right[:1])
+    assert pos == [(2 * 4, 1 * 4), (2 * 4, 1 * 4)]
+    expect = np.asarray(p1)[np.asarray(inv[0])]
+    assert list(expect) == [2, 0, 1, 3]
+
+
 def test_weak_scaling_only_for_coordinate_stripes():
     b = _bench()
     a = argparse.Namespace(layout="coord", scaling="weak", dim=100, learners=4,

@@ -116,3 +116,28 @@ def test_invalid_arguments_raise_value_error():
         mixing.permutation_for_step(4, -1, 1)
     with pytest.raises(TypeError):
         mixing.sample_permutation(4, np.random.default_rng(0))
+
+
+def test_stream_is_generator_compatible():
+    """seeding.stream(...) behaves like the reference's numpy Generator (seeding.py:35-37):
+    device permutations and device standard normals, then any other Generator method
+    (lognormal of the simulated clock, simulation.py:112; integers; normal) continues at
+    the same position on the host — the same numbers as numpy throughout."""
+    from paper_2002_01119_b200 import seeding
+    ent = (12345, seeding.TAG_CLOCK, 7)
+    ref = np.random.default_rng(np.random.SeedSequence(ent))
+    s = seeding.stream(*ent)
+    assert np.array_equal(s.permutation(16), ref.permutation(16))
+    assert np.array_equal(s.permutation(9), ref.permutation(9))      # buffered half carried
+    assert np.array_equal(s.lognormal(0.1, 0.5, 16), ref.lognormal(0.1, 0.5, 16))
+    assert np.array_equal(s.permutation(5), ref.permutation(5))      # now on the host
+    assert np.array_equal(s.integers(0, 100, 7), ref.integers(0, 100, 7))
+    # a fresh stream's large standard_normal runs on the device; later draws continue
+    ent2 = (3, seeding.TAG_GRADIENT, 11, 2)
+    ref2 = np.random.default_rng(np.random.SeedSequence(ent2))
+    s2 = seeding.stream(*ent2)
+    n = seeding.DeviceStream.DEVICE_NORMAL_MIN + 17
+    assert np.array_equal(s2.standard_normal(n), ref2.standard_normal(n))
+    assert np.array_equal(s2.standard_normal((3, 4)), ref2.standard_normal((3, 4)))
+    assert np.array_equal(s2.permutation(33), ref2.permutation(33))
+    assert s2.bit_generator.state == ref2.bit_generator.state

@@ -64,6 +64,20 @@ def main():
         torch.cuda.synchronize()
         ok_d1d = ok_d1d and bool(torch.equal(out3, outs[0]))
         nvls = f"{nvls} chunks; fused {len(fu.chunks)} chunks ok={bool(torch.equal(out3, outs[0]))}"
+        # the same fused step through peer tables (unicast NVLink, no multicast): the
+        # cross-rank sum runs in rank order, so it agrees to fp64 rounding of the sum
+        os.environ["RINGMIX_SYM_P2P"] = "1"
+        try:
+            fp = D.LearnerShardedD1DFused(L, d, ring.Lg, dev, chunk_cols=1 << 16)
+        finally:
+            os.environ.pop("RINGMIX_SYM_P2P", None)
+        out5 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
+        for _ in range(3):
+            fp.step(ring.weights, Gl, 0.01, out5)
+        torch.cuda.synchronize()
+        dd5 = (out5.double() - ref[b:e].double()).abs().max().item()
+        ok_d1d = ok_d1d and (not fp.multicast) and dd5 <= 2e-6
+        nvls += f"; fused-p2p maxdiff {dd5:.2e}"
         # no gradients (apply_mixing semantics): the fused kernel's HAS_G = false path
         out4 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
         fu.step(ring.weights, None, 0.01, out4)
@@ -86,6 +100,25 @@ def main():
     except RuntimeError as exc:
         nvls = str(exc)[:100]
     ring.close()
+    # the pull layout with peer-table step ordering (unicast atomics instead of multicast)
+    os.environ["RINGMIX_SYM_P2P"] = "1"
+    try:
+        ring2 = D.LearnerShardedRing(L, d, torch.float32)
+    finally:
+        os.environ.pop("RINGMIX_SYM_P2P", None)
+    ring2.W[0].copy_(full[b:e])
+    ring2.publish()
+    Wref2 = mixing.empty_learner_major(L, d, torch.float32, dev); Wref2.copy_(full)
+    for k in range(3):
+        lt, rt = simulation.rad_tables(L, 12345, k, dev)
+        out = ring2.step(lt, rt, Gl, 0.01)
+        Wref2 = mixing.ring_mix_sgd(Wref2, mixing.empty_learner_major(L, d, torch.float32, dev).copy_(Gf), 0.01, lt, rt)
+    ring2.settle()
+    torch.cuda.synchronize()
+    same = bool(torch.equal(ring2.weights, Wref2[b:e]))
+    pull_steps.append(same and ring2.sync is not None and not ring2.sync.multicast)
+    ok &= pull_steps[-1]
+    ring2.close()
     # RAD in ring-position order (push layout): 3 steps vs the single-GPU reference
     pos = D.LearnerShardedRingPos(L, d, torch.float32)
     tabs = mixing.permutation_tables(L, 12345, 0, 4, dev)

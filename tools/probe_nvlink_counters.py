@@ -18,6 +18,28 @@ c = [NvlinkCounters(i) for i in range(2)]
 for i, x in enumerate(c):
     print(json.dumps({"gpu": i, "ok": x.ok, "method": x.method, "links": x.links,
                       "error": getattr(x, "error", None)}), flush=True)
+# raw NVML return codes of the candidate fields on link 0 / scope 0
+try:
+    import pynvml as nv
+    nv.nvmlInit()
+    h = nv.nvmlDeviceGetHandleByIndex(0)
+    for fid in (202, 204, 138, 139, 140, 141):
+        v = nv.nvmlDeviceGetFieldValues(h, [(fid, 0)])[0]
+        print(json.dumps({"field": fid, "ret": int(v.nvmlReturn), "type": int(v.valueType),
+                          "ull": int(v.value.ullVal)}), flush=True)
+    try:
+        print(json.dumps({"util_counter_link0": str(nv.nvmlDeviceGetNvLinkUtilizationCounter(
+            h, 0, 0))}), flush=True)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"util_counter_error": str(e)}), flush=True)
+except Exception as e:  # noqa: BLE001
+    print(json.dumps({"nvml_error": str(e)}), flush=True)
+for args in (["nvlink", "-gt", "r", "-i", "0"], ["nvlink", "-s", "-i", "0"]):
+    try:
+        print("---- nvidia-smi " + " ".join(args) + "\n" + subprocess.run(
+            ["nvidia-smi"] + args, capture_output=True, text=True, timeout=30).stdout[:1500])
+    except Exception as e:  # noqa: BLE001
+        print(e)
 try:
     smi0 = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", "0"], capture_output=True,
                           text=True, timeout=30).stdout
