@@ -45,6 +45,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -126,12 +130,14 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// RINGMIX_PDL=0 launches without the programmatic-serialization attribute.
+// RINGMIX_PDL=1 launches with the programmatic-serialization attribute.  Off by
+// default: measured on B200 it made consecutive mix launches slower (C1, CUDA graph:
+// 39.9 vs 33.8 us per step; C2 3.31 vs 3.18 ms — profiles/r2_mix_ab2).
 __host__ inline bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* env = getenv("RINGMIX_PDL");
-    on = (env && env[0] == '0') ? 0 : 1;
+    on = (env && env[0] == '1') ? 1 : 0;
   }
   return on == 1;
 }

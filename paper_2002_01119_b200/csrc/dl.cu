@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kDLThreads) mix_dL_kernel(DLArgs a) {
   const int L = a.L, R = a.R;
   int4* s_tri = reinterpret_cast<int4*>(smem);
   double* s_mean = reinterpret_cast<double*>(s_tri + L);
-  T* s_w = reinterpret_cast<T*>(s_mean + R);
+  T* s_w = reinterpret_cast<T*>(s_mean + ((R + 1) & ~1));   // 16-byte aligned rows
   const T* W = static_cast<const T*>(a.W);
   const T* G = static_cast<const T*>(a.G);
   T* out = static_cast<T*>(a.out);
@@ -115,7 +115,7 @@ static int launch_dL(DLArgs a, cudaStream_t st) {
   if (R < 1) R = 1;
   if (R > 1024) R = 1024;
   a.R = R;
-  const size_t smem = (size_t)a.L * sizeof(int4) + (size_t)R * sizeof(double) +
+  const size_t smem = (size_t)a.L * sizeof(int4) + (size_t)((R + 1) & ~1) * sizeof(double) +
                       (size_t)R * a.L * esz;
   auto kern = a.G ? mix_dL_kernel<T, MEAN, true> : mix_dL_kernel<T, MEAN, false>;
   static unsigned long long attr_mask = 0;

@@ -208,3 +208,22 @@ def test_trace_stats_are_deterministic(no_tma, monkeypatch):
         again = simulation.trace_stats(X.T, oracle)
         for x, y in zip(first, again):
             assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("impl", ["", "barrier"])
+@pytest.mark.parametrize("L,d", [(16, 1000), (64, 100_003), (128, 2_049), (200, 3_001),
+                                 (256, 1_025), (300, 777), (1000, 65)])
+def test_trace_stats_every_kernel_and_many_learners(L, d, impl, monkeypatch):
+    """Warp-specialised (default, L <= 256), one-barrier (L <= 128) and generic kernels
+    against the reference's formulas, including L > 128 (numpy's recursive pairwise mean;
+    run_training with more than 128 learners)."""
+    if impl:
+        monkeypatch.setenv("RINGMIX_TRACE_IMPL", impl)
+    oracle = objectives.quadratic_oracle(d, condition_number=3.0, noise_scale=0.0, seed=L)
+    X = mixing.empty_learner_major(L, d, torch.float32, "cuda").normal_()
+    cons, loss_col, avg = simulation.trace_stats(X.T, oracle)
+    W = X.double().cpu().numpy().T                       # (d, L) as the reference holds it
+    dev = W - W.mean(axis=1, keepdims=True)
+    np.testing.assert_allclose(cons.cpu().numpy(), (dev * dev).sum(axis=0), rtol=1e-11)
+    np.testing.assert_allclose(loss_col.cpu().numpy(), oracle.loss_columns(W), rtol=1e-11)
+    assert float(avg) == pytest.approx(oracle.loss(W.mean(axis=1)), rel=1e-11)
