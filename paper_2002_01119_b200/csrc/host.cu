@@ -182,8 +182,12 @@ static int host_dL(const T* W_host, const T* G_host, T* out_host, const int32_t*
                    const int32_t* right_host, int L, int64_t d, double lr, void* workspace,
                    int64_t workspace_bytes, unsigned long long* absmax_bits, void* stream) {
   const bool mean = left_host == nullptr && right_host == nullptr;
+  if (!mean && L < 3) {
+    set_error("degenerate ring topology: need at least 3 learners, got %d", L);
+    return RM_EINVAL;
+  }
   if (W_host == nullptr || out_host == nullptr || workspace == nullptr || L < 1 || L > 512 ||
-      d < 0 || (!mean && (left_host == nullptr || right_host == nullptr || L < 3))) {
+      d < 0 || (!mean && (left_host == nullptr || right_host == nullptr))) {
     set_error("invalid host (d, L) step arguments (L=%d)", L);
     return RM_EINVAL;
   }

@@ -1054,15 +1054,27 @@ RM_DEFINE_D1D_FUSED(bf16, uint16_t, __nv_bfloat16)
 // GPU owns it (P2P store in the epilogue).  The FMA chain still runs in
 // ascending learner id, so the step is bit-identical to the single-GPU step.
 namespace rm {
+// Optional placement tables (NULL = identity, slot x holds position x): with a
+// placement, global slot s (rank s / Lg, row s % Lg) holds ring position
+// pos_of_slot[s], and position q lives in slot slot_of_pos[q]; every rank's slots
+// hold a contiguous arc of positions, so a step still reads exactly two remote
+// boundary rows.  slot_of_pos_next is the placement of step k + 1.
 __global__ void pos_plan_kernel(const int32_t* __restrict__ inv_k,
                                 const int32_t* __restrict__ perm_next, int L, int g0, int Lg,
                                 const uint64_t* __restrict__ next_slot_ptrs,
-                                int32_t* __restrict__ plan, uint64_t* __restrict__ dest) {
+                                int32_t* __restrict__ plan, uint64_t* __restrict__ dest,
+                                const int32_t* __restrict__ pos_tab,
+                                const int32_t* __restrict__ sop_tab,
+                                const int32_t* __restrict__ sop_next) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int xl = (g0 - 1 + L) % L, xr = (g0 + Lg) % L;
+  auto pos_of_slot = [&](int sl) { return pos_tab ? pos_tab[sl] : sl; };
+  auto slot_of_pos = [&](int q) { return sop_tab ? sop_tab[q] : q; };
+  // the arc's outer neighbours: left of the first slot's position, right of the last's
+  const int xl = slot_of_pos((pos_of_slot(g0) - 1 + L) % L);
+  const int xr = slot_of_pos((pos_of_slot(g0 + Lg - 1) + 1) % L);
   const bool local_l = xl >= g0 && xl < g0 + Lg, local_r = xr >= g0 && xr < g0 + Lg;
   if (i == 0) {
-    // remote boundary positions (0, 1 or 2 of them) in the plan's remote list
+    // remote boundary slots (0, 1 or 2 of them) in the plan's remote list
     int R = 0;
     if (!local_l) plan[1 + R++] = xl;
     if (!local_r && xr != xl) plan[1 + R++] = xr;
@@ -1074,7 +1086,7 @@ __global__ void pos_plan_kernel(const int32_t* __restrict__ inv_k,
     if (y == xl && !local_l) return Lg;
     return Lg + (local_l ? 0 : 1);
   };
-  const int x = g0 + i;
+  const int x = pos_of_slot(g0 + i);
   int p[3] = {(x - 1 + L) % L, x, (x + 1) % L};
   int id[3] = {inv_k[p[0]], inv_k[p[1]], inv_k[p[2]]};
   // sort by learner id (the reference's FMA order), carrying positions
@@ -1085,11 +1097,126 @@ __global__ void pos_plan_kernel(const int32_t* __restrict__ inv_k,
         t = p[v]; p[v] = p[v + 1]; p[v + 1] = t;
       }
   int32_t* tri = plan + 1 + 2 * Lg + 4 * i;
-  tri[0] = staged(p[0]);
-  tri[1] = staged(p[1]);
-  tri[2] = staged(p[2]);
+  tri[0] = staged(slot_of_pos(p[0]));
+  tri[1] = staged(slot_of_pos(p[1]));
+  tri[2] = staged(slot_of_pos(p[2]));
   tri[3] = i;
-  dest[i] = next_slot_ptrs[perm_next[inv_k[x]]];
+  const int qn = perm_next[inv_k[x]];
+  dest[i] = next_slot_ptrs[sop_next ? sop_next[qn] : qn];
+}
+
+// Placement of step k + 1 for the ring-position layout (L % world == 0, Lg = L / world):
+// the ring of step k + 1 is cut into `world` arcs of Lg consecutive positions starting
+// at a rotation r, and arc a goes to rank sigma(a).  Any choice gives the same result
+// (the mix only sees neighbour relations); the one chosen keeps the most learners on
+// the rank that computes their output, which is what the relabelling stores move over
+// NVLink.  One CTA, thread r scores rotation r: counts[a][g] = learners whose next
+// position falls in arc a and whose current slot is on rank g; the best arc -> rank
+// assignment (exhaustive for world <= 5, greedy above) maximises the learners that stay.
+// Deterministic (ties: smallest r, first assignment), so every rank computes the same.
+constexpr int kPlMaxWorld = 8;
+
+__device__ __forceinline__ int score_assignment(const int* cnt, int n, int* sigma) {
+  int best = -1;
+  if (n <= 5) {
+    int perm[5] = {0, 1, 2, 3, 4};
+    // lexicographic enumeration (next_permutation)
+    for (;;) {
+      int sc = 0;
+      for (int a = 0; a < n; a++) sc += cnt[a * kPlMaxWorld + perm[a]];
+      if (sc > best) {
+        best = sc;
+        for (int a = 0; a < n; a++) sigma[a] = perm[a];
+      }
+      int i = n - 2;
+      while (i >= 0 && perm[i] >= perm[i + 1]) i--;
+      if (i < 0) break;
+      int j = n - 1;
+      while (perm[j] <= perm[i]) j--;
+      int t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+      for (int lo = i + 1, hi = n - 1; lo < hi; lo++, hi--) {
+        t = perm[lo]; perm[lo] = perm[hi]; perm[hi] = t;
+      }
+    }
+    return best;
+  }
+  bool used_a[kPlMaxWorld] = {}, used_g[kPlMaxWorld] = {};
+  best = 0;
+  for (int step = 0; step < n; step++) {
+    int ba = -1, bg = -1, bv = -1;
+    for (int a = 0; a < n; a++) {
+      if (used_a[a]) continue;
+      for (int g = 0; g < n; g++) {
+        if (used_g[g]) continue;
+        if (cnt[a * kPlMaxWorld + g] > bv) { bv = cnt[a * kPlMaxWorld + g]; ba = a; bg = g; }
+      }
+    }
+    used_a[ba] = used_g[bg] = true;
+    sigma[ba] = bg;
+    best += bv;
+  }
+  return best;
+}
+
+__global__ void pos_placement_kernel(const int32_t* __restrict__ inv_k,
+                                     const int32_t* __restrict__ perm_next,
+                                     const int32_t* __restrict__ sop_k, int L, int n,
+                                     int32_t* __restrict__ pos_next, int32_t* __restrict__ sop_next,
+                                     int32_t* __restrict__ moved) {
+  extern __shared__ int sh[];
+  int* owner = sh;           // [L] rank holding learner l at step k
+  int* qn = owner + L;       // [L] position of learner l at step k + 1
+  int* score = qn + L;       // [blockDim] best score of rotation r
+  int* sig = score + blockDim.x;   // [blockDim] packed sigma (3 bits per arc)
+  __shared__ int s_best_r, s_best_sig;
+  const int Lg = L / n;
+  const int tid = threadIdx.x;
+  for (int q = tid; q < L; q += blockDim.x) {
+    const int l = inv_k[q];
+    owner[l] = (sop_k ? sop_k[q] : q) / Lg;
+    qn[l] = perm_next[l];
+  }
+  __syncthreads();
+  for (int r = tid; r < L; r += blockDim.x) {
+    int cnt[kPlMaxWorld * kPlMaxWorld];
+    for (int i = 0; i < kPlMaxWorld * kPlMaxWorld; i++) cnt[i] = 0;
+    for (int l = 0; l < L; l++) {
+      const int a = ((qn[l] - r + L) % L) / Lg;
+      cnt[a * kPlMaxWorld + owner[l]]++;
+    }
+    int sigma[kPlMaxWorld];
+    const int sc = score_assignment(cnt, n, sigma);
+    int packed = 0;
+    for (int a = 0; a < n; a++) packed |= sigma[a] << (3 * a);
+    if (r < (int)blockDim.x) { score[r] = sc; sig[r] = packed; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int br = 0;
+    for (int r = 1; r < min(L, (int)blockDim.x); r++)
+      if (score[r] > score[br]) br = r;
+    s_best_r = br;
+    s_best_sig = sig[br];
+  }
+  __syncthreads();
+  const int r = s_best_r, packed = s_best_sig;
+  for (int q = tid; q < L; q += blockDim.x) {
+    const int u = (q - r + L) % L;
+    const int a = u / Lg;
+    const int slot = ((packed >> (3 * a)) & 7) * Lg + u % Lg;
+    sop_next[q] = slot;
+    pos_next[slot] = q;
+  }
+  if (moved != nullptr) {
+    __syncthreads();
+    for (int g = tid; g < n; g += blockDim.x) moved[g] = 0;
+    __syncthreads();
+    for (int l = tid; l < L; l += blockDim.x) {
+      const int u = (qn[l] - r + L) % L;
+      const int dst = (packed >> (3 * (u / Lg))) & 7;
+      if (dst != owner[l]) atomicAdd(&moved[owner[l]], 1);
+    }
+  }
 }
 }  // namespace rm
 
@@ -1102,8 +1229,45 @@ extern "C" int rm_pos_plan(const int32_t* inv_k, const int32_t* perm_next, int L
     return RM_EINVAL;
   }
   pos_plan_kernel<<<(Lg + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      inv_k, perm_next, L, g0, Lg, next_slot_ptrs, plan, dest);
+      inv_k, perm_next, L, g0, Lg, next_slot_ptrs, plan, dest, nullptr, nullptr, nullptr);
   RM_CHECK_LAUNCH("pos_plan_kernel");
+  return 0;
+}
+
+extern "C" int rm_pos_plan_placed(const int32_t* inv_k, const int32_t* perm_next,
+                                  const int32_t* pos_of_slot, const int32_t* slot_of_pos,
+                                  const int32_t* slot_of_pos_next, int L, int g0, int Lg,
+                                  const uint64_t* next_slot_ptrs, int32_t* plan, uint64_t* dest,
+                                  void* stream) {
+  if (inv_k == nullptr || perm_next == nullptr || next_slot_ptrs == nullptr || plan == nullptr ||
+      dest == nullptr || pos_of_slot == nullptr || slot_of_pos == nullptr ||
+      slot_of_pos_next == nullptr || L < 4 || Lg < 1 || g0 < 0 || g0 + Lg > L) {
+    set_error("invalid position-plan arguments (L=%d g0=%d Lg=%d)", L, g0, Lg);
+    return RM_EINVAL;
+  }
+  pos_plan_kernel<<<(Lg + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      inv_k, perm_next, L, g0, Lg, next_slot_ptrs, plan, dest, pos_of_slot, slot_of_pos,
+      slot_of_pos_next);
+  RM_CHECK_LAUNCH("pos_plan_kernel");
+  return 0;
+}
+
+extern "C" int rm_pos_placement(const int32_t* inv_k, const int32_t* perm_next,
+                                const int32_t* slot_of_pos, int L, int world,
+                                int32_t* pos_of_slot_next, int32_t* slot_of_pos_next,
+                                int32_t* moved, void* stream) {
+  if (inv_k == nullptr || perm_next == nullptr || pos_of_slot_next == nullptr ||
+      slot_of_pos_next == nullptr || world < 1 || world > kPlMaxWorld || L < world ||
+      L % world != 0 || L > 1024) {
+    set_error("invalid placement arguments (L=%d world=%d; need L %% world == 0, world <= %d, "
+              "L <= 1024)", L, world, kPlMaxWorld);
+    return RM_EINVAL;
+  }
+  const int threads = L < 1024 ? ((L + 31) / 32) * 32 : 1024;
+  const size_t smem = (2 * (size_t)L + 2 * (size_t)threads) * sizeof(int);
+  pos_placement_kernel<<<1, threads, smem, static_cast<cudaStream_t>(stream)>>>(
+      inv_k, perm_next, slot_of_pos, L, world, pos_of_slot_next, slot_of_pos_next, moved);
+  RM_CHECK_LAUNCH("pos_placement_kernel");
   return 0;
 }
 

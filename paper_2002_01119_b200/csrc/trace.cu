@@ -211,6 +211,12 @@ __global__ void __launch_bounds__(kTrThreads, 2)
 
   // phase A of the tile in local slot `it`: wait for its stage, column means
   // (numpy pairwise order) and the average-model loss into buffer it & 1
+  // Phase A split over every warp: lane l < 16 of a warp sums numpy's chains 0-3 of
+  // column col, lane l + 16 chains 4-7 of the same column; the halves meet with one
+  // shuffle in numpy's order ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)).  (One thread per
+  // column left half the warps idle in this phase while the others did both phases:
+  // ncu showed barrier stalls first, profiles/r2_trace_c2_onebarrier_ncu.json.)
+  const int a_lane = tid & 15, a_half = (tid >> 4) & 1, a_warp = tid >> 5;
   auto phase_a = [&](long long t, int it) {
     const int st = it % kTrStages;
     const long long c0 = t * cw;
@@ -218,32 +224,46 @@ __global__ void __launch_bounds__(kTrThreads, 2)
     const T* sW = reinterpret_cast<const T*>(stages + (size_t)st * stage_bytes);
     double* cm = s_cols + (it & 1) * 3 * cw;
     mbar_wait(&full[st], (it / kTrStages) & 1);
-    for (int col = tid; col < width; col += kTrThreads) {
+    for (int cb = a_warp * 16; cb < width; cb += kTrThreads / 2) {
+      const int col = cb + a_lane;
+      const bool live = col < width;
+      double lm = 0.0, wo = 0.0;
+      if (has_obj && live && a_half == 0) {   // issued first: latency under the sums
+        lm = lam[c0 + col];
+        wo = wopt[c0 + col];
+      }
       double res;
       if (L < 8) {
         res = -0.0;
-        for (int i = 0; i < L; i++) res = __dadd_rn(res, (double)E::lds(sW + sidx(i, col)));
+        if (a_half == 0 && live)
+          for (int i = 0; i < L; i++) res = __dadd_rn(res, (double)E::lds(sW + sidx(i, col)));
       } else {
         const int n8 = L - (L % 8);
-        double r[8];
-#pragma unroll
-        for (int k = 0; k < 8; k++) r[k] = (double)E::lds(sW + sidx(k, col));
+        const int k0 = a_half * 4;
+        const int cc = live ? col : 0;
+        double r0 = (double)E::lds(sW + sidx(k0, cc)), r1 = (double)E::lds(sW + sidx(k0 + 1, cc));
+        double r2 = (double)E::lds(sW + sidx(k0 + 2, cc)), r3 = (double)E::lds(sW + sidx(k0 + 3, cc));
         for (int i = 8; i < n8; i += 8) {
-#pragma unroll
-          for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], (double)E::lds(sW + sidx(i + k, col)));
+          r0 = __dadd_rn(r0, (double)E::lds(sW + sidx(i + k0, cc)));
+          r1 = __dadd_rn(r1, (double)E::lds(sW + sidx(i + k0 + 1, cc)));
+          r2 = __dadd_rn(r2, (double)E::lds(sW + sidx(i + k0 + 2, cc)));
+          r3 = __dadd_rn(r3, (double)E::lds(sW + sidx(i + k0 + 3, cc)));
         }
-        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (int i = n8; i < L; i++) res = __dadd_rn(res, (double)E::lds(sW + sidx(i, col)));
+        const double h = __dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3));
+        const double other = __shfl_xor_sync(0xffffffffu, h, 16);
+        res = __dadd_rn(h, other);                 // lane < 16: X + Y in numpy's order
+        if (a_half == 0 && live)
+          for (int i = n8; i < L; i++) res = __dadd_rn(res, (double)E::lds(sW + sidx(i, col)));
       }
-      const double mean = __ddiv_rn(res, (double)L);
-      cm[col] = mean;
-      if (has_obj) {
-        const double lm = lam[c0 + col], wo = wopt[c0 + col];
-        cm[cw + col] = lm;
-        cm[2 * cw + col] = wo;
-        const double dm = __dsub_rn(mean, wo);
-        a_sum += 0.5 * lm * dm * dm;
+      if (a_half == 0 && live) {
+        const double mean = __ddiv_rn(res, (double)L);
+        cm[col] = mean;
+        if (has_obj) {
+          cm[cw + col] = lm;
+          cm[2 * cw + col] = wo;
+          const double dm = __dsub_rn(mean, wo);
+          a_sum += 0.5 * lm * dm * dm;
+        }
       }
     }
   };
@@ -340,284 +360,6 @@ __global__ void __launch_bounds__(kTrThreads, 2)
   }
 }
 
-// Warp-specialised variant (the default for 16-byte aligned rows, L <= 256): the
-// TMA stage ring feeds two consumer roles that never meet at a CTA barrier —
-//   producer warp  : one thread issues the [L x cw] tile loads (full[s] mbarriers)
-//   4 column warps : phase A — each thread owns columns, computes their means in
-//                    numpy's pairwise order (8 chains) plus the average-model loss
-//                    term, and publishes mean / lam / w* into a double-buffered
-//                    column buffer (mfull[b])
-//   8 learner warps: phase B — every thread folds its fixed (row, 16-byte vector)
-//                    items into per-learner register sums as soon as the tile and its
-//                    column buffer are ready, then releases both (empty[s], mempty[b])
-// so phase A of later tiles runs while phase B of earlier ones does (the one-barrier
-// version kept the CTA in lockstep: ncu showed barrier stalls as the top reason and the
-// column warps doing both phases as the critical path).  W crosses HBM once.
-constexpr int kWsA = 128, kWsB = 256;
-constexpr int kWsThreads = 32 + kWsA + kWsB;
-constexpr int kWsStages = 5;
-constexpr int kWsMaxL = 256;
-
-template <typename T>
-__device__ __forceinline__ double column_sum_staged(const T* sW, int col, int L, int lg_bc,
-                                                    int box_stride, int box_c) {
-  using E = Elem<T>;
-  auto at = [&](int r) -> double {
-    return (double)E::lds(sW + (col >> lg_bc) * box_stride + (r << lg_bc) + (col & (box_c - 1)));
-  };
-  if (L < 8) {
-    double res = -0.0;
-    for (int i = 0; i < L; i++) res = __dadd_rn(res, at(i));
-    return res;
-  }
-  if (L <= 128) {
-    const int n8 = L - (L % 8);
-    double r[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) r[k] = at(k);
-    for (int i = 8; i < n8; i += 8) {
-#pragma unroll
-      for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], at(i + k));
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (int i = n8; i < L; i++) res = __dadd_rn(res, at(i));
-    return res;
-  }
-  return pairwise_sum<double>(at, 0, L);   // numpy's recursion for n > 128
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kWsThreads, 1)
-    trace_ws_kernel(const __grid_constant__ CUtensorMap tmW, int L, long long d, int cw,
-                    int lg_nv, long long ntiles, const double* __restrict__ lam,
-                    const double* __restrict__ wopt, double* __restrict__ part) {
-  using E = Elem<T>;
-  constexpr int VEC = E::VEC;
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + kWsStages;
-  uint64_t* mfull = empty + kWsStages;
-  uint64_t* mempty = mfull + 2;
-  double* s_cols = reinterpret_cast<double*>(smem + 256);   // [2][3][cw]
-  double* s_red = s_cols + 6 * cw;                          // [4] column-warp loss sums
-  unsigned char* stages = reinterpret_cast<unsigned char*>(s_red + 4);
-  stages += (128 - ((uintptr_t)stages & 127)) & 127;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int stage_bytes = L * cw * (int)sizeof(T);
-  const bool has_obj = lam != nullptr;
-  const int box_c = cw < 256 ? cw : 256;
-  const int lg_bc = __ffs(box_c) - 1;
-  const int box_stride = L << lg_bc;
-  auto sidx = [&](int r, int c) -> int {
-    return (c >> lg_bc) * box_stride + (r << lg_bc) + (c & (box_c - 1));
-  };
-  if (tid == 0) {
-    tma_prefetch_desc(&tmW);
-    for (int st = 0; st < kWsStages; st++) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], (kWsA + kWsB) / 32);
-    }
-    for (int b = 0; b < 2; b++) {
-      mbar_init(&mfull[b], kWsA / 32);
-      mbar_init(&mempty[b], kWsB / 32);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const long long first = blockIdx.x, stride = gridDim.x;
-  double a_sum = 0.0;
-  double acc_c[kTrItems], acc_l[kTrItems];
-#pragma unroll
-  for (int k = 0; k < kTrItems; k++) acc_c[k] = acc_l[k] = 0.0;
-  const int nv_full = 1 << lg_nv;
-
-  if (warp == 0) {
-    // ---- producer ----
-    if (lane == 0) {
-      int it = 0;
-      for (long long t = first; t < ntiles; t += stride, ++it) {
-        const int st = it % kWsStages;
-        if (it >= kWsStages) mbar_wait(&empty[st], ((it / kWsStages) - 1) & 1);
-        mbar_arrive_expect_tx(&full[st], (uint32_t)stage_bytes);
-        T* dst = reinterpret_cast<T*>(stages + (size_t)st * stage_bytes);
-        for (int cc = 0; cc < cw; cc += box_c)
-          tma_load_2d(dst + sidx(0, cc), &tmW, (int)(t * cw + cc), 0, &full[st]);
-      }
-    }
-  } else if (warp <= kWsA / 32) {
-    // ---- column warps: means, lam, w*, average-model loss ----
-    const int ta = tid - 32;
-    int it = 0;
-    for (long long t = first; t < ntiles; t += stride, ++it) {
-      const int st = it % kWsStages, b = it & 1;
-      const long long c0 = t * cw;
-      const int width = (int)min((long long)cw, d - c0);
-      const T* sW = reinterpret_cast<const T*>(stages + (size_t)st * stage_bytes);
-      double* cm = s_cols + b * 3 * cw;
-      mbar_wait(&full[st], (it / kWsStages) & 1);
-      if (it >= 2) mbar_wait(&mempty[b], ((it >> 1) - 1) & 1);
-      for (int col = ta; col < width; col += kWsA) {
-        const double mean =
-            __ddiv_rn(column_sum_staged<T>(sW, col, L, lg_bc, box_stride, box_c), (double)L);
-        cm[col] = mean;
-        if (has_obj) {
-          const double lm = lam[c0 + col], wo = wopt[c0 + col];
-          cm[cw + col] = lm;
-          cm[2 * cw + col] = wo;
-          const double dm = __dsub_rn(mean, wo);
-          a_sum += 0.5 * lm * dm * dm;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&mfull[b]);
-        mbar_arrive(&empty[st]);
-      }
-    }
-  } else {
-    // ---- learner warps: per-learner consensus / loss sums ----
-    const int tb = tid - 32 - kWsA;
-    const int v = tb & (nv_full - 1);
-    const int row0 = tb >> lg_nv, row_step = kWsB >> lg_nv;
-    const int c = v * VEC;
-    int it = 0;
-    for (long long t = first; t < ntiles; t += stride, ++it) {
-      const int st = it % kWsStages, b = it & 1;
-      const int width = (int)min((long long)cw, d - t * cw);
-      const T* sW = reinterpret_cast<const T*>(stages + (size_t)st * stage_bytes);
-      const double* cm = s_cols + b * 3 * cw;
-      mbar_wait(&full[st], (it / kWsStages) & 1);
-      mbar_wait(&mfull[b], (it >> 1) & 1);
-      if (c < width) {
-        double m[VEC], lm[VEC], wo[VEC];
-#pragma unroll
-        for (int e = 0; e < VEC; e += 2) {
-          const double2 a2 = *reinterpret_cast<const double2*>(cm + c + e);
-          m[e] = a2.x;
-          m[e + 1] = a2.y;
-          if (has_obj) {
-            const double2 l2 = *reinterpret_cast<const double2*>(cm + cw + c + e);
-            const double2 w2 = *reinterpret_cast<const double2*>(cm + 2 * cw + c + e);
-            lm[e] = l2.x;
-            lm[e + 1] = l2.y;
-            wo[e] = w2.x;
-            wo[e + 1] = w2.y;
-          } else {
-            lm[e] = lm[e + 1] = wo[e] = wo[e + 1] = 0.0;
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < kTrItems; k++) {
-          const int j = row0 + k * row_step;
-          if (j < L) {
-            Vec<T> x;
-            x.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
-            double vv = 0.0, qq = 0.0;
-#pragma unroll
-            for (int e = 0; e < VEC; e++) {
-              if (c + e < width) {
-                const double w = (double)E::ld(x.e(), e);
-                const double dv = w - m[e];
-                vv += dv * dv;
-                const double dw = w - wo[e];
-                qq += lm[e] * dw * dw;
-              }
-            }
-            acc_c[k] += vv;
-            acc_l[k] += qq;
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty[st]);
-        mbar_arrive(&mempty[b]);
-      }
-    }
-  }
-  // deterministic in-CTA reduction (every stage has been consumed: the producer issued
-  // no load that was not waited for)
-  __syncthreads();
-  double* s_acc = reinterpret_cast<double*>(stages);  // [kWsB][kTrItems][2]
-  if (warp > kWsA / 32) {
-    const int tb = tid - 32 - kWsA;
-#pragma unroll
-    for (int k = 0; k < kTrItems; k++) {
-      s_acc[(tb * kTrItems + k) * 2] = acc_c[k];
-      s_acc[(tb * kTrItems + k) * 2 + 1] = acc_l[k];
-    }
-  } else if (warp >= 1) {
-    for (int o = 16; o > 0; o >>= 1) a_sum += __shfl_xor_sync(0xffffffffu, a_sum, o);
-    if (lane == 0) s_red[warp - 1] = a_sum;
-  }
-  __syncthreads();
-  const int row_step = kWsB >> lg_nv;
-  double* out = part + (long long)blockIdx.x * (2 * L + 1);
-  for (int j = tid; j < L; j += kWsThreads) {
-    const int k = j / row_step, r = j % row_step;
-    double cs = 0.0, q = 0.0;
-    for (int vv = 0; vv < nv_full; vv++) {
-      const int owner = (r << lg_nv) | vv;
-      cs += s_acc[(owner * kTrItems + k) * 2];
-      q += s_acc[(owner * kTrItems + k) * 2 + 1];
-    }
-    out[j] = cs;
-    out[L + j] = has_obj ? 0.5 * q : 0.0;
-  }
-  if (tid == 0) {
-    double tsum = 0.0;
-    for (int w = 0; w < kWsA / 32; w++) tsum += s_red[w];
-    out[2 * L] = has_obj ? tsum : 0.0;
-  }
-}
-
-template <typename T>
-static int trace_stats_ws(const T* W, int L, int64_t d, int64_t ld, const double* lam,
-                          const double* wopt, double* part, int* nparts, cudaStream_t st,
-                          bool* covered) {
-  using E = Elem<T>;
-  constexpr int VEC = E::VEC;
-  const size_t esz = sizeof(T);
-  *covered = false;
-  // stage ~32 KB: exactly kTrItems (row, vector) items per learner-warp thread
-  int cw = VEC;
-  while ((size_t)(cw * 2) * L * esz <= (size_t)kTrStageTarget && cw * 2 <= 2048) cw *= 2;
-  int nv = cw / VEC, lg = 0;
-  while ((1 << lg) < nv) lg++;
-  if ((long long)L * nv > (long long)kTrItems * kWsB || nv > kWsB || L > kWsMaxL) return 0;
-  const int box_c = cw < 256 ? cw : 256;
-  CUtensorMap tm;
-  if (!tma_map_2d<T>(&tm, W, d, L, ld, box_c, L)) return 0;
-  const size_t stage = (size_t)L * cw * esz;
-  size_t smem = 256 + 6 * (size_t)cw * 8 + 4 * 8 + 128 + (size_t)kWsStages * stage;
-  const size_t red = (size_t)kWsB * kTrItems * 2 * 8;   // final reduction reuses the stages
-  if (kWsStages * stage < red) smem += red - kWsStages * stage;
-  static int max_optin = -1;
-  if (max_optin < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  }
-  if (smem > (size_t)max_optin) return 0;
-  static unsigned long long attr_mask = 0;
-  if (attr_needed(&attr_mask)) {
-    cudaError_t e = cudaFuncSetAttribute(trace_ws_kernel<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
-    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(trace_ws_kernel)");
-    attr_done(&attr_mask);
-  }
-  *covered = true;
-  const long long ntiles = (d + cw - 1) / cw;
-  long long grid = sm_count(-1);
-  if (grid > ntiles) grid = ntiles;
-  *nparts = (int)grid;
-  trace_ws_kernel<T><<<(int)grid, kWsThreads, smem, st>>>(tm, L, d, cw, lg, ntiles, lam, wopt,
-                                                          part);
-  RM_CHECK_LAUNCH("trace_ws_kernel");
-  return 0;
-}
-
 template <typename T>
 static int trace_stats_tma(const T* W, int L, int64_t d, int64_t ld, const double* lam,
                            const double* wopt, double* part, int* nparts, cudaStream_t st,
@@ -682,17 +424,10 @@ static int trace_stats(const T* W, int L, int64_t d, int64_t ld, const double* l
   constexpr int VEC = Elem<T>::VEC;
   const bool aligned = ((reinterpret_cast<uintptr_t>(W) | (uintptr_t)(ld * sizeof(T))) & 15) == 0;
   bool covered = false;
-  const char* impl = getenv("RINGMIX_TRACE_IMPL");   // "barrier": the one-barrier kernel
-  if (aligned && d >= VEC && d < (1LL << 31) && L <= kWsMaxL && tma_encode_fn() != nullptr &&
+  if (aligned && d >= VEC && d < (1LL << 31) && L <= kTrMaxL && tma_encode_fn() != nullptr &&
       getenv("RINGMIX_TRACE_NO_TMA") == nullptr) {
-    if (impl == nullptr || impl[0] != 'b') {
-      const int rc = trace_stats_ws<T>(W, L, d, ld, lam, wopt, part, &nparts, st, &covered);
-      if (rc != 0) return rc;
-    }
-    if (!covered && L <= 128) {
-      const int rc = trace_stats_tma<T>(W, L, d, ld, lam, wopt, part, &nparts, st, &covered);
-      if (rc != 0) return rc;
-    }
+    const int rc = trace_stats_tma<T>(W, L, d, ld, lam, wopt, part, &nparts, st, &covered);
+    if (rc != 0) return rc;
   }
   if (!covered) {
     long long blocks = (d + kTrThreads - 1) / kTrThreads;

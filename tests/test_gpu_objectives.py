@@ -210,15 +210,15 @@ def test_trace_stats_are_deterministic(no_tma, monkeypatch):
             assert torch.equal(x, y)
 
 
-@pytest.mark.parametrize("impl", ["", "barrier"])
-@pytest.mark.parametrize("L,d", [(16, 1000), (64, 100_003), (128, 2_049), (200, 3_001),
-                                 (256, 1_025), (300, 777), (1000, 65)])
-def test_trace_stats_every_kernel_and_many_learners(L, d, impl, monkeypatch):
-    """Warp-specialised (default, L <= 256), one-barrier (L <= 128) and generic kernels
-    against the reference's formulas, including L > 128 (numpy's recursive pairwise mean;
-    run_training with more than 128 learners)."""
-    if impl:
-        monkeypatch.setenv("RINGMIX_TRACE_IMPL", impl)
+@pytest.mark.parametrize("no_tma", ["", "1"])
+@pytest.mark.parametrize("L,d", [(5, 333), (9, 4097), (16, 1000), (64, 100_003), (128, 2_049),
+                                 (200, 3_001), (256, 1_025), (300, 777), (1000, 65)])
+def test_trace_stats_every_kernel_and_many_learners(L, d, no_tma, monkeypatch):
+    """Tiled TMA kernel (L <= 128; numpy's chains split over lane halves) and the generic
+    kernel against the reference's formulas, including L > 128 (numpy's recursive pairwise
+    mean; run_training with more than 128 learners)."""
+    if no_tma:
+        monkeypatch.setenv("RINGMIX_TRACE_NO_TMA", no_tma)
     oracle = objectives.quadratic_oracle(d, condition_number=3.0, noise_scale=0.0, seed=L)
     X = mixing.empty_learner_major(L, d, torch.float32, "cuda").normal_()
     cons, loss_col, avg = simulation.trace_stats(X.T, oracle)
