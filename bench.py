@@ -615,6 +615,10 @@ def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None
     wl.launches = {key: 0 for key in wl.launches}
     wl.reset_tables()   # the timed region generates its own tables
     c0 = nvc.read() if nvc else None
+    placed = getattr(wl.sharded, "placed", False)
+    if placed:     # per-step learners leaving each rank (the relabelling stores)
+        wl.sharded.moved_log = []
+        wl.sharded.log_moves = True
     if clocks:
         clocks.mark(True)
     k_first = k
@@ -636,6 +640,10 @@ def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None
     if clocks:
         clocks.mark(False)
     c1 = nvc.read() if nvc else None
+    moved = None
+    if placed:
+        wl.sharded.log_moves = False
+        moved = torch.stack(wl.sharded.moved_log).cpu().numpy() if wl.sharded.moved_log else None
     elapsed_ms = t_start.elapsed_time(t_stop)
     # per-launch kernel time: CUDA events around every event_every-th launch; in graph
     # mode the replay time per step (mix + its share of the 1-per-64-steps perm launch)
@@ -672,6 +680,7 @@ def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None
         "k_first": k_first,
         "nvlink_counted": (tx, rx) if tx >= 0 else None,
         "graph": use_graph,
+        "moved": moved,
     }
     return res, wl
 
@@ -728,8 +737,14 @@ def nvlink_object(spec, res, wl, ws, dev, mixing):
         else:
             tb = mixing.permutation_tables(L, SEED, k0, K + 1, dev)
             host = [t.cpu().numpy().astype(np.int64) for t in (tb.perm, tb.inv, tb.left, tb.right)]
-        per_rank = nvlink_traffic(spec.layout, L, d, esz, ws, host[0], host[1], host[2][:-1],
-                                  host[3][:-1])
+        if spec.layout == "position" and res.get("moved") is not None:
+            # arc placement: the relabelling stores each rank issued (rm_pos_placement's count)
+            mv = res["moved"].astype(np.float64).mean(axis=0)
+            per_rank = [(2 * d * esz, m * d * esz) for m in mv]
+            out["placement"] = {"kind": "rotate", "moved_rows_per_step_per_rank": mv.tolist()}
+        else:
+            per_rank = nvlink_traffic(spec.layout, L, d, esz, ws, host[0], host[1],
+                                      host[2][:-1], host[3][:-1])
         rd = max(r for r, _ in per_rank)
         wr = max(w for _, w in per_rank)
         a_rd, a_wr = rd / step_s / 1e9, wr / step_s / 1e9
@@ -817,19 +832,26 @@ def run_ours(args):
         # mixing.ring_mix_sgd_host -> rm_ring_mix_sgd_host_f32.  The resident-W variant
         # (only G crosses PCIe) is reported beside it.
         ms_res = run_e2e_resident(args, spec, torch, wl, dev)
-        ms_host, e2e_cols = None, 0
+        ms_host, ms_lm, e2e_cols = None, None, 0
         if not uniform:
             budget = min(24 << 30, host_pinned_budget() // ws)
             e2e_cols = min(wl.cols, max(32, (budget // (3 * L * 4)) // 32 * 32))
             ms_host = run_e2e(args, spec, torch, dev, cols=e2e_cols)
+            release_pinned(torch)
+            ms_lm = run_e2e(args, spec, torch, dev, cols=e2e_cols, layout="learner")
+            release_pinned(torch)
         if ws > 1:
-            t = torch.tensor([ms_res, ms_host or 0.0], device=dev)
+            t = torch.tensor([ms_res, ms_host or 0.0, ms_lm or 0.0], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_res, ms_host = float(t[0]), (float(t[1]) if ms_host else None)
+            ms_res = float(t[0])
+            ms_host, ms_lm = (float(t[1]), float(t[2])) if ms_host else (None, None)
         resident = e2e_resident_line(args, spec, ms_res, ws, wl)
         if ms_host:
             e2e = e2e_line(args, spec, ms_host, ws, e2e_cols)
             e2e["resident_variant"] = resident
+            lm = e2e_line(args, spec, ms_lm, ws, e2e_cols, layout="learner")
+            e2e["learner_major_variant"] = {k: lm[k] for k in ("value", "unit", "ms_per_step",
+                                                               "path")}
         else:
             e2e = resident
     elif want_e2e:
@@ -1026,45 +1048,60 @@ def run_e2e_sharded(args, torch, wl, dev, k0):
     return a.elapsed_time(e) / args.e2e_steps
 
 
-def run_e2e(args, spec, torch, dev, cols=None):
-    """Step through the host-buffer API (W, G pinned host -> W' host) for this
-    rank's column stripe (`cols`, default: the whole problem); returns ms/step."""
+def run_e2e(args, spec, torch, dev, cols=None, layout="dL"):
+    """Step through the host-buffer API for this rank's stripe of `cols` coordinates
+    (default: the whole problem); returns ms/step.  layout "dL": the reference's own
+    (d, L) C-order arrays (mixing.gossip_step_host -> rm_gossip_step_host_dL_f32, contiguous
+    row chunks); "learner": learner-major (L, d) host buffers (mixing.ring_mix_sgd_host ->
+    rm_ring_mix_sgd_host_f32, column chunks)."""
     from paper_2002_01119_b200 import mixing as M
 
     L = spec.learners
     d = spec.dim if cols is None else cols
-    Wh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
-    Gh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
-    Oh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
+    shape = (d, L) if layout == "dL" else (L, d)
+    Wh = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+    Gh = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+    Oh = torch.empty(shape, dtype=torch.float32, pin_memory=True)
     # synthetic host inputs, drawn on the device and copied once (a host RNG is ~100x
     # slower and torchrun runs ranks single-threaded)
     g = torch.Generator(device=dev).manual_seed(7)
+    step_rows = max(1, (1 << 26) // shape[1])
     for host in (Wh, Gh):
-        for r in range(L):
-            host[r].copy_(torch.randn(d, generator=g, device=dev))
-    ws_buf = M.host_workspace(L, 1 << 20, dev)
+        for r0 in range(0, shape[0], step_rows):
+            r1 = min(shape[0], r0 + step_rows)
+            host[r0:r1].copy_(torch.randn((r1 - r0, shape[1]), generator=g, device=dev))
     tabs = M.permutation_tables(L, SEED, 0, args.e2e_steps + 1, dev)
     left = tabs.left.cpu()
     right = tabs.right.cpu()
     stream = torch.cuda.current_stream()
-    # warm-up call
-    M.ring_mix_sgd_host(Wh, Gh, LR, left[0], right[0], out_host=Oh, workspace=ws_buf, sync=True)
+    if layout == "dL":
+        ws_buf = M.workspace_dL(L, max(1, (1 << 24) // L), np.float32, dev)
+
+        def call(src, dst, k, sync):
+            M.gossip_step_host(src, Gh, LR, left[k], right[k], out=dst, workspace=ws_buf,
+                               sync=sync)
+    else:
+        ws_buf = M.host_workspace(L, 1 << 20, dev)
+
+        def call(src, dst, k, sync):
+            M.ring_mix_sgd_host(src, Gh, LR, left[k], right[k], out_host=dst, workspace=ws_buf,
+                                sync=sync)
+    call(Wh, Oh, 0, True)        # warm-up call
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     src, dst = Wh, Oh
     torch.cuda.synchronize()
     a.record(stream)
     for k in range(args.e2e_steps):
-        M.ring_mix_sgd_host(src, Gh, LR, left[k], right[k], out_host=dst, workspace=ws_buf,
-                            sync=False)
+        call(src, dst, k, False)
         src, dst = dst, src
     b.record(stream)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / args.e2e_steps
 
 
-def e2e_line(args, spec, ms, ws, cols=None):
+def e2e_line(args, spec, ms, ws, cols=None, layout="dL"):
     """The step on host buffers: W, G from pinned host memory and W' back every step
-    (12 B/param over PCIe); `cols` columns per rank (default: the whole problem)."""
+    (12 B/param over PCIe); `cols` coordinates per rank (default: the whole problem)."""
     L = spec.learners
     d = total_dim(spec, ws) if cols is None else cols * ws
     sample = None if cols is None or cols * ws == total_dim(spec, ws) else (
@@ -1074,10 +1111,12 @@ def e2e_line(args, spec, ms, ws, cols=None):
             "h2d_bytes_per_step": 2 * L * d * 4 + 2 * L * 4 * ws,
             "d2h_bytes_per_step": L * d * 4,
             "ms_per_step": ms, "steps": args.e2e_steps,
-            "path": "reference-facing call on host buffers: mixing.ring_mix_sgd_host -> "
-                    "rm_ring_mix_sgd_host_f32 (pinned host W, G -> W'; chunked H2D || kernel "
-                    "|| D2H)" + (f"; every rank its column stripe, max over {ws} ranks"
-                                 if ws > 1 else ""),
+            "path": (("reference-facing call on the reference's own (d, L) C-order host arrays: "
+                      "mixing.gossip_step_host -> rm_gossip_step_host_dL_f32 (pinned host W, G "
+                      "-> W'; contiguous row chunks H2D || kernel || D2H)") if layout == "dL"
+                     else ("learner-major (L, d) host buffers: mixing.ring_mix_sgd_host -> "
+                           "rm_ring_mix_sgd_host_f32 (column chunks)"))
+                    + (f"; every rank its column stripe, max over {ws} ranks" if ws > 1 else ""),
             **({"sample": sample} if sample else {})}
 
 
@@ -1097,6 +1136,13 @@ def e2e_resident_line(args, spec, ms, ws, wl):
                      "stream, double-buffered, and max|W'| (the divergence metric) D2H" + (
                          f"; every rank its column stripe, max over {ws} ranks"
                          if ws > 1 else ""))}
+
+
+def release_pinned(torch):
+    """Return cached pinned host blocks to the OS (the e2e variants use large buffers)."""
+    fn = getattr(torch._C, "_host_emptyCache", None)
+    if fn is not None:
+        fn()
 
 
 def free_port() -> int:

@@ -287,6 +287,22 @@ int rm_ring_mix_sgd_sharded_bf16(const uint64_t* row_ptrs, const uint16_t* W_loc
  * single-GPU step) and writes every output straight to its next-step slot. */
 int rm_pos_plan(const int32_t* inv_k, const int32_t* perm_next, int L, int g0, int Lg,
                 const uint64_t* next_slot_ptrs, int32_t* plan, uint64_t* dest, void* stream);
+/* Placed ring-position layout: global slot s (rank s / Lg, row s % Lg) holds ring position
+ * pos_of_slot[s] and position q lives in slot slot_of_pos[q] (device int32[L] each; every
+ * rank's slots hold a contiguous arc of positions), slot_of_pos_next is step k+1's
+ * placement.  rm_pos_plan is the identity placement (slot x = position x). */
+int rm_pos_plan_placed(const int32_t* inv_k, const int32_t* perm_next, const int32_t* pos_of_slot,
+                       const int32_t* slot_of_pos, const int32_t* slot_of_pos_next, int L, int g0,
+                       int Lg, const uint64_t* next_slot_ptrs, int32_t* plan, uint64_t* dest,
+                       void* stream);
+/* Placement of step k+1 (L % world == 0, world <= 8, L <= 1024): the rotation of the arcs
+ * and the arc -> rank assignment that keep the most learners on the rank computing their
+ * output (fewest relabelling stores over NVLink), given step k's placement slot_of_pos
+ * (NULL = identity), inv_k and perm_next.  Deterministic: every rank computes the same.
+ * moved (optional, device int32[world]): learners leaving each rank in this relabelling. */
+int rm_pos_placement(const int32_t* inv_k, const int32_t* perm_next, const int32_t* slot_of_pos,
+                     int L, int world, int32_t* pos_of_slot_next, int32_t* slot_of_pos_next,
+                     int32_t* moved, void* stream);
 int rm_ring_mix_sgd_pos_f32(const uint64_t* slot_ptrs, const float* W_local, const float* G_local,
                             int L, int g0, int Lg, int64_t d, int64_t ldw, int64_t ldg,
                             const int32_t* plan, const uint64_t* dest, double lr,

@@ -70,6 +70,8 @@ _SIGNATURES = {
     "rm_column_mean_bf16": ([vp, i32, i64, i64, vp, vp], i32),
 }
 _SIGNATURES["rm_pos_plan"] = ([vp, vp, i32, i32, i32, vp, vp, vp, vp], i32)
+_SIGNATURES["rm_pos_plan_placed"] = ([vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp], i32)
+_SIGNATURES["rm_pos_placement"] = ([vp, vp, vp, i32, i32, vp, vp, vp, vp], i32)
 _SIGNATURES["rm_step_sync_wait"] = ([vp, vp], i32)
 _SIGNATURES["rm_xgpu_status"] = ([vp], i32)
 for _sfx in ("f32", "f64"):

@@ -364,16 +364,20 @@ def _slot_table(layout: "ShardLayout", bases: list[int], ld: int, esz: int,
 class LearnerShardedRingPos:
     """RAD with learners stored in ring-POSITION order (SURVEY §8(e) "push").
 
-    Rank g owns ring positions [g0, g0+Lg); at step k its slot x holds the learner
-    at position x of p_k.  The mix reads only the two boundary slots from the
-    neighbouring ranks, and each output is stored straight into the learner's
-    slot for step k+1 (p_{k+1}[l]) on whichever rank owns it — so a step moves
-    ~Lg (n-1)/n + 2 rows over NVLink per rank instead of the ~2 Lg (n-1)/n the
-    learner-ordered pull needs.  Bit-identical to the single-GPU step.
+    Rank g owns Lg slots; at step k they hold a contiguous arc of ring positions of p_k
+    (slot i: position ``slot_positions()[i]``, learner ``slot_learners(inv_k)[i]``).  The
+    mix reads only the two boundary slots from the neighbouring ranks, and each output is
+    stored straight into the learner's slot for step k+1 on whichever rank owns it — so a
+    step moves ~Lg (n-1)/n + 2 rows over NVLink per rank instead of the ~2 Lg (n-1)/n the
+    learner-ordered pull needs.  Where the arcs of step k+1 start and which rank gets which
+    arc is free (the mix only sees neighbour relations): with equal shards every step picks
+    the rotation and arc -> rank assignment that keeps the most learners on the rank that
+    computes them (``rm_pos_placement``, deterministic on every rank; ~15 % fewer
+    relabelling stores than slot x = position x).  Bit-identical to the single-GPU step.
     """
 
     def __init__(self, L: int, d: int, dtype=torch.float32, group=None, device=None,
-                 step_sync: bool = True):
+                 step_sync: bool = True, placement: str | None = None):
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed must be initialised")
         _lib.require_cuda()
@@ -402,6 +406,18 @@ class LearnerShardedRingPos:
         self.cur = 0
         self._fn = getattr(lib, f"rm_ring_mix_sgd_pos_{mixing._suffix(self.W[0])}")
         self.sync = _make_step_sync(group, self.device, step_sync)
+        # arc placement (rotation + arc -> rank per step, chosen to keep learners local):
+        # needs equal shards; RINGMIX_POS_PLACEMENT=fixed keeps slot x = position x
+        if placement is None:
+            placement = os.environ.get("RINGMIX_POS_PLACEMENT", "rotate")
+        self.placed = (placement == "rotate" and self.world > 1 and L % self.world == 0
+                       and self.world <= 8 and L <= 1024)
+        ident = torch.arange(L, dtype=torch.int32, device=self.device)
+        # [pos_of_slot, slot_of_pos] for the current and the next step
+        self.place = [[ident.clone(), ident.clone()], [ident.clone(), ident.clone()]]
+        self.pc = 0
+        self.moved = torch.zeros(self.world, dtype=torch.int32, device=self.device)
+        self.moved_log: list[torch.Tensor] = []
 
     @property
     def slots_local(self) -> torch.Tensor:
@@ -436,9 +452,23 @@ class LearnerShardedRingPos:
         gradients in slot order (Lg, d)."""
         lib = _lib.load()
         s = _lib.stream_ptr()
-        _lib.check(lib.rm_pos_plan(inv_k.data_ptr(), perm_next.data_ptr(), self.L, self.g0,
-                                   self.Lg, self.slots[1 - self.cur].data_ptr(),
-                                   self.plan.data_ptr(), self.dest.data_ptr(), s), "rm_pos_plan")
+        if self.placed:
+            cur, nxt = self.place[self.pc], self.place[1 - self.pc]
+            _lib.check(lib.rm_pos_placement(inv_k.data_ptr(), perm_next.data_ptr(),
+                                            cur[1].data_ptr(), self.L, self.world,
+                                            nxt[0].data_ptr(), nxt[1].data_ptr(),
+                                            self.moved.data_ptr(), s), "rm_pos_placement")
+            _lib.check(lib.rm_pos_plan_placed(inv_k.data_ptr(), perm_next.data_ptr(),
+                                              cur[0].data_ptr(), cur[1].data_ptr(),
+                                              nxt[1].data_ptr(), self.L, self.g0, self.Lg,
+                                              self.slots[1 - self.cur].data_ptr(),
+                                              self.plan.data_ptr(), self.dest.data_ptr(), s),
+                       "rm_pos_plan_placed")
+        else:
+            _lib.check(lib.rm_pos_plan(inv_k.data_ptr(), perm_next.data_ptr(), self.L, self.g0,
+                                       self.Lg, self.slots[1 - self.cur].data_ptr(),
+                                       self.plan.data_ptr(), self.dest.data_ptr(), s),
+                       "rm_pos_plan")
         src = self.W[self.cur]
         if G is not None:
             mixing._same(src, G, "G")
@@ -452,8 +482,24 @@ class LearnerShardedRingPos:
         if self.sync is not None:
             self.sync.commit()
         self.cur = 1 - self.cur
+        if self.placed:
+            self.pc = 1 - self.pc
+            if self.log_moves:
+                self.moved_log.append(self.moved.clone())
         if barrier:
             self.barrier()
+
+    log_moves = False
+
+    def slot_positions(self) -> torch.Tensor:
+        """Ring positions held by this rank's slots at the current step (device int32[Lg]):
+        slot i holds the learner inv_k[slot_positions()[i]]."""
+        return self.place[self.pc][0][self.g0:self.g0 + self.Lg]
+
+    def slot_learners(self, inv_k: torch.Tensor) -> torch.Tensor:
+        """Learner ids in this rank's slots for the current step, given that step's inv_k
+        (e.g. to produce their gradients in slot order)."""
+        return inv_k[self.slot_positions().long()]
 
     def close(self):
         torch.cuda.synchronize(self.device)

@@ -366,3 +366,125 @@ def test_oracle_pins_the_emulated_sharded_step():
     G64 = Gf.double().cpu().numpy().T.copy()
     want = O.c_ring_mix_sgd(W64, G64, 0.01, left, right).astype(np.float32)
     assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------------------
+# ring-position layout with arc placement (rm_pos_placement / rm_pos_plan_placed)
+# ---------------------------------------------------------------------------
+
+def _best_placement_numpy(inv_k, perm_next, sop_k, L, n):
+    """Restatement of rm_pos_placement: best (rotation, arc -> rank) by exhaustive search
+    (n <= 5), ties to the smallest rotation and the lexicographically first assignment."""
+    import itertools
+    Lg = L // n
+    owner = np.empty(L, dtype=np.int64)
+    qn = np.empty(L, dtype=np.int64)
+    for q in range(L):
+        owner[inv_k[q]] = sop_k[q] // Lg
+    qn[:] = perm_next
+    best = (-1, None, None)
+    for r in range(L):
+        arc = ((qn - r) % L) // Lg
+        cnt = np.zeros((n, n), dtype=np.int64)
+        np.add.at(cnt, (arc, owner), 1)
+        for sig in itertools.permutations(range(n)):
+            sc = sum(cnt[a, sig[a]] for a in range(n))
+            if sc > best[0]:
+                best = (sc, r, sig)
+    return best
+
+
+@pytest.mark.parametrize("L,n", [(12, 3), (16, 2), (24, 4), (40, 5), (64, 8)])
+def test_pos_placement_matches_exhaustive_search(L, n):
+    lib = _lib.load()
+    tabs = mixing.permutation_tables(L, 99, 0, 5)
+    sop = torch.arange(L, dtype=torch.int32, device="cuda")
+    pos_n = torch.empty(L, dtype=torch.int32, device="cuda")
+    sop_n = torch.empty(L, dtype=torch.int32, device="cuda")
+    moved = torch.zeros(n, dtype=torch.int32, device="cuda")
+    for k in range(4):
+        _lib.check(lib.rm_pos_placement(tabs.inv[k].contiguous().data_ptr(),
+                                        tabs.perm[k + 1].contiguous().data_ptr(), sop.data_ptr(),
+                                        L, n, pos_n.data_ptr(), sop_n.data_ptr(),
+                                        moved.data_ptr(), _lib.stream_ptr()))
+        torch.cuda.synchronize()
+        inv_k, pn = tabs.inv[k].cpu().numpy(), tabs.perm[k + 1].cpu().numpy()
+        s_k, s_n, p_n = sop.cpu().numpy(), sop_n.cpu().numpy(), pos_n.cpu().numpy()
+        Lg = L // n
+        # a placement: bijection, every rank an arc of consecutive positions
+        assert sorted(s_n.tolist()) == list(range(L)) and np.array_equal(p_n[s_n], np.arange(L))
+        for g in range(n):
+            arc = p_n[g * Lg:(g + 1) * Lg]
+            assert np.all((np.diff(arc) % L) == 1)
+        stay = sum(1 for q in range(L) if s_k[q] // Lg == s_n[pn[inv_k[q]]] // Lg)
+        if n <= 5:
+            best = _best_placement_numpy(inv_k, pn, s_k, L, n)
+            assert stay == best[0]
+        owner = {inv_k[q]: s_k[q] // Lg for q in range(L)}
+        want_moved = np.zeros(n, dtype=np.int64)
+        for l in range(L):
+            if s_n[pn[l]] // Lg != owner[l]:
+                want_moved[owner[l]] += 1
+        assert np.array_equal(moved.cpu().numpy(), want_moved)
+        assert stay >= sum(1 for q in range(L) if q // Lg == pn[inv_k[q]] // Lg) or n > 5
+        sop.copy_(sop_n)
+
+
+@pytest.mark.parametrize("L,d,world", [(24, 3001, 4), (16, 515, 2), (40, 77, 8)])
+def test_placed_position_layout_steps_bit_identical(L, d, world):
+    """Ring-position layout with the per-step arc placement, every rank emulated on this
+    GPU, in-kernel ordering: after each step slot i of rank r holds learner
+    inv_{k+1}[pos_of_slot[r * Lg + i]], equal to the single-GPU step."""
+    dtype = torch.float32
+    lay, full, Gf = _full_and_parts(L, d, world, dtype, 7 * L + d)
+    Lg = L // world
+    K = 5
+    tabs = mixing.permutation_tables(L, 4321, 0, K + 1)
+    inv = tabs.inv
+    bufs = [[mixing.empty_learner_major(Lg, d, dtype) for _ in range(2)] for _ in range(world)]
+    esz = full.element_size()
+    slots = [D._slot_table(lay, [bufs[r][p].data_ptr() for r in range(world)],
+                           bufs[0][0].stride(0), esz, "cuda") for p in range(2)]
+    lib = _lib.load()
+    sync = _EmuSync(world)
+    _lib.check(lib.rm_set_xgpu_timeout(30.0))
+    ident = torch.arange(L, dtype=torch.int32, device="cuda")
+    place = [[ident.clone(), ident.clone()], [ident.clone(), ident.clone()]]
+    inv0 = inv[0].long()
+    for r in range(world):
+        bufs[r][0].copy_(full[inv0[r * Lg:(r + 1) * Lg]])
+    plans = [torch.empty(lib.rm_shard_plan_ints(Lg), dtype=torch.int32, device="cuda")
+             for _ in range(world)]
+    dests = [torch.empty(Lg, dtype=torch.int64, device="cuda") for _ in range(world)]
+    ref, cur, pc = full, 0, 0
+    for k in range(K):
+        ik, pn = inv[k].contiguous(), tabs.perm[k + 1].contiguous()
+        cp, npl = place[pc], place[1 - pc]
+        _lib.check(lib.rm_pos_placement(ik.data_ptr(), pn.data_ptr(), cp[1].data_ptr(), L, world,
+                                        npl[0].data_ptr(), npl[1].data_ptr(), None,
+                                        _lib.stream_ptr()))
+        for r in range(world):
+            _lib.check(lib.rm_pos_plan_placed(ik.data_ptr(), pn.data_ptr(), cp[0].data_ptr(),
+                                              cp[1].data_ptr(), npl[1].data_ptr(), L, r * Lg, Lg,
+                                              slots[1 - cur].data_ptr(), plans[r].data_ptr(),
+                                              dests[r].data_ptr(), _lib.stream_ptr()))
+            learners = ik[cp[0][r * Lg:(r + 1) * Lg].long()].long()
+            Gs = mixing.empty_learner_major(Lg, d, dtype)
+            Gs.copy_(Gf[learners])
+            src = bufs[r][cur]
+            a = sync.args(r, k + 1)
+            _lib.check(lib.rm_ring_mix_sgd_pos_f32(
+                slots[cur].data_ptr(), src.data_ptr(), Gs.data_ptr(), L, r * Lg, Lg, d,
+                src.stride(0), Gs.stride(0), plans[r].data_ptr(), dests[r].data_ptr(), 0.02, None,
+                _lib.stream_ptr(), ctypes.byref(a)))
+        cur, pc = 1 - cur, 1 - pc
+        lt, rt = tabs.step(k)
+        ref = mixing.ring_mix_sgd(ref, Gf, 0.02, lt.contiguous(), rt.contiguous())
+        _lib.check(lib.rm_step_sync_wait(ctypes.byref(sync.args(0, k + 1)), _lib.stream_ptr()))
+        torch.cuda.synchronize()
+        nxt = inv[k + 1].long()
+        pos_slots = place[pc][0].long()
+        for r in range(world):
+            learners = nxt[pos_slots[r * Lg:(r + 1) * Lg]]
+            assert torch.equal(bufs[r][cur], ref[learners]), (k, r)
+    assert _status() == 0

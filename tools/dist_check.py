@@ -131,14 +131,16 @@ def main():
     torch.cuda.synchronize(); dist.barrier()
     for k in range(3):
         Gs = mixing.empty_learner_major(pos.Lg, d, torch.float32, dev)
-        Gs.copy_(Gf[tabs.inv[k][g0:g1].long()])
+        Gs.copy_(Gf[pos.slot_learners(tabs.inv[k]).long()])
         pos.step(tabs.inv[k].contiguous(), tabs.perm[k + 1].contiguous(), Gs, 0.01)
         lt, rt = tabs.step(k)
         Wr = mixing.ring_mix_sgd(Wr, Gfull, 0.01, lt.contiguous(), rt.contiguous())
         torch.cuda.synchronize()
-        same = bool(torch.equal(pos.slots_local, Wr[tabs.inv[k + 1][g0:g1].long()]))
+        same = bool(torch.equal(pos.slots_local, Wr[pos.slot_learners(tabs.inv[k + 1]).long()]))
         pos_steps.append(same)
         ok_pos &= same
+    pos_steps.append(bool(pos.placed) == (L % world == 0 and world <= 8))
+    ok_pos &= pos_steps[-1]
     pos.close()
     detail = torch.tensor([int(x) for x in pull_steps + pos_steps], device=dev)
     all_detail = [torch.zeros_like(detail) for _ in range(world)]
