@@ -49,6 +49,23 @@ def test_host_buffer_binding_matches_oracle():
         b["gossip_step_f32"](W[:2], G[:2], 0.05, left[:2], right[:2], ws)   # L < 3
 
 
+def test_reference_layout_binding_matches_oracle():
+    """gossip_step_dL on the reference's (d, L) float64 arrays: ring[p, p] and uniform."""
+    b = _binding()
+    L, d = 16, 50_001
+    rng = np.random.default_rng(4)
+    W = rng.standard_normal((d, L))
+    G = rng.standard_normal((d, L))
+    left, right = _tables(L, 77, 5)
+    ws = b["Workspace"](L, chunk_cols=1 << 12, itemsize=8)
+    out = b["gossip_step_dL"](W, G, 0.05, left, right, ws)
+    assert np.array_equal(out, O.c_ring_mix_sgd(W, G, 0.05, left, right))
+    mean = b["gossip_step_dL"](W, G, 0.05, None, None, ws)
+    assert np.array_equal(mean, O.c_mean_sgd(W, G, 0.05))
+    with pytest.raises(ValueError, match="degenerate ring"):
+        b["gossip_step_dL"](W[:, :2].copy(), G[:, :2].copy(), 0.05, left[:2], right[:2], ws)
+
+
 def test_device_binding_matches_drop_in():
     b = _binding()
     L, d, seed, k = 64, 4099, 1234, 17
