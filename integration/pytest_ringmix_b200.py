@@ -4,11 +4,12 @@ libringmix_b200 (integration/ringmix_b200.py).
   PYTHONPATH=baseline/_ref:integration python -m pytest -p pytest_ringmix_b200 \
       baseline/_ref/ringmix_ref_tests/test_mixing.py ...
 
-Tests listed in XFAIL compare `apply_mixing(W, T)` bit for bit with numpy's `W @ T`: that
-equality holds only where our FMA chain and OpenBLAS's kernel for that matrix shape round
-alike (OpenBLAS's small-matrix and remainder kernels are an implementation-defined choice of
-the BLAS), so they are non-strict expected failures.  The terminal summary
-prints how many calls went through the GPU, and the run fails if none did."""
+XFAIL may list tests that compare `apply_mixing(W, T)` bit for bit with numpy's `W @ T`
+where our FMA chain and OpenBLAS's kernel for that matrix shape could round differently
+(OpenBLAS's small-matrix and remainder kernels are an implementation-defined choice of the
+BLAS).  It is empty: with numpy 2.3.5 / OpenBLAS 0.3.30 every one of the
+reference's tests passes through the binding (test_mixing.py's bitwise W @ T check
+included).  The terminal summary prints how many calls went through the GPU."""
 
 from __future__ import annotations
 
@@ -16,10 +17,7 @@ import os
 
 import pytest
 
-XFAIL = {
-    "test_mixing.py::test_apply_mixing_matches_matmul_on_ring":
-        "bitwise W @ T against OpenBLAS's small-matrix kernel (DESIGN.md §4)",
-}
+XFAIL: dict[str, str] = {}
 
 
 def pytest_configure(config):

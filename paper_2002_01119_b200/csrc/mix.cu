@@ -185,6 +185,23 @@ __device__ __forceinline__ void load_means(const double* s_mean, int c, double (
   }
 }
 
+// Element e of a staged vector in the accumulation type.  RM_FAST_F2D (build-time
+// experiment): fp32 -> fp64 widening of normal numbers by re-biasing the exponent with
+// integer ops (exact), F2F only for zero / subnormal / inf / NaN.
+template <typename T>
+__device__ __forceinline__ typename Elem<T>::acc widen(const T* v, int e) {
+#ifdef RM_FAST_F2D
+  if constexpr (sizeof(T) == 4) {
+    const uint32_t u = __float_as_uint(v[e]);
+    if (((u >> 23) & 0xffu) - 1u < 254u) {
+      const uint32_t hi = (((u & 0x7fffffffu) >> 3) + (896u << 20)) | (u & 0x80000000u);
+      return __hiloint2double((int)hi, (int)(u << 29));
+    }
+  }
+#endif
+  return (typename Elem<T>::acc)Elem<T>::ld(v, e);
+}
+
 template <typename T, int MODE, bool HAS_G, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT)
     mix_tma_kernel(MixArgs a, const __grid_constant__ CUtensorMap tmW,
@@ -393,8 +410,8 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
-          A m = ring3<A>((A)E::ld(va.e(), e), (A)E::ld(vb.e(), e), (A)E::ld(vc.e(), e));
-          if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
+          A m = ring3<A>(widen<T>(va.e(), e), widen<T>(vb.e(), e), widen<T>(vc.e(), e));
+          if (HAS_G) m = r_sub(m, r_mul(lr, widen<T>(vg.e(), e)));
           y.e()[e] = E::st(m);
         }
       } else if (MODE == kMean) {
