@@ -105,3 +105,38 @@ def test_reference_arm_prints_the_contract_line():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_resolve_picks_the_baseline_config_per_world_size():
+    """N = 1: configs[1] (C2) on one GPU; N > 1: configs[2] (C3) learner-sharded in
+    ring-position order for RAD, the learner layout for D1D / the fixed ring; an explicit
+    coordinate layout keeps C2 stripes with weak scaling."""
+    b = _bench()
+    a = b.parse([])
+    r1 = b.resolve(a, 1)
+    assert (r1.learners, r1.dim, r1.layout, r1.config_index) == (64, 25_557_032, "coord", 1)
+    r2 = b.resolve(a, 2)
+    assert (r2.learners, r2.dim, r2.layout, r2.scaling, r2.config_index) == \
+        (128, 43_154_944, "position", "strong", 2)
+    d = b.resolve(b.parse(["--strategy", "d1d"]), 4)
+    assert (d.layout, d.learners, d.config_index) == ("learner", 64, 3)
+    c = b.resolve(b.parse(["--layout", "coord"]), 4)
+    assert (c.layout, c.scaling, c.learners) == ("coord", "weak", 64)
+    assert b.total_dim(c, 4) == 4 * 25_557_032
+    assert "configs[2]" in b.config_dict(r2, 2)["workload"]
+
+
+def test_self_launch_command(monkeypatch):
+    """`--gpus N` without WORLD_SIZE re-runs bench.py under torch.distributed.run with N
+    local ranks on 127.0.0.1."""
+    import sys
+    b = _bench()
+    seen = {}
+    monkeypatch.setattr(b.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "7"])
+    a = b.parse(["--gpus", "4", "--steps", "7"])
+    b.self_launch(a)
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "7"]

@@ -96,3 +96,24 @@ def test_gloo_world2_exchange_and_plans():
         assert ranks == [0, 1] and offs == [0, 4096] and blob_ok
         for x in served:
             assert D.ShardLayout(16, 2).owner(x) == rank
+
+
+def test_symmetric_addresses_multicast_or_peer_table(monkeypatch):
+    """A symmetric buffer is reached through its multicast address when the handle has one,
+    else (or with RINGMIX_SYM_P2P=1) through a table of every rank's address."""
+    from paper_2002_01119_b200 import distributed as D
+
+    class H:
+        multicast_ptr = 0x7000
+        buffer_ptrs = [0x1000, 0x2000, 0x3000]
+        offset = 0x40
+
+    mc, tab = D._sym_addresses(H, "cpu")
+    assert mc == 0x7040 and tab is None
+    monkeypatch.setenv("RINGMIX_SYM_P2P", "1")
+    mc, tab = D._sym_addresses(H, "cpu")
+    assert mc == 0 and tab.tolist() == [0x1040, 0x2040, 0x3040]
+    monkeypatch.delenv("RINGMIX_SYM_P2P")
+    H.multicast_ptr = 0
+    mc, tab = D._sym_addresses(H, "cpu")
+    assert mc == 0 and tab.tolist() == [0x1040, 0x2040, 0x3040]
