@@ -600,13 +600,21 @@ def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     graph = None
     if use_graph:
-        # the K timed steps captured once (perm-table launches + mix launches, PDL edges
-        # between consecutive mixes), replayed once untimed, then timed
+        # the K timed steps captured once (perm-table launches + mix launches), replayed
+        # once untimed, then timed: the package's simulation.GraphedRingSteps for the ring
+        # strategies, the bench's own step otherwise
         wl.reset_tables()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for i in range(K):
-                wl.step(k + i)
+        if spec.strategy in ("rand_psgd", "adpsgd_fixed") and wl.layout == "single":
+            from paper_2002_01119_b200 import simulation as S
+            gs = S.GraphedRingSteps(wl.W[wl.cur], wl.G, LR, K,
+                                    seed=SEED if spec.strategy == "rand_psgd" else None, k0=k)
+            graph = gs.graph
+            wl.graphed = gs
+        else:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for i in range(K):
+                    wl.step(k + i)
         graph.replay()
     torch.cuda.synchronize()
     if ws > 1:
@@ -649,6 +657,8 @@ def measure(spec, torch, dist, dev, ws, rank, local, args, clocks=None, nvc=None
     # mode the replay time per step (mix + its share of the 1-per-64-steps perm launch)
     kern_ms = [a.elapsed_time(b) for a, b in kev.values()] or [elapsed_ms / K]
     bits = wl.amax[:k].cpu().numpy().view(np.float64)
+    if getattr(wl, "graphed", None) is not None:
+        bits = np.concatenate([bits, wl.graphed.absmax.cpu().numpy().view(np.float64)])
     if not np.all(np.isfinite(bits)):
         raise RuntimeError("non-finite weights in the benchmark run")
     tx = rx = -1.0
@@ -922,8 +932,8 @@ def run_ours(args):
                                      "mix_tma_kernel") + f" ({spec.strategy}, {spec.dtype})"),
                          "algorithmic_bytes_per_launch": res["algo_bytes"],
                          "avg_launch_ms": res["kern_avg_s"] * 1e3,
-                         "timing": ("CUDA-graph replay of the K steps / K (PDL between "
-                                    "consecutive mix launches)" if res["graph"] else
+                         "timing": ("CUDA-graph replay of the K steps / K "
+                                    "(simulation.GraphedRingSteps)" if res["graph"] else
                                     f"CUDA events around every {args.event_every}-th mix launch"),
                          "peak_source": res["peak_src"]},
             "cpu_baseline": cpu,

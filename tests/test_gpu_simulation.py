@@ -227,3 +227,29 @@ def test_consensus_distance_matches_reference_formula():
     ref = float(np.sqrt((dev * dev).sum(axis=0).max()))
     assert simulation.consensus_distance(torch.from_numpy(W).cuda()) == pytest.approx(ref,
                                                                                       rel=1e-12)
+
+
+@pytest.mark.parametrize("seed", [12345, None])
+def test_graphed_ring_steps_equal_eager_steps(seed):
+    """simulation.GraphedRingSteps (K steps in one CUDA graph) gives the same bits as K eager
+    ring_mix_sgd calls (RAD with the device permutation tables, or the fixed ring), and a
+    replay repeats them from the current W[0]."""
+    L, d, K = 16, 5000, 70           # more than one 64-step table block
+    g = torch.Generator(device="cuda").manual_seed(8)
+    W0 = mixing.empty_learner_major(L, d, torch.float32)
+    W0.copy_(torch.randn((L, d), generator=g, device="cuda"))
+    G = mixing.empty_learner_major(L, d, torch.float32)
+    G.copy_(torch.randn((L, d), generator=g, device="cuda"))
+    start = W0.clone()
+    gs = simulation.GraphedRingSteps(W0, G, 0.01, K, seed=seed, k0=5)
+    out = gs.replay().clone()
+    ref = start
+    fixed = simulation.fixed_ring_tables(L, "cuda")
+    for k in range(5, 5 + K):
+        lt, rt = simulation.rad_tables(L, seed, k, "cuda") if seed is not None else fixed
+        ref = mixing.ring_mix_sgd(ref, G, 0.01, lt, rt)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    assert simulation.absmax_value(gs.absmax[K - 1]) == float(ref.abs().max())
+    gs.W[0].copy_(start)
+    assert torch.equal(gs.replay(), ref)

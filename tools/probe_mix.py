@@ -22,6 +22,7 @@ ap.add_argument("--n", type=int, default=30)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--ceiling", action="store_true")
 ap.add_argument("--fixed", action="store_true")
+ap.add_argument("--mode", choices=["ring", "mean"], default="ring")
 args = ap.parse_args()
 dt = getattr(torch, args.dtype)
 esz = torch.tensor([], dtype=dt).element_size()
@@ -54,7 +55,11 @@ def timeit(fn, n):
 
 env = {k: v for k, v in os.environ.items() if k.startswith("RINGMIX_")}
 for rep in range(args.reps):
-    ms = timeit(lambda i: mixing.ring_mix_sgd(W[i % 2], G, 0.01, lt, rt, out=W[1 - i % 2]), args.n)
+    if args.mode == "mean":
+        ms = timeit(lambda i: mixing.mean_mix_sgd(W[i % 2], G, 0.01, out=W[1 - i % 2]), args.n)
+    else:
+        ms = timeit(lambda i: mixing.ring_mix_sgd(W[i % 2], G, 0.01, lt, rt, out=W[1 - i % 2]),
+                    args.n)
     print(json.dumps({"what": "mix", "L": L, "d": d, "dtype": args.dtype, "env": env, "rep": rep,
                       "ms": ms, "GBs": bytes_ / ms / 1e6}), flush=True)
 # correctness spot check of this variant against the per-item formula on a few columns
