@@ -48,7 +48,8 @@ static void xgpu_config() {
 }
 
 constexpr int kShThreads = 512;
-constexpr int kShStages = 3;
+constexpr int kShMaxStages = 6;
+constexpr int kShStagesDefault = 3;
 constexpr int kShStageTarget = 64 * 1024;
 
 // plan layout (int32): [0] = R (distinct remote rows), [1 .. 1+2Lg) remote
@@ -112,6 +113,7 @@ struct ShardArgs {
   SymRef sync_flag;  // `done` on every rank (multicast address or peer table)
   uint32_t* sync_cnt;
   uint32_t sync_target;
+  int nstages;       // shared-memory stages in flight (RINGMIX_SHARD_STAGES, default 3)
 };
 
 template <typename T, bool HAS_G>
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(kShThreads, 1)
   if (tid == 0) {
     tma_prefetch_desc(&tmW);
     if (HAS_G) tma_prefetch_desc(&tmG);
-    for (int s = 0; s < kShStages; s++) mbar_init(&full[s], 1 + kShThreads);
+    for (int s = 0; s < a.nstages; s++) mbar_init(&full[s], 1 + kShThreads);
     fence_mbar_init();
   }
   for (int j = tid; j < Lg; j += kShThreads) {
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(kShThreads, 1)
   };
 
   const long long first = blockIdx.x, stride = gridDim.x;
-  for (int s = 0; s < kShStages; s++) {
+  for (int s = 0; s < a.nstages; s++) {
     long long t = first + s * stride;
     if (t < a.ntiles) issue(s, t);
   }
@@ -204,8 +206,8 @@ __global__ void __launch_bounds__(kShThreads, 1)
 
   int it = 0;
   for (long long t = first; t < a.ntiles; t += stride, ++it) {
-    const int s = it % kShStages;
-    const uint32_t parity = (it / kShStages) & 1;
+    const int s = it % a.nstages;
+    const uint32_t parity = (it / a.nstages) & 1;
     const long long c0 = t * cw;
     const int width = (int)min((long long)cw, a.d - c0);
     const T* sW = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes);
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kShThreads, 1)
       }
     }
     __syncthreads();
-    long long tn = t + (long long)kShStages * stride;
+    long long tn = t + (long long)a.nstages * stride;
     if (tn < a.ntiles) issue(s, tn);
   }
   if (a.absmax) absmax_publish(a.absmax, E::amax_bits(amax));
@@ -410,8 +412,18 @@ static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
   const int rows = a.Lg * 2 + a.Rmax;  // staged rows per column (W local+remote, G)
+  // tuning knobs (measured defaults): stages in flight and the stage size target
+  static int env_stages = -1, env_kb = -1;
+  if (env_stages < 0) {
+    const char* e1 = getenv("RINGMIX_SHARD_STAGES");
+    const char* e2 = getenv("RINGMIX_SHARD_STAGE_KB");
+    env_stages = e1 ? atoi(e1) : 0;
+    env_kb = e2 ? atoi(e2) : 0;
+  }
+  a.nstages = (env_stages >= 2 && env_stages <= kShMaxStages) ? env_stages : kShStagesDefault;
+  const size_t target = (env_kb >= 8 && env_kb <= 128) ? (size_t)env_kb * 1024 : kShStageTarget;
   int cw = VEC;
-  while ((size_t)(cw * 2) * rows * esz <= (size_t)kShStageTarget && cw * 2 <= 2048) cw *= 2;
+  while ((size_t)(cw * 2) * rows * esz <= target && cw * 2 <= 2048) cw *= 2;
   while (cw > VEC && (a.d + cw - 1) / cw < 4LL * sm_count(-1) && cw * esz > 256) cw /= 2;
   if (const char* env = getenv("RINGMIX_TILE_COLS")) {
     int v = atoi(env);
@@ -420,7 +432,7 @@ static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G
   const size_t stage = (size_t)rows * cw * esz;
   const size_t smem = 128 + ((size_t)(a.Lg * 16 + 127) / 128) * 128 +
                       ((size_t)((a.Rmax > 0 ? a.Rmax : 1) * 8 + 127) / 128) * 128 +
-                      kShStages * stage;
+                      a.nstages * stage;
   if (smem > (size_t)max_optin) {
     set_error("sharded tile does not fit shared memory (Lg=%d)", a.Lg);
     return RM_ERANGE;
