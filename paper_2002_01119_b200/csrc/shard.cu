@@ -421,7 +421,11 @@ static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G
     env_kb = e2 ? atoi(e2) : 0;
   }
   a.nstages = (env_stages >= 2 && env_stages <= kShMaxStages) ? env_stages : kShStagesDefault;
-  const size_t target = (env_kb >= 8 && env_kb <= 128) ? (size_t)env_kb * 1024 : kShStageTarget;
+  // position layout with <= 32 local rows: 72 KB stages give 1 KB row segments (256 fp32
+  // columns) — measured at C3 on 4 GPUs 863 vs 849 G/s; at 64 local rows the 64 KB target
+  // (256-byte segments) stays ahead (746-753 vs 736-743), profiles/r2_n4_sweep/
+  const size_t dflt = (a.dest != nullptr && a.Lg <= 32) ? 72 * 1024 : kShStageTarget;
+  const size_t target = (env_kb >= 8 && env_kb <= 128) ? (size_t)env_kb * 1024 : dflt;
   int cw = VEC;
   while ((size_t)(cw * 2) * rows * esz <= target && cw * 2 <= 2048) cw *= 2;
   while (cw > VEC && (a.d + cw - 1) / cw < 4LL * sm_count(-1) && cw * esz > 256) cw /= 2;
