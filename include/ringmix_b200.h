@@ -448,6 +448,31 @@ int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int appen
                            int nstreams, int64_t n, double* Z, int64_t ldz, void* workspace,
                            int64_t workspace_bytes, void* stream);
 
+/* ---- one training step with the quadratic oracle's gradient fused into the mix ----
+ * (simulation.py:263-268 with gradient_matrix simulation.py:226-238 and the oracle
+ * objectives.py:84-90):
+ *   Wout = apply_mixing(W, T) - lr * G,   G[l] = fl(lam * (Phi[l] - wopt) + noise_sd * z_l)
+ * T = the ring given by left/right (randomized or fixed ring), or the uniform matrix when
+ * left == right == NULL (D1D).  G is produced inside the mix kernel from the generator's
+ * normals and never written: bit-identical to rm_quadratic_grad_* followed by
+ * rm_ring_mix_sgd_* / rm_mean_sgd_*.  Phi == NULL (or Phi == W with ldp == ldw) takes the
+ * gradient at W itself (synchronous strategies) and reads W once.
+ * workspace: device, >= rm_quadratic_mix_workspace_bytes(L, d). */
+int64_t rm_quadratic_mix_workspace_bytes(int L, int64_t d);
+int rm_quadratic_mix_step_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                              const float* W, const float* Phi, float* Wout, const int32_t* left,
+                              const int32_t* right, int L, int64_t d, int64_t ldw, int64_t ldp,
+                              int64_t ldo, const double* lam, const double* wopt, double noise_sd,
+                              double lr, unsigned long long* absmax_bits, void* workspace,
+                              int64_t workspace_bytes, void* stream);
+int rm_quadratic_mix_step_f64(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                              const double* W, const double* Phi, double* Wout,
+                              const int32_t* left, const int32_t* right, int L, int64_t d,
+                              int64_t ldw, int64_t ldp, int64_t ldo, const double* lam,
+                              const double* wopt, double noise_sd, double lr,
+                              unsigned long long* absmax_bits, void* workspace,
+                              int64_t workspace_bytes, void* stream);
+
 /* ---- fused trace reductions (run_training's _record, simulation.py:398-409) ----
  * One pass over W (L <= 128 learners, learner-major): cons_sq[l] += sum_c (W[l,c]-mean_c)^2
  * (consensus_distance), and when lam != NULL: loss_col[l] += 0.5 sum_c lam_c (W[l,c]-wopt_c)^2,

@@ -31,6 +31,7 @@
 #include "common.cuh"
 #include "tma_host.cuh"
 #include "arith.cuh"
+#include "zsrc.cuh"
 #include "../../include/ringmix_b200.h"
 
 #include <stdlib.h>
@@ -39,7 +40,13 @@
 
 namespace rm {
 
-enum Mode { kRing = 0, kMean = 1, kSpsgd = 2 };
+// kRingZ / kMeanZ: the ring / uniform step with the quadratic oracle's gradient
+// produced in the epilogue from the generator's normals (zsrc.cuh); HAS_G then means
+// "Phi (the weights the gradient is taken at) is staged separately" — without it Phi = W.
+enum Mode { kRing = 0, kMean = 1, kSpsgd = 2, kRingZ = 3, kMeanZ = 4 };
+
+__host__ __device__ constexpr bool mode_ring(int m) { return m == kRing || m == kRingZ; }
+__host__ __device__ constexpr bool mode_z(int m) { return m == kRingZ || m == kMeanZ; }
 
 // items per thread in flight in the output phase (build-time tuning knob)
 #ifndef RM_RING_UNROLL
@@ -50,6 +57,14 @@ constexpr int kRingUnroll = RM_RING_UNROLL;
 constexpr int kRingThreads = 512;   // ring tiles: one 512-thread CTA per SM
 constexpr int kMeanThreads = 256;   // mean tiles: two 256-thread CTAs per SM
 constexpr int kStages = 3;
+// Z modes: more (smaller) W stages, and the normals of iteration i + kZDist are copied
+// (cp.async, 8 bytes per thread and element) into one of kZBufs shared buffers while
+// iteration i computes
+constexpr int kZStages = 5;
+constexpr int kZDist = 2;
+constexpr int kZBufs = kZDist + 1;
+constexpr int kZTileRing = 4096;   // L * cw per z buffer (fp64 elements): 32 KB
+constexpr int kZTileMean = 2048;   // two CTAs per SM: 16 KB
 constexpr int kMaxTmaL = 256;   // one TMA row box per tile
 constexpr int kStageTarget = 64 * 1024;      // ring
 constexpr int kMeanStageTarget = 32 * 1024;  // mean (two CTAs per SM)
@@ -65,13 +80,27 @@ struct MixArgs {
   int L;
   int cw;        // tile width (elements), power of two, multiple of VEC
   int log2_nv;   // log2(cw / VEC)
+  int zdcols;    // Z modes: descriptor columns (uint64) per staged tile
+  int zslots;    // Z modes: doubles per z buffer
   long long ntiles;
   const int32_t* left;
   const int32_t* right;
   double lr;
   unsigned long long* absmax;  // may be null
   unsigned int* mismatch;      // kSpsgd: set nonzero if W rows differ
+  ZSrc z;                      // kRingZ / kMeanZ
 };
+
+// gradient element (row j, column c) of the Z modes in the accumulation type, rounded to
+// the storage type first exactly as the generator's G output
+template <typename T>
+__device__ __forceinline__ typename Elem<T>::acc z_grad_elem(const ZSrc& z, int j, long long c,
+                                                             double phi) {
+  using E = Elem<T>;
+  const double zv = __ldcs(z.scratch + z_index(z, z_desc(z, j, c), c));
+  return (typename E::acc)E::st(
+      (typename E::acc)z_grad(__ldg(z.lam + c), __ldg(z.wopt + c), z.sd, phi, zv));
+}
 
 // ----------------------------------------------------------------------------
 // scalar path: any alignment / any L; one thread per (row, column)
@@ -88,19 +117,23 @@ __global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_
   const long long total = ncols * a.L;
   unsigned long long amax = 0;
   const A lr = (A)a.lr;
-  if (MODE != kRing) {
+  if (!mode_ring(MODE)) {
     // one thread per column: the column mean once (numpy pairwise, any L),
     // then every learner's output
     for (long long cc = blockIdx.x * (long long)blockDim.x + threadIdx.x; cc < ncols;
          cc += (long long)gridDim.x * blockDim.x) {
       const long long c = c_begin + cc;
-      const T* src = MODE == kMean ? W : G;
-      const long long lds = MODE == kMean ? a.ldw : a.ldg;
+      const T* src = MODE == kSpsgd ? G : W;
+      const long long lds = MODE == kSpsgd ? a.ldg : a.ldw;
       auto get = [&](int i) { return (A)E::ld(src + i * lds + c, 0); };
       const A m = r_div(pairwise_sum<A>(get, 0, a.L), (A)a.L);
       for (int j = 0; j < a.L; j++) {
         A y;
-        if (MODE == kMean) {
+        if (MODE == kMeanZ) {
+          const double phi = HAS_G ? (double)E::ld(G + j * a.ldg + c, 0)
+                                   : (double)E::ld(W + j * a.ldw + c, 0);
+          y = r_sub(m, r_mul(lr, z_grad_elem<T>(a.z, j, c, phi)));
+        } else if (MODE == kMean) {
           y = HAS_G ? r_sub(m, r_mul(lr, (A)E::ld(G + j * a.ldg + c, 0))) : m;
         } else {  // kSpsgd: W - lr * mean_l(G)
           if (a.mismatch && !(W[j * a.ldw + c] == W[c])) atomicOr(a.mismatch, 1u);
@@ -127,7 +160,13 @@ __global__ void __launch_bounds__(256) mix_scalar_kernel(MixArgs a, long long c_
       if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
       y = ring3<A>(E::ld(W + x0 * a.ldw + c, 0), E::ld(W + x1 * a.ldw + c, 0),
                    E::ld(W + x2 * a.ldw + c, 0));
-      if (HAS_G) y = r_sub(y, r_mul(lr, E::ld(G + j * a.ldg + c, 0)));
+      if (MODE == kRingZ) {
+        const double phi = HAS_G ? (double)E::ld(G + j * a.ldg + c, 0)
+                                 : (double)E::ld(W + j * a.ldw + c, 0);
+        y = r_sub(y, r_mul(lr, z_grad_elem<T>(a.z, j, c, phi)));
+      } else if (HAS_G) {
+        y = r_sub(y, r_mul(lr, E::ld(G + j * a.ldg + c, 0)));
+      }
     }
     T ys = E::st(y);
     out[j * a.ldo + c] = ys;
@@ -205,7 +244,10 @@ __device__ __forceinline__ typename Elem<T>::acc widen(const T* v, int e) {
 template <typename T, int MODE, bool HAS_G, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT)
     mix_tma_kernel(MixArgs a, const __grid_constant__ CUtensorMap tmW,
-                   const __grid_constant__ CUtensorMap tmG) {
+                   const __grid_constant__ CUtensorMap tmG,
+                   const __grid_constant__ CUtensorMap tmD,
+                   const __grid_constant__ CUtensorMap tmLam,
+                   const __grid_constant__ CUtensorMap tmOpt) {
   constexpr int kThreads = NT;
   using E = Elem<T>;
   using A = typename E::acc;
@@ -216,7 +258,16 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   const int cw = a.cw;
   const int w_bytes = L * cw * (int)sizeof(T);
   constexpr bool stage_g = HAS_G || MODE == kSpsgd;
-  const int stage_bytes = w_bytes * (stage_g ? 2 : 1);
+  constexpr bool ZM = mode_z(MODE);
+  constexpr int kSt = ZM ? kZStages : kStages;
+  // Z modes: the tile's normal descriptors [L][zdcols] (uint64) and its lam / w* columns
+  // (fp64 [cw] each) ride in the stage, each piece 128-byte aligned
+  const int wg_bytes = w_bytes * (stage_g ? 2 : 1);
+  const int zd_off = (wg_bytes + 127) & ~127;
+  const int zl_off = zd_off + ((L * a.zdcols * 8 + 127) & ~127);
+  const int zo_off = zl_off + ((cw * 8 + 127) & ~127);
+  const int stage_bytes = ZM ? zo_off + ((cw * 8 + 127) & ~127) : wg_bytes;
+  const uint32_t stage_tx = ZM ? wg_bytes + L * a.zdcols * 8 + 2 * cw * 8 : wg_bytes;
 
   // layout: [mbarriers | tri table (L x int4) | stages | per-column mean]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -224,10 +275,13 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   unsigned char* stages = smem + 128 + ((L * 16 + 127) / 128) * 128;
   double* s_mean = nullptr;
   A* s_part = nullptr;  // [8][cw] partial sums in the accumulation type (narrow tiles)
-  if (MODE != kRing) {
-    s_mean = reinterpret_cast<double*>(stages + kStages * stage_bytes);
+  unsigned char* tail = stages + kSt * stage_bytes;
+  if (!mode_ring(MODE)) {
+    s_mean = reinterpret_cast<double*>(tail);
     s_part = reinterpret_cast<A*>(s_mean + cw);
+    tail += a.zslots ? ((size_t)cw * sizeof(double) + 8 * cw * sizeof(A) + 15) / 16 * 16 : 0;
   }
+  double* zbuf = ZM ? reinterpret_cast<double*>(tail) : nullptr;  // [kZBufs][zslots]
 
   T* out = static_cast<T*>(a.out);
   const int tid = threadIdx.x;
@@ -235,13 +289,18 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   if (tid == 0) {
     tma_prefetch_desc(&tmW);
     if (stage_g) tma_prefetch_desc(&tmG);
-    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
+    if (ZM) {
+      tma_prefetch_desc(&tmD);
+      tma_prefetch_desc(&tmLam);
+      tma_prefetch_desc(&tmOpt);
+    }
+    for (int s = 0; s < kSt; s++) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   // Programmatic dependent launch: everything above overlaps the previous kernel's
   // tail; W, G and the neighbour tables may be its outputs, so wait for it here.
   pdl_wait();
-  if (MODE == kRing) {
+  if (mode_ring(MODE)) {
     for (int j = tid; j < L; j += kThreads) {
       int x0 = a.left[j], x1 = j, x2 = a.right[j], t;
       if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
@@ -260,13 +319,20 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   auto issue = [&](int s, long long t) {
     const int c0 = (int)(t * cw);
     unsigned char* st = stages + (size_t)s * stage_bytes;
-    mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+    mbar_arrive_expect_tx(&full[s], stage_tx);
     // L <= 256: one row box; column boxes of box_c land one after another,
     // each [L][box_c] (see sidx)
     for (int cc = 0; cc < cw; cc += box_c) {
       const int off = cc * L * (int)sizeof(T);
       tma_load_2d(st + off, &tmW, c0 + cc, 0, &full[s]);
       if (stage_g) tma_load_2d(st + w_bytes + off, &tmG, c0 + cc, 0, &full[s]);
+    }
+    if (ZM) {
+      tma_load_2d(st + zd_off, &tmD, (c0 >> kZGroupLog2) * 2, 0, &full[s]);
+      for (int cc = 0; cc < cw; cc += box_c) {
+        tma_load_2d(st + zl_off + cc * 8, &tmLam, c0 + cc, 0, &full[s]);
+        tma_load_2d(st + zo_off + cc * 8, &tmOpt, c0 + cc, 0, &full[s]);
+      }
     }
   };
   // element (r, c) of a stage tile (box_c is a power of two)
@@ -277,7 +343,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   };
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; s++) {
+    for (int s = 0; s < kSt; s++) {
       long long t = first + s * stride;
       if (t < a.ntiles) issue(s, t);
     }
@@ -289,10 +355,60 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   const int nv_full = 1 << log2_nv;
   const int warp = tid >> 5, lane = tid & 31;
 
+  // Z modes: copy the normals of iteration i's tile into z buffer i % kZBufs, laid out
+  // [L][cw] like the W tile.  Copy mapping: the thread that would own column vector v of
+  // a row instead copies the lane-contiguous columns cb + ln + grp * e (e < VEC) of it —
+  // each warp's 8-byte cp.async then read consecutive scratch doubles, and the run lies
+  // in one 128-column descriptor group (one descriptor per row and thread).  The
+  // descriptors come from the stage, which the TMA filled kSt - kZDist iterations ahead.
+  // Every thread commits one cp.async group per call; a buffer is read only after
+  // cp_async_wait and the CTA barrier that ends the previous iteration.
+  const int lg_cw = __ffs(cw) - 1;
+  const int zgrp = nv_full < 32 ? nv_full : 32;
+  const int zv_ = tid & (nv_full - 1);
+  const int zcb = (zv_ & ~(zgrp - 1)) * VEC, zln = zv_ & (zgrp - 1);
+  auto zissue = [&](int i) {
+    const long long t = first + (long long)i * stride;
+    if (t < a.ntiles) {
+      const int si = i % kSt;
+      mbar_wait(&full[si], (uint32_t)(i / kSt) & 1);
+      const uint64_t* sD =
+          reinterpret_cast<const uint64_t*>(stages + (size_t)si * stage_bytes + zd_off);
+      const long long c0 = t * cw;
+      const int width = (int)min((long long)cw, a.d - c0);
+      double* zb = zbuf + (size_t)(i % kZBufs) * a.zslots;
+      const int gi = (int)(((c0 + zcb) >> kZGroupLog2) - (c0 >> kZGroupLog2));
+      const int total = L << log2_nv;
+      if (zcb + zln < width) {
+        for (int idx = tid; idx < total; idx += kThreads) {
+          const int j = idx >> log2_nv;
+          const uint64_t d0 = sD[j * a.zdcols + 2 * gi], d1 = sD[j * a.zdcols + 2 * gi + 1];
+          ZDesc gd;
+          gd.zb = (long long)d0;
+          gd.dz = (int)(uint32_t)d1;
+          gd.brk = (int)(uint32_t)(d1 >> 32);
+#pragma unroll
+          for (int e = 0; e < VEC; e++) {
+            const int c = zcb + zln + zgrp * e;
+            if (c < width)
+              cp_async_8(zb + (j << lg_cw) + c, a.z.scratch + z_index(a.z, gd, c0 + c));
+          }
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  if constexpr (ZM) {
+    for (int i = 0; i < kZDist; i++) zissue(i);
+    cp_async_wait<kZDist - 1>();
+    __syncthreads();
+  }
+
   int it = 0;
   for (long long t = first; t < a.ntiles; t += stride, ++it) {
-    const int s = it % kStages;
-    const uint32_t parity = (it / kStages) & 1;
+    const int s = it % kSt;
+    const uint32_t parity = (it / kSt) & 1;
+    if constexpr (ZM) zissue(it + kZDist);
     const long long c0 = t * cw;
     const int width = (int)min((long long)cw, a.d - c0);
     const T* sW = reinterpret_cast<const T*>(stages + (size_t)s * stage_bytes);
@@ -305,13 +421,13 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     if (tid == 0 && t + stride >= a.ntiles) pdl_launch_dependents();
     mbar_wait(&full[s], parity);
 
-    if (MODE != kRing) {
+    if (!mode_ring(MODE)) {
       // numpy pairwise mean per column over the L staged rows: one thread per
       // column keeps numpy's 8 partial sums r[0..7] (8 <= n <= 128) in
       // registers (8 independent add chains) and combines them in numpy's
       // order ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail.  Lanes
       // read consecutive columns of one staged row: no bank conflicts.
-      const T* src = (MODE == kMean) ? sW : sG;
+      const T* src = (MODE == kSpsgd) ? sG : sW;
       const int groups = cw <= kThreads / 2 ? min(8, kThreads / cw) : 1;
       // 2-byte elements: a thread owns a column pair (one 32-bit shared load
       // feeds two columns' chains, full 128-byte wavefronts per warp)
@@ -388,73 +504,134 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     // mean modes: a thread's column vector is the same for all its items (the
     // host guarantees nv_full divides the CTA size), so its means are read once
     A ma[VEC];
-    if (MODE != kRing) {
+    if (!mode_ring(MODE)) {
       double mv[VEC];
       load_means<VEC>(s_mean, (tid & (nv_full - 1)) * VEC, mv);
 #pragma unroll
       for (int e = 0; e < VEC; e++) ma[e] = (A)mv[e];
     }
-#pragma unroll kRingUnroll
-    for (int idx = tid; idx < total; idx += kThreads) {
-      const int j = idx >> log2_nv;
-      const int v = idx & (nv_full - 1);
-      if (v >= nv) continue;
-      const int c = v * VEC;
-      Vec<T> y;
-      if (MODE == kRing) {
-        const int4 tri = s_tri[j];
-        Vec<T> va, vb, vc, vg;
-        va.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.x, c));
-        vb.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.y, c));
-        vc.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.z, c));
-        if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
-#pragma unroll
-        for (int e = 0; e < VEC; e++) {
-          A m = ring3<A>(widen<T>(va.e(), e), widen<T>(vb.e(), e), widen<T>(vc.e(), e));
-          if (HAS_G) m = r_sub(m, r_mul(lr, widen<T>(vg.e(), e)));
-          y.e()[e] = E::st(m);
-        }
-      } else if (MODE == kMean) {
-        Vec<T> vg;
-        if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
-#pragma unroll
-        for (int e = 0; e < VEC; e++) {
-          A m = ma[e];
-          if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
-          y.e()[e] = E::st(m);
-        }
-      } else {  // kSpsgd
-        Vec<T> vw, w0;
-        vw.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
-        w0.raw = *reinterpret_cast<const uint4*>(sW + sidx(0, c));
-        bool diff = false;
-#pragma unroll
-        for (int e = 0; e < VEC; e++) {
-          if (c + e < width) diff |= !(vw.e()[e] == w0.e()[e]);
-          A m = ma[e];
-          y.e()[e] = E::st(r_sub((A)E::ld(vw.e(), e), r_mul(lr, m)));
-        }
-        if (diff && a.mismatch) atomicOr(a.mismatch, 1u);
+    // Z modes: lam / w* (and the means) of the thread's columns, the same for all its items
+    double zlam[ZM ? VEC : 1], zopt[ZM ? VEC : 1];
+    if constexpr (ZM) {
+      const double* sLam = reinterpret_cast<const double*>(stages + (size_t)s * stage_bytes + zl_off);
+      const double* sOpt = reinterpret_cast<const double*>(stages + (size_t)s * stage_bytes + zo_off);
+      const int cv = (tid & (nv_full - 1)) * VEC;
+      if (cv < width) {
+        load_means<VEC>(sLam, cv, zlam);
+        load_means<VEC>(sOpt, cv, zopt);
       }
-      T* dst = out + (long long)j * a.ldo + c0 + c;
-      if (c + VEC <= width) {
+    }
+    if constexpr (ZM) {
+      const double* zb = zbuf + (size_t)(it % kZBufs) * a.zslots;
+#pragma unroll kRingUnroll
+      for (int idx = tid; idx < total; idx += kThreads) {
+        const int j = idx >> log2_nv;
+        const int v = idx & (nv_full - 1);
+        if (v >= nv) continue;
+        const int c = v * VEC;
+        // Phi row j: its own staged tile, or W's row j (Phi = W)
+        Vec<T> vp, y;
+        vp.raw = *reinterpret_cast<const uint4*>((HAS_G ? sG : sW) + sidx(j, c));
+        double zv[VEC];
+        load_means<VEC>(zb + (j << lg_cw), c, zv);
+        A m[VEC];
+        if (MODE == kRingZ) {
+          const int4 tri = s_tri[j];
+          Vec<T> va, vb, vc;
+          va.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.x, c));
+          vb.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.y, c));
+          vc.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.z, c));
 #pragma unroll
-        for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
-        st_cs_v4(dst, y.raw);
-      } else {
+          for (int e = 0; e < VEC; e++)
+            m[e] = ring3<A>(widen<T>(va.e(), e), widen<T>(vb.e(), e), widen<T>(vc.e(), e));
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; e++) m[e] = ma[e];
+        }
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
-          if (c + e < width) {
-            amax = E::amax_acc(amax, y.e()[e]);
-            dst[e] = y.e()[e];
+          const T g = E::st((A)z_grad(zlam[e], zopt[e], a.z.sd, (double)E::ld(vp.e(), e), zv[e]));
+          y.e()[e] = E::st(r_sub(m[e], r_mul(lr, (A)g)));
+        }
+        T* dst = out + (long long)j * a.ldo + c0 + c;
+        if (c + VEC <= width) {
+#pragma unroll
+          for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
+          st_cs_v4(dst, y.raw);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; e++) {
+            if (c + e < width) {
+              amax = E::amax_acc(amax, y.e()[e]);
+              dst[e] = y.e()[e];
+            }
+          }
+        }
+      }
+    } else {
+#pragma unroll kRingUnroll
+      for (int idx = tid; idx < total; idx += kThreads) {
+        const int j = idx >> log2_nv;
+        const int v = idx & (nv_full - 1);
+        if (v >= nv) continue;
+        const int c = v * VEC;
+        Vec<T> y;
+        if (MODE == kRing) {
+          const int4 tri = s_tri[j];
+          Vec<T> va, vb, vc, vg;
+          va.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.x, c));
+          vb.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.y, c));
+          vc.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.z, c));
+          if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
+#pragma unroll
+          for (int e = 0; e < VEC; e++) {
+            A m = ring3<A>(widen<T>(va.e(), e), widen<T>(vb.e(), e), widen<T>(vc.e(), e));
+            if (HAS_G) m = r_sub(m, r_mul(lr, widen<T>(vg.e(), e)));
+            y.e()[e] = E::st(m);
+          }
+        } else if (MODE == kMean) {
+          Vec<T> vg;
+          if (HAS_G) vg.raw = *reinterpret_cast<const uint4*>(sG + sidx(j, c));
+#pragma unroll
+          for (int e = 0; e < VEC; e++) {
+            A m = ma[e];
+            if (HAS_G) m = r_sub(m, r_mul(lr, (A)E::ld(vg.e(), e)));
+            y.e()[e] = E::st(m);
+          }
+        } else {  // kSpsgd
+          Vec<T> vw, w0;
+          vw.raw = *reinterpret_cast<const uint4*>(sW + sidx(j, c));
+          w0.raw = *reinterpret_cast<const uint4*>(sW + sidx(0, c));
+          bool diff = false;
+#pragma unroll
+          for (int e = 0; e < VEC; e++) {
+            if (c + e < width) diff |= !(vw.e()[e] == w0.e()[e]);
+            A m = ma[e];
+            y.e()[e] = E::st(r_sub((A)E::ld(vw.e(), e), r_mul(lr, m)));
+          }
+          if (diff && a.mismatch) atomicOr(a.mismatch, 1u);
+        }
+        T* dst = out + (long long)j * a.ldo + c0 + c;
+        if (c + VEC <= width) {
+#pragma unroll
+          for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
+          st_cs_v4(dst, y.raw);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; e++) {
+            if (c + e < width) {
+              amax = E::amax_acc(amax, y.e()[e]);
+              dst[e] = y.e()[e];
+            }
           }
         }
       }
     }
 
-    __syncthreads();  // stage s fully consumed (and s_mean free)
+    if constexpr (ZM) cp_async_wait<kZDist - 1>();  // own copies for the next tile landed
+    __syncthreads();  // stage s fully consumed (and s_mean free); next z buffer visible
     if (tid == 0) {
-      long long tn = t + (long long)kStages * stride;
+      long long tn = t + (long long)kSt * stride;
       if (tn < a.ntiles) issue(s, tn);
     }
   }
@@ -477,15 +654,25 @@ static int launch_scalar(const MixArgs& a, long long c_begin, cudaStream_t st) {
 }
 
 static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode,
-                             int kThreads) {
+                             int kThreads, int zdcols = 0, int zslots = 0) {
   size_t stage = (size_t)L * cw * elem * (stage_g ? 2 : 1);
+  if (mode_z(mode)) {
+    // descriptor and lam / w* tiles per stage (128-byte aligned pieces), kZStages stages,
+    // the mean region at full size (see the kernel), kZBufs normal buffers
+    auto r128 = [](size_t x) { return (x + 127) & ~(size_t)127; };
+    stage = r128(stage) + r128((size_t)L * zdcols * 8) + 2 * r128((size_t)cw * 8);
+    size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kZStages * stage;
+    const size_t acc = elem == 2 ? sizeof(float) : sizeof(double);
+    if (!mode_ring(mode)) bytes += ((size_t)cw * sizeof(double) + 8 * cw * acc + 15) / 16 * 16;
+    return bytes + (size_t)kZBufs * zslots * sizeof(double);
+  }
   size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kStages * stage;
   // per-column means, plus [8][cw] partial sums when the mean phase splits a
   // column's 8 chains over several threads (see the mean phase)
   const bool split = cw <= kThreads / 2 || (elem == 2 && cw <= kThreads);
   // (the partials are in the accumulation type: float for 2-byte elements)
   const size_t acc = elem == 2 ? sizeof(float) : sizeof(double);
-  if (mode != kRing) bytes += (size_t)cw * sizeof(double) + (split ? 8 * cw * acc : 0);
+  if (!mode_ring(mode)) bytes += (size_t)cw * sizeof(double) + (split ? 8 * cw * acc : 0);
   return bytes;
 }
 
@@ -505,7 +692,10 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
       reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.out) |
       (stage_g ? reinterpret_cast<uintptr_t>(a.G) : 0) | (uintptr_t)(a.ldw * esz) |
       (uintptr_t)(a.ldo * esz) | (stage_g ? (uintptr_t)(a.ldg * esz) : 0);
-  const bool aligned = (align_bits & 15) == 0;
+  const uintptr_t z_bits = mode_z(MODE) ? reinterpret_cast<uintptr_t>(a.z.lam) |
+                                              reinterpret_cast<uintptr_t>(a.z.wopt)
+                                        : 0;
+  const bool aligned = ((align_bits | z_bits) & 15) == 0;
   static int max_optin = -1;
   if (max_optin < 0) {
     int dev = 0;
@@ -513,7 +703,7 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
   // the tiled mean phase covers numpy's non-recursive pairwise case (8 <= L <= 128)
-  const bool mean_ok = MODE == kRing || (a.L >= 8 && a.L <= 128);
+  const bool mean_ok = mode_ring(MODE) || (a.L >= 8 && a.L <= 128);
   bool use_tma = aligned && mean_ok && a.L <= kMaxTmaL && a.d >= VEC && a.d < (1LL << 31) &&
                  tma_encode_fn() != nullptr;
   int cw = 0;
@@ -523,7 +713,7 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     size_t per_col = (size_t)a.L * esz * (stage_g ? 2 : 1);
     cw = VEC;
     size_t target = NT == kRingThreads ? kStageTarget
-                                       : (MODE == kRing ? kSmallRingStageTarget : kMeanStageTarget);
+                                       : (mode_ring(MODE) ? kSmallRingStageTarget : kMeanStageTarget);
     // bf16 ring tiles: 32 KB stages (128 columns at L = 64) measured 0.93 of HBM at C2
     // against 0.84 with 64 KB (256 columns) — tools/gpu_bf16_sweep.sh
     if (NT == kRingThreads && esz == 2) target = kStageTarget / 2;
@@ -532,20 +722,40 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
       if (kb >= 4 && kb <= 96) target = (size_t)kb * 1024;
     }
     while ((size_t)(cw * 2) * per_col <= target && cw * 2 <= 2048) cw *= 2;
+    if (mode_z(MODE)) {
+      // Z modes: a z buffer holds L * cw normals (kZTileRing / kZTileMean)
+      const int zt = NT == kRingThreads ? kZTileRing : kZTileMean;
+      cw = VEC;
+      while (a.L * cw * 2 <= zt && cw * 2 <= 2048) cw *= 2;
+    }
     const long long want_tiles = 4LL * sm_count(-1);
     while (cw > VEC && (a.d + cw - 1) / cw < want_tiles && cw * esz > 256) cw /= 2;
     if (const char* env = getenv("RINGMIX_TILE_COLS")) {  // tuning override
       int v = atoi(env);
       if (v >= VEC && (v & (v - 1)) == 0) cw = v;
     }
+  }
+  if (use_tma) {
     const size_t cap = NT == kRingThreads ? (size_t)max_optin : (size_t)(max_optin / 2 - 1024);
-    if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT) > cap) use_tma = false;
+    for (;;) {
+      if (mode_z(MODE)) {
+        a.zdcols = 2 * (cw >> kZGroupLog2 > 1 ? cw >> kZGroupLog2 : 1);
+        a.zslots = a.L * cw;   // one [L][cw] tile of normals per z buffer
+      }
+      if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT, a.zdcols, a.zslots) <= cap) break;
+      // Z modes with Phi staged separately: narrower tiles until the stages fit
+      if (!mode_z(MODE) || cw <= VEC) {
+        use_tma = false;
+        break;
+      }
+      cw /= 2;
+    }
   }
   if (!use_tma) return launch_scalar<T, MODE, HAS_G>(a, 0, st);
-
   int nv = cw / VEC, lg = 0;
   while ((1 << lg) < nv) lg++;
-  // mean modes read a thread's column means once per tile (see the kernel)
+
+  // mean and Z modes read a thread's column means / lam / w* once per tile (see the kernel)
   if (MODE != kRing && (1 << lg) > NT) return launch_scalar<T, MODE, HAS_G>(a, 0, st);
   a.cw = cw;
   a.d_main = a.d;
@@ -566,7 +776,20 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   } else {
     tmG = tmW;
   }
-  size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT);
+  CUtensorMap tmD = tmW, tmLam = tmW, tmOpt = tmW;
+  if (mode_z(MODE)) {
+    // normal descriptors as a [L][2 * ngroups] uint64 matrix, box [L][zdcols]; lam and
+    // w* as one-row fp64 matrices (zero fill past d), boxes of box_c columns
+    const long long ld1 = (a.d + 1) & ~1LL;
+    if (!tma_map_2d<uint64_t>(&tmD, a.z.desc, 2 * a.z.ngroups, a.L, 2 * a.z.ngroups, a.zdcols,
+                              box_r) ||
+        !tma_map_2d<double>(&tmLam, a.z.lam, a.d, 1, ld1, box_c, 1) ||
+        !tma_map_2d<double>(&tmOpt, a.z.wopt, a.d, 1, ld1, box_c, 1)) {
+      set_error("cuTensorMapEncodeTiled failed for the fused gradient's tables");
+      return RM_EINVAL;
+    }
+  }
+  size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT, a.zdcols, a.zslots);
   static unsigned long long attr_set_mask = 0;
   if (attr_needed(&attr_set_mask)) {
     cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT>,
@@ -577,7 +800,7 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   long long grid = (long long)sm_count(-1) * (512 / NT);
   if (grid > a.ntiles) grid = a.ntiles;
   cudaError_t e = launch_pdl(mix_tma_kernel<T, MODE, HAS_G, NT>, dim3((unsigned)grid), dim3(NT),
-                             smem, st, a, tmW, tmG);
+                             smem, st, a, tmW, tmG, tmD, tmLam, tmOpt);
   if (e != cudaSuccess) return fail_cuda(e, "mix_tma_kernel");
   return RM_OK;
 }
@@ -585,7 +808,8 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
 template <typename T, int MODE>
 static int dispatch(const void* W, const void* G, void* out, int L, long long d, long long ldw,
                     long long ldg, long long ldo, const int32_t* left, const int32_t* right,
-                    double lr, unsigned long long* absmax, unsigned int* mismatch, void* stream) {
+                    double lr, unsigned long long* absmax, unsigned int* mismatch, void* stream,
+                    const ZSrc* z = nullptr) {
   // d == 0 (empty parameter vectors) is valid and may come with null buffers
   if (L < 1 || d < 0 || (d > 0 && (W == nullptr || out == nullptr))) {
     set_error("invalid arguments: L=%d d=%lld", L, d);
@@ -595,13 +819,13 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
     set_error("leading dimension smaller than d");
     return RM_EINVAL;
   }
-  if (MODE == kRing && L == 3) {
+  if (mode_ring(MODE) && L == 3) {
     // mixing.py:122-124: every entry of the 3-ring equals 1/L, so the
     // reference takes the exact column-mean path.
-    return dispatch<T, kMean>(W, G, out, L, d, ldw, ldg, ldo, nullptr, nullptr, lr, absmax,
-                              nullptr, stream);
+    return dispatch<T, MODE == kRing ? kMean : kMeanZ>(W, G, out, L, d, ldw, ldg, ldo, nullptr,
+                                                       nullptr, lr, absmax, nullptr, stream, z);
   }
-  if (MODE == kRing) {
+  if (mode_ring(MODE)) {
     if (L < 3) {
       set_error("degenerate ring topology: need at least 3 learners, got %d", L);
       return RM_EINVAL;
@@ -614,6 +838,10 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
   if (d == 0) return RM_OK;
   if (MODE == kSpsgd && G == nullptr) {
     set_error("spsgd needs gradients");
+    return RM_EINVAL;
+  }
+  if (mode_z(MODE) && z == nullptr) {
+    set_error("fused gradient step needs the generator's normals");
     return RM_EINVAL;
   }
   if (W == out) {
@@ -634,6 +862,7 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
   a.lr = lr;
   a.absmax = absmax;
   a.mismatch = mismatch;
+  if (z) a.z = *z;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // ring tiles: one 512-thread CTA per SM by default; RINGMIX_RING_NT=256 runs
   // two 256-thread CTAs per SM (tuning experiments)
@@ -648,7 +877,7 @@ static int dispatch(const void* W, const void* G, void* out, int L, long long d,
   const int ring_nt = ring_nt_env == 256 || ring_nt_env == 512 ? ring_nt_env
                                                                : (L <= 32 ? 256 : 512);
   const bool hg = MODE == kSpsgd || G != nullptr;
-  if (MODE != kRing)
+  if (!mode_ring(MODE))
     return hg ? launch_mix<T, MODE, true, kMeanThreads>(a, st)
               : launch_mix<T, MODE, false, kMeanThreads>(a, st);
   if (ring_nt == 256)
@@ -732,3 +961,71 @@ extern "C" int rm_ring_mix_batched_f64(const double* X, double* Y, const int32_t
   RM_CHECK_LAUNCH("ring_batched_kernel");
   return 0;
 }
+
+// ----------------------------------------------------------------------------
+// Training step with the quadratic oracle's gradient fused into the mix (zsrc.cuh):
+// the generator runs up to its normals, then one mix pass produces G in its epilogue.
+// ----------------------------------------------------------------------------
+namespace rm {
+template <typename T>
+static int quad_mix_step(const uint32_t* prefix, int nprefix, uint64_t k, const T* W,
+                         const T* Phi, T* out, const int32_t* left, const int32_t* right, int L,
+                         long long d, long long ldw, long long ldp, long long ldo,
+                         const double* lam, const double* wopt, double sd, double lr,
+                         unsigned long long* absmax, void* ws, long long ws_bytes, void* stream) {
+  if (L < 1 || d < 0 || (d > 0 && (W == nullptr || out == nullptr || lam == nullptr ||
+                                   wopt == nullptr))) {
+    set_error("invalid fused step arguments: L=%d d=%lld", L, d);
+    return RM_EINVAL;
+  }
+  const bool uniform = left == nullptr && right == nullptr;
+  if (!uniform && (left == nullptr || right == nullptr)) {
+    set_error("ring mix needs left/right neighbour tables");
+    return RM_EINVAL;
+  }
+  if (!uniform && L < 3) {
+    set_error("degenerate ring topology: need at least 3 learners, got %d", L);
+    return RM_EINVAL;
+  }
+  if (Phi == W && ldp == ldw) Phi = nullptr;
+  if (Phi != nullptr && ldp < d) {
+    set_error("leading dimension smaller than d");
+    return RM_EINVAL;
+  }
+  if (d == 0) return RM_OK;
+  if (W == out || Phi == out) {
+    set_error("in-place mixing is a read-after-write hazard across learners; use distinct buffers");
+    return RM_EINVAL;
+  }
+  ZSrc z{};
+  int rc = quad_z_prepare(prefix, nprefix, k, L, d, ws, ws_bytes, stream, &z);
+  if (rc) return rc;
+  z.lam = lam;
+  z.wopt = wopt;
+  z.sd = sd;
+  if (uniform)
+    return dispatch<T, kMeanZ>(W, Phi, out, L, d, ldw, ldp, ldo, nullptr, nullptr, lr, absmax,
+                               nullptr, stream, &z);
+  return dispatch<T, kRingZ>(W, Phi, out, L, d, ldw, ldp, ldo, left, right, lr, absmax, nullptr,
+                             stream, &z);
+}
+}  // namespace rm
+
+extern "C" int64_t rm_quadratic_mix_workspace_bytes(int L, int64_t d) {
+  if (L < 1 || d < 0) return -1;
+  return (int64_t)rm::quad_z_workspace_bytes(L, d);
+}
+
+#define RM_DEFINE_QMIX(SUFFIX, CT, T)                                                             \
+  extern "C" int rm_quadratic_mix_step_##SUFFIX(                                                 \
+      const uint32_t* prefix_words, int n_prefix, uint64_t k, const CT* W, const CT* Phi,       \
+      CT* Wout, const int32_t* left, const int32_t* right, int L, int64_t d, int64_t ldw,        \
+      int64_t ldp, int64_t ldo, const double* lam, const double* wopt, double noise_sd,         \
+      double lr, unsigned long long* absmax_bits, void* workspace, int64_t workspace_bytes,     \
+      void* stream) {                                                                            \
+    return rm::quad_mix_step<T>(prefix_words, n_prefix, k, W, Phi, Wout, left, right, L, d, ldw, \
+                                ldp, ldo, lam, wopt, noise_sd, lr, absmax_bits, workspace,       \
+                                workspace_bytes, stream);                                        \
+  }
+RM_DEFINE_QMIX(f32, float, float)
+RM_DEFINE_QMIX(f64, double, double)

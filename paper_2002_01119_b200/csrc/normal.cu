@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "arith.cuh"
 #include "ziggurat_tables.h"
+#include "zsrc.cuh"
 #include <math_constants.h>
 #include "../../include/ringmix_b200.h"
 
@@ -539,11 +540,15 @@ __global__ void __launch_bounds__(128)
 // Sequential repair of blocks whose speculative path did not merge: one
 // thread per stream walks its bad blocks in order and re-simulates from the
 // true entry until the path merges again with the next block's speculation.
+// Blocks the walk passes through that the merge pass had accepted (so they are on
+// neither list) are appended to the merge-failure list `app`, so the fixup regenerates
+// them too.
 __global__ void zig_repair_kernel(ZArgs a, const ZStream* __restrict__ seeds,
                                   const BlockInfo* __restrict__ info, uint32_t* __restrict__ entry,
                                   uint32_t* __restrict__ tcount, const uint8_t* __restrict__ merged,
                                   uint8_t* __restrict__ valid, const uint32_t* __restrict__ nbad,
-                                  const uint64_t* __restrict__ bad) {
+                                  const uint64_t* __restrict__ bad, uint32_t* __restrict__ napp,
+                                  uint64_t* __restrict__ app) {
   __shared__ ZigTables T;
   const uint32_t nb = *nbad;
   if (nb == 0) return;  // uniform: no leftover blocks (the common case)
@@ -589,6 +594,7 @@ __global__ void zig_repair_kernel(ZArgs a, const ZStream* __restrict__ seeds,
         valid[g2] = 1;
         break;  // merged again; later blocks keep their speculative entries
       }
+      if (merged[g2]) app[atomicAdd(napp, 1u)] = (uint64_t)g2;
       b = b + 1;
     }
   }
@@ -875,6 +881,124 @@ extern "C" int64_t rm_normal_workspace_bytes_fast(int nstreams, int64_t n) {
   return base + 256 + nblocks * nstreams * kZBlock * (int64_t)sizeof(double);
 }
 
+namespace rm {
+
+static int z_nblocks(long long n) {
+  return (int)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) / kZBlock) + 8;
+}
+
+// Workspace carve-up shared by every generator entry (the layout rm_normal_stats_offset
+// describes; the scratch and the fused step's tables follow the base layout).
+struct ZWs {
+  BlockInfo* info;
+  unsigned long long* offs;
+  uint32_t* entry;
+  uint32_t* tcount;
+  uint64_t* bad;
+  unsigned long long* total;
+  ZStream* seeds;
+  uint64_t* left;
+  uint8_t* merged;
+  uint32_t* nbad;
+  uint32_t* nleft;
+  uint8_t* valid;
+  double* scratch;   // null: compact layout
+  uint32_t* skip;    // fused step only
+  ZDesc* desc;       // fused step only
+};
+
+static long long z_groups(long long n) { return (n + kZGroup - 1) / kZGroup; }
+
+static ZWs z_carve(const ZArgs& a, void* workspace, bool fast, bool fused) {
+  const long long nb = (long long)a.nblocks * a.nstreams;
+  ZWs w{};
+  char* ws = static_cast<char*>(workspace);
+  w.info = reinterpret_cast<BlockInfo*>(ws);
+  ws += nb * sizeof(BlockInfo);
+  w.offs = reinterpret_cast<unsigned long long*>(ws);
+  ws += nb * 8;
+  w.entry = reinterpret_cast<uint32_t*>(ws);
+  ws += nb * 4;
+  w.tcount = reinterpret_cast<uint32_t*>(ws);
+  ws += nb * 4;
+  w.bad = reinterpret_cast<uint64_t*>(ws);
+  ws += nb * 8;
+  w.total = reinterpret_cast<unsigned long long*>(ws);
+  ws += a.nstreams * 8;
+  ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 63) & ~(uintptr_t)63);
+  w.seeds = reinterpret_cast<ZStream*>(ws);
+  ws += a.nstreams * sizeof(ZStream);
+  w.left = reinterpret_cast<uint64_t*>(ws);
+  ws += nb * 8;
+  w.merged = reinterpret_cast<uint8_t*>(ws);
+  ws += nb;
+  ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 15) & ~(uintptr_t)15);
+  w.nbad = reinterpret_cast<uint32_t*>(ws);
+  w.nleft = w.nbad + 1;
+  ws += 16;
+  // validity of the speculative outputs per block (1 = merged at its true entry)
+  w.valid = reinterpret_cast<uint8_t*>(ws);
+  ws += nb;
+  if (fast) {
+    ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255);
+    w.scratch = reinterpret_cast<double*>(ws);
+    ws += nb * kZBlock * sizeof(double);
+  }
+  if (fused) {
+    w.skip = reinterpret_cast<uint32_t*>(ws);
+    ws += nb * 4;
+    ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 15) & ~(uintptr_t)15);
+    w.desc = reinterpret_cast<ZDesc*>(ws);
+  }
+  return w;
+}
+
+// seeding, speculation, merge, repairs and the per-stream scan (steps 1-3)
+static int z_front(const ZArgs& a, const ZWs& w, cudaStream_t st) {
+  const long long nb = (long long)a.nblocks * a.nstreams;
+  cudaError_t e = cudaMemsetAsync(w.nbad, 0, 8, st);
+  if (e != cudaSuccess) return fail_cuda(e, "cudaMemsetAsync");
+  const int threads = 128;
+  const long long grid = (nb + threads - 1) / threads;
+  zig_seed_kernel<<<(a.nstreams + 63) / 64, 64, 0, st>>>(a, w.seeds);
+  RM_CHECK_LAUNCH("zig_seed_kernel");
+  if (w.scratch)
+    zig_spec_kernel<true><<<(int)grid, threads, 0, st>>>(a, w.seeds, w.info, w.scratch);
+  else
+    zig_spec_kernel<false><<<(int)grid, threads, 0, st>>>(a, w.seeds, w.info, w.scratch);
+  RM_CHECK_LAUNCH("zig_spec_kernel");
+  zig_merge_kernel<<<(int)grid, threads, 0, st>>>(a, w.info, w.entry, w.tcount, w.merged, w.nbad,
+                                                  w.bad);
+  RM_CHECK_LAUNCH("zig_merge_kernel");
+  e = cudaMemcpyAsync(w.valid, w.merged, nb, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return fail_cuda(e, "cudaMemcpyAsync(valid)");
+  // isolated failures in parallel (grid sized for the worst case; idle CTAs exit at once)
+  zig_repair_par_kernel<<<(int)grid, threads, 0, st>>>(a, w.seeds, w.info, w.entry, w.tcount,
+                                                        w.merged, w.valid, w.nbad, w.bad, w.nleft,
+                                                        w.left);
+  RM_CHECK_LAUNCH("zig_repair_par_kernel");
+  zig_repair_kernel<<<(a.nstreams + 31) / 32, 32, 0, st>>>(a, w.seeds, w.info, w.entry, w.tcount,
+                                                           w.merged, w.valid, w.nleft, w.left,
+                                                           w.nbad, w.bad);
+  RM_CHECK_LAUNCH("zig_repair_kernel");
+  zig_scan_kernel<<<a.nstreams, 1024, 0, st>>>(a, w.tcount, w.offs, w.total);
+  RM_CHECK_LAUNCH("zig_scan_kernel");
+  return 0;
+}
+
+static int z_args(ZArgs* a, const uint32_t* prefix, int nprefix, int append, uint64_t k,
+                  int nstreams, long long n) {
+  *a = ZArgs{};
+  for (int i = 0; i < nprefix; i++) a->prefix[i] = prefix[i];
+  a->nprefix = nprefix;
+  a->append = append;
+  a->k = k;
+  a->nstreams = nstreams;
+  a->n = n;
+  a->nblocks = z_nblocks(n);
+  return ensure_jump_tables();
+}
+
 // Quadratic-oracle gradients for all learners of step k (see header).
 template <typename T>
 static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k, int nstreams,
@@ -896,90 +1020,160 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
     set_error("normal workspace too small: need %lld bytes", (long long)need);
     return RM_ERANGE;
   }
-  int rc = ensure_jump_tables();
+  ZArgs a;
+  int rc = z_args(&a, prefix, nprefix, append, k, nstreams, n);
   if (rc) return rc;
-  ZArgs a{};
-  for (int i = 0; i < nprefix; i++) a.prefix[i] = prefix[i];
-  a.nprefix = nprefix;
-  a.append = append;
-  a.k = k;
-  a.nstreams = nstreams;
-  a.n = n;
-  a.nblocks = (int)((1.04 * (double)n + 64.0 * sqrt((double)n + 1.0)) / kZBlock) + 8;
   const long long nb = (long long)a.nblocks * nstreams;
-  char* ws = static_cast<char*>(workspace);
-  BlockInfo* info = reinterpret_cast<BlockInfo*>(ws);
-  ws += nb * sizeof(BlockInfo);
-  unsigned long long* offs = reinterpret_cast<unsigned long long*>(ws);
-  ws += nb * 8;
-  uint32_t* entry = reinterpret_cast<uint32_t*>(ws);
-  ws += nb * 4;
-  uint32_t* tcount = reinterpret_cast<uint32_t*>(ws);
-  ws += nb * 4;
-  uint64_t* bad = reinterpret_cast<uint64_t*>(ws);
-  ws += nb * 8;
-  unsigned long long* total = reinterpret_cast<unsigned long long*>(ws);
-  ws += nstreams * 8;
-  ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 63) & ~(uintptr_t)63);
-  ZStream* seeds = reinterpret_cast<ZStream*>(ws);
-  ws += nstreams * sizeof(ZStream);
-  uint64_t* left = reinterpret_cast<uint64_t*>(ws);
-  ws += nb * 8;
-  uint8_t* merged = reinterpret_cast<uint8_t*>(ws);
-  ws += nb;
-  ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 15) & ~(uintptr_t)15);
-  uint32_t* nbad = reinterpret_cast<uint32_t*>(ws);
-  uint32_t* nleft = nbad + 1;
-  ws += 16;
-  // validity of the speculative outputs per block (1 = merged at its true entry)
-  uint8_t* valid = reinterpret_cast<uint8_t*>(ws);
-  ws += nb;
-  double* scratch = nullptr;
-  if (workspace_bytes >= rm_normal_workspace_bytes_fast(nstreams, n)) {
-    ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255);
-    scratch = reinterpret_cast<double*>(ws);
-  }
+  const ZWs w = z_carve(a, workspace,
+                        workspace_bytes >= rm_normal_workspace_bytes_fast(nstreams, n), false);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(nbad, 0, 8, st);
-  if (e != cudaSuccess) return fail_cuda(e, "cudaMemsetAsync");
-  const int threads = 128;
-  const long long grid = (nb + threads - 1) / threads;
-  zig_seed_kernel<<<(nstreams + 63) / 64, 64, 0, st>>>(a, seeds);
-  RM_CHECK_LAUNCH("zig_seed_kernel");
-  if (scratch)
-    zig_spec_kernel<true><<<(int)grid, threads, 0, st>>>(a, seeds, info, scratch);
-  else
-    zig_spec_kernel<false><<<(int)grid, threads, 0, st>>>(a, seeds, info, scratch);
-  RM_CHECK_LAUNCH("zig_spec_kernel");
-  zig_merge_kernel<<<(int)grid, threads, 0, st>>>(a, info, entry, tcount, merged, nbad, bad);
-  RM_CHECK_LAUNCH("zig_merge_kernel");
-  e = cudaMemcpyAsync(valid, merged, nb, cudaMemcpyDeviceToDevice, st);
-  if (e != cudaSuccess) return fail_cuda(e, "cudaMemcpyAsync(valid)");
-  // isolated failures in parallel (grid sized for the worst case; idle CTAs exit at once)
-  zig_repair_par_kernel<<<(int)grid, threads, 0, st>>>(a, seeds, info, entry, tcount, merged,
-                                                        valid, nbad, bad, nleft, left);
-  RM_CHECK_LAUNCH("zig_repair_par_kernel");
-  zig_repair_kernel<<<(nstreams + 31) / 32, 32, 0, st>>>(a, seeds, info, entry, tcount, merged,
-                                                         valid, nleft, left);
-  RM_CHECK_LAUNCH("zig_repair_kernel");
-  zig_scan_kernel<<<nstreams, 1024, 0, st>>>(a, tcount, offs, total);
-  RM_CHECK_LAUNCH("zig_scan_kernel");
-  if (scratch) {
+  if ((rc = z_front(a, w, st))) return rc;
+  if (w.scratch) {
     zig_copy_kernel<T><<<(int)((nb * 32 + 255) / 256), 256, 0, st>>>(
-        a, info, entry, tcount, offs, valid, scratch, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+        a, w.info, w.entry, w.tcount, w.offs, w.valid, w.scratch, Phi, ldp, lam, wopt, sd, G, ldg,
+        Z, ldz);
     RM_CHECK_LAUNCH("zig_copy_kernel");
     zig_fixup_kernel<T><<<(int)((2 * nb + 127) / 128), 128, 0, st>>>(
-        a, seeds, entry, offs, valid, nbad, bad, nleft, left, Phi, ldp, lam, wopt, sd, G, ldg, Z,
-        ldz);
+        a, w.seeds, w.entry, w.offs, w.valid, w.nbad, w.bad, w.nleft, w.left, Phi, ldp, lam, wopt,
+        sd, G, ldg, Z, ldz);
     RM_CHECK_LAUNCH("zig_fixup_kernel");
   } else {
     const long long groups = (a.nblocks + kZGenThreads - 1) / kZGenThreads;
     zig_gen_kernel<T><<<(int)(groups * nstreams), kZGenThreads, 0, st>>>(
-        a, seeds, entry, tcount, offs, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
+        a, w.seeds, w.entry, w.tcount, w.offs, Phi, ldp, lam, wopt, sd, G, ldg, Z, ldz);
     RM_CHECK_LAUNCH("zig_gen_kernel");
   }
   return 0;
 }
+
+// ---- fused gradient + mix step (zsrc.cuh) ----
+// Blocks whose speculation did not merge: their true outputs are regenerated into their
+// own scratch slot from index 0 (skip 0 in the descriptors).
+__global__ void __launch_bounds__(128)
+    zig_fixup_scratch_kernel(ZArgs a, const ZStream* __restrict__ seeds,
+                             const uint32_t* __restrict__ entry, const uint8_t* __restrict__ valid,
+                             const uint32_t* __restrict__ nbad, const uint64_t* __restrict__ bad,
+                             const uint32_t* __restrict__ nleft, const uint64_t* __restrict__ left,
+                             double* __restrict__ scratch) {
+  __shared__ ZigTables Tb;
+  const uint32_t n1 = *nbad, n2 = *nleft;
+  if (blockIdx.x * blockDim.x >= n1 + n2) return;  // CTA-uniform
+  load_tables(&Tb);
+  __syncthreads();
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n1 + n2) return;
+  const long long gid = (long long)(i < n1 ? bad[i] : left[i - n1]);
+  if (valid[gid]) return;
+  const int stream = (int)(gid / a.nblocks);
+  const int b = (int)(gid % a.nblocks);
+  const ZStream zs = seeds[stream];
+  uint32_t pos = entry[gid], cnt = 0;
+  ZGen g{z_jump(zs, (uint64_t)b * kZBlock + pos), zs.inc};
+  double* dst = scratch + gid * kZBlock;
+  while (pos < (uint32_t)kZBlock) {
+    double x;
+    int extra;
+    if (z_attempt(Tb, g, g.next64(), &x, &extra)) dst[cnt++] = x;
+    pos += 1 + extra;
+  }
+}
+
+__device__ __forceinline__ uint32_t z_skip_of(const BlockInfo* info, const uint32_t* entry,
+                                              const uint8_t* valid, long long gid) {
+  if (!valid[gid]) return 0u;
+  const uint32_t e = entry[gid];
+  return __popc(info[gid].outs & ((1u << e) - 1u));
+}
+
+// skip per block and the (stream, 128-column group) descriptors of zsrc.cuh: the block
+// that holds a group's first column writes the group's descriptor
+__global__ void __launch_bounds__(256)
+    zig_zindex_kernel(ZArgs a, const BlockInfo* __restrict__ info,
+                      const uint32_t* __restrict__ entry, const uint32_t* __restrict__ tcount,
+                      const unsigned long long* __restrict__ offs,
+                      const uint8_t* __restrict__ valid, uint32_t* __restrict__ skip,
+                      ZDesc* __restrict__ desc, long long ngroups, int force_walk) {
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)a.nstreams * a.nblocks) return;
+  const int stream = (int)(gid / a.nblocks);
+  const int b = (int)(gid % a.nblocks);
+  const uint32_t sk = z_skip_of(info, entry, valid, gid);
+  skip[gid] = sk;
+  const long long lo = (long long)offs[gid], cnt = tcount[gid], hi = lo + cnt;
+  if (cnt == 0 || lo >= a.n) return;
+  for (long long s = (lo + kZGroup - 1) & ~(long long)(kZGroup - 1); s < hi && s < a.n;
+       s += kZGroup) {
+    ZDesc g;
+    g.zb = gid * kZBlock + sk - lo;
+    g.dz = 0;
+    g.brk = kZGroup;
+    const long long e = min(s + kZGroup, a.n);
+    if (force_walk) {
+      g.zb = gid;
+      g.brk = -1;
+    } else if (hi < e) {
+      // the group continues in block b + 1 (which exists: the stream has outputs left)
+      const long long g1 = gid + 1;
+      const long long cnt1 = b + 1 < a.nblocks ? (long long)tcount[g1] : 0;
+      if (cnt1 == 0 || hi + cnt1 < e) {
+        g.zb = gid;   // three or more blocks: walk (zsrc.cuh)
+        g.brk = -1;
+      } else {
+        const long long zb1 = g1 * kZBlock + z_skip_of(info, entry, valid, g1) - hi;
+        g.dz = (int)(zb1 - g.zb);
+        g.brk = (int)(hi - s);
+      }
+    }
+    desc[(long long)stream * ngroups + (s >> kZGroupLog2)] = g;
+  }
+}
+
+long long quad_z_workspace_bytes(int nstreams, long long n) {
+  const int64_t fast = rm_normal_workspace_bytes_fast(nstreams, n);
+  if (fast < 0) return fast;
+  const long long nb = (long long)z_nblocks(n) * nstreams;
+  return fast + nb * 4 + 16 + (long long)nstreams * z_groups(n) * (long long)sizeof(ZDesc);
+}
+
+int quad_z_prepare(const uint32_t* prefix, int nprefix, uint64_t k, int nstreams, long long n,
+                   void* workspace, long long workspace_bytes, void* stream, ZSrc* z) {
+  if (nprefix < 0 || nprefix > kZMaxPrefix || nstreams < 1 || n < 0 || workspace == nullptr) {
+    set_error("invalid fused gradient arguments");
+    return RM_EINVAL;
+  }
+  if (n == 0) return 0;
+  const long long need = quad_z_workspace_bytes(nstreams, n);
+  if (workspace_bytes < need) {
+    set_error("fused gradient workspace too small: need %lld bytes", need);
+    return RM_ERANGE;
+  }
+  ZArgs a;
+  int rc = z_args(&a, prefix, nprefix, 2, k, nstreams, n);
+  if (rc) return rc;
+  const long long nb = (long long)a.nblocks * nstreams;
+  const ZWs w = z_carve(a, workspace, true, true);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = z_front(a, w, st))) return rc;
+  zig_fixup_scratch_kernel<<<(int)((2 * nb + 127) / 128), 128, 0, st>>>(
+      a, w.seeds, w.entry, w.valid, w.nbad, w.bad, w.nleft, w.left, w.scratch);
+  RM_CHECK_LAUNCH("zig_fixup_scratch_kernel");
+  const long long ngroups = z_groups(n);
+  // RINGMIX_ZDESC_WALK=1 (tests): every lookup takes the walk fallback of zsrc.cuh
+  const char* walk = getenv("RINGMIX_ZDESC_WALK");
+  zig_zindex_kernel<<<(int)((nb + 255) / 256), 256, 0, st>>>(
+      a, w.info, w.entry, w.tcount, w.offs, w.valid, w.skip, w.desc, ngroups,
+      walk != nullptr && walk[0] == '1');
+  RM_CHECK_LAUNCH("zig_zindex_kernel");
+  z->scratch = w.scratch;
+  z->desc = w.desc;
+  z->ngroups = ngroups;
+  z->offs = w.offs;
+  z->tcount = w.tcount;
+  z->skip = w.skip;
+  return 0;
+}
+
+}  // namespace rm
 
 extern "C" int rm_quadratic_grad_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k,
                                      int L, int64_t d, const float* Phi, int64_t ldp,

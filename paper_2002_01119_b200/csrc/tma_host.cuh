@@ -35,6 +35,10 @@ struct TmaType<double> {
   static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
 };
 template <>
+struct TmaType<uint64_t> {
+  static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_UINT64;
+};
+template <>
 struct TmaType<__nv_bfloat16> {
   static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 };

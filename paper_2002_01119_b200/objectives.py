@@ -128,6 +128,47 @@ class QuadraticObjective:
                        "rm_quadratic_grad")
         return G
 
+    def device_mix_step(self, W: torch.Tensor, Phi: torch.Tensor | None, tables, lr: float,
+                        cfg, k: int, absmax: torch.Tensor | None = None) -> torch.Tensor:
+        """One training step with this oracle's gradient fused into the mix
+        (rm_quadratic_mix_step_*): apply_mixing(W, T) - lr * G(Phi) with G never written
+        to HBM, bit-identical to ``device_gradients`` followed by the ring / mean step
+        (simulation.py:263-268, objectives.py:84-90).  W, Phi: learner-major (L, d);
+        Phi None = the gradient at W; tables = (left, right) or None (uniform matrix).
+        Returns the learner-major result."""
+        L, d = W.shape
+        if d != self.dimension:
+            raise ValueError(f"W has {d} columns, oracle dimension is {self.dimension}")
+        sfx = {torch.float32: "f32", torch.float64: "f64"}.get(W.dtype)
+        if sfx is None:
+            raise TypeError("the fused gradient step supports float32/float64 weights")
+        lib = _lib.load()
+        ldw = mixing._rows(W, "W")[2]
+        if Phi is None:
+            Phi, ldp = W, ldw
+        else:
+            if Phi.shape != W.shape or Phi.dtype != W.dtype or Phi.device != W.device:
+                raise ValueError("Phi must match W in shape, dtype and device")
+            ldp = mixing._rows(Phi, "Phi")[2]
+        need = int(lib.rm_quadratic_mix_workspace_bytes(L, d))
+        ws = getattr(self, "_ws_fused", None)
+        if ws is None or ws.numel() < need or ws.device != W.device:
+            self._ws_fused = None
+            self._ws_fused = ws = torch.empty(need, dtype=torch.uint8, device=W.device)
+        out = mixing.empty_learner_major(L, d, W.dtype, W.device)
+        lam, opt = self._lam.to(W.device), self._opt.to(W.device)
+        words = seeding.entropy_words(cfg.seed, seeding.TAG_GRADIENT)
+        noise_sd = float(self.noise_scale / np.sqrt(cfg.batch_size))
+        left, right = (None, None) if tables is None else tables
+        fn = getattr(lib, f"rm_quadratic_mix_step_{sfx}")
+        with torch.cuda.device(W.device):
+            _lib.check(fn(words.ctypes.data, len(words), int(k), W.data_ptr(), Phi.data_ptr(),
+                          out.data_ptr(), _lib.ptr(left), _lib.ptr(right), L, d, ldw, ldp,
+                          out.stride(0), lam.data_ptr(), opt.data_ptr(), noise_sd, float(lr),
+                          _lib.ptr(absmax), ws.data_ptr(), ws.numel(), _lib.stream_ptr()),
+                       "rm_quadratic_mix_step")
+        return out
+
     def device_loss_columns(self, X: torch.Tensor) -> torch.Tensor:
         dev = X.to(torch.float64) - self._opt.to(X.device)
         return 0.5 * (self._lam.to(X.device) * dev * dev).sum(dim=1)
