@@ -60,7 +60,7 @@ constexpr int kStages = 3;
 // Z modes: more (smaller) W stages, and the normals of iteration i + kZDist are copied
 // (cp.async, 8 bytes per thread and element) into one of kZBufs shared buffers while
 // iteration i computes
-constexpr int kZStages = 5;
+constexpr int kZStages = 4;
 constexpr int kZDist = 2;
 constexpr int kZBufs = kZDist + 1;
 constexpr int kZTileRing = 4096;   // L * cw per z buffer (fp64 elements): 32 KB
@@ -257,8 +257,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   const int L = a.L;
   const int cw = a.cw;
   const int w_bytes = L * cw * (int)sizeof(T);
-  constexpr bool stage_g = HAS_G || MODE == kSpsgd;
   constexpr bool ZM = mode_z(MODE);
+  // Z modes take a separate Phi through the cp.async buffers, not the stage
+  constexpr bool stage_g = (HAS_G && !ZM) || MODE == kSpsgd;
   constexpr int kSt = ZM ? kZStages : kStages;
   // Z modes: the tile's normal descriptors [L][zdcols] (uint64) and its lam / w* columns
   // (fp64 [cw] each) ride in the stage, each piece 128-byte aligned
@@ -282,6 +283,8 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     tail += a.zslots ? ((size_t)cw * sizeof(double) + 8 * cw * sizeof(A) + 15) / 16 * 16 : 0;
   }
   double* zbuf = ZM ? reinterpret_cast<double*>(tail) : nullptr;  // [kZBufs][zslots]
+  // Z modes with a separate Phi: [kZBufs][L][cw] Phi tiles after the normals
+  T* pbuf = ZM && HAS_G ? reinterpret_cast<T*>(zbuf + (size_t)kZBufs * a.zslots) : nullptr;
 
   T* out = static_cast<T*>(a.out);
   const int tid = threadIdx.x;
@@ -306,7 +309,8 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
       if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
       if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
-      s_tri[j] = make_int4(x0, x1, x2, j);
+      // .w: where learner j itself sits in the sorted triple (Z modes take Phi = W from it)
+      s_tri[j] = make_int4(x0, x1, x2, x0 == j ? 0 : (x1 == j ? 1 : 2));
     }
   }
   __syncthreads();
@@ -364,6 +368,12 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   // Every thread commits one cp.async group per call; a buffer is read only after
   // cp_async_wait and the CTA barrier that ends the previous iteration.
   const int lg_cw = __ffs(cw) - 1;
+  // position of normal column c in a buffer row: with VEC = 4 (fp32) the two column pairs
+  // of a vector live in separate halves of the row, so the consumer's two 16-byte loads
+  // per vector are each lane-contiguous (no shared-memory bank conflicts)
+  auto zpos = [&](int c) -> int {
+    return VEC == 4 ? (((c >> 1) & 1) << (lg_cw - 1)) + ((c >> 2) << 1) + (c & 1) : c;
+  };
   const int zgrp = nv_full < 32 ? nv_full : 32;
   const int zv_ = tid & (nv_full - 1);
   const int zcb = (zv_ & ~(zgrp - 1)) * VEC, zln = zv_ & (zgrp - 1);
@@ -379,6 +389,24 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       double* zb = zbuf + (size_t)(i % kZBufs) * a.zslots;
       const int gi = (int)(((c0 + zcb) >> kZGroupLog2) - (c0 >> kZGroupLog2));
       const int total = L << log2_nv;
+      if constexpr (ZM && HAS_G && sizeof(T) >= 4) {
+        // Phi: the thread's own column vector of each row, 16-byte copies
+        const T* P = static_cast<const T*>(a.G);
+        T* pb = pbuf + (size_t)(i % kZBufs) * a.zslots;
+        const int cv = (tid & (nv_full - 1)) * VEC;
+        if (cv < width) {
+          for (int idx = tid; idx < total; idx += kThreads) {
+            const int j = idx >> log2_nv;
+            const T* src = P + (long long)j * a.ldg + c0 + cv;
+            T* dst = pb + (j << lg_cw) + cv;
+            if (cv + VEC <= width) {
+              cp_async_16(dst, src);
+            } else {
+              for (int e = 0; e < width - cv; e++) cp_async_elem(dst + e, src + e);
+            }
+          }
+        }
+      }
       if (zcb + zln < width) {
         for (int idx = tid; idx < total; idx += kThreads) {
           const int j = idx >> log2_nv;
@@ -391,7 +419,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
           for (int e = 0; e < VEC; e++) {
             const int c = zcb + zln + zgrp * e;
             if (c < width)
-              cp_async_8(zb + (j << lg_cw) + c, a.z.scratch + z_index(a.z, gd, c0 + c));
+              cp_async_8(zb + (j << lg_cw) + zpos(c), a.z.scratch + z_index(a.z, gd, c0 + c));
           }
         }
       }
@@ -529,11 +557,31 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         const int v = idx & (nv_full - 1);
         if (v >= nv) continue;
         const int c = v * VEC;
-        // Phi row j: its own staged tile, or W's row j (Phi = W)
-        Vec<T> vp, y;
-        vp.raw = *reinterpret_cast<const uint4*>((HAS_G ? sG : sW) + sidx(j, c));
+        Vec<T> y;
         double zv[VEC];
-        load_means<VEC>(zb + (j << lg_cw), c, zv);
+        {
+          const double* zr = zb + (j << lg_cw);
+          if (VEC == 4) {
+            const double2 p0 = *reinterpret_cast<const double2*>(zr + (c >> 1));
+            const double2 p1 = *reinterpret_cast<const double2*>(zr + (cw >> 1) + (c >> 1));
+            zv[0] = p0.x;
+            zv[1] = p0.y;
+            zv[VEC > 2 ? 2 : 0] = p1.x;
+            zv[VEC > 3 ? 3 : 0] = p1.y;
+          } else {
+            load_means<VEC>(zr, c, zv);
+          }
+        }
+        // Phi: its cp.async tile, or (Phi = W) learner j's own operand of the ring
+        double phi[VEC];
+        if (HAS_G || MODE == kMeanZ) {
+          Vec<T> vp;
+          vp.raw = HAS_G ? *reinterpret_cast<const uint4*>(
+                               pbuf + (size_t)(it % kZBufs) * a.zslots + (j << lg_cw) + c)
+                         : *reinterpret_cast<const uint4*>(sW + sidx(j, c));
+#pragma unroll
+          for (int e = 0; e < VEC; e++) phi[e] = (double)E::ld(vp.e(), e);
+        }
         A m[VEC];
         if (MODE == kRingZ) {
           const int4 tri = s_tri[j];
@@ -542,15 +590,18 @@ __global__ void __launch_bounds__(NT, 512 / NT)
           vb.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.y, c));
           vc.raw = *reinterpret_cast<const uint4*>(sW + sidx(tri.z, c));
 #pragma unroll
-          for (int e = 0; e < VEC; e++)
-            m[e] = ring3<A>(widen<T>(va.e(), e), widen<T>(vb.e(), e), widen<T>(vc.e(), e));
+          for (int e = 0; e < VEC; e++) {
+            const A xa = widen<T>(va.e(), e), xb = widen<T>(vb.e(), e), xc = widen<T>(vc.e(), e);
+            m[e] = ring3<A>(xa, xb, xc);
+            if (!HAS_G) phi[e] = (double)(tri.w == 0 ? xa : (tri.w == 1 ? xb : xc));
+          }
         } else {
 #pragma unroll
           for (int e = 0; e < VEC; e++) m[e] = ma[e];
         }
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
-          const T g = E::st((A)z_grad(zlam[e], zopt[e], a.z.sd, (double)E::ld(vp.e(), e), zv[e]));
+          const T g = E::st((A)z_grad(zlam[e], zopt[e], a.z.sd, phi[e], zv[e]));
           y.e()[e] = E::st(r_sub(m[e], r_mul(lr, (A)g)));
         }
         T* dst = out + (long long)j * a.ldo + c0 + c;
@@ -654,7 +705,7 @@ static int launch_scalar(const MixArgs& a, long long c_begin, cudaStream_t st) {
 }
 
 static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode,
-                             int kThreads, int zdcols = 0, int zslots = 0) {
+                             int kThreads, int zdcols = 0, int zslots = 0, bool zphi = false) {
   size_t stage = (size_t)L * cw * elem * (stage_g ? 2 : 1);
   if (mode_z(mode)) {
     // descriptor and lam / w* tiles per stage (128-byte aligned pieces), kZStages stages,
@@ -664,7 +715,7 @@ static size_t tma_smem_bytes(int L, int cw, size_t elem, bool stage_g, int mode,
     size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kZStages * stage;
     const size_t acc = elem == 2 ? sizeof(float) : sizeof(double);
     if (!mode_ring(mode)) bytes += ((size_t)cw * sizeof(double) + 8 * cw * acc + 15) / 16 * 16;
-    return bytes + (size_t)kZBufs * zslots * sizeof(double);
+    return bytes + (size_t)kZBufs * zslots * (sizeof(double) + (zphi ? elem : 0));
   }
   size_t bytes = 128 + ((size_t)(L * 16 + 127) / 128) * 128 + kStages * stage;
   // per-column means, plus [8][cw] partial sums when the mean phase splits a
@@ -687,14 +738,15 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const size_t esz = sizeof(T);
-  const bool stage_g = HAS_G || MODE == kSpsgd;
+  const bool stage_g = (HAS_G && !mode_z(MODE)) || MODE == kSpsgd;
   const uintptr_t align_bits =
       reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.out) |
       (stage_g ? reinterpret_cast<uintptr_t>(a.G) : 0) | (uintptr_t)(a.ldw * esz) |
       (uintptr_t)(a.ldo * esz) | (stage_g ? (uintptr_t)(a.ldg * esz) : 0);
-  const uintptr_t z_bits = mode_z(MODE) ? reinterpret_cast<uintptr_t>(a.z.lam) |
-                                              reinterpret_cast<uintptr_t>(a.z.wopt)
-                                        : 0;
+  const uintptr_t z_bits =
+      mode_z(MODE) ? reinterpret_cast<uintptr_t>(a.z.lam) | reinterpret_cast<uintptr_t>(a.z.wopt) |
+                         (HAS_G ? reinterpret_cast<uintptr_t>(a.G) | (uintptr_t)(a.ldg * esz) : 0)
+                   : 0;
   const bool aligned = ((align_bits | z_bits) & 15) == 0;
   static int max_optin = -1;
   if (max_optin < 0) {
@@ -742,7 +794,8 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
         a.zdcols = 2 * (cw >> kZGroupLog2 > 1 ? cw >> kZGroupLog2 : 1);
         a.zslots = a.L * cw;   // one [L][cw] tile of normals per z buffer
       }
-      if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT, a.zdcols, a.zslots) <= cap) break;
+      if (tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT, a.zdcols, a.zslots, HAS_G) <= cap)
+        break;
       // Z modes with Phi staged separately: narrower tiles until the stages fit
       if (!mode_z(MODE) || cw <= VEC) {
         use_tma = false;
@@ -789,7 +842,7 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
       return RM_EINVAL;
     }
   }
-  size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT, a.zdcols, a.zslots);
+  size_t smem = tma_smem_bytes(a.L, cw, esz, stage_g, MODE, NT, a.zdcols, a.zslots, HAS_G);
   static unsigned long long attr_set_mask = 0;
   if (attr_needed(&attr_set_mask)) {
     cudaError_t e = cudaFuncSetAttribute(mix_tma_kernel<T, MODE, HAS_G, NT>,

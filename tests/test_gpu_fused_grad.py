@@ -127,14 +127,31 @@ def test_run_training_fused_equals_unfused(strategy, dtype, monkeypatch):
     oracle = objectives.quadratic_oracle(d, condition_number=20.0, noise_scale=1.0, seed=6)
     cfg = RunConfig(n_learners=L, iterations=9, lr=0.05, batch_size=4, seed=13, log_every=2,
                     dtype=dtype)
-    monkeypatch.setattr(simulation, "FUSED_GRADIENT", True)
+    monkeypatch.setattr(simulation, "FUSED_GRADIENT", "all")
     a = simulation.run_training(strategy, oracle, cfg)
-    monkeypatch.setattr(simulation, "FUSED_GRADIENT", False)
+    monkeypatch.setattr(simulation, "FUSED_GRADIENT", "off")
     b = simulation.run_training(strategy, oracle, cfg)
     assert torch.equal(a.state.weights, b.state.weights)
     assert torch.equal(a.state.last_gradients, b.state.last_gradients)
     assert [r.mean_loss for r in a.records] == [r.mean_loss for r in b.records]
     assert [r.consensus_dist for r in a.records] == [r.consensus_dist for r in b.records]
+
+
+def test_fused_policy():
+    """auto: ring steps at W itself only; all: every gossip step; off: none."""
+    X = torch.empty((4, 8), dtype=torch.float32, device="cuda")
+    o = objectives.quadratic_oracle(8, seed=1)
+    f = simulation._fused_ok
+    assert f(o, X, False) and not f(o, X, False, stale=True) and not f(o, X, False, ring=False)
+    assert not f(o, X, True)
+    assert not f(o, X.to(torch.bfloat16), False)
+    simulation.FUSED_GRADIENT, old = "all", simulation.FUSED_GRADIENT
+    try:
+        assert f(o, X, False, ring=False, stale=True)
+        simulation.FUSED_GRADIENT = "off"
+        assert not f(o, X, False)
+    finally:
+        simulation.FUSED_GRADIENT = old
 
 
 def test_fused_step_argument_errors():

@@ -3,7 +3,8 @@ fp32): gradient pass + ring mix (two passes, G in HBM) against the fused step
 (rm_quadratic_mix_step_*: G produced in the mix kernel's epilogue).  Checks the two agree
 bit for bit, prints median step times.
 
-  python tools/bench_fused_grad.py [L] [d] [reps] [stale]
+  python tools/bench_fused_grad.py [L] [d] [reps] [stale] [uniform]
+uniform=1: the D1D step (uniform matrix) instead of the randomized ring.
 """
 import json
 import os
@@ -17,7 +18,7 @@ from paper_2002_01119_b200 import mixing, objectives, simulation  # noqa: E402
 from paper_2002_01119_b200.simulation import RunConfig  # noqa: E402
 
 
-def main(L=64, d=25_557_032, reps=7, stale=0):
+def main(L=64, d=25_557_032, reps=7, stale=0, uniform=0):
     dev = torch.device("cuda")
     oracle = objectives.quadratic_oracle(d, condition_number=10.0, noise_scale=1.0, seed=1,
                                          optimum=np.zeros(d))
@@ -26,12 +27,14 @@ def main(L=64, d=25_557_032, reps=7, stale=0):
     cfg = RunConfig(n_learners=L, iterations=1, lr=0.01, batch_size=32, seed=5, dtype="float32")
 
     def two_pass(k):
-        tabs = simulation.rad_tables(L, cfg.seed, k, dev)
         G = oracle.device_gradients(X if Phi is None else Phi, cfg, k)
+        if uniform:
+            return mixing.mean_mix_sgd(X, G, 0.01)
+        tabs = simulation.rad_tables(L, cfg.seed, k, dev)
         return mixing.ring_mix_sgd(X, G, 0.01, tabs[0], tabs[1])
 
     def fused(k):
-        tabs = simulation.rad_tables(L, cfg.seed, k, dev)
+        tabs = None if uniform else simulation.rad_tables(L, cfg.seed, k, dev)
         return oracle.device_mix_step(X, Phi, tabs, 0.01, cfg, k)
 
     res = {}
@@ -51,7 +54,8 @@ def main(L=64, d=25_557_032, reps=7, stale=0):
             del out
         res.setdefault(name, []).append(float(np.median(ts)))
     same = bool(torch.equal(two_pass(3), fused(3)))
-    print(json.dumps({"L": L, "d": d, "stale": bool(stale), "step_ms": res,
+    print(json.dumps({"L": L, "d": d, "stale": bool(stale), "uniform": bool(uniform),
+                      "step_ms": res,
                       "bit_identical": same}), flush=True)
 
 
