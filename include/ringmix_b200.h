@@ -27,8 +27,10 @@
  *                         <- the same step on the reference's own (d, L) C-order arrays
  *                            (device or host), ring or uniform T   simulation.py:263-268
  *   rm_quadratic_grad_*   <- simulation.gradient_matrix with   simulation.py:226-238,
- *                            QuadraticObjective.stochastic_   objectives.py:84-90
+ *   (and _shard_*)           QuadraticObjective.stochastic_   objectives.py:84-90
  *                            gradient (bit-exact numpy normals)
+ *   rm_quadratic_mix_step_* <- gradient_matrix + _gossip_step  simulation.py:226-238 +
+ *                            in one pass (G never in HBM)      :263-268 / :304-312
  *   rm_standard_normal_f64 <- seeding.stream(...).standard_normal  seeding.py:35-37
  *   rm_trace_stats_*      <- run_training._record: consensus   simulation.py:398-409,
  *                            distance + loss_columns + loss   :359-362, objectives.py:77-79
@@ -442,6 +444,18 @@ int rm_quadratic_grad_f64(const uint32_t* prefix_words, int n_prefix, uint64_t k
                           int64_t d, const double* Phi, int64_t ldp, const double* lam,
                           const double* wopt, double noise_sd, double* G, int64_t ldg,
                           void* workspace, int64_t workspace_bytes, void* stream);
+/* The same for learners [learner0, learner0 + L) of a learner-sharded run: row l of Phi / G is
+ * learner learner0 + l and draws stream(seed, TAG_GRADIENT, k, learner0 + l). */
+int rm_quadratic_grad_shard_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                                int64_t learner0, int L, int64_t d, const float* Phi, int64_t ldp,
+                                const double* lam, const double* wopt, double noise_sd, float* G,
+                                int64_t ldg, void* workspace, int64_t workspace_bytes,
+                                void* stream);
+int rm_quadratic_grad_shard_f64(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                                int64_t learner0, int L, int64_t d, const double* Phi,
+                                int64_t ldp, const double* lam, const double* wopt,
+                                double noise_sd, double* G, int64_t ldg, void* workspace,
+                                int64_t workspace_bytes, void* stream);
 /* numpy stream(prefix [, k [, s]]).standard_normal(n) for s < nstreams (append = number of
  * trailing entropy ints: 0, 1 = k, 2 = k and the stream index); Z: (nstreams, n) fp64. */
 int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int append, uint64_t k,

@@ -58,6 +58,10 @@ _SIGNATURES = {
     "rm_quadratic_grad_f64": ([vp, i32, u64, i32, i64, vp, i64, vp, vp, dbl, vp, i64, vp, i64, vp],
                               i32),
     "rm_standard_normal_f64": ([vp, i32, i32, u64, i32, i64, vp, i64, vp, i64, vp], i32),
+    "rm_quadratic_grad_shard_f32": ([vp, i32, u64, i64, i32, i64, vp, i64, vp, vp, dbl, vp, i64,
+                                     vp, i64, vp], i32),
+    "rm_quadratic_grad_shard_f64": ([vp, i32, u64, i64, i32, i64, vp, i64, vp, vp, dbl, vp, i64,
+                                     vp, i64, vp], i32),
     "rm_quadratic_mix_workspace_bytes": ([i32, i64], i64),
     "rm_quadratic_mix_step_f32": ([vp, i32, u64, vp, vp, vp, vp, vp, i32, i64, i64, i64, i64, vp,
                                    vp, dbl, dbl, vp, vp, i64, vp], i32),

@@ -63,6 +63,7 @@ struct ZArgs {
   int nstreams;                  // learners
   long long n;                   // normals per stream (d)
   int nblocks;                   // raw blocks per stream
+  long long stream0;             // stream s draws entropy stream0 + s (learner-sharded runs)
 };
 
 __device__ __forceinline__ uint32_t zs_hashmix(uint32_t v, uint32_t& hc) {
@@ -92,7 +93,7 @@ __device__ ZStream z_seed(const ZArgs& a, int stream) {
     }
   };
   if (a.append >= 1) limbs(a.k);
-  if (a.append >= 2) limbs((uint64_t)stream);
+  if (a.append >= 2) limbs((uint64_t)(stream + a.stream0));
   uint32_t pool[4];
   uint32_t hc = 0x43b0d7e5u;
   for (int i = 0; i < 4; i++) pool[i] = zs_hashmix(i < n ? ent[i] : 0u, hc);
@@ -987,7 +988,7 @@ static int z_front(const ZArgs& a, const ZWs& w, cudaStream_t st) {
 }
 
 static int z_args(ZArgs* a, const uint32_t* prefix, int nprefix, int append, uint64_t k,
-                  int nstreams, long long n) {
+                  int nstreams, long long n, long long stream0 = 0) {
   *a = ZArgs{};
   for (int i = 0; i < nprefix; i++) a->prefix[i] = prefix[i];
   a->nprefix = nprefix;
@@ -996,6 +997,7 @@ static int z_args(ZArgs* a, const uint32_t* prefix, int nprefix, int append, uin
   a->nstreams = nstreams;
   a->n = n;
   a->nblocks = z_nblocks(n);
+  a->stream0 = stream0;
   return ensure_jump_tables();
 }
 
@@ -1005,8 +1007,9 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
                      int64_t n,
                      const T* Phi, int64_t ldp, const double* lam, const double* wopt, double sd,
                      T* G, int64_t ldg, double* Z, int64_t ldz, void* workspace,
-                     int64_t workspace_bytes, void* stream) {
+                     int64_t workspace_bytes, void* stream, long long stream0 = 0) {
   if (nprefix < 0 || nprefix > kZMaxPrefix || nstreams < 1 || n < 0 || append < 0 ||
+      stream0 < 0 ||
       append > 2 || (append < 2 && nstreams != 1) ||
       workspace == nullptr || (G != nullptr && (Phi == nullptr || lam == nullptr ||
                                                 wopt == nullptr || ldg < n || ldp < n)) ||
@@ -1021,7 +1024,7 @@ static int quad_grad(const uint32_t* prefix, int nprefix, int append, uint64_t k
     return RM_ERANGE;
   }
   ZArgs a;
-  int rc = z_args(&a, prefix, nprefix, append, k, nstreams, n);
+  int rc = z_args(&a, prefix, nprefix, append, k, nstreams, n, stream0);
   if (rc) return rc;
   const long long nb = (long long)a.nblocks * nstreams;
   const ZWs w = z_carve(a, workspace,
@@ -1136,8 +1139,10 @@ long long quad_z_workspace_bytes(int nstreams, long long n) {
 }
 
 int quad_z_prepare(const uint32_t* prefix, int nprefix, uint64_t k, int nstreams, long long n,
-                   void* workspace, long long workspace_bytes, void* stream, ZSrc* z) {
-  if (nprefix < 0 || nprefix > kZMaxPrefix || nstreams < 1 || n < 0 || workspace == nullptr) {
+                   void* workspace, long long workspace_bytes, void* stream, ZSrc* z,
+                   long long stream0) {
+  if (nprefix < 0 || nprefix > kZMaxPrefix || nstreams < 1 || n < 0 || workspace == nullptr ||
+      stream0 < 0) {
     set_error("invalid fused gradient arguments");
     return RM_EINVAL;
   }
@@ -1148,7 +1153,7 @@ int quad_z_prepare(const uint32_t* prefix, int nprefix, uint64_t k, int nstreams
     return RM_ERANGE;
   }
   ZArgs a;
-  int rc = z_args(&a, prefix, nprefix, 2, k, nstreams, n);
+  int rc = z_args(&a, prefix, nprefix, 2, k, nstreams, n, stream0);
   if (rc) return rc;
   const long long nb = (long long)a.nblocks * nstreams;
   const ZWs w = z_carve(a, workspace, true, true);
@@ -1191,6 +1196,27 @@ extern "C" int rm_quadratic_grad_f64(const uint32_t* prefix_words, int n_prefix,
                                      int64_t workspace_bytes, void* stream) {
   return quad_grad<double>(prefix_words, n_prefix, 2, k, L, d, Phi, ldp, lam, wopt, noise_sd, G, ldg,
                            nullptr, 0, workspace, workspace_bytes, stream);
+}
+
+// Learners [learner0, learner0 + L) of a learner-sharded run (stream index learner0 + l).
+extern "C" int rm_quadratic_grad_shard_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                                           int64_t learner0, int L, int64_t d, const float* Phi,
+                                           int64_t ldp, const double* lam, const double* wopt,
+                                           double noise_sd, float* G, int64_t ldg,
+                                           void* workspace, int64_t workspace_bytes,
+                                           void* stream) {
+  return quad_grad<float>(prefix_words, n_prefix, 2, k, L, d, Phi, ldp, lam, wopt, noise_sd, G, ldg,
+                          nullptr, 0, workspace, workspace_bytes, stream, learner0);
+}
+
+extern "C" int rm_quadratic_grad_shard_f64(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                                           int64_t learner0, int L, int64_t d, const double* Phi,
+                                           int64_t ldp, const double* lam, const double* wopt,
+                                           double noise_sd, double* G, int64_t ldg,
+                                           void* workspace, int64_t workspace_bytes,
+                                           void* stream) {
+  return quad_grad<double>(prefix_words, n_prefix, 2, k, L, d, Phi, ldp, lam, wopt, noise_sd, G,
+                           ldg, nullptr, 0, workspace, workspace_bytes, stream, learner0);
 }
 
 extern "C" int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int append,

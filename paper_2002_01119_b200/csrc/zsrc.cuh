@@ -72,7 +72,8 @@ __device__ __forceinline__ double z_grad(double lam, double wopt, double sd, dou
 // Generator side: run the generator for step k up to the normals (scratch + descriptors)
 // and fill `z` (device pointers into `workspace`).  Defined in normal.cu.
 int quad_z_prepare(const uint32_t* prefix, int nprefix, uint64_t k, int nstreams, long long n,
-                   void* workspace, long long workspace_bytes, void* stream, ZSrc* z);
+                   void* workspace, long long workspace_bytes, void* stream, ZSrc* z,
+                   long long stream0 = 0);
 long long quad_z_workspace_bytes(int nstreams, long long n);
 
 }  // namespace rm

@@ -559,43 +559,68 @@ class LearnerShardedD1DNVLS:
         env = os.environ.get("RINGMIX_D1D_CTAS", "4,2,2").split(",")
         self.ctas_per_sm = tuple(int(x) for x in env)
 
+    def _launch_partial(self, W: torch.Tensor, i: int, stream) -> torch.cuda.Event:
+        """Partial sums of chunk i on `stream`, then (comm stream) the in-switch mean of this
+        rank's slice of it; returns the event after which every rank's means of chunk i are
+        in M."""
+        lib = _lib.load()
+        b, e = self.chunks[i]
+        esz = W.element_size()
+        psum = getattr(lib, f"rm_partial_sum_{mixing._suffix(W)}")
+        _lib.check(psum(W.data_ptr() + b * esz, self.Lg, e - b, W.stride(0),
+                        self.P.data_ptr() + b * 8, stream.cuda_stream), "rm_partial_sum")
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.comm.wait_event(ev)
+        c0, c1 = self.shards[i]
+        with torch.cuda.stream(self.comm):
+            self.hP.barrier(channel=i)          # every rank's partials of chunk i
+            _lib.check(lib.rm_nvls_mean_f64(self.hP.multicast_ptr, self.hM.multicast_ptr,
+                                            c0, c1, self.L, self.comm.cuda_stream),
+                       "rm_nvls_mean_f64")
+            self.hM.barrier(channel=i)          # every rank's means of chunk i
+            done = torch.cuda.Event()
+            done.record(self.comm)
+        return done
+
+    def _launch_apply(self, W, G, lr, out, absmax, i: int, ready, stream) -> None:
+        lib = _lib.load()
+        apply = getattr(lib, f"rm_apply_mean_sgd_{mixing._suffix(W)}")
+        b, e = self.chunks[i]
+        esz = W.element_size()
+        stream.wait_event(ready)
+        # M holds the means already (L = 1: no per-learner division)
+        gp = None if G is None else G.data_ptr() + b * esz
+        _lib.check(apply(self.M.data_ptr() + b * 8, gp, out.data_ptr() + b * esz, self.Lg,
+                         1, e - b, G.stride(0) if G is not None else 0, out.stride(0),
+                         float(lr), _lib.ptr(absmax), stream.cuda_stream),
+                   "rm_apply_mean_sgd")
+
+    def mean_async(self, W: torch.Tensor, stream) -> list[torch.cuda.Event]:
+        """The global column means of W (every rank's learners) into M, launched on
+        `stream` (partial sums) and the comm stream (in-switch reduction); returns one
+        event per chunk.  Pair with ``apply``."""
+        return [self._launch_partial(W, i, stream) for i in range(len(self.chunks))]
+
+    def apply(self, W: torch.Tensor, G: torch.Tensor | None, lr: float, out: torch.Tensor,
+              ready: list[torch.cuda.Event], absmax: torch.Tensor | None = None) -> torch.Tensor:
+        """out = M - lr * G on the current stream, chunk by chunk after `ready`."""
+        compute = torch.cuda.current_stream(self.device)
+        for i in range(len(self.chunks)):
+            self._launch_apply(W, G, lr, out, absmax, i, ready[i], compute)
+        return out
+
     def step(self, W: torch.Tensor, G: torch.Tensor | None, lr: float, out: torch.Tensor,
              absmax: torch.Tensor | None = None) -> torch.Tensor:
         lib = _lib.load()
-        sfx = mixing._suffix(W)
-        psum = getattr(lib, f"rm_partial_sum_{sfx}")
-        apply = getattr(lib, f"rm_apply_mean_sgd_{sfx}")
         compute = torch.cuda.current_stream(self.device)
-        esz = W.element_size()
         ready: list[torch.cuda.Event] = []
 
         def launch_partial(i):
-            b, e = self.chunks[i]
-            _lib.check(psum(W.data_ptr() + b * esz, self.Lg, e - b, W.stride(0),
-                            self.P.data_ptr() + b * 8, compute.cuda_stream), "rm_partial_sum")
-            ev = torch.cuda.Event()
-            ev.record(compute)
-            self.comm.wait_event(ev)
-            c0, c1 = self.shards[i]
-            with torch.cuda.stream(self.comm):
-                self.hP.barrier(channel=i)          # every rank's partials of chunk i
-                _lib.check(lib.rm_nvls_mean_f64(self.hP.multicast_ptr, self.hM.multicast_ptr,
-                                                c0, c1, self.L, self.comm.cuda_stream),
-                           "rm_nvls_mean_f64")
-                self.hM.barrier(channel=i)          # every rank's means of chunk i
-                done = torch.cuda.Event()
-                done.record(self.comm)
-            ready.append(done)
+            ready.append(self._launch_partial(W, i, compute))
 
         def launch_apply(i):
-            b, e = self.chunks[i]
-            compute.wait_event(ready[i])
-            # M holds the means already (L = 1: no per-learner division)
-            gp = None if G is None else G.data_ptr() + b * esz
-            _lib.check(apply(self.M.data_ptr() + b * 8, gp, out.data_ptr() + b * esz, self.Lg,
-                             1, e - b, G.stride(0) if G is not None else 0, out.stride(0),
-                             float(lr), _lib.ptr(absmax), compute.cuda_stream),
-                       "rm_apply_mean_sgd")
+            self._launch_apply(W, G, lr, out, absmax, i, ready[i], compute)
 
         n = len(self.chunks)
         if n > 1:
@@ -748,3 +773,50 @@ class LearnerShardedD1D:
                 launch_apply(i - 1)
         launch_apply(n - 1)
         return out
+
+
+class ShardedD1DTrainer:
+    """One D1D training step of a learner-sharded run with a device oracle
+    (simulation.py:304-312 with gradient_matrix :226-238):
+        W_{k+1}[local] = mean_all(W_k) - lr * G(W_{k-1}[local])
+    The paper's D1D concurrency: the global average of W_k does not
+    depend on the gradient, so with ``overlap`` it runs — partial sums on a side stream,
+    the in-switch reduction on the NVLS comm stream (LearnerShardedD1DNVLS.mean_async) —
+    concurrently with the oracle's gradient of W_{k-1} on the compute stream, and one
+    apply pass finishes the step.  Without it the gradient runs first, then the
+    single-kernel fused D1D step (LearnerShardedD1DFused).  Both give the same bits.
+    learner0: this rank's first learner (its rows draw the gradient streams
+    learner0 + l)."""
+
+    def __init__(self, L: int, d: int, Lg: int, learner0: int, device, oracle, group=None,
+                 overlap: bool | None = None):
+        self.L, self.d, self.Lg, self.learner0 = L, d, Lg, learner0
+        self.device = torch.device(device)
+        self.oracle = oracle
+        if overlap is None:
+            overlap = os.environ.get("RINGMIX_D1D_TRAIN_OVERLAP", "0") == "1"
+        self.overlap = overlap
+        self.nvls = LearnerShardedD1DNVLS(L, d, Lg, device, group=group) if overlap else None
+        self.fused = None if overlap else LearnerShardedD1DFused(L, d, Lg, device, group=group)
+        # high priority: the memory-bound partial sums take SM slots as the compute-bound
+        # generator's CTAs retire instead of queueing behind all of them
+        self.side = torch.cuda.Stream(device=self.device, priority=-1)
+        self.G = None
+
+    def step(self, W: torch.Tensor, W_prev: torch.Tensor, cfg, k: int, lr: float,
+             out: torch.Tensor, absmax: torch.Tensor | None = None) -> torch.Tensor:
+        main = torch.cuda.current_stream(self.device)
+        if self.G is None or self.G.shape != W.shape or self.G.dtype != W.dtype:
+            self.G = mixing.empty_learner_major(self.Lg, self.d, W.dtype, self.device)
+        if not self.overlap:
+            G = self.oracle.device_gradients(W_prev, cfg, k, learner0=self.learner0, out=self.G)
+            return self.fused.step(W, G, lr, out, absmax=absmax)
+        self.side.wait_stream(main)
+        ready = self.nvls.mean_async(W, self.side)
+        G = self.oracle.device_gradients(W_prev, cfg, k, learner0=self.learner0, out=self.G)
+        self.nvls.apply(W, G, lr, out, ready, absmax=absmax)
+        main.wait_stream(self.side)
+        return out
+
+    def close(self):
+        pass

@@ -103,7 +103,10 @@ class QuadraticObjective:
         return self.gradient(w) + noise_sd * z.cpu().numpy()
 
     # ---- device protocol (simulation.gradient_matrix) ----
-    def device_gradients(self, Phi: torch.Tensor, cfg, k: int) -> torch.Tensor:
+    def device_gradients(self, Phi: torch.Tensor, cfg, k: int, learner0: int = 0,
+                         out: torch.Tensor | None = None) -> torch.Tensor:
+        """Gradients of learners [learner0, learner0 + L) at Phi (L, d); learner0 > 0 for a
+        rank's shard of a learner-sharded run (same bits as the rows of the full call)."""
         L, d = Phi.shape
         if d != self.dimension:
             raise ValueError(f"Phi has {d} columns, oracle dimension is {self.dimension}")
@@ -111,7 +114,9 @@ class QuadraticObjective:
         if sfx is None:
             raise TypeError("device quadratic gradients support float32/float64 weights")
         ldp = mixing._rows(Phi, "Phi")[2]
-        G = mixing.empty_learner_major(L, d, Phi.dtype, Phi.device)
+        G = mixing.empty_learner_major(L, d, Phi.dtype, Phi.device) if out is None else out
+        if G.shape != Phi.shape or G.dtype != Phi.dtype or G.device != Phi.device:
+            raise ValueError("out must match Phi in shape, dtype and device")
         need = int(_lib.load().rm_normal_workspace_bytes(L, d))
         if self._ws is None or self._ws.numel() < need or self._ws.device != Phi.device:
             self._ws = None
@@ -120,11 +125,12 @@ class QuadraticObjective:
         lam, opt = self._lam.to(Phi.device), self._opt.to(Phi.device)
         words = seeding.entropy_words(cfg.seed, seeding.TAG_GRADIENT)
         noise_sd = float(self.noise_scale / np.sqrt(cfg.batch_size))
-        fn = getattr(_lib.load(), f"rm_quadratic_grad_{sfx}")
+        fn = getattr(_lib.load(), f"rm_quadratic_grad_shard_{sfx}")
         with torch.cuda.device(Phi.device):
-            _lib.check(fn(words.ctypes.data, len(words), int(k), L, d, Phi.data_ptr(), ldp,
-                          lam.data_ptr(), opt.data_ptr(), noise_sd, G.data_ptr(), G.stride(0),
-                          self._ws.data_ptr(), self._ws.numel(), _lib.stream_ptr()),
+            _lib.check(fn(words.ctypes.data, len(words), int(k), int(learner0), L, d,
+                          Phi.data_ptr(), ldp, lam.data_ptr(), opt.data_ptr(), noise_sd,
+                          G.data_ptr(), G.stride(0), self._ws.data_ptr(), self._ws.numel(),
+                          _lib.stream_ptr()),
                        "rm_quadratic_grad")
         return G
 

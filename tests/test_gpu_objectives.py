@@ -227,3 +227,21 @@ def test_trace_stats_every_kernel_and_many_learners(L, d, no_tma, monkeypatch):
     np.testing.assert_allclose(cons.cpu().numpy(), (dev * dev).sum(axis=0), rtol=1e-11)
     np.testing.assert_allclose(loss_col.cpu().numpy(), oracle.loss_columns(W), rtol=1e-11)
     assert float(avg) == pytest.approx(oracle.loss(W.mean(axis=1)), rel=1e-11)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_sharded_gradients_equal_rows_of_the_full_call(dtype):
+    """rm_quadratic_grad_shard_*: a rank's learners [b, e) draw streams b..e-1, so its
+    gradients are rows b..e-1 of the all-learner call (learner-sharded D1D training)."""
+    L, d, k = 12, 30_001, 4
+    oracle = objectives.quadratic_oracle(d, condition_number=5.0, noise_scale=1.0, seed=2)
+    cfg = RunConfig(n_learners=L, iterations=1, lr=0.1, batch_size=2, seed=17)
+    Phi = mixing.empty_learner_major(L, d, dtype)
+    Phi.copy_(torch.randn((L, d), device="cuda", dtype=torch.float64).to(dtype))
+    full = oracle.device_gradients(Phi, cfg, k).clone()
+    for b, e in ((0, 5), (5, 12), (7, 8)):
+        part = oracle.device_gradients(Phi[b:e], cfg, k, learner0=b)
+        assert torch.equal(part, full[b:e]), (b, e)
+    out = torch.empty_like(Phi[:4])
+    assert oracle.device_gradients(Phi[3:7], cfg, k, learner0=3, out=out) is out
+    assert torch.equal(out, full[3:7])
