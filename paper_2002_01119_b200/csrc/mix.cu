@@ -1050,6 +1050,20 @@ static int quad_mix_step(const uint32_t* prefix, int nprefix, uint64_t k, const 
     set_error("in-place mixing is a read-after-write hazard across learners; use distinct buffers");
     return RM_EINVAL;
   }
+  // Two fused kernels compute the same bits: "tile" produces the gradient in
+  // mix_tma_kernel's epilogue (kRingZ / kMeanZ); "copy" folds the mix into the generator's
+  // output pass (zig_mix_kernel, one warp per raw block, neighbour rows from L2).
+  // Measured at C2: tile for ring steps (15.7 vs 16.7 ms), copy for the
+  // uniform matrix (17.2 vs 18.2 ms); RINGMIX_FUSED_KERNEL=tile|copy overrides.
+  const char* kind = getenv("RINGMIX_FUSED_KERNEL");
+  const bool copy_side = kind && kind[0] ? kind[0] == 'c' : (uniform || L == 3);
+  if (copy_side) {
+    // mixing.py:122-124: the 3-ring is the uniform matrix
+    const bool uni = uniform || L == 3;
+    return quad_mix_copy<T>(prefix, nprefix, k, W, Phi, out, uni ? nullptr : left,
+                            uni ? nullptr : right, L, d, ldw, ldp, ldo, lam, wopt, sd, lr,
+                            absmax, ws, ws_bytes, stream);
+  }
   ZSrc z{};
   int rc = quad_z_prepare(prefix, nprefix, k, L, d, ws, ws_bytes, stream, &z);
   if (rc) return rc;

@@ -906,6 +906,7 @@ struct ZWs {
   double* scratch;   // null: compact layout
   uint32_t* skip;    // fused step only
   ZDesc* desc;       // fused step only
+  double* means;     // fused uniform step (copy side): column means
 };
 
 static long long z_groups(long long n) { return (n + kZGroup - 1) / kZGroup; }
@@ -950,6 +951,9 @@ static ZWs z_carve(const ZArgs& a, void* workspace, bool fast, bool fused) {
     ws += nb * 4;
     ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 15) & ~(uintptr_t)15);
     w.desc = reinterpret_cast<ZDesc*>(ws);
+    ws += (long long)a.nstreams * z_groups(a.n) * (long long)sizeof(ZDesc);
+    ws = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255);
+    w.means = reinterpret_cast<double*>(ws);
   }
   return w;
 }
@@ -1131,11 +1135,170 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- fused gradient + mix, copy side ----
+// One warp per raw block of one stream (stream-fastest order, like zig_copy_kernel): the
+// warp's true normals are read coalesced from the scratch and, for each output column c,
+//   out[j][c] = fl_T( ring3(W[a][c], W[b][c], W[cc][c]) - fl(lr * g) )    (ring)
+//   out[j][c] = fl_T( M[c] - fl(lr * g) )                                 (uniform)
+// with g = fl_T(lam[c] (Phi[j][c] - w*[c]) + sd z) — the operations of the two-pass path.
+// Concurrent warps cover the same column window of every stream (the streams' output
+// offsets differ by a few blocks), so the neighbour rows' W is read from HBM once and
+// served from L2 to the other two readers.
+template <typename T, bool RING, bool PHI>
+__global__ void __launch_bounds__(256)
+    zig_mix_kernel(ZArgs a, const BlockInfo* __restrict__ info, const uint32_t* __restrict__ entry,
+                   const uint32_t* __restrict__ tcount, const unsigned long long* __restrict__ offs,
+                   const uint8_t* __restrict__ valid, const double* __restrict__ scratch,
+                   const T* __restrict__ W, long long ldw, const T* __restrict__ Phi,
+                   long long ldp, const int32_t* __restrict__ left,
+                   const int32_t* __restrict__ right, const double* __restrict__ means,
+                   const double* __restrict__ lam, const double* __restrict__ wopt, double sd,
+                   double lr, T* __restrict__ out, long long ldo,
+                   unsigned long long* __restrict__ absmax) {
+  using E = Elem<T>;
+  using A = typename E::acc;
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  typename E::amax_t amax = 0;
+  if (w < (long long)a.nstreams * a.nblocks) {
+    const int j = (int)(w % a.nstreams);
+    const long long gid = (long long)j * a.nblocks + w / a.nstreams;
+    const unsigned long long base = offs[gid];
+    if (base < (unsigned long long)a.n) {
+      const uint32_t skip = z_skip_of(info, entry, valid, gid);
+      const uint32_t lim = min((unsigned long long)tcount[gid], (unsigned long long)a.n - base);
+      const double* src = scratch + gid * kZBlock + skip;
+      int x0 = j, x1 = j, x2 = j, self = 0;
+      if (RING) {
+        int t;
+        x0 = left[j];
+        x2 = right[j];
+        if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+        if (x2 < x1) { t = x1; x1 = x2; x2 = t; }
+        if (x1 < x0) { t = x0; x0 = x1; x1 = t; }
+        self = x0 == j ? 0 : (x1 == j ? 1 : 2);
+      }
+      const T* wa = W + (long long)x0 * ldw + base;
+      const T* wb = W + (long long)x1 * ldw + base;
+      const T* wc = W + (long long)x2 * ldw + base;
+      const T* ph = PHI ? Phi + (long long)j * ldp + base : W + (long long)j * ldw + base;
+      T* dst = out + (long long)j * ldo + base;
+      // two halves of four 32-column runs: every load of a half is issued before use
+#pragma unroll
+      for (int h = 0; h < kZBlock / 32; h += 4) {
+        double z[4], lm[4], wo[4], mm[4], pv[4];
+        A va[4], vb[4], vc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t i = lane + 32 * (h + q);
+          const bool on = i < lim;
+          const unsigned long long c = base + i;
+          z[q] = on ? __ldcs(src + i) : 0.0;
+          lm[q] = on ? __ldg(lam + c) : 0.0;
+          wo[q] = on ? __ldg(wopt + c) : 0.0;
+          if (RING) {
+            va[q] = on ? (A)E::ld(wa + i, 0) : (A)0;
+            vb[q] = on ? (A)E::ld(wb + i, 0) : (A)0;
+            vc[q] = on ? (A)E::ld(wc + i, 0) : (A)0;
+          } else {
+            mm[q] = on ? __ldg(means + c) : 0.0;
+          }
+          if (PHI || !RING) pv[q] = on ? (double)E::ld(ph + i, 0) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t i = lane + 32 * (h + q);
+          if (i >= lim) continue;
+          A m;
+          double phi;
+          if (RING) {
+            m = ring3<A>(va[q], vb[q], vc[q]);
+            phi = PHI ? pv[q] : (double)(self == 0 ? va[q] : (self == 1 ? vb[q] : vc[q]));
+          } else {
+            m = (A)mm[q];
+            phi = pv[q];
+          }
+          const T g = E::st((A)z_grad(lm[q], wo[q], sd, phi, z[q]));
+          const T y = E::st(r_sub(m, r_mul((A)lr, (A)g)));
+          amax = E::amax_acc(amax, y);
+          __stcs(dst + i, y);
+        }
+      }
+    }
+  }
+  if (absmax) {
+    unsigned long long bits = E::amax_bits(amax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+      bits = other > bits ? other : bits;
+    }
+    if (lane == 0) absmax_publish(absmax, bits);
+  }
+}
+
+template <typename T>
+int quad_mix_copy(const uint32_t* prefix, int nprefix, uint64_t k, const T* W, const T* Phi,
+                  T* out, const int32_t* left, const int32_t* right, int L, long long d,
+                  long long ldw, long long ldp, long long ldo, const double* lam,
+                  const double* wopt, double sd, double lr, unsigned long long* absmax, void* ws,
+                  long long ws_bytes, void* stream) {
+  const long long need = quad_z_workspace_bytes(L, d);
+  if (ws == nullptr || ws_bytes < need) {
+    set_error("fused gradient workspace too small: need %lld bytes", need);
+    return RM_ERANGE;
+  }
+  ZArgs a;
+  int rc = z_args(&a, prefix, nprefix, 2, k, L, d);
+  if (rc) return rc;
+  const long long nb = (long long)a.nblocks * L;
+  const ZWs w = z_carve(a, ws, true, true);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool ring = left != nullptr;
+  if (!ring) {
+    // the uniform step's column means (numpy pairwise order, the two-pass mean's bits)
+    rc = sizeof(T) == 4 ? rm_column_mean_f32(reinterpret_cast<const float*>(W), L, d, ldw,
+                                             w.means, stream)
+                        : rm_column_mean_f64(reinterpret_cast<const double*>(W), L, d, ldw,
+                                             w.means, stream);
+    if (rc) return rc;
+  }
+  if ((rc = z_front(a, w, st))) return rc;
+  zig_fixup_scratch_kernel<<<(int)((2 * nb + 127) / 128), 128, 0, st>>>(
+      a, w.seeds, w.entry, w.valid, w.nbad, w.bad, w.nleft, w.left, w.scratch);
+  RM_CHECK_LAUNCH("zig_fixup_scratch_kernel");
+  const long long grid = (nb * 32 + 255) / 256;
+  auto launch = [&](auto kern) {
+    kern<<<(int)grid, 256, 0, st>>>(a, w.info, w.entry, w.tcount, w.offs, w.valid, w.scratch, W,
+                                     ldw, Phi, ldp, left, right, w.means, lam, wopt, sd, lr, out,
+                                     ldo, absmax);
+  };
+  if (ring) {
+    if (Phi) launch(zig_mix_kernel<T, true, true>);
+    else launch(zig_mix_kernel<T, true, false>);
+  } else {
+    if (Phi) launch(zig_mix_kernel<T, false, true>);
+    else launch(zig_mix_kernel<T, false, false>);
+  }
+  RM_CHECK_LAUNCH("zig_mix_kernel");
+  return 0;
+}
+template int quad_mix_copy<float>(const uint32_t*, int, uint64_t, const float*, const float*,
+                                  float*, const int32_t*, const int32_t*, int, long long,
+                                  long long, long long, long long, const double*, const double*,
+                                  double, double, unsigned long long*, void*, long long, void*);
+template int quad_mix_copy<double>(const uint32_t*, int, uint64_t, const double*, const double*,
+                                   double*, const int32_t*, const int32_t*, int, long long,
+                                   long long, long long, long long, const double*, const double*,
+                                   double, double, unsigned long long*, void*, long long, void*);
+
 long long quad_z_workspace_bytes(int nstreams, long long n) {
   const int64_t fast = rm_normal_workspace_bytes_fast(nstreams, n);
   if (fast < 0) return fast;
   const long long nb = (long long)z_nblocks(n) * nstreams;
-  return fast + nb * 4 + 16 + (long long)nstreams * z_groups(n) * (long long)sizeof(ZDesc);
+  // + the column means of the uniform step (copy-side fused kernel)
+  return fast + nb * 4 + 16 + (long long)nstreams * z_groups(n) * (long long)sizeof(ZDesc) +
+         n * 8 + 256;
 }
 
 int quad_z_prepare(const uint32_t* prefix, int nprefix, uint64_t k, int nstreams, long long n,

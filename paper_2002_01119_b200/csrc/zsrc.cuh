@@ -75,5 +75,12 @@ int quad_z_prepare(const uint32_t* prefix, int nprefix, uint64_t k, int nstreams
                    void* workspace, long long workspace_bytes, void* stream, ZSrc* z,
                    long long stream0 = 0);
 long long quad_z_workspace_bytes(int nstreams, long long n);
+// The fused step on the generator's copy side (zig_mix_kernel): left == nullptr = uniform.
+template <typename T>
+int quad_mix_copy(const uint32_t* prefix, int nprefix, uint64_t k, const T* W, const T* Phi,
+                  T* out, const int32_t* left, const int32_t* right, int L, long long d,
+                  long long ldw, long long ldp, long long ldo, const double* lam,
+                  const double* wopt, double sd, double lr, unsigned long long* absmax, void* ws,
+                  long long ws_bytes, void* stream);
 
 }  // namespace rm

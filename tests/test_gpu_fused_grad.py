@@ -25,6 +25,13 @@ from paper_2002_01119_b200.simulation import RunConfig, Strategy
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["copy", "tile"], autouse=True)
+def fused_kernel(request, monkeypatch):
+    """Both fused kernels (generator-side zig_mix_kernel, mix_tma_kernel's Z modes)."""
+    monkeypatch.setenv("RINGMIX_FUSED_KERNEL", request.param)
+    return request.param
+
+
 def _two_pass(oracle, X, Phi, tables, lr, cfg, k):
     G = oracle.device_gradients(X if Phi is None else Phi, cfg, k)
     absmax = torch.zeros((), dtype=torch.int64, device=X.device)
