@@ -54,6 +54,12 @@ __host__ __device__ constexpr bool mode_z(int m) { return m == kRingZ || m == kM
 #endif
 
 constexpr int kRingUnroll = RM_RING_UNROLL;
+// RM_TMA_STORE (build-time experiment): ring steps with G write W' over their G tile in
+// shared memory and one thread stores the tile with a 2-D tensor-map TMA store; a stage is
+// refilled one tile later, after its store has read it
+#ifndef RM_TMA_STORE
+#define RM_TMA_STORE 0
+#endif
 constexpr int kRingThreads = 512;   // ring tiles: one 512-thread CTA per SM
 constexpr int kMeanThreads = 256;   // mean tiles: two 256-thread CTAs per SM
 constexpr int kStages = 3;
@@ -258,6 +264,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   const int cw = a.cw;
   const int w_bytes = L * cw * (int)sizeof(T);
   constexpr bool ZM = mode_z(MODE);
+  constexpr bool TSTORE = RM_TMA_STORE && MODE == kRing && HAS_G;
   // Z modes take a separate Phi through the cp.async buffers, not the stage
   constexpr bool stage_g = (HAS_G && !ZM) || MODE == kSpsgd;
   constexpr int kSt = ZM ? kZStages : kStages;
@@ -663,7 +670,13 @@ __global__ void __launch_bounds__(NT, 512 / NT)
           if (diff && a.mismatch) atomicOr(a.mismatch, 1u);
         }
         T* dst = out + (long long)j * a.ldo + c0 + c;
-        if (c + VEC <= width) {
+        if (TSTORE) {
+          // over this thread's own G vector (read above); the TMA store clips columns >= d
+          *reinterpret_cast<uint4*>(const_cast<T*>(sG) + sidx(j, c)) = y.raw;
+#pragma unroll
+          for (int e = 0; e < VEC; e++)
+            if (c + e < width) amax = E::amax_acc(amax, y.e()[e]);
+        } else if (c + VEC <= width) {
 #pragma unroll
           for (int e = 0; e < VEC; e++) amax = E::amax_acc(amax, y.e()[e]);
           st_cs_v4(dst, y.raw);
@@ -680,11 +693,27 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     }
 
     if constexpr (ZM) cp_async_wait<kZDist - 1>();  // own copies for the next tile landed
+    if constexpr (TSTORE) fence_proxy_async_smem();  // W' tile visible to the TMA
     __syncthreads();  // stage s fully consumed (and s_mean free); next z buffer visible
     if (tid == 0) {
-      long long tn = t + (long long)kSt * stride;
-      if (tn < a.ntiles) issue(s, tn);
+      if constexpr (TSTORE) {
+        const unsigned char* sg = stages + (size_t)s * stage_bytes + w_bytes;
+        for (int cc = 0; cc < cw; cc += box_c)
+          tma_store_2d(&tmD, sg + cc * L * (int)sizeof(T), (int)(c0 + cc), 0);
+        bulk_commit();
+        if (it > 0) {
+          bulk_wait_read<1>();   // the previous tile's store has read its stage
+          const long long tn = t - stride + (long long)kSt * stride;
+          if (tn < a.ntiles) issue((it - 1) % kSt, tn);
+        }
+      } else {
+        long long tn = t + (long long)kSt * stride;
+        if (tn < a.ntiles) issue(s, tn);
+      }
     }
+  }
+  if constexpr (TSTORE) {
+    if (tid == 0) bulk_wait<0>();
   }
   if (a.absmax) absmax_publish(a.absmax, E::amax_bits(amax));
 }
@@ -830,6 +859,11 @@ static int launch_mix(MixArgs a, cudaStream_t st) {
     tmG = tmW;
   }
   CUtensorMap tmD = tmW, tmLam = tmW, tmOpt = tmW;
+  if (RM_TMA_STORE && MODE == kRing && HAS_G &&
+      !make_map<T>(&tmD, a.out, a.d, a.L, a.ldo, box_c, box_r)) {
+    set_error("cuTensorMapEncodeTiled failed for W'");
+    return RM_EINVAL;
+  }
   if (mode_z(MODE)) {
     // normal descriptors as a [L][2 * ngroups] uint64 matrix, box [L][zdcols]; lam and
     // w* as one-row fp64 matrices (zero fill past d), boxes of box_c columns
