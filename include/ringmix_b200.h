@@ -505,6 +505,26 @@ int rm_trace_stats_bf16(const uint16_t* W, int L, int64_t d, int64_t ld, const d
                         const double* wopt, double* cons_sq, double* loss_col, double* avg_loss,
                         void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Exact-order variant (same outputs, WRITTEN rather than accumulated): numpy's own
+ * summation order, bit for bit — each learner's sums run sequentially over c like the
+ * reference's axis-0 sum and einsum (simulation.py:361, objectives.py:79), the average-model
+ * loss is numpy's pairwise sum (objectives.py:72).  d dependent adds per learner
+ * (latency-bound): meant for small d (run_training's records, sweeps); any L <= 4096.
+ * workspace: device, >= rm_trace_stats_exact_workspace_bytes(d). */
+int64_t rm_trace_stats_exact_workspace_bytes(int64_t d);
+int rm_trace_stats_exact_f32(const float* W, int L, int64_t d, int64_t ld, const double* lam,
+                             const double* wopt, double* cons_sq, double* loss_col,
+                             double* avg_loss, void* workspace, int64_t workspace_bytes,
+                             void* stream);
+int rm_trace_stats_exact_f64(const double* W, int L, int64_t d, int64_t ld, const double* lam,
+                             const double* wopt, double* cons_sq, double* loss_col,
+                             double* avg_loss, void* workspace, int64_t workspace_bytes,
+                             void* stream);
+int rm_trace_stats_exact_bf16(const uint16_t* W, int L, int64_t d, int64_t ld,
+                              const double* lam, const double* wopt, double* cons_sq,
+                              double* loss_col, double* avg_loss, void* workspace,
+                              int64_t workspace_bytes, void* stream);
+
 /* Column means M[c] = (numpy pairwise sum over the L learners) / L, fp64, bit-identical
  * to the mean of rm_mean_sgd_*.  With rm_apply_mean_sgd_*(M, G, out, L, 1, ...) it
  * splits the D1D step so the average of W_k runs on a side stream while the

@@ -74,6 +74,10 @@ _SIGNATURES = {
     "rm_trace_stats_f32": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
     "rm_trace_stats_f64": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
     "rm_trace_stats_bf16": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
+    "rm_trace_stats_exact_workspace_bytes": ([i64], i64),
+    "rm_trace_stats_exact_f32": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
+    "rm_trace_stats_exact_f64": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
+    "rm_trace_stats_exact_bf16": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
     "rm_column_mean_f32": ([vp, i32, i64, i64, vp, vp], i32),
     "rm_column_mean_f64": ([vp, i32, i64, i64, vp, vp], i32),
     "rm_column_mean_bf16": ([vp, i32, i64, i64, vp, vp], i32),

@@ -519,3 +519,181 @@ __global__ void __launch_bounds__(256)
 RM_DEFINE_COLMEAN(f32, float, float)
 RM_DEFINE_COLMEAN(f64, double, double)
 RM_DEFINE_COLMEAN(bf16, uint16_t, __nv_bfloat16)
+
+// ---- exact-order trace reductions: numpy's own summation order, bit for bit ----
+// The reference's reductions over the parameters are sequential in c:
+//   (dev * dev).sum(axis=0)             -> axis-0 reduce of a C-order (d, L) array: one
+//                                          running sum per learner, c = 0, 1, ... (simulation.py:361)
+//   einsum("i,il,il->l", lam, dev, dev)  -> the same, of fl(fl(lam_c dev) dev)  (objectives.py:79)
+// and the average-model loss np.sum(lam * dev * dev) over a contiguous vector is numpy's
+// pairwise sum (objectives.py:72).  A running sum cannot be re-associated without changing
+// its rounding, so each learner's chain is one thread walking its row; the pairwise sum is
+// parallel over the subtrees of numpy's recursion at a fixed depth (every node above that
+// depth has more than 128 values, so it splits exactly as numpy's does) and its top levels
+// are combined in tree order.  Cost: d dependent fp64 adds per learner (latency-bound), so
+// the host uses it for small d (run_training's records, the sweep) and the one-pass kernel above otherwise.
+namespace rm {
+constexpr int kExactMaxDepth = 12;   // at most 4096 pairwise subtrees
+
+__host__ __device__ inline int exact_pairwise_depth(long long d) {
+  int D = 0;
+  while (D < kExactMaxDepth && (d >> (D + 1)) >= 256) D++;
+  return D;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128)
+    trace_exact_rows_kernel(const T* __restrict__ W, int L, long long d, long long ld,
+                            const double* __restrict__ M, const double* __restrict__ lam,
+                            const double* __restrict__ wopt, double* __restrict__ cons_sq,
+                            double* __restrict__ loss_col) {
+  using E = Elem<T>;
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const T* row = W + (long long)l * ld;
+  double cons = 0.0, loss = 0.0;
+  constexpr int U = 8;   // loads of the next columns issued ahead of the two running sums
+  long long c = 0;
+  for (; c + U <= d; c += U) {
+    double w[U], m[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      w[u] = E::ld(row + c + u, 0);
+      m[u] = M[c + u];
+    }
+    if (lam != nullptr) {
+      double lm[U], wo[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        lm[u] = lam[c + u];
+        wo[u] = wopt[c + u];
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const double dw = __dsub_rn(w[u], wo[u]);
+        loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(lm[u], dw), dw));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const double dv = __dsub_rn(w[u], m[u]);
+      cons = __dadd_rn(cons, __dmul_rn(dv, dv));
+    }
+  }
+  for (; c < d; c++) {
+    const double w = E::ld(row + c, 0);
+    const double dv = __dsub_rn(w, M[c]);
+    cons = __dadd_rn(cons, __dmul_rn(dv, dv));
+    if (lam != nullptr) {
+      const double dw = __dsub_rn(w, wopt[c]);
+      loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(lam[c], dw), dw));
+    }
+  }
+  cons_sq[l] = cons;
+  if (loss_col != nullptr) loss_col[l] = __dmul_rn(0.5, loss);
+}
+
+// subtree t of numpy's pairwise recursion over the terms fl(fl(lam_c dm) dm), dm = M_c - w*_c
+__global__ void __launch_bounds__(128)
+    trace_exact_avg_leaves_kernel(const double* __restrict__ M, const double* __restrict__ lam,
+                                  const double* __restrict__ wopt, long long d, int depth,
+                                  double* __restrict__ part) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (1 << depth)) return;
+  long long lo = 0, n = d;
+  for (int j = depth - 1; j >= 0; j--) {   // descend: bit j of t picks the half
+    long long n2 = n / 2;
+    n2 -= n2 % 8;
+    if ((t >> j) & 1) {
+      lo += n2;
+      n -= n2;
+    } else {
+      n = n2;
+    }
+  }
+  auto term = [&](int i) {
+    const long long c = lo + i;
+    const double dm = __dsub_rn(M[c], wopt[c]);
+    return __dmul_rn(__dmul_rn(lam[c], dm), dm);
+  };
+  part[t] = pairwise_sum<double>(term, 0, (int)n);
+}
+
+// the top `depth` levels of the recursion: left + right, level by level
+__global__ void __launch_bounds__(1024)
+    trace_exact_avg_top_kernel(const double* __restrict__ part, int depth,
+                               double* __restrict__ avg_loss) {
+  __shared__ double s[1 << kExactMaxDepth];
+  const int n = 1 << depth;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = part[i];
+  __syncthreads();
+  for (int w = n; w > 1; w >>= 1) {
+    double v[4];
+    const int h = w >> 1;
+    int q = 0;
+    for (int i = threadIdx.x; i < h; i += blockDim.x) v[q++] = __dadd_rn(s[2 * i], s[2 * i + 1]);
+    __syncthreads();
+    q = 0;
+    for (int i = threadIdx.x; i < h; i += blockDim.x) s[i] = v[q++];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *avg_loss = __dmul_rn(0.5, s[0]);
+}
+
+static int64_t trace_exact_workspace_bytes(int64_t d) {
+  return (d + (1LL << kExactMaxDepth)) * (int64_t)sizeof(double);
+}
+
+template <typename T>
+static int trace_stats_exact(const T* W, int L, int64_t d, int64_t ld, const double* lam,
+                             const double* wopt, double* cons_sq, double* loss_col,
+                             double* avg_loss, void* workspace, int64_t workspace_bytes,
+                             void* stream) {
+  if (W == nullptr || cons_sq == nullptr || L < 1 || L > kTrMaxLAny || d < 1 || ld < d ||
+      (lam != nullptr && (wopt == nullptr || loss_col == nullptr || avg_loss == nullptr))) {
+    set_error("invalid exact trace-stat arguments (L=%d, at most %d; d >= 1)", L, kTrMaxLAny);
+    return RM_EINVAL;
+  }
+  if (workspace == nullptr || workspace_bytes < trace_exact_workspace_bytes(d)) {
+    set_error("exact trace-stat workspace too small (need %lld bytes)",
+              (long long)trace_exact_workspace_bytes(d));
+    return RM_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* M = static_cast<double*>(workspace);
+  double* part = M + d;
+  long long blocks = (d + 255) / 256;
+  if (blocks > 16LL * sm_count(-1)) blocks = 16LL * sm_count(-1);
+  column_mean_kernel<T><<<(int)blocks, 256, 0, st>>>(W, L, d, ld, M);
+  RM_CHECK_LAUNCH("column_mean_kernel");
+  trace_exact_rows_kernel<T><<<(L + 127) / 128, 128, 0, st>>>(W, L, d, ld, M, lam, wopt,
+                                                               cons_sq, lam ? loss_col : nullptr);
+  RM_CHECK_LAUNCH("trace_exact_rows_kernel");
+  if (lam != nullptr) {
+    const int depth = exact_pairwise_depth(d);
+    trace_exact_avg_leaves_kernel<<<((1 << depth) + 127) / 128, 128, 0, st>>>(M, lam, wopt, d,
+                                                                             depth, part);
+    RM_CHECK_LAUNCH("trace_exact_avg_leaves_kernel");
+    trace_exact_avg_top_kernel<<<1, 1024, 0, st>>>(part, depth, avg_loss);
+    RM_CHECK_LAUNCH("trace_exact_avg_top_kernel");
+  }
+  return 0;
+}
+}  // namespace rm
+
+extern "C" int64_t rm_trace_stats_exact_workspace_bytes(int64_t d) {
+  if (d < 1) return -1;
+  return trace_exact_workspace_bytes(d);
+}
+
+#define RM_DEFINE_TRACE_EXACT(SUFFIX, CT, T)                                                   \
+  extern "C" int rm_trace_stats_exact_##SUFFIX(                                                \
+      const CT* W, int L, int64_t d, int64_t ld, const double* lam, const double* wopt,         \
+      double* cons_sq, double* loss_col, double* avg_loss, void* workspace,                     \
+      int64_t workspace_bytes, void* stream) {                                                  \
+    return trace_stats_exact<T>(reinterpret_cast<const T*>(W), L, d, ld, lam, wopt, cons_sq,   \
+                                loss_col, avg_loss, workspace, workspace_bytes, stream);       \
+  }
+RM_DEFINE_TRACE_EXACT(f32, float, float)
+RM_DEFINE_TRACE_EXACT(f64, double, double)
+RM_DEFINE_TRACE_EXACT(bf16, uint16_t, __nv_bfloat16)

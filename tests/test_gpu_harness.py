@@ -1,7 +1,6 @@
 """run_sweep on the GPU vs the reference's own sweep artefacts (tests/golden/sweep/):
-same files, same rows, seeds / iterations / simulated times / rho exact, losses and
-consensus within fp64 rounding of the reference (parallel vs sequential sums over the
-parameters), and the device run is byte-stable run to run."""
+same files, same rows, every value (the records reduce in numpy's order for small d), the
+files byte for byte, and the device run is byte-stable run to run."""
 
 from __future__ import annotations
 
@@ -67,3 +66,13 @@ def test_verify_bounds_matches_reference_report():
     np.testing.assert_allclose(rows[:, 4:], ref[:, 4:], rtol=1e-6, atol=1e-6)
     assert rep.ok and "overall: PASS" in str(z["render"])
     assert rep.render().splitlines()[:2] == str(z["render"]).splitlines()[:2]
+
+
+def test_sweep_csvs_are_byte_identical_to_reference(tmp_path):
+    """With the records reduced in numpy's order (rm_trace_stats_exact_*, used for
+    d <= simulation.TRACE_EXACT_MAX_D) every artefact of the sweep — traces, summary,
+    aggregate — is the reference's own file byte for byte (harness.py:115-122)."""
+    harness.run_sweep(CFG, tmp_path / "a", quiet=True)
+    diff = [p.name for p in sorted(GOLD.glob("*.csv"))
+            if (tmp_path / "a" / p.name).read_bytes() != p.read_bytes()]
+    assert not diff, diff

@@ -131,7 +131,7 @@ def test_fused_trace_stats_match_reference_formulas(L, d, dtype):
     g = torch.Generator(device="cuda").manual_seed(5)
     X = mixing.empty_learner_major(L, d, dtype)
     X.copy_(torch.randn((L, d), generator=g, device="cuda", dtype=torch.float64).to(dtype))
-    cons_sq, loss_col, avg = simulation.trace_stats(X.T, oracle)
+    cons_sq, loss_col, avg = simulation.trace_stats(X.T, oracle, exact=False)
     W = X.double().cpu().numpy().T              # reference (d, L) layout
     dev = W - W.mean(axis=1, keepdims=True)
     assert np.allclose(cons_sq.cpu().numpy(), (dev * dev).sum(axis=0), rtol=1e-12)
@@ -139,6 +139,33 @@ def test_fused_trace_stats_match_reference_formulas(L, d, dtype):
     assert np.isclose(float(avg), oracle.loss(W.mean(axis=1)), rtol=1e-12)
     assert simulation.consensus_distance(X.T) == pytest.approx(
         float(np.sqrt((dev * dev).sum(axis=0).max())), rel=1e-12)
+
+
+@pytest.mark.parametrize("L,d,dtype", [(4, 24, torch.float64), (8, 1000, torch.float64),
+                                       (3, 1, torch.float64), (5, 7, torch.float64),
+                                       (16, 100_003, torch.float64), (130, 2_000, torch.float64),
+                                       (64, 70_001, torch.float32), (16, 3_000, torch.bfloat16)])
+def test_exact_trace_stats_are_bitwise_numpy(L, d, dtype, monkeypatch):
+    """rm_trace_stats_exact_*: numpy's own summation order, so the record values are the
+    reference's bits (simulation.py:359-362, 398-409; objectives.py:72-79): the axis-0 sum
+    and the einsum run sequentially over the parameters, the average-model loss is numpy's
+    pairwise sum (split over the subtrees of its recursion on the GPU)."""
+    oracle = objectives.quadratic_oracle(d, condition_number=9.0, noise_scale=1.0, seed=L)
+    g = torch.Generator(device="cuda").manual_seed(d)
+    X = mixing.empty_learner_major(L, d, dtype)
+    X.copy_((torch.randn((L, d), generator=g, device="cuda", dtype=torch.float64)
+             * torch.exp(2 * torch.randn((1, d), generator=g, device="cuda",
+                                         dtype=torch.float64))).to(dtype))
+    cons_sq, loss_col, avg = simulation.trace_stats(X.T, oracle, exact=True)
+    W = X.double().cpu().numpy().T.copy()       # the reference's (d, L) C-order array
+    dev = W - W.mean(axis=1, keepdims=True)
+    assert np.array_equal(cons_sq.cpu().numpy(), (dev * dev).sum(axis=0))
+    assert np.array_equal(loss_col.cpu().numpy(), oracle.loss_columns(W))
+    assert float(avg) == oracle.loss(W.mean(axis=1))
+    monkeypatch.setenv("RINGMIX_TRACE_EXACT", "1")
+    assert simulation.consensus_distance(X.T) == float(np.sqrt((dev * dev).sum(axis=0).max()))
+    c2, l2, a2 = simulation.trace_stats(X.T, None, exact=True)
+    assert torch.equal(c2, cons_sq) and l2 is None and a2 is None
 
 
 @pytest.mark.parametrize("side_stream", [True, False])
@@ -179,9 +206,9 @@ def test_trace_stats_tiled_and_generic_kernels_agree(dtype, monkeypatch):
         oracle = objectives.quadratic_oracle(d, condition_number=3.0, noise_scale=0.0, seed=L)
         X = mixing.empty_learner_major(L, d, dtype, "cuda").normal_()
         monkeypatch.delenv("RINGMIX_TRACE_NO_TMA", raising=False)
-        a = simulation.trace_stats(X.T, oracle)
+        a = simulation.trace_stats(X.T, oracle, exact=False)
         monkeypatch.setenv("RINGMIX_TRACE_NO_TMA", "1")
-        b = simulation.trace_stats(X.T, oracle)
+        b = simulation.trace_stats(X.T, oracle, exact=False)
         for x, y in zip(a, b):
             assert torch.allclose(x, y, rtol=1e-12, atol=1e-12)
         # and the reference's formulas on the host
@@ -203,9 +230,9 @@ def test_trace_stats_are_deterministic(no_tma, monkeypatch):
     L, d = 64, 3_000_017
     oracle = objectives.quadratic_oracle(d, condition_number=7.0, noise_scale=0.0, seed=2)
     X = mixing.empty_learner_major(L, d, torch.float32, "cuda").normal_()
-    first = simulation.trace_stats(X.T, oracle)
+    first = simulation.trace_stats(X.T, oracle, exact=False)
     for _ in range(5):
-        again = simulation.trace_stats(X.T, oracle)
+        again = simulation.trace_stats(X.T, oracle, exact=False)
         for x, y in zip(first, again):
             assert torch.equal(x, y)
 
