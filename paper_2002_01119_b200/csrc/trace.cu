@@ -360,11 +360,257 @@ __global__ void __launch_bounds__(kTrThreads, 2)
   }
 }
 
+// Compile-time-shaped variant for L in {8, 16, 32, 64, 128} (the configs' learner
+// counts): the tile [L x CW] is one TMA box, every shared-memory offset is an immediate,
+// full tiles run without column checks, and phase B's items are independent
+// accumulator chains the compiler can interleave (the runtime-L kernel above keeps a
+// branch per item, which serialised them: ncu showed fixed-latency `wait` stalls first).
+// Phase A: TPC = 256 / CW threads per column, each summing CPT = 8 / TPC of numpy's eight
+// interleaved chains; the chains' tree ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) is finished
+// inside the thread and then across the column's threads with xor shuffles (IEEE addition
+// commutes, so only the tree matters).  L is a power of two: sum / L == sum * (1 / L).
+template <typename T, int L>
+struct TrShape {
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  static constexpr int CW0 = kTrStageTarget / (L * (int)sizeof(T));
+  static constexpr int CW = CW0 > 256 ? 256 : CW0;
+  static constexpr int NV = CW / VEC;
+  static constexpr int ITEMS = L * NV / kTrThreads;
+  static constexpr int ROW_STEP = kTrThreads / NV;
+  static constexpr int TPC = kTrThreads / CW;
+  static constexpr int CPT = 8 / TPC;
+  static constexpr int NCW = 32 / TPC;
+  static constexpr int STAGE = L * CW * (int)sizeof(T);
+  static_assert(L % 8 == 0 && L <= 128, "numpy's 8-chain form");
+  static_assert(TPC >= 1 && TPC <= 8 && ITEMS >= 1 && L * NV == ITEMS * kTrThreads, "shape");
+};
+
+template <typename T, int L>
+__global__ void __launch_bounds__(kTrThreads, 2)
+    trace_tile_kernel(const __grid_constant__ CUtensorMap tmW, long long d, long long ntiles,
+                      const double* __restrict__ lam, const double* __restrict__ wopt,
+                      double* __restrict__ part) {
+  using E = Elem<T>;
+  using S = TrShape<T, L>;
+  constexpr int VEC = S::VEC, CW = S::CW, NV = S::NV, ITEMS = S::ITEMS;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  double* s_cols = reinterpret_cast<double*>(smem + 128);  // [2][3][CW]
+  double* s_red = s_cols + 6 * CW;                            // [kTrWarps]
+  unsigned char* stages = smem + 128 + ((6 * CW + kTrWarps) * 8 + 127) / 128 * 128;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool has_obj = lam != nullptr;
+  if (tid == 0) {
+    tma_prefetch_desc(&tmW);
+    for (int st = 0; st < kTrStages; st++) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int st, long long t) {
+    mbar_arrive_expect_tx(&full[st], (uint32_t)S::STAGE);
+    tma_load_2d(stages + (size_t)st * S::STAGE, &tmW, (int)(t * CW), 0, &full[st]);
+  };
+  const long long first = blockIdx.x, stride = gridDim.x;
+  if (tid == 0)
+    for (int st = 0; st < kTrStages; st++)
+      if (first + st * stride < ntiles) issue(st, first + st * stride);
+
+  // phase A lanes: column a_col of the tile, chains [a_part * CPT, (a_part + 1) * CPT)
+  const int a_col = warp * S::NCW + (lane % S::NCW);
+  const int a_part = lane / S::NCW;
+  // phase B items: vector b_v of rows b_row0 + k * ROW_STEP
+  const int b_v = tid % NV, b_row0 = tid / NV;
+  double acc_c[ITEMS], acc_l[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; k++) acc_c[k] = acc_l[k] = 0.0;
+  double a_sum = 0.0;
+
+  auto phase_a = [&](long long t, int it) {
+    const int st = it % kTrStages;
+    const long long c0 = t * CW;
+    const T* sW = reinterpret_cast<const T*>(stages + (size_t)st * S::STAGE);
+    double* cm = s_cols + (it & 1) * 3 * CW;
+    const bool live = c0 + a_col < d;
+    double lm = 0.0, wo = 0.0;
+    if (has_obj && live && a_part == 0) {   // issued first: latency under the sums
+      lm = lam[c0 + a_col];
+      wo = wopt[c0 + a_col];
+    }
+    mbar_wait(&full[st], (it / kTrStages) & 1);
+    // columns past d hold TMA's zero fill: summed harmlessly, never stored
+    const T* col = sW + a_col;
+    double r[S::CPT];
+#pragma unroll
+    for (int q = 0; q < S::CPT; q++) r[q] = (double)E::lds(col + (a_part * S::CPT + q) * CW);
+#pragma unroll
+    for (int i = 8; i < L; i += 8) {
+#pragma unroll
+      for (int q = 0; q < S::CPT; q++)
+        r[q] = __dadd_rn(r[q], (double)E::lds(col + (i + a_part * S::CPT + q) * CW));
+    }
+#pragma unroll
+    for (int w = 1; w < S::CPT; w *= 2) {   // this thread's subtree of the chains
+#pragma unroll
+      for (int q = 0; q < S::CPT; q += 2 * w) r[q] = __dadd_rn(r[q], r[q + w]);
+    }
+    double res = r[0];
+#pragma unroll
+    for (int off = S::NCW; off < 32; off *= 2) res = __dadd_rn(res, __shfl_xor_sync(0xffffffffu, res, off));
+    if (a_part == 0 && live) {
+      const double mean = __dmul_rn(res, 1.0 / L);
+      cm[a_col] = mean;
+      if (has_obj) {
+        cm[CW + a_col] = lm;
+        cm[2 * CW + a_col] = wo;
+        const double dm = __dsub_rn(mean, wo);
+        a_sum += 0.5 * lm * dm * dm;
+      }
+    }
+  };
+  auto phase_b = [&](long long t, int it) {
+    const int st = it % kTrStages;
+    const long long c0 = t * CW;
+    const int width = (int)min((long long)CW, d - c0);
+    const T* sW = reinterpret_cast<const T*>(stages + (size_t)st * S::STAGE);
+    const double* cm = s_cols + (it & 1) * 3 * CW;
+    const int c = b_v * VEC;
+    double m[VEC], lm[VEC], wo[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; e += 2) {
+      const double2 a2 = *reinterpret_cast<const double2*>(cm + c + e);
+      m[e] = a2.x;
+      m[e + 1] = a2.y;
+      if (has_obj) {
+        const double2 l2 = *reinterpret_cast<const double2*>(cm + CW + c + e);
+        const double2 w2 = *reinterpret_cast<const double2*>(cm + 2 * CW + c + e);
+        lm[e] = l2.x;
+        lm[e + 1] = l2.y;
+        wo[e] = w2.x;
+        wo[e + 1] = w2.y;
+      } else {
+        lm[e] = lm[e + 1] = wo[e] = wo[e + 1] = 0.0;
+      }
+    }
+    if (width == CW) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; k++) {
+        Vec<T> x;
+        x.raw = *reinterpret_cast<const uint4*>(sW + (b_row0 + k * S::ROW_STEP) * CW + c);
+#pragma unroll
+        for (int e = 0; e < VEC; e++) {
+          const double w = (double)E::ld(x.e(), e);
+          const double dv = w - m[e];
+          acc_c[k] += dv * dv;
+          const double dw = w - wo[e];
+          acc_l[k] += lm[e] * dw * dw;
+        }
+      }
+    } else if (c < width) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; k++) {
+        Vec<T> x;
+        x.raw = *reinterpret_cast<const uint4*>(sW + (b_row0 + k * S::ROW_STEP) * CW + c);
+#pragma unroll
+        for (int e = 0; e < VEC; e++) {
+          if (c + e < width) {
+            const double w = (double)E::ld(x.e(), e);
+            const double dv = w - m[e];
+            acc_c[k] += dv * dv;
+            const double dw = w - wo[e];
+            acc_l[k] += lm[e] * dw * dw;
+          }
+        }
+      }
+    }
+  };
+
+  if (first < ntiles) phase_a(first, 0);
+  __syncthreads();
+  int it = 0;
+  for (long long t = first; t < ntiles; t += stride, ++it) {
+    if (t + stride < ntiles) phase_a(t + stride, it + 1);
+    phase_b(t, it);
+    __syncthreads();  // tile t's stage and mean buffer are free, tile t+1's means ready
+    if (tid == 0) {
+      const long long tn = t + (long long)kTrStages * stride;
+      if (tn < ntiles) issue(it % kTrStages, tn);
+    }
+  }
+  // deterministic in-CTA reduction (as trace_stats_tma_kernel): thread j sums the owners
+  // of learner j in thread order
+  __syncthreads();
+  double* s_acc = reinterpret_cast<double*>(stages);  // [kTrThreads][ITEMS][2]
+#pragma unroll
+  for (int k = 0; k < ITEMS; k++) {
+    s_acc[(tid * ITEMS + k) * 2] = acc_c[k];
+    s_acc[(tid * ITEMS + k) * 2 + 1] = acc_l[k];
+  }
+  for (int o = 16; o > 0; o >>= 1) a_sum += __shfl_xor_sync(0xffffffffu, a_sum, o);
+  if (lane == 0) s_red[warp] = a_sum;
+  __syncthreads();
+  double* out = part + (long long)blockIdx.x * (2 * L + 1);
+  for (int j = tid; j < L; j += kTrThreads) {
+    const int k = j / S::ROW_STEP, r0 = j % S::ROW_STEP;
+    double cs = 0.0, q = 0.0;
+    for (int vv = 0; vv < NV; vv++) {
+      const int owner = r0 * NV + vv;
+      cs += s_acc[(owner * ITEMS + k) * 2];
+      q += s_acc[(owner * ITEMS + k) * 2 + 1];
+    }
+    out[j] = cs;
+    out[L + j] = has_obj ? 0.5 * q : 0.0;
+  }
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kTrWarps; w++) t += s_red[w];
+    out[2 * L] = has_obj ? t : 0.0;
+  }
+}
+
+template <typename T, int L>
+static int trace_tile_launch(const T* W, int64_t d, int64_t ld, const double* lam,
+                             const double* wopt, double* part, int* nparts, cudaStream_t st,
+                             bool* covered) {
+  using S = TrShape<T, L>;
+  CUtensorMap tm;
+  if (!tma_map_2d<T>(&tm, W, d, L, ld, S::CW, L)) return 0;
+  const size_t smem = 128 + ((6 * S::CW + kTrWarps) * 8 + 127) / 128 * 128 +
+                      (size_t)kTrStages * S::STAGE;
+  static_assert((size_t)kTrThreads * S::ITEMS * 16 <= (size_t)kTrStages * S::STAGE,
+                "accumulators fit in the drained stages");
+  static unsigned long long attr_mask = 0;
+  if (attr_needed(&attr_mask)) {
+    cudaError_t e = cudaFuncSetAttribute(trace_tile_kernel<T, L>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(trace_tile_kernel)");
+    attr_done(&attr_mask);
+  }
+  *covered = true;
+  const long long ntiles = (d + S::CW - 1) / S::CW;
+  long long grid = 2LL * sm_count(-1);
+  if (grid > ntiles) grid = ntiles;
+  *nparts = (int)grid;
+  trace_tile_kernel<T, L><<<(int)grid, kTrThreads, smem, st>>>(tm, d, ntiles, lam, wopt, part);
+  RM_CHECK_LAUNCH("trace_tile_kernel");
+  return 0;
+}
+
 template <typename T>
 static int trace_stats_tma(const T* W, int L, int64_t d, int64_t ld, const double* lam,
                            const double* wopt, double* part, int* nparts, cudaStream_t st,
                            bool* covered) {
   using E = Elem<T>;
+  if (getenv("RINGMIX_TRACE_RUNTIME_L") == nullptr) {
+    switch (L) {
+      case 8: return trace_tile_launch<T, 8>(W, d, ld, lam, wopt, part, nparts, st, covered);
+      case 16: return trace_tile_launch<T, 16>(W, d, ld, lam, wopt, part, nparts, st, covered);
+      case 32: return trace_tile_launch<T, 32>(W, d, ld, lam, wopt, part, nparts, st, covered);
+      case 64: return trace_tile_launch<T, 64>(W, d, ld, lam, wopt, part, nparts, st, covered);
+      case 128: return trace_tile_launch<T, 128>(W, d, ld, lam, wopt, part, nparts, st, covered);
+      default: break;
+    }
+  }
   constexpr int VEC = E::VEC;
   const size_t esz = sizeof(T);
   // tile width: power of two, stage ~32 KB, exactly kTrItems items per thread
@@ -541,47 +787,113 @@ __host__ __device__ inline int exact_pairwise_depth(long long d) {
   return D;
 }
 
+// One warp per 32 learners; lane l's running sums walk row l.  The row tiles [32 x kExCT]
+// (and M, lam, w* of those columns) are staged into shared memory by coalesced cp.async
+// copies kExBuf - 1 tiles ahead, so the chains wait on shared-memory latency only (direct
+// row loads left every 8-column batch waiting for a global round trip: 7.5 ms at
+// 64 x 2^16).  Rows are padded by one element: lane l reading column c of its own row
+// hits a different bank than its neighbours.
+constexpr int kExCT = 128;
+constexpr int kExBuf = 4;
+
 template <typename T>
-__global__ void __launch_bounds__(128)
+struct ExTile {
+  static constexpr int ROW = kExCT + 1;
+  static constexpr size_t W_BYTES = ((size_t)32 * ROW * sizeof(T) + 15) / 16 * 16;
+  static constexpr size_t BYTES = W_BYTES + 3 * kExCT * sizeof(double);
+};
+
+template <typename T>
+__global__ void __launch_bounds__(32)
     trace_exact_rows_kernel(const T* __restrict__ W, int L, long long d, long long ld,
                             const double* __restrict__ M, const double* __restrict__ lam,
                             const double* __restrict__ wopt, double* __restrict__ cons_sq,
                             double* __restrict__ loss_col) {
   using E = Elem<T>;
+  using X = ExTile<T>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x;
+  const int l0 = blockIdx.x * 32;
+  const int nrows = min(32, L - l0);
+  const long long ntiles = (d + kExCT - 1) / kExCT;
+  const bool has_obj = lam != nullptr;
+  auto tile_w = [&](int b) { return reinterpret_cast<T*>(smem + (size_t)b * X::BYTES); };
+  auto tile_c = [&](int b) {
+    return reinterpret_cast<double*>(smem + (size_t)b * X::BYTES + X::W_BYTES);
+  };
+  auto issue = [&](long long t) {
+    const int b = (int)(t % kExBuf);
+    const long long c0 = t * kExCT;
+    const int width = (int)min((long long)kExCT, d - c0);
+    T* sw = tile_w(b);
+    double* sc = tile_c(b);
+    for (int r = 0; r < nrows; r++) {
+      const T* src = W + (long long)(l0 + r) * ld + c0;
+      for (int c = lane; c < width; c += 32) cp_async_elem(sw + r * X::ROW + c, src + c);
+    }
+    for (int c = lane; c < width; c += 32) {
+      cp_async_elem(sc + c, M + c0 + c);
+      if (has_obj) {
+        cp_async_elem(sc + kExCT + c, lam + c0 + c);
+        cp_async_elem(sc + 2 * kExCT + c, wopt + c0 + c);
+      }
+    }
+  };
+  // one commit group per tile slot (empty groups past the end keep the count uniform)
+#pragma unroll
+  for (int t = 0; t < kExBuf - 1; t++) {
+    if (t < ntiles) issue(t);
+    cp_async_commit();
+  }
+  double cons = 0.0, loss = 0.0;
+  for (long long t = 0; t < ntiles; t++) {
+    if (t + kExBuf - 1 < ntiles) issue(t + kExBuf - 1);
+    cp_async_commit();
+    cp_async_wait<kExBuf - 1>();
+    __syncwarp();
+    const int b = (int)(t % kExBuf);
+    const int width = (int)min((long long)kExCT, d - t * kExCT);
+    const T* row = tile_w(b) + lane * X::ROW;
+    const double* sc = tile_c(b);
+    if (lane < nrows) {
+      if (has_obj) {
+#pragma unroll 8
+        for (int c = 0; c < width; c++) {
+          const double w = (double)row[c];
+          const double dv = __dsub_rn(w, sc[c]);
+          cons = __dadd_rn(cons, __dmul_rn(dv, dv));
+          const double dw = __dsub_rn(w, sc[2 * kExCT + c]);
+          loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(sc[kExCT + c], dw), dw));
+        }
+      } else {
+#pragma unroll 8
+        for (int c = 0; c < width; c++) {
+          const double dv = __dsub_rn((double)row[c], sc[c]);
+          cons = __dadd_rn(cons, __dmul_rn(dv, dv));
+        }
+      }
+    }
+    __syncwarp();   // buffer b is refilled by the next iteration's issue
+  }
+  cp_async_wait<0>();
+  if (lane < nrows) {
+    cons_sq[l0 + lane] = cons;
+    if (loss_col != nullptr) loss_col[l0 + lane] = __dmul_rn(0.5, loss);
+  }
+}
+
+// bf16 (2-byte elements, no cp.async of that size): direct row walk
+__global__ void __launch_bounds__(128)
+    trace_exact_rows_bf16_kernel(const __nv_bfloat16* __restrict__ W, int L, long long d,
+                                 long long ld, const double* __restrict__ M,
+                                 const double* __restrict__ lam, const double* __restrict__ wopt,
+                                 double* __restrict__ cons_sq, double* __restrict__ loss_col) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
-  const T* row = W + (long long)l * ld;
+  const __nv_bfloat16* row = W + (long long)l * ld;
   double cons = 0.0, loss = 0.0;
-  constexpr int U = 8;   // loads of the next columns issued ahead of the two running sums
-  long long c = 0;
-  for (; c + U <= d; c += U) {
-    double w[U], m[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      w[u] = E::ld(row + c + u, 0);
-      m[u] = M[c + u];
-    }
-    if (lam != nullptr) {
-      double lm[U], wo[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        lm[u] = lam[c + u];
-        wo[u] = wopt[c + u];
-      }
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const double dw = __dsub_rn(w[u], wo[u]);
-        loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(lm[u], dw), dw));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      const double dv = __dsub_rn(w[u], m[u]);
-      cons = __dadd_rn(cons, __dmul_rn(dv, dv));
-    }
-  }
-  for (; c < d; c++) {
-    const double w = E::ld(row + c, 0);
+  for (long long c = 0; c < d; c++) {
+    const double w = (double)__bfloat162float(row[c]);
     const double dv = __dsub_rn(w, M[c]);
     cons = __dadd_rn(cons, __dmul_rn(dv, dv));
     if (lam != nullptr) {
@@ -666,9 +978,23 @@ static int trace_stats_exact(const T* W, int L, int64_t d, int64_t ld, const dou
   if (blocks > 16LL * sm_count(-1)) blocks = 16LL * sm_count(-1);
   column_mean_kernel<T><<<(int)blocks, 256, 0, st>>>(W, L, d, ld, M);
   RM_CHECK_LAUNCH("column_mean_kernel");
-  trace_exact_rows_kernel<T><<<(L + 127) / 128, 128, 0, st>>>(W, L, d, ld, M, lam, wopt,
-                                                               cons_sq, lam ? loss_col : nullptr);
-  RM_CHECK_LAUNCH("trace_exact_rows_kernel");
+  if constexpr (sizeof(T) == 2) {
+    trace_exact_rows_bf16_kernel<<<(L + 127) / 128, 128, 0, st>>>(
+        W, L, d, ld, M, lam, wopt, cons_sq, lam ? loss_col : nullptr);
+    RM_CHECK_LAUNCH("trace_exact_rows_bf16_kernel");
+  } else {
+    const size_t smem = (size_t)kExBuf * ExTile<T>::BYTES;
+    static unsigned long long attr_mask = 0;
+    if (attr_needed(&attr_mask)) {
+      cudaError_t e = cudaFuncSetAttribute(trace_exact_rows_kernel<T>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(trace_exact_rows_kernel)");
+      attr_done(&attr_mask);
+    }
+    trace_exact_rows_kernel<T><<<(L + 31) / 32, 32, smem, st>>>(W, L, d, ld, M, lam, wopt,
+                                                                cons_sq, lam ? loss_col : nullptr);
+    RM_CHECK_LAUNCH("trace_exact_rows_kernel");
+  }
   if (lam != nullptr) {
     const int depth = exact_pairwise_depth(d);
     trace_exact_avg_leaves_kernel<<<((1 << depth) + 127) / 128, 128, 0, st>>>(M, lam, wopt, d,
