@@ -342,8 +342,10 @@ int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, in
  * means sum/L to every rank (multimem.st); apply with rm_apply_mean_sgd_*(L = 1).
  * P_mc / M_mc: multicast addresses of symmetric buffers (e.g. torch symmetric
  * memory).  Caller orders it with cross-rank barriers. */
-/* Caps, for the calling host thread, on the CTAs per SM launched by rm_partial_sum_*,
- * rm_apply_mean_sgd_* and rm_nvls_mean_f64; 0 restores the defaults (16 / 8 / 8).  A chunk
+/* Caps, for the calling host thread, on the CTAs per SM launched by rm_partial_sum_* (and
+ * rm_column_mean_*), rm_apply_mean_sgd_* and rm_nvls_mean_f64; 0 restores the defaults
+ * (16 / 8 / 8).  The D1D training step lowers the first so the average runs beside the
+ * gradient generator instead of displacing it.  A chunk
  * pipeline lowers them so the in-switch reduction of one chunk is co-resident (threads and
  * registers) with the local kernels of its neighbours. */
 int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls);
@@ -486,6 +488,26 @@ int rm_quadratic_mix_step_f64(const uint32_t* prefix_words, int n_prefix, uint64
                               const double* wopt, double noise_sd, double lr,
                               unsigned long long* absmax_bits, void* workspace,
                               int64_t workspace_bytes, void* stream);
+
+/* D1D step of a learner-sharded run with the quadratic oracle's gradient fused in
+ * (simulation.py:304-312, objectives.py:84-90): Wout[l] = M - lr * G(Phi[l]) for this rank's
+ * learners learner0 + l, l < L, G never written.  M: the global column means (fp64, device),
+ * produced concurrently elsewhere (partial sums + cross-GPU reduction on other streams); the
+ * generator starts at once and only the final mix waits for `means_ready` (a cudaEvent_t, or
+ * NULL).  Same bits as rm_quadratic_grad_shard_* followed by rm_apply_mean_sgd_*(M, G, L=1).
+ * workspace: >= rm_quadratic_mix_workspace_bytes(L, d). */
+int rm_quadratic_mean_step_shard_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                                     int64_t learner0, const double* M, const float* Phi,
+                                     float* Wout, int L, int64_t d, int64_t ldp, int64_t ldo,
+                                     const double* lam, const double* wopt, double noise_sd,
+                                     double lr, unsigned long long* absmax_bits, void* workspace,
+                                     int64_t workspace_bytes, void* stream, void* means_ready);
+int rm_quadratic_mean_step_shard_f64(const uint32_t* prefix_words, int n_prefix, uint64_t k,
+                                     int64_t learner0, const double* M, const double* Phi,
+                                     double* Wout, int L, int64_t d, int64_t ldp, int64_t ldo,
+                                     const double* lam, const double* wopt, double noise_sd,
+                                     double lr, unsigned long long* absmax_bits, void* workspace,
+                                     int64_t workspace_bytes, void* stream, void* means_ready);
 
 /* ---- fused trace reductions (run_training's _record, simulation.py:398-409) ----
  * One pass over W (L <= 128 learners, learner-major): cons_sq[l] += sum_c (W[l,c]-mean_c)^2

@@ -74,6 +74,10 @@ _SIGNATURES = {
     "rm_trace_stats_f32": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
     "rm_trace_stats_f64": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
     "rm_trace_stats_bf16": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
+    "rm_quadratic_mean_step_shard_f32": ([vp, i32, u64, i64, vp, vp, vp, i32, i64, i64, i64, vp,
+                                          vp, dbl, dbl, vp, vp, i64, vp, vp], i32),
+    "rm_quadratic_mean_step_shard_f64": ([vp, i32, u64, i64, vp, vp, vp, i32, i64, i64, i64, vp,
+                                          vp, dbl, dbl, vp, vp, i64, vp, vp], i32),
     "rm_trace_stats_exact_workspace_bytes": ([i64], i64),
     "rm_trace_stats_exact_f32": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),
     "rm_trace_stats_exact_f64": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),

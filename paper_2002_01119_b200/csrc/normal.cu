@@ -1242,20 +1242,25 @@ int quad_mix_copy(const uint32_t* prefix, int nprefix, uint64_t k, const T* W, c
                   T* out, const int32_t* left, const int32_t* right, int L, long long d,
                   long long ldw, long long ldp, long long ldo, const double* lam,
                   const double* wopt, double sd, double lr, unsigned long long* absmax, void* ws,
-                  long long ws_bytes, void* stream) {
+                  long long ws_bytes, void* stream, long long stream0, const double* ext_means,
+                  void* means_ready) {
   const long long need = quad_z_workspace_bytes(L, d);
   if (ws == nullptr || ws_bytes < need) {
     set_error("fused gradient workspace too small: need %lld bytes", need);
     return RM_ERANGE;
   }
   ZArgs a;
-  int rc = z_args(&a, prefix, nprefix, 2, k, L, d);
+  int rc = z_args(&a, prefix, nprefix, 2, k, L, d, stream0);
   if (rc) return rc;
   const long long nb = (long long)a.nblocks * L;
-  const ZWs w = z_carve(a, ws, true, true);
+  ZWs w = z_carve(a, ws, true, true);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool ring = left != nullptr;
-  if (!ring) {
+  if (ext_means != nullptr) {
+    // means computed elsewhere (a learner-sharded run's global average, produced
+    // concurrently on other streams / GPUs): only the mix waits for them
+    w.means = const_cast<double*>(ext_means);
+  } else if (!ring) {
     // the uniform step's column means (numpy pairwise order, the two-pass mean's bits)
     rc = sizeof(T) == 4 ? rm_column_mean_f32(reinterpret_cast<const float*>(W), L, d, ldw,
                                              w.means, stream)
@@ -1267,6 +1272,10 @@ int quad_mix_copy(const uint32_t* prefix, int nprefix, uint64_t k, const T* W, c
   zig_fixup_scratch_kernel<<<(int)((2 * nb + 127) / 128), 128, 0, st>>>(
       a, w.seeds, w.entry, w.valid, w.nbad, w.bad, w.nleft, w.left, w.scratch);
   RM_CHECK_LAUNCH("zig_fixup_scratch_kernel");
+  if (means_ready != nullptr) {
+    const cudaError_t e = cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(means_ready), 0);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaStreamWaitEvent(means_ready)");
+  }
   const long long grid = (nb * 32 + 255) / 256;
   auto launch = [&](auto kern) {
     kern<<<(int)grid, 256, 0, st>>>(a, w.info, w.entry, w.tcount, w.offs, w.valid, w.scratch, W,
@@ -1286,11 +1295,13 @@ int quad_mix_copy(const uint32_t* prefix, int nprefix, uint64_t k, const T* W, c
 template int quad_mix_copy<float>(const uint32_t*, int, uint64_t, const float*, const float*,
                                   float*, const int32_t*, const int32_t*, int, long long,
                                   long long, long long, long long, const double*, const double*,
-                                  double, double, unsigned long long*, void*, long long, void*);
+                                  double, double, unsigned long long*, void*, long long, void*,
+                                  long long, const double*, void*);
 template int quad_mix_copy<double>(const uint32_t*, int, uint64_t, const double*, const double*,
                                    double*, const int32_t*, const int32_t*, int, long long,
                                    long long, long long, long long, const double*, const double*,
-                                   double, double, unsigned long long*, void*, long long, void*);
+                                   double, double, unsigned long long*, void*, long long, void*,
+                                   long long, const double*, void*);
 
 long long quad_z_workspace_bytes(int nstreams, long long n) {
   const int64_t fast = rm_normal_workspace_bytes_fast(nstreams, n);
@@ -1381,6 +1392,29 @@ extern "C" int rm_quadratic_grad_shard_f64(const uint32_t* prefix_words, int n_p
   return quad_grad<double>(prefix_words, n_prefix, 2, k, L, d, Phi, ldp, lam, wopt, noise_sd, G,
                            ldg, nullptr, 0, workspace, workspace_bytes, stream, learner0);
 }
+
+// D1D step of a learner-sharded run with the oracle's gradient fused in:
+//   Wout[l] = M - lr * G(Phi[l]),  G of learner learner0 + l  (simulation.py:304-312)
+// M = the global column means, produced concurrently (other streams / GPUs); the generator
+// runs at once and only the final mix waits for `means_ready` (a cudaEvent_t, may be NULL).
+#define RM_DEFINE_MEAN_STEP_SHARD(SUFFIX, CT)                                                  \
+  extern "C" int rm_quadratic_mean_step_shard_##SUFFIX(                                        \
+      const uint32_t* prefix_words, int n_prefix, uint64_t k, int64_t learner0,               \
+      const double* M, const CT* Phi, CT* Wout, int L, int64_t d, int64_t ldp, int64_t ldo,   \
+      const double* lam, const double* wopt, double noise_sd, double lr,                       \
+      unsigned long long* absmax_bits, void* workspace, int64_t workspace_bytes, void* stream, \
+      void* means_ready) {                                                                     \
+    if (M == nullptr || Phi == nullptr || Wout == nullptr || lam == nullptr || wopt == nullptr || \
+        L < 1 || d < 1 || ldp < d || ldo < d || learner0 < 0) {                                \
+      set_error("invalid sharded mean-step arguments");                                       \
+      return RM_EINVAL;                                                                        \
+    }                                                                                          \
+    return quad_mix_copy<CT>(prefix_words, n_prefix, k, Phi, Phi, Wout, nullptr, nullptr, L, d, \
+                             ldp, ldp, ldo, lam, wopt, noise_sd, lr, absmax_bits, workspace,   \
+                             workspace_bytes, stream, learner0, M, means_ready);               \
+  }
+RM_DEFINE_MEAN_STEP_SHARD(f32, float)
+RM_DEFINE_MEAN_STEP_SHARD(f64, double)
 
 extern "C" int rm_standard_normal_f64(const uint32_t* prefix_words, int n_prefix, int append,
                                       uint64_t k, int nstreams, int64_t n, double* Z,

@@ -691,6 +691,12 @@ static thread_local int g_d1d_psum_cap = 0;
 static thread_local int g_d1d_apply_cap = 0;
 static thread_local int g_d1d_nvls_cap = 0;
 
+// the partial-sum cap also bounds rm_column_mean_* (the single-GPU D1D average that runs
+// beside the gradient generator)
+namespace rm {
+int d1d_psum_cap() { return g_d1d_psum_cap; }
+}  // namespace rm
+
 extern "C" int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls) {
   if (partial_sum < 0 || partial_sum > 16 || apply < 0 || apply > 16 || nvls < 0 || nvls > 16) {
     set_error("CTAs per SM must be in [0, 16] (0 = default)");

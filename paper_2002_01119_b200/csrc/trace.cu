@@ -727,6 +727,8 @@ RM_DEFINE_TRACE(bf16, uint16_t, __nv_bfloat16)
 // gradient of W_{k-1} is produced (simulation.step_d1d; north-star (c)), after
 // which rm_apply_mean_sgd_*(M, G, L = 1) finishes the step.
 namespace rm {
+int d1d_psum_cap();   // shard.cu: rm_set_d1d_ctas_per_sm's partial-sum cap (0 = default)
+
 template <typename T>
 __global__ void __launch_bounds__(256)
     column_mean_kernel(const T* __restrict__ W, int L, long long d, long long ld,
@@ -756,7 +758,8 @@ __global__ void __launch_bounds__(256)
     }                                                                                         \
     if (d == 0) return 0;                                                                     \
     long long blocks = (d + 255) / 256;                                                       \
-    if (blocks > 16LL * sm_count(-1)) blocks = 16LL * sm_count(-1);                           \
+    const long long cap = (d1d_psum_cap() ? d1d_psum_cap() : 16) * (long long)sm_count(-1);   \
+    if (blocks > cap) blocks = cap;                                                           \
     column_mean_kernel<T><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(       \
         reinterpret_cast<const T*>(W), L, d, ld, M);                                          \
     RM_CHECK_LAUNCH("column_mean_kernel");                                                    \

@@ -81,6 +81,7 @@ int quad_mix_copy(const uint32_t* prefix, int nprefix, uint64_t k, const T* W, c
                   T* out, const int32_t* left, const int32_t* right, int L, long long d,
                   long long ldw, long long ldp, long long ldo, const double* lam,
                   const double* wopt, double sd, double lr, unsigned long long* absmax, void* ws,
-                  long long ws_bytes, void* stream);
+                  long long ws_bytes, void* stream, long long stream0 = 0,
+                  const double* ext_means = nullptr, void* means_ready = nullptr);
 
 }  // namespace rm

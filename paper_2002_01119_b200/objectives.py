@@ -134,6 +134,44 @@ class QuadraticObjective:
                        "rm_quadratic_grad")
         return G
 
+    def device_mean_step(self, M: torch.Tensor, Phi: torch.Tensor, lr: float, cfg, k: int,
+                         ready: torch.cuda.Event | None = None, learner0: int = 0,
+                         absmax: torch.Tensor | None = None,
+                         out: torch.Tensor | None = None) -> torch.Tensor:
+        """The D1D step with this oracle's gradient fused into the generator's final pass
+        (rm_quadratic_mean_step_shard_*): out = M - lr * G(Phi) for learners
+        [learner0, learner0 + L), G never written (simulation.py:304-312, objectives.py:84-90).
+        M: the column means (fp64, d), possibly still being produced on another stream or GPU
+        — only the final pass waits for ``ready``.  Same bits as ``device_gradients`` followed
+        by the mean apply."""
+        L, d = Phi.shape
+        if d != self.dimension or M.numel() != d or M.dtype != torch.float64:
+            raise ValueError("M must be the fp64 column means of the oracle's dimension")
+        sfx = {torch.float32: "f32", torch.float64: "f64"}.get(Phi.dtype)
+        if sfx is None:
+            raise TypeError("the fused gradient step supports float32/float64 weights")
+        lib = _lib.load()
+        ldp = mixing._rows(Phi, "Phi")[2]
+        need = int(lib.rm_quadratic_mix_workspace_bytes(L, d))
+        ws = getattr(self, "_ws_fused", None)
+        if ws is None or ws.numel() < need or ws.device != Phi.device:
+            self._ws_fused = None
+            self._ws_fused = ws = torch.empty(need, dtype=torch.uint8, device=Phi.device)
+        if out is None:
+            out = mixing.empty_learner_major(L, d, Phi.dtype, Phi.device)
+        lam, opt = self._lam.to(Phi.device), self._opt.to(Phi.device)
+        words = seeding.entropy_words(cfg.seed, seeding.TAG_GRADIENT)
+        noise_sd = float(self.noise_scale / np.sqrt(cfg.batch_size))
+        fn = getattr(lib, f"rm_quadratic_mean_step_shard_{sfx}")
+        with torch.cuda.device(Phi.device):
+            _lib.check(fn(words.ctypes.data, len(words), int(k), int(learner0), M.data_ptr(),
+                          Phi.data_ptr(), out.data_ptr(), L, d, ldp, out.stride(0),
+                          lam.data_ptr(), opt.data_ptr(), noise_sd, float(lr),
+                          _lib.ptr(absmax), ws.data_ptr(), ws.numel(), _lib.stream_ptr(),
+                          None if ready is None else ready.cuda_event),
+                       "rm_quadratic_mean_step_shard")
+        return out
+
     def device_mix_step(self, W: torch.Tensor, Phi: torch.Tensor | None, tables, lr: float,
                         cfg, k: int, absmax: torch.Tensor | None = None) -> torch.Tensor:
         """One training step with this oracle's gradient fused into the mix

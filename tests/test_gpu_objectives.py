@@ -168,6 +168,31 @@ def test_exact_trace_stats_are_bitwise_numpy(L, d, dtype, monkeypatch):
     assert torch.equal(c2, cons_sq) and l2 is None and a2 is None
 
 
+@pytest.mark.parametrize("overlap,ctas", [(True, 1), (True, 4), (True, 0), (False, 0)])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_d1d_step_mean_beside_fused_generator_is_bit_identical(dtype, overlap, ctas, monkeypatch):
+    """step_d1d for steps whose gradients are not kept: the uniform fused step (default), or
+    (RINGMIX_D1D_OVERLAP=1) the average of W_k on a side stream (capped CTAs) beside the
+    generator, whose final pass writes mean - lr G(W_{k-1}) (rm_quadratic_mean_step_shard_*)
+    — both equal to the gradient followed by the fused mean/SGD kernel (simulation.py:304-312)."""
+    monkeypatch.setattr(simulation, "D1D_MEAN_CTAS", ctas)
+    monkeypatch.setattr(simulation, "D1D_FUSED_OVERLAP", overlap)
+    L, d = 16, 70_001
+    oracle = objectives.quadratic_oracle(d, condition_number=5.0, noise_scale=1.0, seed=3)
+    cfg = RunConfig(n_learners=L, iterations=3, lr=0.05, batch_size=2, seed=4, dtype=dtype)
+    st = simulation.initial_state(oracle, cfg)
+    st.weights.copy_(st.weights + torch.randn_like(st.weights) * 0.1)
+    for _ in range(3):
+        new = simulation.step_d1d(st, oracle, cfg, keep_gradients=False)
+        assert new.last_gradients is None
+        G = oracle.device_gradients(st.prev_weights.T, cfg, st.iteration)
+        ref = mixing.mean_mix_sgd(st.weights.T, G, simulation.learning_rate(cfg, st.iteration))
+        torch.cuda.synchronize()
+        assert torch.equal(new.weights.T, ref)
+        assert simulation.absmax_value(new.absmax_bits) == float(ref.abs().max())
+        st = new
+
+
 @pytest.mark.parametrize("side_stream", [True, False])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_overlapped_d1d_step_is_bit_identical_to_fused(dtype, side_stream, monkeypatch):

@@ -38,8 +38,20 @@ def main(L=64, d=25_557_032, steps=10):
     Wp.copy_(torch.randn((Lg, d), generator=g, device=dev))
     outs = {}
     res = {}
-    for mode in ("serial", "overlap", "serial", "overlap"):
-        tr = D.ShardedD1DTrainer(L, d, Lg, b, dev, oracle, overlap=(mode == "overlap"))
+    # RINGMIX_D1D_TRAIN_CTAS_LIST="16,0,0;1,0,1": overlap modes with those CTA caps
+    caps = [tuple(int(x) for x in c.split(",")) for c in
+            os.environ.get("RINGMIX_D1D_TRAIN_CTAS_LIST", "1,0,1").split(";")]
+    # overlapped modes: "apply" = gradient to HBM then one apply pass, "fused" = the
+    # generator's final pass writes M - lr G (rm_quadratic_mean_step_shard_*)
+    kinds = os.environ.get("RINGMIX_D1D_TRAIN_KINDS", "apply,fused").split(",")
+    modes = ["serial", "serial_fused"] + [f"{kd}{c}" for kd in kinds for c in caps]
+    conf = {"serial": (False, None, False), "serial_fused": (False, None, True)}
+    for kd in kinds:
+        for c in caps:
+            conf[f"{kd}{c}"] = (True, c, kd == "fused")
+    for mode in modes + modes:
+        ov, cap, fz = conf[mode]
+        tr = D.ShardedD1DTrainer(L, d, Lg, b, dev, oracle, overlap=ov, ctas=cap, fuse_grad=fz)
         out = mixing.empty_learner_major(Lg, d, torch.float32, dev)
         for k in range(3):
             tr.step(W, Wp, cfg, k, 0.01, out)
@@ -62,7 +74,8 @@ def main(L=64, d=25_557_032, steps=10):
         del tr
         torch.cuda.synchronize()
         dist.barrier()
-    same = torch.tensor([int(torch.equal(outs["serial"], outs["overlap"]))], device=dev)
+    same = torch.tensor([int(all(torch.equal(outs["serial"], outs[m]) for m in modes))],
+                        device=dev)
     dist.all_reduce(same, op=dist.ReduceOp.MIN)
     if rank == 0:
         print(json.dumps({"world": world, "L": L, "d": d, "step_ms": res,
