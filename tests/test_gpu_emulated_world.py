@@ -394,7 +394,7 @@ def _best_placement_numpy(inv_k, perm_next, sop_k, L, n):
     return best
 
 
-@pytest.mark.parametrize("L,n", [(12, 3), (16, 2), (24, 4), (40, 5), (64, 8)])
+@pytest.mark.parametrize("L,n", [(12, 3), (16, 2), (24, 4), (40, 5), (64, 8), (128, 8)])
 def test_pos_placement_matches_exhaustive_search(L, n):
     lib = _lib.load()
     tabs = mixing.permutation_tables(L, 99, 0, 5)
@@ -430,7 +430,8 @@ def test_pos_placement_matches_exhaustive_search(L, n):
         sop.copy_(sop_n)
 
 
-@pytest.mark.parametrize("L,d,world", [(24, 3001, 4), (16, 515, 2), (40, 77, 8)])
+@pytest.mark.parametrize("L,d,world", [(24, 3001, 4), (16, 515, 2), (40, 77, 8),
+                                       (128, 4099, 8), (128, 2051, 4)])
 def test_placed_position_layout_steps_bit_identical(L, d, world):
     """Ring-position layout with the per-step arc placement, every rank emulated on this
     GPU, in-kernel ordering: after each step slot i of rank r holds learner
