@@ -12,8 +12,10 @@ prints ONE JSON line on rank 0.  `--gpus N` without torchrun launches N ranks it
   epilogue.  W rotates between two HBM buffers.
 * N = 1: BASELINE.json configs[1] — RAD-PSGD, 64 learners x 25,557,032 fp32 params
   (ResNet-50-sized flat vectors), synthetic N(0,1) weights and gradients, lr = 0.01.
-  `extras.c3_single_gpu` times configs[2] (128 x 43,154,944) on the same GPU: the
-  strong-scaling reference point of the N > 1 runs.
+  `extras` time the other BASELINE configs on the same GPU: `c1_demo` (configs[0],
+  16 x 2^20, CUDA-graph replay), `c2_adpsgd_fixed` (configs[1]'s fixed ring), `c4_d1d`
+  (configs[3], the D1D mean step) and `c3_single_gpu` (configs[2], 128 x 43,154,944:
+  the strong-scaling reference point of the N > 1 runs).
 * N > 1 (one process per GPU): strong scaling of BASELINE.json configs[2] — RAD-PSGD,
   128 learners x 43,154,944 fp32 (LSTM acoustic model), learners sharded over the
   ranks (north-star (d)) in ring-POSITION order (`--layout position`, the default):
@@ -22,8 +24,8 @@ prints ONE JSON line on rank 0.  `--gpus N` without torchrun launches N ranks it
   consecutive steps order themselves inside the kernels (no collective).
   `extras.learner_pull` times the learner-ordered pull layout on the same problem
   and `extras.coord_weak` the zero-communication coordinate stripes (every rank a
-  64 x 25,557,032 stripe, weak scaling).  D1D (`--strategy d1d`) shards learners
-  with the fused partial-sum / cross-GPU-reduce / apply kernel.
+  64 x 25,557,032 stripe, weak scaling).  D1D (`--strategy d1d`, and `extras.c4_d1d_sharded`
+  on configs[3]) shards learners with the fused partial-sum / cross-GPU-reduce / apply kernel.
 * `value`: whole-job learner-params / s, device time (CUDA events), max over ranks.
 * `e2e`: the same step through the public API with the step's inputs and results
   crossing PCIe every step: N = 1 host buffers in and out (W, G -> W',
@@ -66,6 +68,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "learner-params mixed/sec"
 UNIT = "learner-params/s"
+C1 = (16, 1 << 20)             # BASELINE.json configs[0] (the reference's demo scale)
 C2 = (64, 25_557_032)          # BASELINE.json configs[1] (and configs[3], D1D)
 C3 = (128, 43_154_944)         # BASELINE.json configs[2]
 LR = 0.01
@@ -153,7 +156,8 @@ def total_dim(args, ws):
 
 
 def config_name(L, d):
-    return {C2: "ResNet-50-sized", C3: "LSTM-acoustic-model-sized"}.get((L, d), "custom")
+    return {C1: "reference CPU demo scale", C2: "ResNet-50-sized",
+            C3: "LSTM-acoustic-model-sized"}.get((L, d), "custom")
 
 
 def config_dict(args, ws):
@@ -796,7 +800,8 @@ def extra_line(spec, res, ws, dev, wl, mixing):
          "scaling": "weak" if weak(spec, ws) else "strong",
          "value": res["value"], "unit": UNIT, "ms_per_step": res["ms_per_step"],
          "kernel_avg_ms": res["kern_avg_s"] * 1e3,
-         "hbm_frac": res["achieved"] / res["peak"]}
+         "hbm_frac": res["achieved"] / res["peak"],
+         "timing": "CUDA-graph replay / K" if res["graph"] else "CUDA events"}
     if ws > 1 and spec.layout in ("learner", "position"):
         e["nvlink"] = nvlink_object(spec, res, wl, ws, dev, mixing)
     return e
@@ -885,9 +890,17 @@ def run_ours(args):
             and args.learners is None and args.dim is None:
         todo = []
         if ws == 1:
+            # the other BASELINE configs on the same GPU, so the driver's run measures them
+            todo.append(("c1_demo", dict(layout="coord", learners=C1[0], dim=C1[1],
+                                         scaling="strong", config_index=0)))
+            todo.append(("c2_adpsgd_fixed", dict(strategy="adpsgd_fixed", config_index=1)))
+            todo.append(("c4_d1d", dict(strategy="d1d", config_index=3)))
             todo.append(("c3_single_gpu", dict(layout="coord", learners=C3[0], dim=C3[1],
                                                scaling="strong", config_index=2)))
         else:
+            todo.append(("c4_d1d_sharded", dict(strategy="d1d", layout="learner",
+                                                learners=C2[0], dim=C2[1], scaling="strong",
+                                                config_index=3)))
             if spec.layout != "learner":
                 todo.append(("learner_pull", dict(layout="learner", learners=C3[0], dim=C3[1],
                                                   scaling="strong", config_index=2)))
