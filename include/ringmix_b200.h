@@ -349,6 +349,19 @@ int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, in
  * pipeline lowers them so the in-switch reduction of one chunk is co-resident (threads and
  * registers) with the local kernels of its neighbours. */
 int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls);
+/* numpy-order learner-sharded D1D, for the calling host thread: `chains` (1, 2, 4, 8; 0 =
+ * off) of numpy's eight pairwise chains per rank.  Rank g then holds learners
+ * {l : l % 8 in [g chains, (g + 1) chains)} in ascending order (L % 8 == 0, 8 <= L <= 128),
+ * rm_partial_sum_* / rm_d1d_fused_* compute numpy's tree over those chains, and the
+ * cross-rank sums (rm_p2p_mean_f64, the fused kernels' reduce role) combine ranks in the
+ * tree order, so the mean is W.mean(axis=1) bit for bit (mixing.py:122-124) — the sharded
+ * step equals the single-GPU step.  Above 2 ranks this needs peer tables (the in-switch
+ * sum of more than two addends has no specified order); fp32 / fp64 only. */
+int rm_set_d1d_numpy_order(int chains);
+/* The learner interleave of the gradient streams of the following rm_quadratic_grad_shard_* /
+ * rm_quadratic_mean_step_shard_* calls of this host thread: stream s is learner
+ * learner0 + (s / run) * period + s % run (run = 0: learner0 + s). */
+int rm_set_shard_streams(int run, int64_t period);
 /* D1D across GPUs in ONE launch per rank (simulation.py:304-312 with the learners sharded):
  * the CTAs split into partial-sum / in-switch-reduce / apply roles that walk the column
  * chunks in order and hand chunks to each other (and to the other ranks) through flags.

@@ -271,6 +271,25 @@ __device__ __forceinline__ double sym_ld_sum_f64(const SymRef& s, long long i) {
   return v;
 }
 
+// sum over ranks of element i in numpy's pairwise tree order: ((x0 + x1) + (x2 + x3)) + ...
+// (world a power of two <= 8).  Multicast: the in-switch sum, exact for world <= 2 only (the
+// switch's order of more addends is unspecified; callers use peer tables there).
+__device__ __forceinline__ double sym_ld_sum_tree_f64(const SymRef& s, long long i) {
+  if (s.mc || s.world <= 2) return sym_ld_sum_f64(s, i);
+  double v[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++)
+    if (r < s.world)
+      asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v[r]) : "l"(s.peers[r] + 8 * i)
+                   : "memory");
+#pragma unroll
+  for (int w = 1; w < 8; w *= 2)
+#pragma unroll
+    for (int r = 0; r + w < 8; r += 2 * w)
+      if (r + w < s.world) v[r] = __dadd_rn(v[r], v[r + w]);
+  return v[0];
+}
+
 // element i := v on every rank
 __device__ __forceinline__ void sym_st_f64(const SymRef& s, long long i, double v) {
   if (s.mc) {

@@ -64,6 +64,8 @@ struct ZArgs {
   long long n;                   // normals per stream (d)
   int nblocks;                   // raw blocks per stream
   long long stream0;             // stream s draws entropy stream0 + s (learner-sharded runs)
+  int run;                       // > 0: stream0 + (s / run) * period + s % run (interleaved
+  long long period;              //      learner sets, rm_set_shard_streams)
 };
 
 __device__ __forceinline__ uint32_t zs_hashmix(uint32_t v, uint32_t& hc) {
@@ -93,7 +95,9 @@ __device__ ZStream z_seed(const ZArgs& a, int stream) {
     }
   };
   if (a.append >= 1) limbs(a.k);
-  if (a.append >= 2) limbs((uint64_t)(stream + a.stream0));
+  if (a.append >= 2)
+    limbs((uint64_t)(a.stream0 + (a.run > 0 ? (stream / a.run) * a.period + stream % a.run
+                                             : (long long)stream)));
   uint32_t pool[4];
   uint32_t hc = 0x43b0d7e5u;
   for (int i = 0; i < 4; i++) pool[i] = zs_hashmix(i < n ? ent[i] : 0u, hc);
@@ -991,9 +995,15 @@ static int z_front(const ZArgs& a, const ZWs& w, cudaStream_t st) {
   return 0;
 }
 
+// rm_set_shard_streams: the calling thread's learner interleave for the next generator calls
+static thread_local int g_stream_run = 0;
+static thread_local long long g_stream_period = 0;
+
 static int z_args(ZArgs* a, const uint32_t* prefix, int nprefix, int append, uint64_t k,
                   int nstreams, long long n, long long stream0 = 0) {
   *a = ZArgs{};
+  a->run = g_stream_run;
+  a->period = g_stream_period;
   for (int i = 0; i < nprefix; i++) a->prefix[i] = prefix[i];
   a->nprefix = nprefix;
   a->append = append;
@@ -1353,6 +1363,20 @@ int quad_z_prepare(const uint32_t* prefix, int nprefix, uint64_t k, int nstreams
 }
 
 }  // namespace rm
+
+// Learner sets of an interleaved sharding (numpy-order D1D: a rank holds runs of `run`
+// consecutive learners every `period`): stream s of the following rm_quadratic_grad_shard_* /
+// rm_quadratic_mean_step_shard_* calls from this host thread is learner
+// learner0 + (s / run) * period + s % run.  run = 0 restores contiguous learners.
+extern "C" int rm_set_shard_streams(int run, int64_t period) {
+  if (run < 0 || (run > 0 && period < run)) {
+    set_error("invalid learner interleave (run %d, period %lld)", run, (long long)period);
+    return RM_EINVAL;
+  }
+  g_stream_run = run;
+  g_stream_period = run > 0 ? period : 0;
+  return 0;
+}
 
 extern "C" int rm_quadratic_grad_f32(const uint32_t* prefix_words, int n_prefix, uint64_t k,
                                      int L, int64_t d, const float* Phi, int64_t ldp,

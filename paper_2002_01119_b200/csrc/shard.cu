@@ -266,12 +266,79 @@ __global__ void __launch_bounds__(kShThreads, 1)
 // thread; the scalar tail handles d % VEC columns.  The bodies are range
 // functions over (worker, nworkers) so the fused D1D kernel (below) can run them
 // on a subset of its CTAs.
+// numpy order (R = chains per rank > 0; fp32 / fp64): the rank holds the learners of
+// numpy's pairwise chains [g R, (g + 1) R) — local row i is in chain i % R — and its partial is
+// numpy's tree over those chains: chain q summed from its first element, ((c0 + c1) + ...).
+// With the ranks' partials combined in the tree order too (sym_ld_sum_tree_f64) the mean is
+// numpy's W.mean(axis=1) bit for bit, as on one GPU (8 <= L <= 128, L % 8 == 0).
+template <typename T, int R>
+__device__ __forceinline__ void partial_sum_numpy_range(const T* __restrict__ W, int Lg,
+                                                        long long d, long long ld,
+                                                        double* __restrict__ S, long long worker,
+                                                        long long nworkers) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  const long long nvec = d / VEC;
+  for (long long v = worker; v < nvec; v += nworkers) {
+    double s[R][VEC];
+    const T* p = W + v * VEC;
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      Vec<T> x;
+      x.raw = __ldcs(reinterpret_cast<const uint4*>(p + (long long)q * ld));
+#pragma unroll
+      for (int e = 0; e < VEC; e++) s[q][e] = (double)E::ld(x.e(), e);
+    }
+    for (int l = R; l < Lg; l += R) {
+      Vec<T> x[R];
+#pragma unroll
+      for (int q = 0; q < R; q++)
+        x[q].raw = __ldcs(reinterpret_cast<const uint4*>(p + (long long)(l + q) * ld));
+#pragma unroll
+      for (int q = 0; q < R; q++)
+#pragma unroll
+        for (int e = 0; e < VEC; e++) s[q][e] = __dadd_rn(s[q][e], (double)E::ld(x[q].e(), e));
+    }
+#pragma unroll
+    for (int w = 1; w < R; w *= 2)
+#pragma unroll
+      for (int q = 0; q + w < R; q += 2 * w)
+#pragma unroll
+        for (int e = 0; e < VEC; e++) s[q][e] = __dadd_rn(s[q][e], s[q + w][e]);
+#pragma unroll
+    for (int e = 0; e < VEC; e++) S[v * VEC + e] = s[0][e];
+  }
+  for (long long c = nvec * VEC + worker; c < d; c += nworkers) {
+    double s[R];
+#pragma unroll
+    for (int q = 0; q < R; q++) s[q] = (double)E::ld(W + (long long)q * ld + c, 0);
+    for (int l = R; l < Lg; l += R)
+#pragma unroll
+      for (int q = 0; q < R; q++) s[q] = __dadd_rn(s[q], (double)E::ld(W + (long long)(l + q) * ld + c, 0));
+#pragma unroll
+    for (int w = 1; w < R; w *= 2)
+#pragma unroll
+      for (int q = 0; q + w < R; q += 2 * w) s[q] = __dadd_rn(s[q], s[q + w]);
+    S[c] = s[0];
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void partial_sum_range(const T* __restrict__ W, int Lg, long long d,
                                                   long long ld, double* __restrict__ S,
-                                                  long long worker, long long nworkers) {
+                                                  long long worker, long long nworkers,
+                                                  int chains = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
+  if constexpr (sizeof(T) >= 4) {
+    switch (chains) {
+      case 1: return partial_sum_numpy_range<T, 1>(W, Lg, d, ld, S, worker, nworkers);
+      case 2: return partial_sum_numpy_range<T, 2>(W, Lg, d, ld, S, worker, nworkers);
+      case 4: return partial_sum_numpy_range<T, 4>(W, Lg, d, ld, S, worker, nworkers);
+      case 8: return partial_sum_numpy_range<T, 8>(W, Lg, d, ld, S, worker, nworkers);
+      default: break;
+    }
+  }
   const long long nvec = d / VEC;
   for (long long v = worker; v < nvec; v += nworkers) {
     double s[VEC];
@@ -309,9 +376,9 @@ __device__ __forceinline__ void partial_sum_range(const T* __restrict__ W, int L
 template <typename T>
 __global__ void __launch_bounds__(256)
     partial_sum_kernel(const T* __restrict__ W, int Lg, long long d, long long ld,
-                       double* __restrict__ S) {
+                       double* __restrict__ S, int chains) {
   partial_sum_range<T>(W, Lg, d, ld, S, blockIdx.x * (long long)blockDim.x + threadIdx.x,
-                       (long long)gridDim.x * blockDim.x);
+                       (long long)gridDim.x * blockDim.x, chains);
 }
 
 // out[j][c] = S[c]/L - lr*G[j][c] for the Lg local learners.  One thread per
@@ -688,6 +755,9 @@ extern "C" int rm_shard_plan(const int32_t* left, const int32_t* right, int L, i
 // pipeline that runs the in-switch reduction concurrently with the local
 // partial-sum / apply kernels lowers them so the kernels can be co-resident.
 static thread_local int g_d1d_psum_cap = 0;
+// numpy-order D1D (rm_set_d1d_numpy_order): chains per rank of the partial sums, 0 = legacy
+// ascending-row sums and ascending-rank cross-rank sums
+static thread_local int g_d1d_chains = 0;
 static thread_local int g_d1d_apply_cap = 0;
 static thread_local int g_d1d_nvls_cap = 0;
 
@@ -696,6 +766,15 @@ static thread_local int g_d1d_nvls_cap = 0;
 namespace rm {
 int d1d_psum_cap() { return g_d1d_psum_cap; }
 }  // namespace rm
+
+extern "C" int rm_set_d1d_numpy_order(int chains) {
+  if (chains != 0 && chains != 1 && chains != 2 && chains != 4 && chains != 8) {
+    set_error("numpy-order D1D: chains per rank must be 0, 1, 2, 4 or 8");
+    return RM_EINVAL;
+  }
+  g_d1d_chains = chains;
+  return 0;
+}
 
 extern "C" int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls) {
   if (partial_sum < 0 || partial_sum > 16 || apply < 0 || apply > 16 || nvls < 0 || nvls > 16) {
@@ -729,8 +808,12 @@ extern "C" int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls) {
     long long blocks = (d + 255) / 256;                                                         \
     const long long cap = (g_d1d_psum_cap ? g_d1d_psum_cap : 16) * (long long)sm_count(-1);     \
     if (blocks > cap) blocks = cap;                                                             \
+    if (g_d1d_chains && (sizeof(CT) < 4 || Lg % g_d1d_chains)) {                               \
+      set_error("numpy-order partial sums need fp32/fp64 and Lg a multiple of the chains");    \
+      return RM_EINVAL;                                                                         \
+    }                                                                                           \
     partial_sum_kernel<T><<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(         \
-        reinterpret_cast<const T*>(W), Lg, d, ld, S);                                           \
+        reinterpret_cast<const T*>(W), Lg, d, ld, S, g_d1d_chains);                             \
     RM_CHECK_LAUNCH("partial_sum_kernel");                                                      \
     return 0;                                                                                   \
   }                                                                                             \
@@ -772,14 +855,14 @@ RM_DEFINE_SHARD(bf16, uint16_t, __nv_bfloat16)
 namespace rm {
 __device__ __forceinline__ void nvls_sum_range(const SymRef& P, const SymRef& M, long long c0,
                                                long long c1, double L, long long worker,
-                                               long long nworkers) {
+                                               long long nworkers, bool tree = false) {
   constexpr int U = 8;
   for (long long c = c0 + worker; c < c1; c += U * nworkers) {
     double v[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const long long cc = c + u * nworkers;
-      if (cc < c1) v[u] = sym_ld_sum_f64(P, cc);
+      if (cc < c1) v[u] = tree ? sym_ld_sum_tree_f64(P, cc) : sym_ld_sum_f64(P, cc);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
@@ -790,9 +873,9 @@ __device__ __forceinline__ void nvls_sum_range(const SymRef& P, const SymRef& M,
 }
 
 __global__ void __launch_bounds__(256)
-    nvls_sum_kernel(SymRef P, SymRef M, long long c0, long long c1, double L) {
+    nvls_sum_kernel(SymRef P, SymRef M, long long c0, long long c1, double L, bool tree) {
   nvls_sum_range(P, M, c0, c1, L, blockIdx.x * (long long)blockDim.x + threadIdx.x,
-                 (long long)gridDim.x * blockDim.x);
+                 (long long)gridDim.x * blockDim.x, tree);
 }
 
 static int launch_sym_mean(const SymRef& P, const SymRef& M, int64_t c0, int64_t c1, int L,
@@ -801,8 +884,13 @@ static int launch_sym_mean(const SymRef& P, const SymRef& M, int64_t c0, int64_t
   long long blocks = (c1 - c0 + 2047) / 2048;
   const long long cap = (g_d1d_nvls_cap ? g_d1d_nvls_cap : 8) * (long long)sm_count(-1);
   if (blocks > cap) blocks = cap;
-  nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(P, M, c0, c1,
-                                                                             (double)L);
+  if (g_d1d_chains && P.mc && P.world > 2) {
+    set_error("numpy-order D1D over more than 2 ranks needs peer tables (the switch's "
+              "summation order is unspecified)");
+    return RM_EINVAL;
+  }
+  nvls_sum_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      P, M, c0, c1, (double)L, g_d1d_chains != 0);
   RM_CHECK_LAUNCH("nvls_sum_kernel");
   return 0;
 }
@@ -879,6 +967,7 @@ struct D1DFusedArgs {
   int nchunks, max_chunks;
   uint32_t epoch;
   int nP, nR, nA;
+  int chains;                // numpy-order partial sums (0 = ascending rows / ranks)
 };
 
 template <typename T, bool HAS_G, int MINB>
@@ -900,7 +989,7 @@ __global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(const __grid_const
     const long long nw = (long long)a.nP * blockDim.x;
     for (int c = 0; c < a.nchunks; c++) {
       const long long b = c * a.chunk, e = min(b + a.chunk, a.d);
-      partial_sum_range<T>(W + b, R.Lg, e - b, a.ldw, R.P + b, w, nw);
+      partial_sum_range<T>(W + b, R.Lg, e - b, a.ldw, R.P + b, w, nw, a.chains);
       xgpu_arrive(cntP + c, (uint32_t)a.nP * a.epoch, a.F, c);
     }
   } else if (bid < a.nP + a.nR) {
@@ -912,7 +1001,7 @@ __global__ void __launch_bounds__(256, MINB) d1d_fused_kernel(const __grid_const
       sl = (sl + 31) / 32 * 32;
       const long long s0 = min(e, b + R.rank * sl), s1 = min(e, s0 + sl);
       xgpu_wait(flagsA + c, all_ranks);
-      nvls_sum_range(a.P, a.M, s0, s1, (double)a.L, w, nw);
+      nvls_sum_range(a.P, a.M, s0, s1, (double)a.L, w, nw, a.chains != 0);
       xgpu_arrive(cntR + c, (uint32_t)a.nR * a.epoch, a.F, a.max_chunks + c);
     }
   } else {
@@ -960,6 +1049,17 @@ static int d1d_fused(const D1DRank* ranks, int nlocal, int L, int64_t d, int64_t
       set_error("fused D1D needs 16-byte aligned rows");
       return RM_EINVAL;
     }
+  }
+  if (g_d1d_chains) {
+    if (sizeof(T) < 4 || (P.mc && world > 2)) {
+      set_error("numpy-order D1D needs fp32/fp64 and, above 2 ranks, peer tables");
+      return RM_EINVAL;
+    }
+    for (int i = 0; i < nlocal; i++)
+      if (ranks[i].Lg % g_d1d_chains) {
+        set_error("numpy-order D1D: Lg must be a multiple of the chains per rank");
+        return RM_EINVAL;
+      }
   }
   if (chunk_cols < 32LL * world || chunk_cols % (32LL * world) != 0) {
     set_error("chunk_cols must be a positive multiple of 32 * world");
@@ -1014,6 +1114,7 @@ static int d1d_fused(const D1DRank* ranks, int nlocal, int L, int64_t d, int64_t
   a.nP = max(1, per_rank * pct_partial / 100);
   a.nR = max(1, per_rank * pct_reduce / 100);
   a.nA = per_rank - a.nP - a.nR;
+  a.chains = g_d1d_chains;
   if (a.nA < 1) {
     set_error("fused D1D: no CTAs left for the apply role");
     return RM_EINVAL;

@@ -65,6 +65,63 @@ class ShardLayout:
         return learner - self.bounds[self.owner(learner)][0]
 
 
+def d1d_numpy_chains(L: int, world: int, multicast_reduce: bool = False) -> int:
+    """Chains per rank of the numpy-order learner-sharded D1D (rm_set_d1d_numpy_order), or 0
+    where it does not apply: numpy's non-recursive pairwise mean needs 8 <= L <= 128 with
+    L % 8 == 0, the eight chains must split evenly (world 1, 2, 4 or 8), and an in-switch
+    (or NCCL) reduction of more than two ranks has no specified order.
+    RINGMIX_D1D_NUMPY_ORDER=0 turns it off."""
+    if os.environ.get("RINGMIX_D1D_NUMPY_ORDER", "1") == "0":
+        return 0
+    if L % 8 or not 8 <= L <= 128 or world not in (1, 2, 4, 8):
+        return 0
+    if multicast_reduce and world > 2:
+        return 0
+    return 8 // world
+
+
+def d1d_learners(L: int, world: int, rank: int, chains: int) -> list[int]:
+    """Global learner ids of `rank`'s local rows: with numpy-order chains, the learners of
+    numpy's pairwise chains [rank * chains, (rank + 1) * chains) in ascending order
+    (local row i = learner (i // chains) * 8 + rank * chains + i % chains); else the
+    contiguous block of ShardLayout."""
+    if chains:
+        return [(i // chains) * 8 + rank * chains + i % chains for i in range(L // world)]
+    b, e = ShardLayout(L, world).bounds[rank]
+    return list(range(b, e))
+
+
+class _NumpyOrder:
+    """Scope of rm_set_d1d_numpy_order for the calling thread's launches."""
+
+    def __init__(self, chains: int):
+        self.chains = chains
+
+    def __enter__(self):
+        if self.chains:
+            _lib.check(_lib.load().rm_set_d1d_numpy_order(self.chains), "rm_set_d1d_numpy_order")
+
+    def __exit__(self, *exc):
+        if self.chains:
+            _lib.load().rm_set_d1d_numpy_order(0)
+
+
+class _ShardStreams:
+    """Scope of rm_set_shard_streams: the generator draws the numpy-order learner set
+    (runs of `chains` learners every 8) for the calling thread's launches."""
+
+    def __init__(self, chains: int):
+        self.chains = chains
+
+    def __enter__(self):
+        if self.chains:
+            _lib.check(_lib.load().rm_set_shard_streams(self.chains, 8), "rm_set_shard_streams")
+
+    def __exit__(self, *exc):
+        if self.chains:
+            _lib.load().rm_set_shard_streams(0, 0)
+
+
 def plan_reference(left, right, row0: int, Lg: int):
     """Host restatement of rm_shard_plan: (remote ids, staged triples) for the
     rank owning [row0, row0+Lg).  Used by the tests to check the device planner."""
@@ -558,6 +615,9 @@ class LearnerShardedD1DNVLS:
         # (partial sum, apply, in-switch reduce); apply needs 75 registers per thread
         env = os.environ.get("RINGMIX_D1D_CTAS", "4,2,2").split(",")
         self.ctas_per_sm = tuple(int(x) for x in env)
+        # numpy-order partial sums (bit-identical to the one-GPU mean) where the in-switch
+        # sum is exact; local rows then hold d1d_learners(L, world, rank, chains)
+        self.chains = d1d_numpy_chains(L, self.world, multicast_reduce=True)
 
     def _launch_partial(self, W: torch.Tensor, i: int, stream) -> torch.cuda.Event:
         """Partial sums of chunk i on `stream`, then (comm stream) the in-switch mean of this
@@ -567,8 +627,9 @@ class LearnerShardedD1DNVLS:
         b, e = self.chunks[i]
         esz = W.element_size()
         psum = getattr(lib, f"rm_partial_sum_{mixing._suffix(W)}")
-        _lib.check(psum(W.data_ptr() + b * esz, self.Lg, e - b, W.stride(0),
-                        self.P.data_ptr() + b * 8, stream.cuda_stream), "rm_partial_sum")
+        with _NumpyOrder(self.chains if W.element_size() >= 4 else 0):
+            _lib.check(psum(W.data_ptr() + b * esz, self.Lg, e - b, W.stride(0),
+                            self.P.data_ptr() + b * 8, stream.cuda_stream), "rm_partial_sum")
         ev = torch.cuda.Event()
         ev.record(stream)
         self.comm.wait_event(ev)
@@ -669,6 +730,13 @@ class LearnerShardedD1DFused:
         # (unicast NVLink loads / stores, rm_d1d_fused_p2p_*)
         handles = (self.hP, self.hM, self.hF)
         self.multicast = all(_use_multicast(h) for h in handles)
+        # numpy order (the one-GPU step's bits): free with the in-switch sum up to 2 ranks;
+        # above that only with peer tables (RINGMIX_D1D_NUMPY_ORDER=1 switches to them)
+        self.chains = d1d_numpy_chains(L, self.world, multicast_reduce=self.multicast)
+        if (not self.chains and self.multicast and self.world > 2
+                and os.environ.get("RINGMIX_D1D_NUMPY_ORDER") == "1"):
+            self.multicast = False
+            self.chains = d1d_numpy_chains(L, self.world)
         self._sym = [_sym_addresses(h, self.device) if self.multicast
                      else (0, _peer_table(h, self.device)) for h in handles]
         self.counters = torch.zeros(2 * self.MAX_CHUNKS, dtype=torch.int32, device=self.device)
@@ -694,6 +762,12 @@ class LearnerShardedD1DFused:
         sfx = mixing._suffix(W)
         epoch = self.epoch + 1       # committed only once the launch succeeded
         ldg = G.stride(0) if G is not None else 0
+        with _NumpyOrder(self.chains if W.element_size() >= 4 else 0):
+            self._launch(lib, sfx, W, G, ldg, lr, out, absmax, epoch)
+        self.epoch = epoch
+        return out
+
+    def _launch(self, lib, sfx, W, G, ldg, lr, out, absmax, epoch):
         if self.multicast:
             (pmc, _), (mmc, _), (fmc, _) = self._sym
             _lib.check(getattr(lib, f"rm_d1d_fused_nvls_{sfx}")(
@@ -712,8 +786,6 @@ class LearnerShardedD1DFused:
                 pt.data_ptr(), mt.data_ptr(), ft.data_ptr(), self.world, self.chunk,
                 self.MAX_CHUNKS, epoch, self.split[0], self.split[1], _lib.stream_ptr()),
                 "rm_d1d_fused_p2p")
-        self.epoch = epoch
-        return out
 
 
 class LearnerShardedD1D:
@@ -729,6 +801,8 @@ class LearnerShardedD1D:
         self.chunks = [(b, min(b + step, d)) for b in range(0, d, step)]
         self.S = torch.empty(d, dtype=torch.float64, device=self.device)
         self.comm = torch.cuda.Stream(device=self.device)
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.chains = d1d_numpy_chains(L, world, multicast_reduce=True)
         # co-residency of the pipelined kernels: (local partial-sum/apply, in-switch)
         # (partial sum, apply, in-switch reduce); apply needs 75 registers per thread
         env = os.environ.get("RINGMIX_D1D_CTAS", "4,2,2").split(",")
@@ -746,8 +820,10 @@ class LearnerShardedD1D:
 
         def launch_partial(i):
             b, e = self.chunks[i]
-            _lib.check(psum(W.data_ptr() + b * esz, self.Lg, e - b, W.stride(0),
-                            self.S.data_ptr() + b * 8, compute.cuda_stream), "rm_partial_sum")
+            with _NumpyOrder(self.chains if W.element_size() >= 4 else 0):
+                _lib.check(psum(W.data_ptr() + b * esz, self.Lg, e - b, W.stride(0),
+                                self.S.data_ptr() + b * 8, compute.cuda_stream),
+                           "rm_partial_sum")
             ev = torch.cuda.Event()
             ev.record(compute)
             self.comm.wait_event(ev)
@@ -790,7 +866,9 @@ class ShardedD1DTrainer:
     Without ``overlap`` the gradient runs first, then the single-kernel fused D1D step
     (LearnerShardedD1DFused).  All modes give the same bits.
     learner0: this rank's first learner (its rows draw the gradient streams
-    learner0 + l)."""
+    learner0 + l) — with the numpy-order D1D sharding (``chains`` > 0, the default where it
+    is exact) local row i is learner d1d_learners(L, world, rank, chains)[i] instead, and
+    the generator draws those learners' streams (rm_set_shard_streams)."""
 
     def __init__(self, L: int, d: int, Lg: int, learner0: int, device, oracle, group=None,
                  overlap: bool | None = None, ctas: tuple[int, int, int] | None = None,
@@ -815,6 +893,9 @@ class ShardedD1DTrainer:
         split = overlap or fuse_grad   # the average as its own pipeline (mean_async)
         self.nvls = LearnerShardedD1DNVLS(L, d, Lg, device, group=group) if split else None
         self.fused = None if split else LearnerShardedD1DFused(L, d, Lg, device, group=group)
+        self.chains = (self.nvls or self.fused).chains
+        if self.chains:
+            self.learner0 = dist.get_rank(group) * self.chains
         # high priority: the memory-bound partial sums take SM slots as the compute-bound
         # generator's CTAs retire instead of queueing behind all of them
         self.side = torch.cuda.Stream(device=self.device, priority=-1)
@@ -826,7 +907,9 @@ class ShardedD1DTrainer:
         if self.G is None or self.G.shape != W.shape or self.G.dtype != W.dtype:
             self.G = mixing.empty_learner_major(self.Lg, self.d, W.dtype, self.device)
         if self.fused is not None:
-            G = self.oracle.device_gradients(W_prev, cfg, k, learner0=self.learner0, out=self.G)
+            with _ShardStreams(self.chains):
+                G = self.oracle.device_gradients(W_prev, cfg, k, learner0=self.learner0,
+                                                 out=self.G)
             return self.fused.step(W, G, lr, out, absmax=absmax)
         lib = _lib.load()
         if self.overlap:
@@ -841,7 +924,9 @@ class ShardedD1DTrainer:
         if self.fuse_grad and W.dtype in (torch.float32, torch.float64):
             self._fused_mean_step(W_prev, cfg, k, lr, out, ready[-1], absmax)
         else:
-            G = self.oracle.device_gradients(W_prev, cfg, k, learner0=self.learner0, out=self.G)
+            with _ShardStreams(self.chains):
+                G = self.oracle.device_gradients(W_prev, cfg, k, learner0=self.learner0,
+                                                 out=self.G)
             self.nvls.apply(W, G, lr, out, ready, absmax=absmax)
         main.wait_stream(self.side)
         return out
@@ -849,8 +934,9 @@ class ShardedD1DTrainer:
     def _fused_mean_step(self, W_prev, cfg, k, lr, out, ready, absmax):
         """out = M - lr * G(W_prev) with the gradient fused into the final pass; the
         generator runs now, its mix waits for `ready` (every chunk's global means)."""
-        self.oracle.device_mean_step(self.nvls.M, W_prev, lr, cfg, k, ready=ready,
-                                     learner0=self.learner0, absmax=absmax, out=out)
+        with _ShardStreams(self.chains):
+            self.oracle.device_mean_step(self.nvls.M, W_prev, lr, cfg, k, ready=ready,
+                                         learner0=self.learner0, absmax=absmax, out=out)
 
     def close(self):
         pass

@@ -24,7 +24,7 @@ import pytest
 import torch
 
 from oracle import ringmix_oracle as O
-from paper_2002_01119_b200 import _lib, distributed as D, mixing
+from paper_2002_01119_b200 import _lib, distributed as D, mixing, simulation
 
 pytestmark = pytest.mark.gpu
 
@@ -169,6 +169,111 @@ def test_fused_d1d_emulated_equals_single_gpu_to_fp64_rounding():
     scale = W.double().abs().mean(0, keepdim=True) + 0.01 * G.double().abs()
     assert bool((diff <= 2.0**-23 * (ref.double().abs() + scale)).all())
     assert float((out != ref).double().mean()) < 1e-4
+
+
+@pytest.mark.parametrize("L,d,world", [(16, 1000, 2), (64, 100_003, 4), (64, 25_001, 8),
+                                       (128, 4099, 2), (8, 777, 1), (64, 5000, 1)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_numpy_order_d1d_emulated_world_equals_single_gpu(L, d, world, dtype):
+    """rm_set_d1d_numpy_order: rank g holds the learners of numpy's pairwise chains
+    [g R, (g + 1) R) (R = 8 / world); its partial is numpy's tree over them and the ranks are
+    combined in the tree order, so every rank's rows are the single-GPU D1D step's rows bit
+    for bit (mixing.py:122-124, simulation.py:304-312) — the fused kernel over peer tables,
+    several epochs."""
+    chains = D.d1d_numpy_chains(L, world)
+    assert chains == 8 // world
+    g = torch.Generator(device="cuda").manual_seed(L + d + world)
+    W = _rand(L, d, dtype, g)
+    G = _rand(L, d, dtype, g)
+    lr = 0.01
+    ids = [torch.tensor(D.d1d_learners(L, world, r, chains), device="cuda") for r in range(world)]
+    Lg = L // world
+    def gather(X, i):
+        t = mixing.empty_learner_major(Lg, d, dtype)
+        t.copy_(X[i])
+        return t
+
+    cur = [gather(W, i) for i in ids]
+    Gs = [gather(G, i) for i in ids]
+    outs = [[mixing.empty_learner_major(Lg, d, dtype) for _ in range(world)] for _ in range(2)]
+    P = [torch.empty(d, dtype=torch.float64, device="cuda") for _ in range(world)]
+    M = [torch.empty(d, dtype=torch.float64, device="cuda") for _ in range(world)]
+    F = [torch.zeros(2 * MAX_CHUNKS, dtype=torch.int32, device="cuda") for _ in range(world)]
+    C = [torch.zeros(2 * MAX_CHUNKS, dtype=torch.int32, device="cuda") for _ in range(world)]
+    amax = [torch.zeros((), dtype=torch.int64, device="cuda") for _ in range(world)]
+    tP, tM, tF = _table(P), _table(M), _table(F)
+    lib = _lib.load()
+    fn = getattr(lib, f"rm_d1d_fused_p2p_{mixing._suffix(W)}")
+    _lib.check(lib.rm_set_xgpu_timeout(30.0))
+    full = W
+    try:
+        _lib.check(lib.rm_set_d1d_numpy_order(chains))
+        for epoch in (1, 2, 3):
+            ref = mixing.mean_mix_sgd(full, G, lr)
+            dst = outs[epoch % 2]
+            ranks = (_lib.D1DRank * world)()
+            for r in range(world):
+                amax[r].zero_()
+                ranks[r] = _lib.D1DRank(cur[r].data_ptr(), Gs[r].data_ptr(), dst[r].data_ptr(),
+                                        amax[r].data_ptr(), P[r].data_ptr(), M[r].data_ptr(),
+                                        F[r].data_ptr(), C[r].data_ptr(), Lg, r)
+            _lib.check(fn(ctypes.byref(ranks), world, L, d, cur[0].stride(0), Gs[0].stride(0),
+                          dst[0].stride(0), lr, tP.data_ptr(), tM.data_ptr(), tF.data_ptr(),
+                          world, 32 * world * 64, MAX_CHUNKS, epoch, 30, 10, _lib.stream_ptr()),
+                       "rm_d1d_fused_p2p")
+            torch.cuda.synchronize()
+            assert _status() == 0
+            for r in range(world):
+                assert torch.equal(dst[r], ref[ids[r]]), (epoch, r)
+                assert simulation.absmax_value(amax[r]) == float(ref[ids[r]].abs().max())
+            cur = dst
+            full = ref
+        # the chunk-pipeline pieces: partial sums + peer-table tree reduction == column mean
+        S = [torch.empty(d, dtype=torch.float64, device="cuda") for _ in range(world)]
+        Mm = [torch.empty(d, dtype=torch.float64, device="cuda") for _ in range(world)]
+        psum = getattr(lib, f"rm_partial_sum_{mixing._suffix(W)}")
+        for r in range(world):
+            _lib.check(psum(cur[r].data_ptr(), Lg, d, cur[r].stride(0), S[r].data_ptr(),
+                            _lib.stream_ptr()), "rm_partial_sum")
+        tS, tMm = _table(S), _table(Mm)   # kept alive until the kernel has run
+        _lib.check(lib.rm_p2p_mean_f64(tS.data_ptr(), tMm.data_ptr(), world, 0, d, L,
+                                       _lib.stream_ptr()), "rm_p2p_mean_f64")
+        torch.cuda.synchronize()
+    finally:
+        lib.rm_set_d1d_numpy_order(0)
+    colmean = torch.empty(d, dtype=torch.float64, device="cuda")
+    _lib.check(getattr(lib, f"rm_column_mean_{mixing._suffix(W)}")(
+        full.data_ptr(), L, d, full.stride(0), colmean.data_ptr(), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    for r in range(world):
+        assert torch.equal(Mm[r], colmean)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_interleaved_gradient_streams_are_rows_of_the_full_call(world):
+    """rm_set_shard_streams: a numpy-order rank's learner set (runs of R learners every 8)
+    draws exactly those learners' gradient streams (objectives.py:84-90)."""
+    from paper_2002_01119_b200 import objectives
+    from paper_2002_01119_b200.simulation import RunConfig
+    L, d = 32, 3001
+    chains = 8 // world
+    oracle = objectives.quadratic_oracle(d, condition_number=4.0, noise_scale=1.0, seed=2)
+    cfg = RunConfig(n_learners=L, iterations=1, lr=0.1, batch_size=3, seed=11)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Phi = _rand(L, d, torch.float32, g)
+    full = oracle.device_gradients(Phi, cfg, 4)
+    lib = _lib.load()
+    for r in range(world):
+        ids = torch.tensor(D.d1d_learners(L, world, r, chains), device="cuda")
+        try:
+            _lib.check(lib.rm_set_shard_streams(chains, 8))
+            P = mixing.empty_learner_major(len(ids), d, torch.float32)
+            P.copy_(Phi[ids])
+            part = oracle.device_gradients(P, cfg, 4, learner0=r * chains)
+        finally:
+            lib.rm_set_shard_streams(0, 0)
+        torch.cuda.synchronize()
+        assert torch.equal(part, full[ids])
 
 
 # ---------------------------------------------------------------------------

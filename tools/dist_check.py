@@ -34,68 +34,91 @@ def main():
         same = bool(torch.equal(out, Wref[b:e]))
         pull_steps.append(same)
         ok &= same
-    # D1D
-    d1d = D.LearnerShardedD1D(L, d, ring.Lg, dev, chunk_cols=1 << 18)
-    out = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
-    d1d.step(ring.weights, Gl, 0.01, out)
+    # D1D: each layout's rows are the learners it holds — numpy-order chains (bit-identical to
+    # the one-GPU step) where the class uses them, else the contiguous block (fp64 rounding)
     ref = mixing.mean_mix_sgd(Wref, mixing.empty_learner_major(L, d, torch.float32, dev).copy_(Gf), 0.01)
+    Lg = ring.Lg
+
+    def shard(obj, X, dt=torch.float32):
+        ids = torch.tensor(D.d1d_learners(L, world, rank, getattr(obj, "chains", 0)), device=dev)
+        return ids, mixing.empty_learner_major(len(ids), d, dt, dev).copy_(X[ids].to(dt))
+
+    def check(obj, out, ids, refm, tol=2e-6):
+        if getattr(obj, "chains", 0):
+            return bool(torch.equal(out, refm[ids]))
+        return (out.double() - refm[ids].double()).abs().max().item() <= tol
+
+    d1d = D.LearnerShardedD1D(L, d, Lg, dev, chunk_cols=1 << 18)
+    ids, Wl = shard(d1d, Wref)
+    _, Gs = shard(d1d, Gf)
+    out = mixing.empty_learner_major(Lg, d, torch.float32, dev)
+    d1d.step(Wl, Gs, 0.01, out)
     torch.cuda.synchronize()
-    dd = (out.double() - ref[b:e].double()).abs().max().item()
-    ok_d1d = dd <= 2e-6
+    dd = (out.double() - ref[ids].double()).abs().max().item()
+    ok_d1d = check(d1d, out, ids, ref)
+    nvls = f"nccl chains={d1d.chains} maxdiff {dd:.2e}"
     # NVSwitch multicast variant (our own in-switch reduction kernel)
     try:
         outs = []
         for cc in (None, 1 << 16):   # one chunk, and the chunk pipeline
-            nv = D.LearnerShardedD1DNVLS(L, d, ring.Lg, dev, chunk_cols=cc)
-            out2 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
+            nv = D.LearnerShardedD1DNVLS(L, d, Lg, dev, chunk_cols=cc)
+            ids, Wl = shard(nv, Wref)
+            _, Gs = shard(nv, Gf)
+            out2 = mixing.empty_learner_major(Lg, d, torch.float32, dev)
             for _ in range(2):
-                nv.step(ring.weights, Gl, 0.01, out2)
+                nv.step(Wl, Gs, 0.01, out2)
             torch.cuda.synchronize()
-            dd2 = (out2.double() - ref[b:e].double()).abs().max().item()
-            ok_d1d = ok_d1d and dd2 <= 2e-6
+            ok_d1d = ok_d1d and check(nv, out2, ids, ref)
             outs.append(out2)
         ok_d1d = ok_d1d and bool(torch.equal(outs[0], outs[1]))
-        nvls = len(nv.chunks)
-        # one-kernel variant: same bits as the NVLS pipeline, over several epochs
-        fu = D.LearnerShardedD1DFused(L, d, ring.Lg, dev, chunk_cols=1 << 16)
-        out3 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
+        nvls += f"; nvls {len(nv.chunks)} chunks chains={nv.chains}"
+        # one-kernel variant over several epochs
+        fu = D.LearnerShardedD1DFused(L, d, Lg, dev, chunk_cols=1 << 16)
+        ids, Wl = shard(fu, Wref)
+        _, Gs = shard(fu, Gf)
+        out3 = mixing.empty_learner_major(Lg, d, torch.float32, dev)
         for _ in range(3):
-            fu.step(ring.weights, Gl, 0.01, out3)
+            fu.step(Wl, Gs, 0.01, out3)
         torch.cuda.synchronize()
-        ok_d1d = ok_d1d and bool(torch.equal(out3, outs[0]))
-        nvls = f"{nvls} chunks; fused {len(fu.chunks)} chunks ok={bool(torch.equal(out3, outs[0]))}"
-        # the same fused step through peer tables (unicast NVLink, no multicast): the
-        # cross-rank sum runs in rank order, so it agrees to fp64 rounding of the sum
+        ok3 = check(fu, out3, ids, ref)
+        ok_d1d = ok_d1d and ok3
+        nvls += f"; fused {len(fu.chunks)} chunks chains={fu.chains} ok={ok3}"
+        # the same fused step through peer tables (unicast NVLink, no multicast); numpy order
+        # over any power-of-two world there (RINGMIX_D1D_NUMPY_ORDER=1 above 2 ranks)
         os.environ["RINGMIX_SYM_P2P"] = "1"
+        os.environ["RINGMIX_D1D_NUMPY_ORDER"] = "1"
         try:
-            fp = D.LearnerShardedD1DFused(L, d, ring.Lg, dev, chunk_cols=1 << 16)
+            fp = D.LearnerShardedD1DFused(L, d, Lg, dev, chunk_cols=1 << 16)
         finally:
             os.environ.pop("RINGMIX_SYM_P2P", None)
-        out5 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
+            os.environ.pop("RINGMIX_D1D_NUMPY_ORDER", None)
+        ids5, Wl5 = shard(fp, Wref)
+        _, Gs5 = shard(fp, Gf)
+        out5 = mixing.empty_learner_major(Lg, d, torch.float32, dev)
         for _ in range(3):
-            fp.step(ring.weights, Gl, 0.01, out5)
+            fp.step(Wl5, Gs5, 0.01, out5)
         torch.cuda.synchronize()
-        dd5 = (out5.double() - ref[b:e].double()).abs().max().item()
-        ok_d1d = ok_d1d and (not fp.multicast) and dd5 <= 2e-6
-        nvls += f"; fused-p2p maxdiff {dd5:.2e}"
+        dd5 = (out5.double() - ref[ids5].double()).abs().max().item()
+        ok_d1d = ok_d1d and (not fp.multicast) and check(fp, out5, ids5, ref)
+        nvls += f"; fused-p2p chains={fp.chains} maxdiff {dd5:.2e}"
         # no gradients (apply_mixing semantics): the fused kernel's HAS_G = false path
-        out4 = mixing.empty_learner_major(ring.Lg, d, torch.float32, dev)
-        fu.step(ring.weights, None, 0.01, out4)
+        out4 = mixing.empty_learner_major(Lg, d, torch.float32, dev)
+        fu.step(Wl, None, 0.01, out4)
         ref4 = mixing.mean_mix_sgd(Wref, None, 0.01)
         torch.cuda.synchronize()
-        ok_d1d = ok_d1d and (out4.double() - ref4[b:e].double()).abs().max().item() <= 2e-6
+        ok_d1d = ok_d1d and check(fu, out4, ids, ref4)
         # other storage types: the fused kernel against the single-GPU mean kernel
         for dt, tol in ((torch.float64, 1e-13), (torch.bfloat16, 1e-2)):
-            Wd = mixing.empty_learner_major(ring.Lg, d, dt, dev).copy_(full[b:e].to(dt))
-            Gd = mixing.empty_learner_major(ring.Lg, d, dt, dev).copy_(Gf[b:e].to(dt))
-            od = mixing.empty_learner_major(ring.Lg, d, dt, dev)
+            idd, Wd = shard(fu, full, dt)
+            _, Gd = shard(fu, Gf, dt)
+            od = mixing.empty_learner_major(Lg, d, dt, dev)
             fu.step(Wd, Gd, 0.01, od)
             Fd = mixing.empty_learner_major(L, d, dt, dev).copy_(full.to(dt))
             GFd = mixing.empty_learner_major(L, d, dt, dev).copy_(Gf.to(dt))
             rd = mixing.mean_mix_sgd(Fd, GFd, 0.01)
             torch.cuda.synchronize()
-            err = (od.double() - rd[b:e].double()).abs().max().item()
-            ok_d1d = ok_d1d and err <= tol
+            err = (od.double() - rd[idd].double()).abs().max().item()
+            ok_d1d = ok_d1d and (err == 0.0 if (fu.chains and dt == torch.float64) else err <= tol)
             nvls += f"; {dt} maxdiff {err:.2e}"
     except RuntimeError as exc:
         nvls = str(exc)[:100]
