@@ -15,7 +15,7 @@ import torch
 
 from golden_io import normal_cases, training_cases
 from oracle import ringmix_oracle as O
-from paper_2002_01119_b200 import mixing, objectives, seeding, simulation
+from paper_2002_01119_b200 import _lib, mixing, objectives, seeding, simulation
 from paper_2002_01119_b200.simulation import RunConfig, Strategy
 
 pytestmark = pytest.mark.gpu
@@ -297,3 +297,43 @@ def test_sharded_gradients_equal_rows_of_the_full_call(dtype):
     out = torch.empty_like(Phi[:4])
     assert oracle.device_gradients(Phi[3:7], cfg, k, learner0=3, out=out) is out
     assert torch.equal(out, full[3:7])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("L,d,b,e", [(16, 5_003, 4, 12), (64, 40_000, 32, 64), (8, 777, 0, 3)])
+def test_sharded_mean_step_equals_rows_of_the_two_pass_step(dtype, L, d, b, e):
+    """rm_quadratic_mean_step_shard_*: a rank's learners [b, e) of a learner-sharded D1D
+    training step with the gradient fused into the generator's final pass and the global
+    means M supplied (and waited for through an event) — rows b..e-1 of the single-GPU
+    step mean(W) - lr * G(Phi) (simulation.py:304-312)."""
+    oracle = objectives.quadratic_oracle(d, condition_number=6.0, noise_scale=1.2, seed=9)
+    cfg = RunConfig(n_learners=L, iterations=1, lr=0.03, batch_size=4, seed=21)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    X, Phi = (mixing.empty_learner_major(L, d, dtype) for _ in range(2))
+    X.copy_(torch.randn((L, d), generator=gen, device="cuda", dtype=torch.float64).to(dtype))
+    Phi.copy_(torch.randn((L, d), generator=gen, device="cuda", dtype=torch.float64).to(dtype))
+    k, lr = 6, 0.03
+    G = oracle.device_gradients(Phi, cfg, k)
+    ref = mixing.mean_mix_sgd(X, G, lr)
+    lib = _lib.load()
+    M = torch.empty(d, dtype=torch.float64, device="cuda")
+    sfx = mixing._suffix(X)
+    _lib.check(getattr(lib, f"rm_column_mean_{sfx}")(X.data_ptr(), L, d, X.stride(0),
+                                                      M.data_ptr(), _lib.stream_ptr()), "mean")
+    ready = torch.cuda.Event()
+    ready.record()
+    Lg = e - b
+    P = Phi[b:e]
+    out = mixing.empty_learner_major(Lg, d, dtype)
+    absmax = torch.zeros((), dtype=torch.int64, device="cuda")
+    ws = torch.empty(int(lib.rm_quadratic_mix_workspace_bytes(Lg, d)), dtype=torch.uint8,
+                     device="cuda")
+    words = seeding.entropy_words(cfg.seed, seeding.TAG_GRADIENT)
+    _lib.check(getattr(lib, f"rm_quadratic_mean_step_shard_{sfx}")(
+        words.ctypes.data, len(words), k, b, M.data_ptr(), P.data_ptr(), out.data_ptr(), Lg, d,
+        P.stride(0), out.stride(0), oracle._lam.data_ptr(), oracle._opt.data_ptr(),
+        float(oracle.noise_scale / np.sqrt(cfg.batch_size)), lr, absmax.data_ptr(),
+        ws.data_ptr(), ws.numel(), _lib.stream_ptr(), ready.cuda_event), "mean step shard")
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref[b:e])
+    assert simulation.absmax_value(absmax) == float(ref[b:e].abs().max())

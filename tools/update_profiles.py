@@ -1,11 +1,13 @@
-"""Copy the round-end captures of tools/gpu_final1.sh (gpurun_out/final/) into profiles/:
+"""Copy the round-end captures of tools/gpu_final1.sh (gpurun_out/final/; or
+`python tools/update_profiles.py <gpurun_out subdir> <file prefix>`) into profiles/:
 ncu summaries of the dominant kernels, the launch lists, and profiles/ncu_summary.json
 (the per-launch DRAM traffic bench.py reports as roofline.traffic)."""
 import json, shutil, subprocess, sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-SRC = ROOT / "gpurun_out" / "final"
+SRC = ROOT / "gpurun_out" / (sys.argv[1] if len(sys.argv) > 1 else "final")
+PREFIX = sys.argv[2] if len(sys.argv) > 2 else "r1_final"
 PROF = ROOT / "profiles"
 CASES = [("mix_rand_psgd_float32_L64_d25557032", "c2_rad", 12),
          ("mix_d1d_float32_L64_d25557032", "c4_d1d", 12),
@@ -23,7 +25,7 @@ def main():
     out = {}
     for key, name, bpp in CASES:
         rep = SRC / f"prof_{name}.ncu-rep"
-        js = PROF / f"r1_final_{name}_ncu.json"
+        js = PROF / f"{PREFIX}_{name}_ncu.json"
         txt = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), str(rep)],
                              capture_output=True, text=True, check=True).stdout
         js.write_text(txt)
@@ -38,7 +40,7 @@ def main():
                     "duration_ms_ncu": num(d["gpu__time_duration.sum"])}
     (PROF / "ncu_summary.json").write_text(json.dumps(out, indent=1) + "\n")
     for f in ("launches_default.csv", "launches_normals_c2.csv"):
-        shutil.copy(SRC / f, PROF / f"r1_final_{f}")
+        shutil.copy(SRC / f, PROF / f"{PREFIX}_{f}")
     print(json.dumps({k: v["traffic_over_algorithmic"] for k, v in out.items()}))
 
 
