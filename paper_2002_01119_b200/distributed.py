@@ -615,9 +615,16 @@ class LearnerShardedD1DNVLS:
         # (partial sum, apply, in-switch reduce); apply needs 75 registers per thread
         env = os.environ.get("RINGMIX_D1D_CTAS", "4,2,2").split(",")
         self.ctas_per_sm = tuple(int(x) for x in env)
-        # numpy-order partial sums (bit-identical to the one-GPU mean) where the in-switch
-        # sum is exact; local rows then hold d1d_learners(L, world, rank, chains)
-        self.chains = d1d_numpy_chains(L, self.world, multicast_reduce=True)
+        # numpy-order partial sums (bit-identical to the one-GPU mean); local rows then hold
+        # d1d_learners(L, world, rank, chains).  Up to 2 ranks the in-switch sum is exact;
+        # above, the reduction runs over peer tables in the tree order (rm_p2p_mean_f64) —
+        # at 4 ranks by default, at 8 on request (same rule as LearnerShardedD1DFused)
+        want = os.environ.get("RINGMIX_D1D_NUMPY_ORDER", "auto")
+        self.chains = d1d_numpy_chains(L, self.world) if (
+            self.world <= 4 or want == "1") else 0
+        self.p2p = bool(self.chains) and self.world > 2
+        if self.p2p:
+            self.tP, self.tM = _peer_table(self.hP, self.device), _peer_table(self.hM, self.device)
 
     def _launch_partial(self, W: torch.Tensor, i: int, stream) -> torch.cuda.Event:
         """Partial sums of chunk i on `stream`, then (comm stream) the in-switch mean of this
@@ -636,9 +643,15 @@ class LearnerShardedD1DNVLS:
         c0, c1 = self.shards[i]
         with torch.cuda.stream(self.comm):
             self.hP.barrier(channel=i)          # every rank's partials of chunk i
-            _lib.check(lib.rm_nvls_mean_f64(self.hP.multicast_ptr, self.hM.multicast_ptr,
-                                            c0, c1, self.L, self.comm.cuda_stream),
-                       "rm_nvls_mean_f64")
+            if self.p2p:
+                with _NumpyOrder(self.chains):  # tree order over the ranks
+                    _lib.check(lib.rm_p2p_mean_f64(self.tP.data_ptr(), self.tM.data_ptr(),
+                                                   self.world, c0, c1, self.L,
+                                                   self.comm.cuda_stream), "rm_p2p_mean_f64")
+            else:
+                _lib.check(lib.rm_nvls_mean_f64(self.hP.multicast_ptr, self.hM.multicast_ptr,
+                                                c0, c1, self.L, self.comm.cuda_stream),
+                           "rm_nvls_mean_f64")
             self.hM.barrier(channel=i)          # every rank's means of chunk i
             done = torch.cuda.Event()
             done.record(self.comm)
@@ -731,12 +744,16 @@ class LearnerShardedD1DFused:
         handles = (self.hP, self.hM, self.hF)
         self.multicast = all(_use_multicast(h) for h in handles)
         # numpy order (the one-GPU step's bits): free with the in-switch sum up to 2 ranks;
-        # above that only with peer tables (RINGMIX_D1D_NUMPY_ORDER=1 switches to them)
+        # above that the tree runs over peer tables — the default at 4 ranks (measured 1,001
+        # vs 1,032 G/s for the in-switch sum at C4, profiles/r3_p2psplit/), on request at 8
+        # (RINGMIX_D1D_NUMPY_ORDER=1; not measured on 8 GPUs)
         self.chains = d1d_numpy_chains(L, self.world, multicast_reduce=self.multicast)
-        if (not self.chains and self.multicast and self.world > 2
-                and os.environ.get("RINGMIX_D1D_NUMPY_ORDER") == "1"):
-            self.multicast = False
+        want = os.environ.get("RINGMIX_D1D_NUMPY_ORDER", "auto")
+        if (not self.chains and self.multicast and self.world > 2 and want != "0"
+                and (self.world <= 4 or want == "1")):
             self.chains = d1d_numpy_chains(L, self.world)
+            if self.chains:
+                self.multicast = False
         self._sym = [_sym_addresses(h, self.device) if self.multicast
                      else (0, _peer_table(h, self.device)) for h in handles]
         self.counters = torch.zeros(2 * self.MAX_CHUNKS, dtype=torch.int32, device=self.device)
@@ -745,7 +762,11 @@ class LearnerShardedD1DFused:
         chunk = max(chunk_cols, -(-d // self.MAX_CHUNKS), quantum)
         self.chunk = -(-chunk // quantum) * quantum
         if split is None:
-            env = os.environ.get("RINGMIX_D1D_FUSED_SPLIT", "30,10").split(",")
+            # CTA shares (partial sums, reduction; the rest apply): the in-switch reduction
+            # needs few CTAs, the peer-table reduction (world loads + world stores per
+            # column) many — 20 / 40 measured 1,001 vs 433 G/s for 30 / 10 at n = 4
+            dflt = "30,10" if self.multicast else "20,40"
+            env = os.environ.get("RINGMIX_D1D_FUSED_SPLIT", dflt).split(",")
             split = (int(env[0]), int(env[1]))
         self.split = split
         self.epoch = 0
