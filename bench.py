@@ -916,7 +916,12 @@ def run_ours(args):
             if float(ok.item()) < 1:
                 extras[name] = {"skipped": "not enough free HBM"}
                 continue
-            r2, w2 = measure(sp, torch, dist, dev, ws, rank, local, args, nvc=nvc)
+            try:
+                r2, w2 = measure(sp, torch, dist, dev, ws, rank, local, args, nvc=nvc)
+            except (RuntimeError, ValueError) as exc:   # an extra never costs the headline line
+                extras[name] = {"error": str(exc)[:200]}
+                torch.cuda.empty_cache()
+                continue
             if rank == 0:
                 extras[name] = extra_line(sp, r2, ws, dev, w2, mixing)
             w2.close()
