@@ -25,7 +25,9 @@ prints ONE JSON line on rank 0.  `--gpus N` without torchrun launches N ranks it
   `extras.learner_pull` times the learner-ordered pull layout on the same problem
   and `extras.coord_weak` the zero-communication coordinate stripes (every rank a
   64 x 25,557,032 stripe, weak scaling).  D1D (`--strategy d1d`, and `extras.c4_d1d_sharded`
-  on configs[3]) shards learners with the fused partial-sum / cross-GPU-reduce / apply kernel.
+  on configs[3]) shards learners with the fused partial-sum / cross-GPU-reduce / apply kernel;
+  `extras.c2_adpsgd_fixed_sharded` is configs[1]'s fixed ring with learners sharded (only the
+  two ring-boundary rows per rank cross GPUs).
 * `value`: whole-job learner-params / s, device time (CUDA events), max over ranks.
 * `e2e`: the same step through the public API with the step's inputs and results
   crossing PCIe every step: N = 1 host buffers in and out (W, G -> W',
@@ -901,6 +903,12 @@ def run_ours(args):
             todo.append(("c4_d1d_sharded", dict(strategy="d1d", layout="learner",
                                                 learners=C2[0], dim=C2[1], scaling="strong",
                                                 config_index=3)))
+            # north-star (d) as the paper states it: the fixed ring, where only the two
+            # ring-boundary rows of each rank cross GPUs (configs[1]'s AD-PSGD)
+            todo.append(("c2_adpsgd_fixed_sharded", dict(strategy="adpsgd_fixed",
+                                                         layout="learner", learners=C2[0],
+                                                         dim=C2[1], scaling="strong",
+                                                         config_index=1)))
             if spec.layout != "learner":
                 todo.append(("learner_pull", dict(layout="learner", learners=C3[0], dim=C3[1],
                                                   scaling="strong", config_index=2)))
