@@ -474,8 +474,11 @@ class Workload:
                 self.d1d_kind = "nccl"
             self.G = synth(self.rows, d)
         else:
-            cls = D.LearnerShardedRingPos if self.layout == "position" else D.LearnerShardedRing
-            self.sharded = cls(L, d, dtype)
+            if self.layout == "position":
+                self.sharded = D.LearnerShardedRingPos(L, d, dtype)
+            else:
+                self.sharded = D.LearnerShardedRing(
+                    L, d, dtype, fixed_ring=spec.strategy == "adpsgd_fixed")
             self.rows, self.cols = self.sharded.Lg, d
             fill(self.sharded.W[0])
             # the initial rows were written outside the step kernels: every rank's

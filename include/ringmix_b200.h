@@ -349,6 +349,11 @@ int rm_apply_mean_sgd_bf16(const double* S, const uint16_t* G, uint16_t* out, in
  * pipeline lowers them so the in-switch reduction of one chunk is co-resident (threads and
  * registers) with the local kernels of its neighbours. */
 int rm_set_d1d_ctas_per_sm(int partial_sum, int apply, int nvls);
+/* Bound, for the calling host thread, on the distinct remote rows a learner-sharded step pulls
+ * (0 = the layout's own bound, 2 * Lg).  A fixed ring with contiguous shards pulls at most 2
+ * (its boundary neighbours): with the bound the stages hold 1 KB row segments instead of
+ * reserving room for 2 * Lg remote rows.  A step whose plan exceeds the bound traps. */
+int rm_set_shard_remote_rows(int max_rows);
 /* numpy-order learner-sharded D1D, for the calling host thread: `chains` (1, 2, 4, 8; 0 =
  * off) of numpy's eight pairwise chains per rank.  Rank g then holds learners
  * {l : l % 8 in [g chains, (g + 1) chains)} in ascending order (L % 8 == 0, 8 <= L <= 128),

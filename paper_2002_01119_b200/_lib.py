@@ -71,6 +71,7 @@ _SIGNATURES = {
     "rm_nvls_mean_f64": ([vp, vp, i64, i64, i32, vp], i32),
     "rm_set_d1d_ctas_per_sm": ([i32, i32, i32], i32),
     "rm_set_d1d_numpy_order": ([i32], i32),
+    "rm_set_shard_remote_rows": ([i32], i32),
     "rm_set_shard_streams": ([i32, i64], i32),
     "rm_trace_stats_workspace_bytes": ([i32], i64),
     "rm_trace_stats_f32": ([vp, i32, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp], i32),

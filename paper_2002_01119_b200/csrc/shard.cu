@@ -47,6 +47,9 @@ static void xgpu_config() {
     attr_done(&g_xgpu_config_mask);
 }
 
+// rm_set_shard_remote_rows: the calling thread's bound on the distinct remote rows of a step
+static thread_local int g_shard_rmax_hint = 0;
+
 constexpr int kShThreads = 512;
 constexpr int kShMaxStages = 6;
 constexpr int kShStagesDefault = 3;
@@ -129,6 +132,7 @@ __global__ void __launch_bounds__(kShThreads, 1)
   const int cw = a.cw;
   const int tid = threadIdx.x;
   const int R = a.plan[0];
+  if (R > a.Rmax) __trap();   // the caller's remote-row bound was wrong: the stage would overflow
   const int Srows = Lg + R;
   const int w_bytes_max = (Lg + a.Rmax) * cw * (int)sizeof(T);
   const int g_bytes = HAS_G ? Lg * cw * (int)sizeof(T) : 0;
@@ -491,7 +495,10 @@ static int launch_shard(ShardArgs a, const T* W_local, long long ldw, const T* G
   // position layout with <= 32 local rows: 72 KB stages give 1 KB row segments (256 fp32
   // columns) — measured at C3 on 4 GPUs 863 vs 849 G/s; at 64 local rows the 64 KB target
   // (256-byte segments) stays ahead (746-753 vs 736-743), profiles/r2_n4_sweep/
-  const size_t dflt = (a.dest != nullptr && a.Lg <= 32) ? 72 * 1024 : kShStageTarget;
+  // few staged rows (position layout, or the fixed ring's two boundary rows) with <= 32
+  // local rows: 72 KB stages give >= 1 KB row segments — at C2 on 2 GPUs the fixed ring's
+  // kernel runs 1.49 ms against 1.87 ms with 512-byte segments (profiles/r3_ad_rmax/)
+  const size_t dflt = (a.Rmax <= 2 && a.Lg <= 32) ? 72 * 1024 : kShStageTarget;
   const size_t target = (env_kb >= 8 && env_kb <= 128) ? (size_t)env_kb * 1024 : dflt;
   int cw = VEC;
   while ((size_t)(cw * 2) * rows * esz <= target && cw * 2 <= 2048) cw *= 2;
@@ -582,6 +589,8 @@ static int shard_dispatch(const uint64_t* row_ptrs, const T* W_local, const T* G
   a.Lg = Lg;
   a.Rmax = (2 * Lg < L - Lg) ? 2 * Lg : L - Lg;
   if (dest != nullptr && a.Rmax > 2) a.Rmax = 2;  // position layout: two boundary rows
+  // caller's bound (rm_set_shard_remote_rows: the fixed ring pulls at most 2 rows)
+  if (g_shard_rmax_hint > 0 && g_shard_rmax_hint < a.Rmax) a.Rmax = g_shard_rmax_hint;
   a.plan = plan;
   a.lr = lr;
   a.absmax = absmax;
@@ -773,6 +782,15 @@ extern "C" int rm_set_d1d_numpy_order(int chains) {
     return RM_EINVAL;
   }
   g_d1d_chains = chains;
+  return 0;
+}
+
+extern "C" int rm_set_shard_remote_rows(int max_rows) {
+  if (max_rows < 0) {
+    set_error("remote-row bound must be >= 0 (0 = the layout's own bound)");
+    return RM_EINVAL;
+  }
+  g_shard_rmax_hint = max_rows;
   return 0;
 }
 

@@ -308,9 +308,13 @@ class LearnerShardedRing:
     """
 
     def __init__(self, L: int, d: int, dtype=torch.float32, group=None, device=None,
-                 step_sync: bool = True):
+                 step_sync: bool = True, fixed_ring: bool = False):
+        """fixed_ring: every step uses the fixed ring (AD-PSGD / D-PSGD), whose contiguous
+        shards pull at most their 2 boundary rows — the kernel's stages then need no room for
+        more (rm_set_shard_remote_rows), which lets them hold 1 KB row segments."""
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed must be initialised")
+        self.fixed_ring = fixed_ring
         _lib.require_cuda()
         self.group = group
         self.rank = dist.get_rank(group)
@@ -382,11 +386,18 @@ class LearnerShardedRing:
             mixing._same(src, G, "G")
         ldg = G.stride(0) if G is not None else self.ld
         args = None if self.sync is None else self.sync.begin()
-        _lib.check(self._fn(self.row_ptrs[self.cur].data_ptr(), src.data_ptr(), _lib.ptr(G),
-                            dst.data_ptr(), self.L, self.row0, self.Lg, self.d, self.ld, ldg,
-                            dst.stride(0), self.plan.data_ptr(), float(lr), _lib.ptr(absmax), s,
-                            None if args is None else ctypes.byref(args)),
-                   "rm_ring_mix_sgd_sharded")
+        if self.fixed_ring:
+            _lib.check(lib.rm_set_shard_remote_rows(2), "rm_set_shard_remote_rows")
+        try:
+            _lib.check(self._fn(self.row_ptrs[self.cur].data_ptr(), src.data_ptr(),
+                                _lib.ptr(G), dst.data_ptr(), self.L, self.row0, self.Lg,
+                                self.d, self.ld, ldg, dst.stride(0), self.plan.data_ptr(),
+                                float(lr), _lib.ptr(absmax), s,
+                                None if args is None else ctypes.byref(args)),
+                       "rm_ring_mix_sgd_sharded")
+        finally:
+            if self.fixed_ring:
+                lib.rm_set_shard_remote_rows(0)
         if self.sync is not None:
             self.sync.commit()
         self.cur = 1 - self.cur

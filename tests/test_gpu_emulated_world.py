@@ -304,14 +304,18 @@ def _full_and_parts(L, d, world, dtype, seed):
     return lay, full, Gf
 
 
-@pytest.mark.parametrize("L,d,world", [(16, 1000, 2), (10, 77, 3), (64, 4099, 8)])
+@pytest.mark.parametrize("L,d,world,fixed", [(16, 1000, 2, False), (10, 77, 3, False),
+                                             (64, 4099, 8, False), (64, 100_003, 2, True),
+                                             (64, 70_001, 4, True), (24, 5003, 3, True)])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_pull_layout_steps_ordered_in_kernel(L, d, world, dtype):
+def test_pull_layout_steps_ordered_in_kernel(L, d, world, fixed, dtype):
     """K consecutive learner-sharded RAD steps, every step kernel ordering itself through
-    the flags (waits for every rank's previous step, bumps every rank's flag)."""
+    the flags (waits for every rank's previous step, bumps every rank's flag).  fixed: the
+    fixed ring with the 2-remote-row bound (rm_set_shard_remote_rows: 1 KB row segments)."""
     lay, full, Gf = _full_and_parts(L, d, world, dtype, L + d)
     K = 4
     tabs = mixing.permutation_tables(L, 4242, 0, K)
+    fixed_tabs = tuple(t.contiguous() for t in simulation.fixed_ring_tables(L, torch.device("cuda")))
     esz = full.element_size()
     bufs = [[mixing.empty_learner_major(e - b, d, dtype) for _ in range(2)] for b, e in lay.bounds]
     Gs = []
@@ -334,21 +338,26 @@ def test_pull_layout_steps_ordered_in_kernel(L, d, world, dtype):
     plans = [torch.empty(lib.rm_shard_plan_ints(e - b), dtype=torch.int32, device="cuda")
              for b, e in lay.bounds]
     ref, cur = full, 0
-    for k in range(K):
-        lt, rt = (t.contiguous() for t in tabs.step(k))
-        epoch = k + 1
-        for r, (b, e) in enumerate(lay.bounds):      # rank order within an epoch
-            Lg = e - b
-            _lib.check(lib.rm_shard_plan(lt.data_ptr(), rt.data_ptr(), L, b, Lg,
-                                         plans[r].data_ptr(), _lib.stream_ptr()))
-            src, dst = bufs[r][cur], bufs[r][1 - cur]
-            a = sync.args(r, epoch)
-            _lib.check(fn(row_ptrs[cur].data_ptr(), src.data_ptr(), Gs[r].data_ptr(),
-                          dst.data_ptr(), L, b, Lg, d, src.stride(0), Gs[r].stride(0),
-                          dst.stride(0), plans[r].data_ptr(), 0.03, None, _lib.stream_ptr(),
-                          ctypes.byref(a)))
-        cur = 1 - cur
-        ref = mixing.ring_mix_sgd(ref, Gf, 0.03, lt, rt)
+    if fixed:
+        _lib.check(lib.rm_set_shard_remote_rows(2))
+    try:
+        for k in range(K):
+            lt, rt = fixed_tabs if fixed else (t.contiguous() for t in tabs.step(k))
+            epoch = k + 1
+            for r, (b, e) in enumerate(lay.bounds):      # rank order within an epoch
+                Lg = e - b
+                _lib.check(lib.rm_shard_plan(lt.data_ptr(), rt.data_ptr(), L, b, Lg,
+                                             plans[r].data_ptr(), _lib.stream_ptr()))
+                src, dst = bufs[r][cur], bufs[r][1 - cur]
+                a = sync.args(r, epoch)
+                _lib.check(fn(row_ptrs[cur].data_ptr(), src.data_ptr(), Gs[r].data_ptr(),
+                              dst.data_ptr(), L, b, Lg, d, src.stride(0), Gs[r].stride(0),
+                              dst.stride(0), plans[r].data_ptr(), 0.03, None,
+                              _lib.stream_ptr(), ctypes.byref(a)))
+            cur = 1 - cur
+            ref = mixing.ring_mix_sgd(ref, Gf, 0.03, lt, rt)
+    finally:
+        lib.rm_set_shard_remote_rows(0)
     # a reader of every rank's last step: stream-ordered wait, then compare
     _lib.check(lib.rm_step_sync_wait(ctypes.byref(sync.args(0, K)), _lib.stream_ptr()))
     torch.cuda.synchronize()

@@ -1,7 +1,8 @@
 """Single-process, two-GPU harness for the learner-sharded RAD pull kernel, so ncu can
 capture it (a multi-rank command cannot be profiled): GPU 0 holds learners [0, L/2)
 and runs rank 0's step; learners [L/2, L) live on GPU 1 and are read over NVLink
-through peer pointers (rm_enable_peer_access).  C2 shapes."""
+through peer pointers (rm_enable_peer_access).  C2 shapes.  PP_FIXED=1: the fixed ring
+(AD-PSGD) instead of RAD — only the two boundary rows cross."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -29,7 +30,8 @@ torch.cuda.set_device(d0)
 res = {}
 ms = []
 for k in range(12):
-    lt, rt = simulation.rad_tables(L, 12345, k, d0)
+    lt, rt = (simulation.fixed_ring_tables(L, d0) if os.environ.get("PP_FIXED") == "1"
+              else simulation.rad_tables(L, 12345, k, d0))
     s = _lib.stream_ptr()
     _lib.check(lib.rm_shard_plan(lt.data_ptr(), rt.data_ptr(), L, 0, Lg, plan.data_ptr(), s))
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
