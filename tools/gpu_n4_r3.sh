@@ -2,7 +2,7 @@
 # the multi-GPU tests on 4 GPUs, the D1D training step (serial vs the default concurrency) at
 # N = 4 and N = 2, dist_check at n = 3 (ragged).
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/n4_r3; mkdir -p $O
+O=gpurun_out/${1:-n4_r3}; mkdir -p $O
 nvidia-smi topo -m > $O/topo.txt 2>&1
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
 ( time timeout 900 python bench.py ) > $O/drv_ours_n1.log 2>&1
