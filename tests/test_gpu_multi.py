@@ -20,7 +20,9 @@ pytestmark = pytest.mark.gpu
 def test_learner_sharded_steps_on_all_visible_gpus(L, d):
     """Balanced and unbalanced learner shards, ragged widths: RAD (pull and position
     layouts, in-kernel step ordering) bit-identical to one GPU; D1D (NCCL, NVLS pipeline,
-    fused kernel; fp32 / fp64 / bf16) within fp64 rounding of the sum."""
+    fused kernel; fp32 / fp64 / bf16) and the D1D training step with the device oracle
+    (ShardedD1DTrainer) bit-identical to one GPU with the numpy-order learner layout, within
+    fp64 rounding of the sum otherwise."""
     import os
     n = min(torch.cuda.device_count(), 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",

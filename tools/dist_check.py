@@ -165,6 +165,35 @@ def main():
     pos_steps.append(bool(pos.placed) == (L % world == 0 and world <= 8))
     ok_pos &= pos_steps[-1]
     pos.close()
+    # the D1D training step with the device oracle (ShardedD1DTrainer: average beside the
+    # generator, gradient fused into its final pass) against the one-GPU step on the same
+    # data — bit for bit with the numpy-order layout, else to fp64 rounding of the mean
+    from paper_2002_01119_b200 import objectives
+    from paper_2002_01119_b200.simulation import RunConfig
+    ok_tr, tr_diff = True, None
+    try:
+        oracle = objectives.quadratic_oracle(d, condition_number=5.0, noise_scale=1.0, seed=3,
+                                             device=dev)
+        cfg = RunConfig(n_learners=L, iterations=1, lr=0.01, batch_size=4, seed=7,
+                        dtype="float32")
+        b0, e0 = D.ShardLayout(L, world).bounds[rank]
+        tr = D.ShardedD1DTrainer(L, d, e0 - b0, b0, dev, oracle)
+        ids = torch.tensor(D.d1d_learners(L, world, rank, tr.chains), device=dev)
+        Wl = mixing.empty_learner_major(len(ids), d, torch.float32, dev).copy_(full[ids])
+        Pl = mixing.empty_learner_major(len(ids), d, torch.float32, dev).copy_(Gf[ids])
+        out_tr = mixing.empty_learner_major(len(ids), d, torch.float32, dev)
+        tr.step(Wl, Pl, cfg, 3, 0.01, out_tr)
+        Gref = oracle.device_gradients(mixing.empty_learner_major(L, d, torch.float32, dev)
+                                       .copy_(Gf), cfg, 3)
+        ref_tr = mixing.mean_mix_sgd(mixing.empty_learner_major(L, d, torch.float32, dev)
+                                     .copy_(full), Gref, 0.01)
+        torch.cuda.synchronize()
+        tr_diff = (out_tr.double() - ref_tr[ids].double()).abs().max().item()
+        ok_tr = tr_diff == 0.0 if tr.chains else tr_diff <= 2e-6
+        nvls += f"; trainer chains={tr.chains} maxdiff {tr_diff:.2e}"
+    except RuntimeError as exc:
+        nvls += f"; trainer: {str(exc)[:80]}"
+    ok_d1d = ok_d1d and ok_tr
     detail = torch.tensor([int(x) for x in pull_steps + pos_steps], device=dev)
     all_detail = [torch.zeros_like(detail) for _ in range(world)]
     dist.all_gather(all_detail, detail)
