@@ -117,3 +117,45 @@ def test_symmetric_addresses_multicast_or_peer_table(monkeypatch):
     H.multicast_ptr = 0
     mc, tab = D._sym_addresses(H, "cpu")
     assert mc == 0 and tab.tolist() == [0x1040, 0x2040, 0x3040]
+
+
+@pytest.mark.parametrize("L,world", [(8, 1), (16, 2), (64, 4), (64, 8), (128, 2), (24, 3),
+                                     (67, 2), (200, 2), (64, 16)])
+def test_numpy_order_d1d_layout(L, world, monkeypatch):
+    """The numpy-order D1D learner layout (distributed.d1d_numpy_chains / d1d_learners):
+    where it applies, rank g holds exactly the learners of numpy's pairwise chains
+    [g R, (g + 1) R) (l % 8), in ascending order, every learner on one rank; numpy's pairwise
+    tree over the ranks' chain subtrees is then its tree over the eight chains (the restated
+    sum below equals numpy's own np.sum bit for bit).  Elsewhere: contiguous blocks."""
+    monkeypatch.delenv("RINGMIX_D1D_NUMPY_ORDER", raising=False)
+    R = D.d1d_numpy_chains(L, world)
+    applies = L % 8 == 0 and 8 <= L <= 128 and world in (1, 2, 4, 8)
+    assert (R == 8 // world) if applies else R == 0
+    sets = [D.d1d_learners(L, world, g, R) for g in range(world)]
+    assert sorted(sum(sets, [])) == list(range(L))
+    if not R:
+        assert all(s == list(range(s[0], s[-1] + 1)) for s in sets if s)
+        return
+    for g, s in enumerate(sets):
+        assert s == sorted(s) and all(g * R <= l % 8 < (g + 1) * R for l in s)
+    rng = np.random.default_rng(L + world)
+    x = rng.standard_normal(L) * rng.lognormal(0, 3, L)
+
+    def subtree(vals):          # numpy's tree over consecutive chains
+        while len(vals) > 1:
+            vals = [vals[i] + vals[i + 1] for i in range(0, len(vals), 2)]
+        return vals[0]
+
+    parts = []
+    for g in range(world):      # rank g: its chains (sequential over its rows), then the tree
+        chains = []
+        for q in range(R):
+            rows = [l for l in sets[g] if l % 8 == g * R + q]
+            acc = x[rows[0]]
+            for l in rows[1:]:
+                acc = acc + x[l]
+            chains.append(acc)
+        parts.append(subtree(chains))
+    assert subtree(parts) == np.sum(x)       # numpy's pairwise sum of L <= 128 values
+    monkeypatch.setenv("RINGMIX_D1D_NUMPY_ORDER", "0")
+    assert D.d1d_numpy_chains(L, world) == 0
