@@ -27,7 +27,9 @@ prints ONE JSON line on rank 0.  `--gpus N` without torchrun launches N ranks it
   64 x 25,557,032 stripe, weak scaling).  D1D (`--strategy d1d`, and `extras.c4_d1d_sharded`
   on configs[3]) shards learners with the fused partial-sum / cross-GPU-reduce / apply kernel;
   `extras.c2_adpsgd_fixed_sharded` is configs[1]'s fixed ring with learners sharded (only the
-  two ring-boundary rows per rank cross GPUs).
+  two ring-boundary rows per rank cross GPUs); `extras.c4_d1d_training_sharded` times
+  configs[3]'s D1D training step with the device oracle — the global average beside the
+  gradient generator (north-star (c)) against the serial order.
 * `value`: whole-job learner-params / s, device time (CUDA events), max over ranks.
 * `e2e`: the same step through the public API with the step's inputs and results
   crossing PCIe every step: N = 1 host buffers in and out (W, G -> W',
@@ -939,6 +941,15 @@ def run_ours(args):
             del w2
             torch.cuda.empty_cache()
 
+    if not args.no_extras and ws > 1 and spec.strategy == "rand_psgd" and \
+            args.dtype == "float32" and args.learners is None and args.dim is None:
+        try:
+            line = d1d_training_extra(torch, dist, dev, ws, rank)
+        except (RuntimeError, ValueError) as exc:
+            line = {"error": str(exc)[:200]}
+        if rank == 0:
+            extras["c4_d1d_training_sharded"] = line
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:   # the CPU baseline is an N = 1 figure
         cpu = cpu_baseline(L, uniform, args.cpu_seconds)
@@ -983,6 +994,62 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def d1d_training_extra(torch, dist, dev, ws, rank, steps=12):
+    """configs[3]'s D1D *training* step with the device quadratic oracle, learners sharded
+    (distributed.ShardedD1DTrainer): the paper's concurrency — the global average of W_k
+    beside the generator of G(W_{k-1}), G fused into the generator's final pass — against
+    the serial order (gradient, then the one-kernel fused D1D step).  Per-step device time
+    (CUDA events, max over ranks, median of `steps`); both orders give the same bits."""
+    from paper_2002_01119_b200 import distributed as D, mixing, objectives
+    from paper_2002_01119_b200.simulation import RunConfig
+    L, d = C2
+    b, e = D.ShardLayout(L, ws).bounds[rank]
+    oracle = objectives.quadratic_oracle(d, condition_number=10.0, noise_scale=1.0, seed=1,
+                                         optimum=np.zeros(d), device=dev)
+    cfg = RunConfig(n_learners=L, iterations=1, lr=LR, batch_size=32, seed=5, dtype="float32")
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    W = mixing.empty_learner_major(e - b, d, torch.float32, dev)
+    Wp = mixing.empty_learner_major(e - b, d, torch.float32, dev)
+    W.copy_(torch.randn((e - b, d), generator=g, device=dev))
+    Wp.copy_(torch.randn((e - b, d), generator=g, device=dev))
+    out = mixing.empty_learner_major(e - b, d, torch.float32, dev)
+    res, outs = {}, {}
+    for mode, overlap in (("serial", False), ("concurrent", True)):
+        tr = D.ShardedD1DTrainer(L, d, e - b, b, dev, oracle, overlap=overlap,
+                                 fuse_grad=overlap)
+        for k in range(3):
+            tr.step(W, Wp, cfg, k, LR, out)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ts = []
+        for k in range(steps):
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            tr.step(W, Wp, cfg, 10 + k, LR, out)
+            z.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(z)], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ts.append(float(t))
+        res[mode] = float(np.median(ts))
+        outs[mode] = out.clone()
+        chains = tr.chains
+        del tr
+        torch.cuda.synchronize()
+        dist.barrier()
+    same = torch.tensor([int(torch.equal(outs["serial"], outs["concurrent"]))], device=dev)
+    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    del W, Wp, out, outs
+    torch.cuda.empty_cache()
+    return {"workload": f"d1d training step (device quadratic oracle, bit-exact numpy "
+                        f"gradient noise), {L} learners x {d} params, BASELINE.json configs[3]",
+            "layout": "learner", "scaling": "strong", "unit": UNIT,
+            "value": L * d / (res["concurrent"] / 1e3), "ms_per_step": res["concurrent"],
+            "serial_ms_per_step": res["serial"], "bit_identical_orders": bool(same.item()),
+            "numpy_order_chains": chains,
+            "timing": "CUDA events per step, max over ranks, median of %d" % steps}
 
 
 def wl_kind(spec, ws):
